@@ -1,0 +1,175 @@
+/* svr.h -- C-ABI of the B200-native sparse-dense SDF rendering path
+ * (libsvr_b200.so, built from paper_2305_13220_b200/csrc/).
+ *
+ * Drop-in boundary for the reference `svrecon` grid/renderer API
+ * (/root/reference/proj/src/core/grid.hpp:100-223, allocation.hpp:22-29,
+ * grid_io.hpp:14-15, renderer ops specified in SPEC.md:268-327).  The reference is a
+ * C++ class library with no FFI of its own; each entry point below names the reference
+ * member it replaces.  Plain pointers and sizes only -- no Eigen, no torch types.
+ *
+ * Memory: every array argument may be HOST memory (pageable or pinned) or DEVICE
+ * memory on the grid's GPU; the library inspects each pointer
+ * (cudaPointerGetAttributes).  A call whose array arguments are all device pointers is
+ * asynchronous on the grid's stream (svr_grid_set_stream); a call with any host array
+ * stages through device scratch and returns after the results are on the host.
+ *
+ * Errors: never throws across the ABI.  Status codes mirror the reference exceptions
+ * (proj/src/core/errors.hpp:8-31) and svr_last_error() returns the thread's last
+ * message.  Queries of unallocated / unobserved space are flags, not errors
+ * (grid.cpp:240-261).
+ *
+ * Threading: one handle = one device + one stream.  Calls on one handle must be
+ * serialised by the caller; activation must not overlap rendering.
+ * Block resolution is specialised to 8 (the paper's 8^3 blocks); other
+ * values return SVR_ERR_CONFIG.  Block coordinates must lie in [-2^20, 2^20) per axis
+ * (64-bit packed keys, 21 bits per axis).
+ */
+#ifndef SVR_H
+#define SVR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVR_ABI_VERSION 1
+
+#define SVR_OK 0
+#define SVR_ERR_CONFIG 2   /* ConfigError   (errors.hpp:12-15) */
+#define SVR_ERR_DATA 3     /* DataError     (errors.hpp:17-20) */
+#define SVR_ERR_DIVERGED 4 /* DivergedError (errors.hpp:22-25) */
+#define SVR_ERR_CAPACITY 5 /* CapacityError (errors.hpp:27-31); see report->unallocated */
+#define SVR_ERR_CUDA 6     /* CUDA runtime / device failure */
+
+#define SVR_INVALID_BLOCK 0xFFFFFFFFu /* SparseDenseGrid::kInvalidBlock (grid.hpp:102) */
+
+#define SVR_LOOKUP_AUTO 0  /* dense AABB index when it fits, else hash */
+#define SVR_LOOKUP_HASH 1  /* always probe the hash table */
+#define SVR_LOOKUP_DENSE 2 /* require the dense AABB index */
+
+typedef struct svr_grid svr_grid;
+
+/* Camera (camera.hpp:16-29): pinhole, camera-to-world x_w = R x_c + t, R row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double R[9];
+    double t[3];
+} svr_camera;
+
+/* AllocationReport (allocation.hpp:13-17) + CapacityError::unallocated_blocks. */
+typedef struct {
+    uint64_t blocks_added;
+    uint64_t blocks_requested;
+    uint64_t pixels_used;
+    uint64_t unallocated;
+} svr_alloc_report;
+
+typedef struct {
+    double voxel_size;
+    int32_t block_res;
+    int32_t label_channels;
+    uint64_t capacity;
+    uint64_t block_count;
+    uint64_t hash_slots;
+    int32_t bounds_lo[3]; /* min block coordinate (grid.hpp:222), valid iff block_count */
+    int32_t bounds_hi[3]; /* max block coordinate */
+    int32_t lookup_mode;  /* SVR_LOOKUP_HASH or SVR_LOOKUP_DENSE actually in use */
+    int32_t device;
+    uint64_t device_bytes; /* device memory owned by the handle */
+} svr_grid_info;
+
+typedef struct {
+    uint64_t rays;           /* rays in the last render_forward */
+    uint64_t samples;        /* marched samples (sum of per-ray counts) */
+    uint64_t valid_samples;  /* samples whose 8 corners were all allocated and observed */
+} svr_render_stats;
+
+const char* svr_last_error(void);
+int svr_abi_version(void);
+int svr_device_count(int32_t* n);
+
+/* SparseDenseGrid(voxel_size, block_res, label_channels, capacity) (grid.hpp:104-107).
+ * capacity 0 = kDefaultCapacity (2^21).  Payload memory grows on demand. */
+int svr_grid_create(double voxel_size, int32_t block_res, int32_t label_channels,
+                    uint64_t capacity, int32_t device, svr_grid** out);
+int svr_grid_destroy(svr_grid* g);
+int svr_grid_set_stream(svr_grid* g, void* cuda_stream);
+int svr_grid_synchronize(svr_grid* g);
+int svr_grid_get_info(svr_grid* g, svr_grid_info* out);
+int svr_grid_set_lookup(svr_grid* g, int32_t mode);
+
+/* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */
+int svr_grid_load_sdgv(const char* path, int32_t device, svr_grid** out);
+int svr_grid_save_sdgv(svr_grid* g, const char* path);
+
+/* allocate_block (grid.cpp:88-108) applied to coords[n][3] in order; idx_out[n] gets the
+ * existing or new index.  Partial allocation then SVR_ERR_CAPACITY at capacity. */
+int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out);
+/* allocate_for_points (allocation.cpp:45-54): block of each point + L-inf dilation.
+ * New blocks get indices in ascending packed-key (z, y, x) order. */
+int svr_grid_activate_points(svr_grid* g, const double* xyz, uint64_t n, int32_t dilation,
+                             svr_alloc_report* report);
+/* allocate_for_frames (allocation.cpp:56-83): depth[n_frames][H][W] (<= 0 invalid),
+ * optional per-frame ScaleField grids scales[n_frames][sf_rows][sf_cols] (NULL = 1). */
+int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* cams,
+                            uint32_t n_frames, const double* scales, int32_t sf_rows,
+                            int32_t sf_cols, int32_t dilation, svr_alloc_report* report);
+/* find_block (grid.hpp:156) for coords[n][3]; SVR_INVALID_BLOCK when absent. */
+int svr_grid_find(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out);
+/* block_coord(i) for all blocks: out[block_count][3]. */
+int svr_grid_coords(svr_grid* g, int32_t* out);
+
+/* VoxelBlock payload (grid.hpp:62-66) for blocks [first, first+n), reference layout per
+ * block: sdf[512], weight[512] (valid iff > 0), rgb[512][3], logits[512][C].
+ * Any pointer may be NULL to skip that channel. */
+int svr_grid_set_payload(svr_grid* g, uint32_t first, uint32_t n, const float* sdf,
+                         const float* weight, const float* rgb, const float* logits);
+int svr_grid_get_payload(svr_grid* g, uint32_t first, uint32_t n, float* sdf, float* weight,
+                         float* rgb, float* logits);
+
+/* query_sdf_with_gradient + color_at + logits_at over CornerCacheD (grid.cpp:157-261),
+ * fp64 with the reference's operation order: x[n][3] -> sdf[n], grad[n][3], rgb[n][3],
+ * logits[n][C], valid[n].  Invalid -> zeros.  Any output may be NULL. */
+int svr_query(svr_grid* g, const double* x, uint64_t n, double* sdf, double* grad, double* rgb,
+              double* logits, uint8_t* valid);
+
+/* march_ray (grid.cpp:263-353) for o[n][3], d[n][3] (unit): counts[n],
+ * t[n][max_samples], delta[n][max_samples] (bit-exact fp64).  t/delta may be NULL. */
+int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double step,
+              uint32_t max_samples, uint32_t* counts, double* t, double* delta);
+
+/* render_ray forward for n rays: rgb[n][3], depth[n], normal[n][3]
+ * (world, un-normalised), wsum[n]; n_samples[n] optional.  Retains the context that
+ * svr_render_backward consumes (device ray buffers must stay valid until then). */
+int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n, double step,
+                       uint32_t max_samples, double beta, float* rgb, float* depth,
+                       float* normal, float* wsum, uint32_t* n_samples);
+/* backward_step render part: upstream d_rgb[n][3], d_depth[n],
+ * d_normal[n][3] of the last forward; accumulates into the grid's gradient planes
+ * (grad_sdf / grad_color, grid.hpp:69) and marks active blocks. */
+int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth,
+                        const float* d_normal);
+int svr_render_get_stats(svr_grid* g, svr_render_stats* out);
+
+/* Gradient planes. grad_get: g_sdf[A][512], g_rgb[A][512][3]. */
+int svr_grad_zero(svr_grid* g);
+int svr_grad_get(svr_grid* g, float* g_sdf, float* g_rgb);
+/* Active blocks (touched by a valid sample since the last grad_zero):
+ * mask[A] (0/1, optional) and/or the ascending index list + count. */
+int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* count);
+/* Multi-GPU plumbing (device pointers): mark blocks from a union mask, then pack /
+ * unpack the gradients of `blocks[n]` as [n][512][4] floats (g_sdf, g_r, g_g, g_b). */
+int svr_active_set_mask(svr_grid* g, const uint8_t* mask);
+int svr_grad_pack(svr_grid* g, const uint32_t* blocks, uint64_t n, float* out);
+int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float* in);
+/* Zero the gradients of the active blocks only and clear the active mask. */
+int svr_grad_zero_active(svr_grid* g);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

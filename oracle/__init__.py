@@ -1,0 +1,347 @@
+"""TEST INFRASTRUCTURE ONLY -- Python handles on the CPU checkers.
+
+* ``OracleGrid``  -> liboracle.so, the C++ restatement (svr_oracle.cpp) of the reference
+  grid / march / activation code plus the spec-restated renderer, fp64 throughout.
+* ``RefGrid``     -> _ref/libsvr_ref.so, the reference's own sources
+  (/root/reference/proj/src/core/{grid,allocation,camera,grid_io,scale_field,parallel}.cpp)
+  compiled verbatim against shim/ (see Makefile), plus ref_capi.cpp's renderer on top.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+may import this package.  The product (paper_2305_13220_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libsvr_ref.so")
+REF_TESTS = os.path.join(HERE, "_ref", "ref_tests")
+REF_ROOT = "/root/reference/proj"
+
+
+def build(ref: bool | None = None) -> None:
+    """make liboracle.so (always) and _ref/* (when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+    if ref is None:
+        ref = os.path.isdir(REF_ROOT)
+    if ref:
+        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("blocks_added", c_uint64), ("blocks_requested", c_uint64),
+                ("pixels_used", c_uint64), ("unallocated", c_uint64)]
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg, report=None):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+        self.report = report
+
+
+P = c_void_p
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a if shape is None else a.reshape(shape)
+
+
+class _Base:
+    _so = None
+    _prefix = ""
+    _protos: dict = {}
+    _lib = None
+
+    @classmethod
+    def lib(cls):
+        if cls._lib is None:
+            if not os.path.exists(cls._so):
+                build()
+            lib = ctypes.CDLL(cls._so)
+            for name, (res, args) in cls._protos.items():
+                fn = getattr(lib, cls._prefix + name)
+                fn.restype = res
+                fn.argtypes = args
+            cls._lib = lib
+        return cls._lib
+
+    def _check(self, st, report=None):
+        if st:
+            msg = getattr(self.lib(), self._prefix + "last_error")().decode()
+            raise OracleError(st, msg, report)
+
+    def __del__(self):
+        try:
+            if self._h.value:
+                getattr(self.lib(), self._prefix + "grid_destroy")(self._h)
+        except Exception:
+            pass
+
+    def block_count(self) -> int:
+        return int(getattr(self.lib(), self._prefix + "block_count")(self._h))
+
+    def coords(self) -> np.ndarray:
+        out = np.empty((self.block_count(), 3), np.int32)
+        getattr(self.lib(), self._prefix + "coords")(self._h, _ptr(out))
+        return out
+
+    def allocate_blocks(self, coords) -> np.ndarray:
+        c = np.ascontiguousarray(coords, np.int32).reshape(-1, 3)
+        idx = np.empty(len(c), np.uint32)
+        self._check(getattr(self.lib(), self._prefix + "allocate_blocks")(self._h, _ptr(c), len(c), _ptr(idx)))
+        return idx
+
+    def allocate_points(self, pts, dilation) -> Report:
+        p = _f64(pts, (-1, 3))
+        rep = Report()
+        st = getattr(self.lib(), self._prefix + "allocate_points")(self._h, _ptr(p), len(p), dilation,
+                                                                   ctypes.byref(rep))
+        self._check(st, rep)
+        return rep
+
+    def allocate_frames(self, depth, cams, dilation, scales=None) -> Report:
+        d = np.ascontiguousarray(depth, np.float32)
+        arr = (_Cam * len(cams))(*[_Cam.from_any(c) for c in cams])
+        sc = None if scales is None else np.ascontiguousarray(scales, np.float64)
+        rows, cols = (0, 0) if sc is None else (sc.shape[-2], sc.shape[-1])
+        rep = Report()
+        st = getattr(self.lib(), self._prefix + "allocate_frames")(
+            self._h, _ptr(d), ctypes.addressof(arr), len(cams), _ptr(sc), rows, cols, dilation,
+            ctypes.byref(rep))
+        self._check(st, rep)
+        return rep
+
+    def find(self, coords) -> np.ndarray:
+        c = np.ascontiguousarray(coords, np.int32).reshape(-1, 3)
+        out = np.empty(len(c), np.uint32)
+        getattr(self.lib(), self._prefix + "find")(self._h, _ptr(c), len(c), _ptr(out))
+        return out
+
+    def set_payload(self, first, n, sdf=None, weight=None, rgb=None, logits=None):
+        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)  # noqa: E731
+        arrs = [f(sdf), f(weight), f(rgb), f(logits)]
+        self._check(getattr(self.lib(), self._prefix + "set_payload")(self._h, first, n, *[_ptr(a) for a in arrs]))
+
+    def march(self, o, d, step, max_samples):
+        o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
+        n = len(o)
+        counts = np.empty(n, np.uint32)
+        t = np.zeros((n, max_samples), np.float64)
+        delta = np.zeros((n, max_samples), np.float64)
+        getattr(self.lib(), self._prefix + "march")(self._h, _ptr(o), _ptr(d), n, step, max_samples,
+                                                    _ptr(counts), _ptr(t), _ptr(delta))
+        return {"counts": counts, "t": t, "delta": delta}
+
+    def save(self, path):
+        self._check(getattr(self.lib(), self._prefix + "save_sdgv")(self._h, str(path).encode()))
+
+
+class _Cam(ctypes.Structure):
+    _fields_ = [("fx", c_double), ("fy", c_double), ("cx", c_double), ("cy", c_double),
+                ("width", c_int32), ("height", c_int32), ("R", c_double * 9), ("t", c_double * 3)]
+
+    @classmethod
+    def from_any(cls, c):
+        out = cls()
+        for k in ("fx", "fy", "cx", "cy", "width", "height"):
+            setattr(out, k, getattr(c, k))
+        out.R[:] = list(c.R)
+        out.t[:] = list(c.t)
+        return out
+
+
+_COMMON = {
+    "last_error": (c_char_p, []),
+    "set_threads": (None, [c_int]),
+    "grid_destroy": (None, [c_void_p]),
+    "block_count": (c_uint64, [c_void_p]),
+    "coords": (None, [c_void_p, P]),
+    "allocate_blocks": (c_int, [c_void_p, P, c_uint64, P]),
+    "allocate_points": (c_int, [c_void_p, P, c_uint64, c_int, POINTER(Report)]),
+    "allocate_frames": (c_int, [c_void_p, P, P, c_uint32, P, c_int, c_int, c_int, POINTER(Report)]),
+    "find": (None, [c_void_p, P, c_uint64, P]),
+    "set_payload": (c_int, [c_void_p, c_uint32, c_uint32, P, P, P, P]),
+    "march": (None, [c_void_p, P, P, c_uint64, c_double, c_uint32, P, P, P]),
+    "save_sdgv": (c_int, [c_void_p, c_char_p]),
+    "load_sdgv": (c_int, [c_char_p, POINTER(c_void_p)]),
+}
+
+
+class OracleGrid(_Base):
+    """The restated CPU oracle (svr_oracle.cpp)."""
+
+    _so = ORACLE_SO
+    _prefix = "svro_"
+    _protos = dict(_COMMON, **{
+        "grid_create": (c_int, [c_double, c_int, c_int, c_uint64, POINTER(c_void_p)]),
+        "bounds": (c_int, [c_void_p, P, P]),
+        "get_payload": (c_int, [c_void_p, c_uint32, c_uint32, P, P, P, P]),
+        "query": (None, [c_void_p, P, c_uint64, P, P, P, P, P]),
+        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P]),
+        "render_backward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P, P]),
+        "sdf_to_density": (c_double, [c_double, c_double]),
+    })
+
+    def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
+        self.C = label_channels
+        self.B = block_res
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = c_void_p()
+        self._check(self.lib().svro_grid_create(voxel_size, block_res, label_channels, capacity, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def load(cls, path, label_channels):
+        h = c_void_p()
+        st = cls.lib().svro_load_sdgv(str(path).encode(), ctypes.byref(h))
+        if st:
+            raise OracleError(st, cls.lib().svro_last_error().decode())
+        return cls(label_channels=label_channels, _handle=h)
+
+    @classmethod
+    def set_threads(cls, n):
+        cls.lib().svro_set_threads(n)
+
+    @classmethod
+    def density(cls, s, beta):
+        return cls.lib().svro_sdf_to_density(s, beta)
+
+    def bounds(self):
+        lo = np.zeros(3, np.int32)
+        hi = np.zeros(3, np.int32)
+        st = self.lib().svro_bounds(self._h, _ptr(lo), _ptr(hi))
+        return (lo, hi) if st == 0 else None
+
+    def get_payload(self, first=0, n=None):
+        n = self.block_count() - first if n is None else n
+        V = self.B ** 3
+        out = {"sdf": np.empty((n, V), np.float32), "weight": np.empty((n, V), np.float32),
+               "rgb": np.empty((n, V, 3), np.float32), "logits": np.empty((n, V, self.C), np.float32)}
+        self._check(self.lib().svro_get_payload(self._h, first, n, *[_ptr(out[k]) for k in
+                                                                     ("sdf", "weight", "rgb", "logits")]))
+        return out
+
+    def query(self, x, logits=False):
+        x = _f64(x, (-1, 3))
+        n = len(x)
+        out = {"sdf": np.empty(n), "grad": np.empty((n, 3)), "rgb": np.empty((n, 3)),
+               "valid": np.empty(n, np.uint8)}
+        lg = np.empty((n, self.C)) if logits else None
+        self.lib().svro_query(self._h, _ptr(x), n, _ptr(out["sdf"]), _ptr(out["grad"]), _ptr(out["rgb"]),
+                              _ptr(lg), _ptr(out["valid"]))
+        if logits:
+            out["logits"] = lg
+        return out
+
+    def render_forward(self, o, d, step, max_samples, beta):
+        o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
+        n = len(o)
+        out = {"rgb": np.empty((n, 3)), "depth": np.empty(n), "normal": np.empty((n, 3)),
+               "wsum": np.empty(n), "n_samples": np.empty(n, np.uint32)}
+        self._check(self.lib().svro_render_forward(self._h, _ptr(o), _ptr(d), n, step, max_samples, beta,
+                                                   _ptr(out["rgb"]), _ptr(out["depth"]), _ptr(out["normal"]),
+                                                   _ptr(out["wsum"]), _ptr(out["n_samples"])))
+        return out
+
+    def render_backward(self, o, d, step, max_samples, beta, d_rgb, d_depth, d_normal):
+        o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
+        n = len(o)
+        A, V = self.block_count(), self.B ** 3
+        gs = np.zeros((A, V))
+        gr = np.zeros((A, V, 3))
+        active = np.zeros(A, np.uint8)
+        up = [_f64(d_rgb, (-1, 3)), _f64(d_depth, (-1,)), _f64(d_normal, (-1, 3))]
+        self._check(self.lib().svro_render_backward(
+            self._h, _ptr(o), _ptr(d), n, step, max_samples, beta, _ptr(up[0]), _ptr(up[1]),
+            _ptr(up[2]), _ptr(gs), _ptr(gr), _ptr(active)))
+        return gs, gr, active
+
+
+class RefGrid(_Base):
+    """The reference's own grid code compiled verbatim (oracle/_ref/libsvr_ref.so)."""
+
+    _so = REF_SO
+    _prefix = "svrr_"
+    _protos = dict(_COMMON, **{
+        "grid_create": (c_int, [c_double, c_int, c_int, c_uint64, POINTER(c_void_p)]),
+        "worker_count": (c_int, []),
+        "bounds": (c_int, [c_void_p, P, P]),
+        "query": (None, [c_void_p, P, c_uint64, P, P, P, P]),
+        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P]),
+        "render_backward": (c_int, [c_void_p, P, P, P]),
+        "grad_get": (c_int, [c_void_p, P, P]),
+    })
+
+    def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
+        self.C = label_channels
+        self.B = block_res
+        if _handle is not None:
+            self._h = _handle
+            return
+        h = c_void_p()
+        self._check(self.lib().svrr_grid_create(voxel_size, block_res, label_channels, capacity, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def load(cls, path, label_channels):
+        h = c_void_p()
+        st = cls.lib().svrr_load_sdgv(str(path).encode(), ctypes.byref(h))
+        if st:
+            raise OracleError(st, cls.lib().svrr_last_error().decode())
+        return cls(label_channels=label_channels, _handle=h)
+
+    @classmethod
+    def set_threads(cls, n):
+        cls.lib().svrr_set_threads(n)
+
+    @classmethod
+    def worker_count(cls):
+        return cls.lib().svrr_worker_count()
+
+    def query(self, x):
+        x = _f64(x, (-1, 3))
+        n = len(x)
+        out = {"sdf": np.empty(n), "grad": np.empty((n, 3)), "rgb": np.empty((n, 3)),
+               "valid": np.empty(n, np.uint8)}
+        self.lib().svrr_query(self._h, _ptr(x), n, _ptr(out["sdf"]), _ptr(out["grad"]), _ptr(out["rgb"]),
+                              _ptr(out["valid"]))
+        return out
+
+    def render_forward(self, o, d, step, max_samples, beta):
+        o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
+        n = len(o)
+        out = {"rgb": np.empty((n, 3), np.float32), "depth": np.empty(n, np.float32),
+               "normal": np.empty((n, 3), np.float32), "wsum": np.empty(n, np.float32)}
+        self._check(self.lib().svrr_render_forward(self._h, _ptr(o), _ptr(d), n, step, max_samples, beta,
+                                                   _ptr(out["rgb"]), _ptr(out["depth"]), _ptr(out["normal"]),
+                                                   _ptr(out["wsum"])))
+        return out
+
+    def render_backward(self, d_rgb, d_depth, d_normal):
+        up = [np.ascontiguousarray(a, np.float32) for a in (d_rgb, d_depth, d_normal)]
+        self._check(self.lib().svrr_render_backward(self._h, *[_ptr(a) for a in up]))
+
+    def grads(self):
+        A, V = self.block_count(), self.B ** 3
+        gs = np.empty((A, V), np.float32)
+        gr = np.empty((A, V, 3), np.float32)
+        self.lib().svrr_grad_get(self._h, _ptr(gs), _ptr(gr))
+        return gs, gr

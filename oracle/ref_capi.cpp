@@ -1,0 +1,385 @@
+// TEST INFRASTRUCTURE ONLY -- C wrapper over the REFERENCE's own grid code
+// (/root/reference/proj/src/core/*.cpp compiled verbatim, see Makefile) so Python
+// tests can (a) validate the restated oracle against the reference and (b) time the
+// reference CPU path for bench.py --impl reference.  The reference has no renderer
+// (SURVEY.md section 0.2); svrr_render_* below restate SPEC.md:268-319 ON TOP of the
+// reference API exactly as the spec prescribes: march_ray -> gather_corners into a
+// retained CornerCache (grid.hpp:76-86) -> sdf_at / sdf_gradient_at / color_at ->
+// Laplace density -> compositing; backward scatters from the retained caches into the
+// reference's grad_sdf / grad_color shadow buffers (grid.hpp:69), rays split with
+// svr::parallel_chunks (parallel.cpp:35-63) and float atomics.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "core/allocation.hpp"
+#include "core/errors.hpp"
+#include "core/grid.hpp"
+#include "core/grid_io.hpp"
+#include "core/parallel.hpp"
+#include "core/scale_field.hpp"
+
+using namespace svr;
+
+namespace {
+thread_local std::string g_err;
+
+struct Retained {
+    CornerCache cc;
+    float s, grad[3], rgb[3];
+    double t, delta;
+    bool valid;
+};
+}  // namespace
+
+struct svrr_grid {
+    std::unique_ptr<SparseDenseGrid> g;
+    // retained forward context for svrr_render_backward
+    std::vector<std::vector<Retained>> rays;
+    double beta = 0.0;
+};
+
+typedef struct {
+    uint64_t blocks_added, blocks_requested, pixels_used, unallocated;
+} svrr_report;
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double R[9];
+    double t[3];
+} svrr_camera;
+
+namespace {
+template <typename Fn>
+int guarded(Fn&& fn, svrr_report* rep = nullptr) {
+    try {
+        fn();
+        return 0;
+    } catch (const CapacityError& e) {
+        g_err = e.what();
+        if (rep) rep->unallocated = e.unallocated_blocks;
+        return 5;
+    } catch (const ConfigError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const DataError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 3;
+    }
+}
+
+Camera to_camera(const svrr_camera& c) {
+    Camera cam;
+    cam.fx = c.fx;
+    cam.fy = c.fy;
+    cam.cx = c.cx;
+    cam.cy = c.cy;
+    cam.width = c.width;
+    cam.height = c.height;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) cam.rotation(i, j) = c.R[3 * i + j];
+    cam.translation = Eigen::Vector3d(c.t[0], c.t[1], c.t[2]);
+    return cam;
+}
+
+inline double density(double s, double beta) {
+    const double ib = 1.0 / beta;
+    return s > 0.0 ? ib * (0.5 * std::exp(-s / beta)) : ib * (1.0 - 0.5 * std::exp(s / beta));
+}
+}  // namespace
+
+extern "C" {
+
+const char* svrr_last_error(void) { return g_err.c_str(); }
+void svrr_set_threads(int n) { set_worker_count(n); }
+int svrr_worker_count(void) { return worker_count(); }
+
+int svrr_grid_create(double h, int B, int C, uint64_t capacity, svrr_grid** out) {
+    return guarded([&] {
+        auto* w = new svrr_grid();
+        w->g = std::make_unique<SparseDenseGrid>(
+            h, B, C, capacity ? capacity : SparseDenseGrid::kDefaultCapacity);
+        *out = w;
+    });
+}
+void svrr_grid_destroy(svrr_grid* w) { delete w; }
+uint64_t svrr_block_count(const svrr_grid* w) { return w->g->block_count(); }
+void svrr_coords(const svrr_grid* w, int32_t* out) {
+    for (uint32_t i = 0; i < w->g->block_count(); ++i) {
+        const BlockCoord& c = w->g->block_coord(i);
+        out[3 * i] = c.x, out[3 * i + 1] = c.y, out[3 * i + 2] = c.z;
+    }
+}
+int svrr_bounds(const svrr_grid* w, double* lo3, double* hi3) {
+    if (w->g->empty()) return 3;
+    const Eigen::AlignedBox3d b = w->g->allocated_bounds();
+    for (int a = 0; a < 3; ++a) lo3[a] = b.min()[a], hi3[a] = b.max()[a];
+    return 0;
+}
+
+int svrr_allocate_blocks(svrr_grid* w, const int32_t* coords, uint64_t n, uint32_t* idx) {
+    return guarded([&] {
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t v =
+                w->g->allocate_block(BlockCoord{coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]});
+            if (idx) idx[i] = v;
+        }
+    });
+}
+
+int svrr_allocate_points(svrr_grid* w, const double* xyz, uint64_t n, int dilation,
+                         svrr_report* rep) {
+    svrr_report r{};
+    const int st = guarded(
+        [&] {
+            std::vector<Eigen::Vector3d> pts(n);
+            for (uint64_t i = 0; i < n; ++i)
+                pts[i] = Eigen::Vector3d(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]);
+            const AllocationReport a = allocate_for_points(*w->g, pts, dilation);
+            r.blocks_added = a.blocks_added;
+            r.blocks_requested = a.blocks_requested;
+            r.pixels_used = a.pixels_used;
+        },
+        &r);
+    if (rep) *rep = r;
+    return st;
+}
+
+int svrr_allocate_frames(svrr_grid* w, const float* depth, const svrr_camera* cams,
+                         uint32_t n_frames, const double* scales, int rows, int cols,
+                         int dilation, svrr_report* rep) {
+    svrr_report r{};
+    const int st = guarded(
+        [&] {
+            std::vector<Frame> frames(n_frames);
+            std::vector<ScaleField> sfs;
+            for (uint32_t f = 0; f < n_frames; ++f) {
+                frames[f].id = static_cast<int>(f);
+                frames[f].camera = to_camera(cams[f]);
+                const int W = cams[f].width, H = cams[f].height;
+                frames[f].depth = ImageF32(W, H, 1);
+                std::memcpy(frames[f].depth.data.data(), depth + static_cast<size_t>(f) * W * H,
+                            static_cast<size_t>(W) * H * 4);
+                if (scales) {
+                    sfs.emplace_back(rows, cols, W, H);
+                    std::memcpy(sfs.back().values().data(),
+                                scales + static_cast<size_t>(f) * rows * cols,
+                                static_cast<size_t>(rows) * cols * 8);
+                }
+            }
+            const AllocationReport a =
+                allocate_for_frames(*w->g, frames, scales ? &sfs : nullptr, dilation);
+            r.blocks_added = a.blocks_added;
+            r.blocks_requested = a.blocks_requested;
+            r.pixels_used = a.pixels_used;
+        },
+        &r);
+    if (rep) *rep = r;
+    return st;
+}
+
+void svrr_find(const svrr_grid* w, const int32_t* coords, uint64_t n, uint32_t* out) {
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = w->g->find_block(BlockCoord{coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]});
+}
+
+int svrr_set_payload(svrr_grid* w, uint32_t first, uint32_t n, const float* sdf,
+                     const float* weight, const float* rgb, const float* logits) {
+    return guarded([&] {
+        if (static_cast<size_t>(first) + n > w->g->block_count())
+            throw DataError("payload: block range out of bounds");
+        const size_t V = w->g->voxels_per_block(), C = w->g->label_channels();
+        for (uint32_t i = 0; i < n; ++i) {
+            VoxelBlock& b = w->g->block(first + i);
+            if (sdf) std::memcpy(b.sdf.data(), sdf + i * V, V * 4);
+            if (weight) std::memcpy(b.weight.data(), weight + i * V, V * 4);
+            if (rgb) std::memcpy(b.color.data(), rgb + 3 * i * V, 3 * V * 4);
+            if (logits) std::memcpy(b.logits.data(), logits + C * i * V, C * V * 4);
+        }
+    });
+}
+
+void svrr_query(const svrr_grid* w, const double* x, uint64_t n, double* sdf, double* grad,
+                double* rgb, uint8_t* valid) {
+    parallel_chunks(n, [&](size_t b, size_t e, int) {
+        for (size_t i = b; i < e; ++i) {
+            const Eigen::Vector3d p(x[3 * i], x[3 * i + 1], x[3 * i + 2]);
+            double s = 0.0;
+            Eigen::Vector3d gr = Eigen::Vector3d::Zero(), col = Eigen::Vector3d::Zero();
+            const bool ok = w->g->query_sdf_with_gradient(p, s, gr);
+            if (ok) {
+                CornerCacheD cc;
+                w->g->gather_corners(p, cc);
+                col = w->g->color_at(cc);
+            }
+            if (sdf) sdf[i] = s;
+            for (int a = 0; a < 3; ++a) {
+                if (grad) grad[3 * i + a] = gr[a];
+                if (rgb) rgb[3 * i + a] = col[a];
+            }
+            if (valid) valid[i] = ok;
+        }
+    });
+}
+
+void svrr_march(const svrr_grid* w, const double* o, const double* d, uint64_t n, double step,
+                uint32_t max_samples, uint32_t* counts, double* t, double* delta) {
+    parallel_chunks(n, [&](size_t b, size_t e, int) {
+        std::vector<SparseDenseGrid::RaySample> s;
+        for (size_t i = b; i < e; ++i) {
+            w->g->march_ray(Eigen::Vector3d(o[3 * i], o[3 * i + 1], o[3 * i + 2]),
+                            Eigen::Vector3d(d[3 * i], d[3 * i + 1], d[3 * i + 2]), step,
+                            max_samples, s);
+            counts[i] = static_cast<uint32_t>(s.size());
+            for (size_t k = 0; k < s.size(); ++k) {
+                if (t) t[i * max_samples + k] = s[k].t;
+                if (delta) delta[i * max_samples + k] = s[k].delta;
+            }
+        }
+    });
+}
+
+// Forward: per sample gather into a retained float CornerCache (grid.hpp:76-86).
+int svrr_render_forward(svrr_grid* w, const double* o, const double* d, uint64_t n, double step,
+                        uint32_t max_samples, double beta, float* rgb, float* depth,
+                        float* normal, float* wsum) {
+    return guarded([&] {
+        if (!(beta > 0.0)) throw ConfigError("render: beta must be positive");
+        w->rays.resize(n);
+        w->beta = beta;
+        parallel_chunks(n, [&](size_t b, size_t e, int) {
+            std::vector<SparseDenseGrid::RaySample> s;
+            for (size_t i = b; i < e; ++i) {
+                const Eigen::Vector3d ro(o[3 * i], o[3 * i + 1], o[3 * i + 2]);
+                const Eigen::Vector3d rd(d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+                w->g->march_ray(ro, rd, step, max_samples, s);
+                std::vector<Retained>& rec = w->rays[i];
+                rec.resize(s.size());
+                double T = 1.0, C[3] = {0, 0, 0}, D = 0, N[3] = {0, 0, 0}, W = 0;
+                for (size_t k = 0; k < s.size(); ++k) {
+                    Retained& r = rec[k];
+                    r.t = s[k].t;
+                    r.delta = s[k].delta;
+                    r.valid = w->g->gather_corners(ro + s[k].t * rd, r.cc);
+                    if (!r.valid) continue;
+                    r.s = w->g->sdf_at(r.cc);
+                    const Eigen::Vector3f gr = w->g->sdf_gradient_at(r.cc);
+                    const Eigen::Vector3f col = w->g->color_at(r.cc);
+                    for (int a = 0; a < 3; ++a) r.grad[a] = gr[a], r.rgb[a] = col[a];
+                    const double tau = density(r.s, beta) * r.delta;
+                    const double wk = T * (1.0 - std::exp(-tau));
+                    for (int a = 0; a < 3; ++a) C[a] += wk * r.rgb[a], N[a] += wk * r.grad[a];
+                    D += wk * r.t;
+                    W += wk;
+                    T *= std::exp(-tau);
+                }
+                for (int a = 0; a < 3; ++a) {
+                    if (rgb) rgb[3 * i + a] = static_cast<float>(C[a]);
+                    if (normal) normal[3 * i + a] = static_cast<float>(N[a]);
+                }
+                if (depth) depth[i] = static_cast<float>(D);
+                if (wsum) wsum[i] = static_cast<float>(W);
+            }
+        });
+    });
+}
+
+// Backward from the retained caches into VoxelBlock::grad_sdf / grad_color.
+int svrr_render_backward(svrr_grid* w, const float* d_rgb, const float* d_depth,
+                         const float* d_normal) {
+    return guarded([&] {
+        const size_t V = w->g->voxels_per_block();
+        for (uint32_t i = 0; i < w->g->block_count(); ++i) {
+            VoxelBlock& b = w->g->block(i);
+            if (b.grad_sdf.size() != V) b.grad_sdf.assign(V, 0.0f);
+            if (b.grad_color.size() != 3 * V) b.grad_color.assign(3 * V, 0.0f);
+        }
+        const double beta = w->beta;
+        parallel_chunks(w->rays.size(), [&](size_t b, size_t e, int) {
+            std::vector<double> wk, Tn, vk;
+            for (size_t i = b; i < e; ++i) {
+                const std::vector<Retained>& rec = w->rays[i];
+                const float* dC = d_rgb + 3 * i;
+                const float* dN = d_normal + 3 * i;
+                const double dD = d_depth[i];
+                wk.assign(rec.size(), 0.0);
+                Tn.assign(rec.size(), 0.0);
+                vk.assign(rec.size(), 0.0);
+                double T = 1.0;
+                for (size_t k = 0; k < rec.size(); ++k) {
+                    const Retained& r = rec[k];
+                    if (!r.valid) {
+                        Tn[k] = T;
+                        continue;
+                    }
+                    const double tau = density(r.s, beta) * r.delta;
+                    wk[k] = T * (1.0 - std::exp(-tau));
+                    T *= std::exp(-tau);
+                    Tn[k] = T;
+                    vk[k] = dC[0] * r.rgb[0] + dC[1] * r.rgb[1] + dC[2] * r.rgb[2] + dD * r.t +
+                            dN[0] * r.grad[0] + dN[1] * r.grad[1] + dN[2] * r.grad[2];
+                }
+                double S = 0.0;
+                for (size_t k = rec.size(); k-- > 0;) {
+                    const Retained& r = rec[k];
+                    if (!r.valid) continue;
+                    const double sig = density(r.s, beta);
+                    const double dsig = r.s > 0.0 ? -sig / beta : -(1.0 / beta - sig) / beta;
+                    const double ds = r.delta * dsig * (Tn[k] * vk[k] - S);
+                    for (int c = 0; c < 8; ++c) {
+                        VoxelBlock& blk = w->g->block(r.cc.block[c]);
+                        const uint32_t v = r.cc.voxel[c];
+                        const double gs = r.cc.w[c] * ds + wk[k] * (r.cc.dw[c][0] * dN[0] +
+                                                                    r.cc.dw[c][1] * dN[1] +
+                                                                    r.cc.dw[c][2] * dN[2]);
+                        std::atomic_ref<float>(blk.grad_sdf[v]).fetch_add(
+                            static_cast<float>(gs), std::memory_order_relaxed);
+                        const double wc = r.cc.w[c] * wk[k];
+                        for (int a = 0; a < 3; ++a)
+                            std::atomic_ref<float>(blk.grad_color[3 * v + a])
+                                .fetch_add(static_cast<float>(wc * dC[a]),
+                                           std::memory_order_relaxed);
+                    }
+                    S += wk[k] * vk[k];
+                }
+            }
+        });
+    });
+}
+
+int svrr_grad_get(const svrr_grid* w, float* g_sdf, float* g_rgb) {
+    const size_t V = w->g->voxels_per_block();
+    for (uint32_t i = 0; i < w->g->block_count(); ++i) {
+        const VoxelBlock& b = w->g->block(i);
+        if (b.grad_sdf.size() == V) {
+            if (g_sdf) std::memcpy(g_sdf + i * V, b.grad_sdf.data(), V * 4);
+            if (g_rgb) std::memcpy(g_rgb + 3 * i * V, b.grad_color.data(), 3 * V * 4);
+        } else {
+            if (g_sdf) std::memset(g_sdf + i * V, 0, V * 4);
+            if (g_rgb) std::memset(g_rgb + 3 * i * V, 0, 3 * V * 4);
+        }
+    }
+    return 0;
+}
+
+int svrr_save_sdgv(const svrr_grid* w, const char* path) {
+    return guarded([&] { save_grid(*w->g, path); });
+}
+int svrr_load_sdgv(const char* path, svrr_grid** out) {
+    return guarded([&] {
+        auto* w = new svrr_grid();
+        w->g = std::make_unique<SparseDenseGrid>(load_grid(path));
+        *out = w;
+    });
+}
+
+}  // extern "C"

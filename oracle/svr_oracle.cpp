@@ -1,0 +1,858 @@
+// TEST INFRASTRUCTURE ONLY -- CPU oracle (checker) for the sparse-dense SDF rendering
+// path.  See svr_oracle.h for the contract.  Every function cites the reference
+// file:line it restates (paths relative to /root/reference/).  Nothing here is on the
+// product path: paper_2305_13220_b200 never links or loads this library.
+#include "svr_oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+int g_threads = 1;
+
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+constexpr int kConfig = 2, kData = 3, kCapacity = 5;
+
+// ---------------------------------------------------------------------------
+// Block coordinates and the hash map (proj/src/core/grid.hpp:11-55,
+// proj/src/core/grid.cpp:11-67).
+// ---------------------------------------------------------------------------
+struct BlockCoord {
+    int32_t x = 0, y = 0, z = 0;
+    bool operator==(const BlockCoord& o) const { return x == o.x && y == o.y && z == o.z; }
+};
+
+// grid.hpp:16-26
+uint64_t hash_block_coord(const BlockCoord& c) {
+    uint64_t h = static_cast<uint32_t>(c.x) * 0x9E3779B185EBCA87ull;
+    h ^= static_cast<uint32_t>(c.y) * 0xC2B2AE3D27D4EB4Full;
+    h += static_cast<uint32_t>(c.z) * 0x165667B19E3779F9ull;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    return h;
+}
+
+// grid.cpp:14-24: the slot-array size table.
+constexpr size_t kPrimes[] = {97,       193,      389,      769,       1543,      3079,
+                              6151,     12289,    24593,    49157,     98317,     196613,
+                              393241,   786433,   1572869,  3145739,   6291469,   12582917,
+                              25165843, 50331653, 100663319, 201326611};
+
+size_t next_prime_size(size_t at_least) {
+    for (size_t p : kPrimes)
+        if (p >= at_least) return p;
+    return kPrimes[std::size(kPrimes) - 1];
+}
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;  // grid.hpp:33
+
+// Exact-key open addressing, linear probing over a prime-sized array, grows at
+// load > 0.75 (grid.cpp:28-67).
+class BlockMap {
+public:
+    BlockMap() : slots_(kPrimes[0]) {}
+    uint32_t find(const BlockCoord& k) const {  // grid.cpp:30-38
+        size_t i = hash_block_coord(k) % slots_.size();
+        for (;;) {
+            const Slot& s = slots_[i];
+            if (s.value == kInvalid) return kInvalid;
+            if (s.key == k) return s.value;
+            if (++i == slots_.size()) i = 0;
+        }
+    }
+    uint32_t insert(const BlockCoord& k, uint32_t v) {  // grid.cpp:40-54
+        if ((count_ + 1) * 4 > slots_.size() * 3) grow();
+        size_t i = hash_block_coord(k) % slots_.size();
+        for (;;) {
+            Slot& s = slots_[i];
+            if (s.value == kInvalid) {
+                s.key = k;
+                s.value = v;
+                ++count_;
+                return v;
+            }
+            if (s.key == k) return s.value;
+            if (++i == slots_.size()) i = 0;
+        }
+    }
+
+private:
+    struct Slot {
+        BlockCoord key;
+        uint32_t value = kInvalid;
+    };
+    void grow() {  // grid.cpp:56-67
+        std::vector<Slot> old;
+        old.swap(slots_);
+        slots_.assign(next_prime_size(old.size() * 2), Slot{});
+        for (const Slot& s : old) {
+            if (s.value == kInvalid) continue;
+            size_t i = hash_block_coord(s.key) % slots_.size();
+            while (slots_[i].value != kInvalid)
+                if (++i == slots_.size()) i = 0;
+            slots_[i] = s;
+        }
+    }
+    std::vector<Slot> slots_;
+    size_t count_ = 0;
+};
+
+// floor_div (grid.hpp:207-210)
+int32_t floor_div(int32_t a, int32_t b) {
+    int32_t q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// Packed 64-bit key, 21 bits/axis biased by 2^20.  Defines the deterministic
+// allocation order this build uses in place of libstdc++ unordered_set iteration
+// order (allocation.cpp:31).
+constexpr int32_t kCoordLim = 1 << 20;
+bool packable(const BlockCoord& c) {
+    return c.x >= -kCoordLim && c.x < kCoordLim && c.y >= -kCoordLim && c.y < kCoordLim &&
+           c.z >= -kCoordLim && c.z < kCoordLim;
+}
+uint64_t pack_key(const BlockCoord& c) {
+    return (static_cast<uint64_t>(c.z + kCoordLim) << 42) |
+           (static_cast<uint64_t>(c.y + kCoordLim) << 21) |
+           static_cast<uint64_t>(c.x + kCoordLim);
+}
+BlockCoord unpack_key(uint64_t k) {
+    const uint64_t m = (1ull << 21) - 1;
+    return BlockCoord{static_cast<int32_t>(k & m) - kCoordLim,
+                      static_cast<int32_t>((k >> 21) & m) - kCoordLim,
+                      static_cast<int32_t>((k >> 42) & m) - kCoordLim};
+}
+
+struct KeyHash {
+    size_t operator()(uint64_t k) const { return static_cast<size_t>(k * 0x9E3779B97F4A7C15ull); }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// The grid (grid.hpp:100-223).  Payload kept as flat arrays in the reference's
+// per-block layout (sdf[V], weight[V], color[3V] interleaved, logits[CV]
+// interleaved; grid.hpp:62-66, grid.cpp:69-75).
+// ---------------------------------------------------------------------------
+struct svro_grid {
+    double h;
+    int B;
+    int C;
+    size_t capacity;
+    int V;  // B^3
+    BlockMap map;
+    std::vector<BlockCoord> coords;
+    std::vector<float> sdf, weight, rgb, logits;
+    BlockCoord lo{0, 0, 0}, hi{0, 0, 0};
+
+    double L() const { return h * B; }  // grid.hpp:112
+
+    // grid.hpp:132-135
+    BlockCoord block_of_voxel(int vx, int vy, int vz) const {
+        return BlockCoord{floor_div(vx, B), floor_div(vy, B), floor_div(vz, B)};
+    }
+    // grid.hpp:136-141: floor(x / L), a true division (not x * (1/L)).
+    BlockCoord block_of_point(const double* x) const {
+        const double Lx = L();
+        return BlockCoord{static_cast<int32_t>(std::floor(x[0] / Lx)),
+                          static_cast<int32_t>(std::floor(x[1] / Lx)),
+                          static_cast<int32_t>(std::floor(x[2] / Lx))};
+    }
+    // grid.hpp:142-147
+    uint32_t local_index(int vx, int vy, int vz, const BlockCoord& b) const {
+        const int lx = vx - b.x * B, ly = vy - b.y * B, lz = vz - b.z * B;
+        return static_cast<uint32_t>(lx + B * (ly + B * lz));
+    }
+
+    // grid.cpp:88-108 (allocate_block), payload zero-init grid.cpp:69-75.
+    uint32_t allocate_block(const BlockCoord& c) {
+        const uint32_t existing = map.find(c);
+        if (existing != kInvalid) return existing;
+        if (coords.size() >= capacity) throw Status(kCapacity, "grid: block capacity exceeded");
+        if (!packable(c)) throw Status(kConfig, "grid: block coordinate outside +-2^20");
+        const uint32_t idx = static_cast<uint32_t>(coords.size());
+        map.insert(c, idx);
+        coords.push_back(c);
+        sdf.resize(sdf.size() + V, 0.0f);
+        weight.resize(weight.size() + V, 0.0f);
+        rgb.resize(rgb.size() + 3 * V, 0.0f);
+        logits.resize(logits.size() + static_cast<size_t>(C) * V, 0.0f);
+        if (coords.size() == 1) {
+            lo = hi = c;
+        } else {
+            lo.x = std::min(lo.x, c.x);
+            lo.y = std::min(lo.y, c.y);
+            lo.z = std::min(lo.z, c.z);
+            hi.x = std::max(hi.x, c.x);
+            hi.y = std::max(hi.y, c.y);
+            hi.z = std::max(hi.z, c.z);
+        }
+        return idx;
+    }
+};
+
+namespace {
+
+// CornerCacheD (grid.hpp:90-96)
+struct Corners {
+    uint32_t block[8];
+    uint32_t voxel[8];
+    double w[8];
+    double dw[8][3];
+};
+
+// gather_impl (grid.cpp:112-155): g = x * (1/h) (multiply by the reciprocal),
+// base = floor(g), corner c takes bit a of c on axis a, re-find only when the
+// corner's block differs from the previous corner's, any missing block or
+// weight <= 0 invalidates the query.
+bool gather(const svro_grid& g, const double* x, Corners& cc) {
+    const double inv_h = 1.0 / g.h;
+    double fx[3];
+    int base[3];
+    for (int a = 0; a < 3; ++a) {
+        const double gg = x[a] * inv_h;
+        const double fl = std::floor(gg);
+        base[a] = static_cast<int>(fl);
+        fx[a] = gg - fl;
+    }
+    const double w0[3] = {1.0 - fx[0], 1.0 - fx[1], 1.0 - fx[2]};
+    BlockCoord last{std::numeric_limits<int32_t>::min(), 0, 0};
+    uint32_t last_idx = kInvalid;
+    for (int c = 0; c < 8; ++c) {
+        const int bx = c & 1, by = (c >> 1) & 1, bz = (c >> 2) & 1;
+        const int vx = base[0] + bx, vy = base[1] + by, vz = base[2] + bz;
+        const BlockCoord bc = g.block_of_voxel(vx, vy, vz);
+        if (!(bc == last)) {
+            last = bc;
+            last_idx = g.map.find(bc);
+        }
+        if (last_idx == kInvalid) return false;
+        const uint32_t vox = g.local_index(vx, vy, vz, bc);
+        if (!(g.weight[static_cast<size_t>(last_idx) * g.V + vox] > 0.0f)) return false;
+        cc.block[c] = last_idx;
+        cc.voxel[c] = vox;
+        const double wx = bx ? fx[0] : w0[0];
+        const double wy = by ? fx[1] : w0[1];
+        const double wz = bz ? fx[2] : w0[2];
+        cc.w[c] = wx * wy * wz;
+        cc.dw[c][0] = (bx ? 1.0 : -1.0) * inv_h * wy * wz;
+        cc.dw[c][1] = (by ? 1.0 : -1.0) * inv_h * wx * wz;
+        cc.dw[c][2] = (bz ? 1.0 : -1.0) * inv_h * wx * wy;
+    }
+    return true;
+}
+
+// sdf_impl / sdf_gradient_impl / color_impl (grid.cpp:157-188), double accumulation.
+struct Interp {
+    double s, grad[3], rgb[3];
+};
+void interpolate(const svro_grid& g, const Corners& cc, Interp& o) {
+    o.s = 0.0;
+    o.grad[0] = o.grad[1] = o.grad[2] = 0.0;
+    o.rgb[0] = o.rgb[1] = o.rgb[2] = 0.0;
+    for (int i = 0; i < 8; ++i) {
+        const size_t v = static_cast<size_t>(cc.block[i]) * g.V + cc.voxel[i];
+        o.s += cc.w[i] * g.sdf[v];
+    }
+    for (int i = 0; i < 8; ++i) {
+        const double s = g.sdf[static_cast<size_t>(cc.block[i]) * g.V + cc.voxel[i]];
+        o.grad[0] += cc.dw[i][0] * s;
+        o.grad[1] += cc.dw[i][1] * s;
+        o.grad[2] += cc.dw[i][2] * s;
+    }
+    for (int i = 0; i < 8; ++i) {
+        const float* col = &g.rgb[3 * (static_cast<size_t>(cc.block[i]) * g.V + cc.voxel[i])];
+        const double w = cc.w[i];
+        o.rgb[0] += w * col[0];
+        o.rgb[1] += w * col[1];
+        o.rgb[2] += w * col[2];
+    }
+}
+
+struct Sample {
+    double t, delta;
+};
+
+// march_intervals + march_ray (grid.cpp:263-353), fused: samples are emitted per
+// allocated block while the DDA walks, with the same cursor rule (phase kept across
+// contiguous blocks, reset to t0 + step/2 after a gap, cursor += step by repeated
+// addition) and stopping once max_samples are produced.  Emitting while
+// cursor < t_exit(block) is identical to the reference's two-pass form because
+// t_exit is non-decreasing along the walk and the merged interval's end equals the
+// t_exit of its last block (grid.cpp:316-335).
+void march_ray(const svro_grid& g, const double* o, const double* d, double step,
+               size_t max_samples, std::vector<Sample>& out) {
+    out.clear();
+    if (g.coords.empty() || max_samples == 0) return;
+    const double L = g.L();
+    const double box_lo[3] = {g.lo.x * L, g.lo.y * L, g.lo.z * L};
+    const double box_hi[3] = {(g.hi.x + 1) * L, (g.hi.y + 1) * L, (g.hi.z + 1) * L};
+    double t0 = 0.0, t1 = std::numeric_limits<double>::max();
+    for (int a = 0; a < 3; ++a) {  // grid.cpp:270-285
+        if (d[a] == 0.0) {
+            if (o[a] < box_lo[a] || o[a] >= box_hi[a]) return;
+            continue;
+        }
+        const double ta = (box_lo[a] - o[a]) / d[a];
+        const double tb = (box_hi[a] - o[a]) / d[a];
+        t0 = std::max(t0, std::min(ta, tb));
+        t1 = std::min(t1, std::max(ta, tb));
+    }
+    if (!(t0 < t1)) return;
+    const double t_eps = 1e-12 * std::max(1.0, std::abs(t0));  // grid.cpp:289-296
+    const double ts = t0 + t_eps;
+    int32_t b[3];
+    const int32_t lo[3] = {g.lo.x, g.lo.y, g.lo.z};
+    const int32_t hi[3] = {g.hi.x, g.hi.y, g.hi.z};
+    for (int a = 0; a < 3; ++a) {
+        const double start = o[a] + ts * d[a];
+        b[a] = static_cast<int32_t>(std::floor(start / L));
+        b[a] = std::clamp(b[a], lo[a], hi[a]);
+    }
+    auto crossing = [&](int a) {  // grid.cpp:298-302
+        if (d[a] == 0.0) return std::numeric_limits<double>::infinity();
+        const double plane = (b[a] + (d[a] > 0.0 ? 1 : 0)) * L;
+        return (plane - o[a]) / d[a];
+    };
+    double t = t0;
+    bool open = false;
+    double cursor = -std::numeric_limits<double>::infinity();
+    while (t < t1) {  // grid.cpp:306-333
+        double t_exit = t1;
+        int axis = -1;
+        for (int a = 0; a < 3; ++a) {
+            const double c = crossing(a);
+            if (c < t_exit) {
+                t_exit = c;
+                axis = a;
+            }
+        }
+        const bool allocated = g.map.find(BlockCoord{b[0], b[1], b[2]}) != kInvalid;
+        if (allocated && !open) {
+            open = true;
+            if (cursor < t) cursor = t + 0.5 * step;  // grid.cpp:345 with iv.t0 = t
+        } else if (!allocated && open) {
+            open = false;
+        }
+        if (allocated) {
+            while (cursor < t_exit && out.size() < max_samples) {  // grid.cpp:346-349
+                out.push_back({cursor, step});
+                cursor += step;
+            }
+            if (out.size() >= max_samples) break;
+        }
+        if (axis < 0) {
+            t = t1;
+            break;
+        }
+        b[axis] += d[axis] > 0.0 ? 1 : -1;
+        t = t_exit;
+        if (b[axis] < lo[axis] || b[axis] > hi[axis]) break;
+    }
+    for (size_t k = 0; k + 1 < out.size(); ++k) out[k].delta = out[k + 1].t - out[k].t;  // :352
+}
+
+// Camera::unproject (camera.cpp:20-25) with R x evaluated row-wise left to right.
+void unproject(const svro_camera& cam, double px, double py, double depth, double* out) {
+    const double xc[3] = {(px - cam.cx) / cam.fx * depth, (py - cam.cy) / cam.fy * depth, depth};
+    for (int i = 0; i < 3; ++i) {
+        double acc = cam.R[3 * i + 0] * xc[0];
+        acc = acc + cam.R[3 * i + 1] * xc[1];
+        acc = acc + cam.R[3 * i + 2] * xc[2];
+        out[i] = acc + cam.t[i];
+    }
+}
+
+// ScaleField::lookup + value (scale_field.cpp:15-60).
+double scale_value(const double* grid, int rows, int cols, int iw, int ih, double px, double py) {
+    const double sx = static_cast<double>(cols - 1) / (iw - 1);
+    const double sy = static_cast<double>(rows - 1) / (ih - 1);
+    const double gx = std::clamp(px * sx, 0.0, static_cast<double>(cols - 1));
+    const double gy = std::clamp(py * sy, 0.0, static_cast<double>(rows - 1));
+    const int c0 = std::min(static_cast<int>(gx), cols - 2);
+    const int r0 = std::min(static_cast<int>(gy), rows - 2);
+    const double fx = gx - c0, fy = gy - r0;
+    const int base = r0 * cols + c0;
+    const int idx[4] = {base, base + 1, base + cols, base + cols + 1};
+    const double w[4] = {(1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy};
+    double v = 0.0;
+    for (int i = 0; i < 4; ++i) v += w[i] * grid[idx[i]];
+    return v;
+}
+
+// commit (allocation.cpp:19-43) with new blocks allocated in ascending packed-key
+// order (deterministic; the reference's unordered_set order is a libstdc++ artefact).
+void commit(svro_grid& g, const std::unordered_set<uint64_t, KeyHash>& base, int dilation,
+            svro_report& rep) {
+    std::unordered_set<uint64_t, KeyHash> wanted;
+    wanted.reserve(base.size() * (dilation > 0 ? 8 : 1));
+    for (uint64_t k : base) {
+        const BlockCoord c = unpack_key(k);
+        for (int dz = -dilation; dz <= dilation; ++dz)
+            for (int dy = -dilation; dy <= dilation; ++dy)
+                for (int dx = -dilation; dx <= dilation; ++dx) {
+                    const BlockCoord n{c.x + dx, c.y + dy, c.z + dz};
+                    if (!packable(n)) throw Status(kConfig, "allocate: block outside +-2^20");
+                    wanted.insert(pack_key(n));
+                }
+    }
+    rep.blocks_requested = wanted.size();
+    std::vector<uint64_t> fresh;
+    for (uint64_t k : wanted)
+        if (g.map.find(unpack_key(k)) == kInvalid) fresh.push_back(k);
+    std::sort(fresh.begin(), fresh.end());
+    uint64_t unallocated = 0;
+    for (uint64_t k : fresh) {
+        if (g.coords.size() >= g.capacity) {
+            ++unallocated;
+            continue;
+        }
+        g.allocate_block(unpack_key(k));
+        ++rep.blocks_added;
+    }
+    rep.unallocated = unallocated;
+    if (unallocated > 0) throw Status(kCapacity, "allocate: grid capacity exceeded");
+}
+
+// Laplace density.
+inline double density(double s, double beta) {
+    const double ib = 1.0 / beta;
+    return s > 0.0 ? ib * (0.5 * std::exp(-s / beta)) : ib * (1.0 - 0.5 * std::exp(s / beta));
+}
+inline double density_ds(double s, double sigma, double beta) {
+    return s > 0.0 ? -sigma / beta : -(1.0 / beta - sigma) / beta;
+}
+
+template <typename F>
+void parallel_chunks(size_t n, F&& fn) {  // proj/src/core/parallel.cpp:35-63
+    const int workers = static_cast<int>(std::min<size_t>(std::max(1, g_threads), n));
+    if (workers <= 1) {
+        if (n) fn(size_t(0), n);
+        return;
+    }
+    const size_t chunk = (n + workers - 1) / workers;
+    std::vector<std::thread> pool;
+    for (int w = 0; w < workers; ++w) {
+        const size_t b = static_cast<size_t>(w) * chunk, e = std::min(n, b + chunk);
+        if (b >= e) break;
+        pool.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& t : pool) t.join();
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const Status& s) {
+        g_err = s.what();
+        return s.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return kData;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* svro_last_error(void) { return g_err.c_str(); }
+void svro_set_threads(int n) { g_threads = n > 0 ? n : 1; }
+
+int svro_grid_create(double voxel_size, int block_res, int label_channels, uint64_t capacity,
+                     svro_grid** out) {
+    return guarded([&] {
+        // grid.cpp:83-85
+        if (!(voxel_size > 0.0)) throw Status(kConfig, "grid: voxel_size must be positive");
+        if (block_res < 2) throw Status(kConfig, "grid: block_res must be >= 2");
+        if (label_channels < 1) throw Status(kConfig, "grid: label_channels must be >= 1");
+        auto* g = new svro_grid();
+        g->h = voxel_size;
+        g->B = block_res;
+        g->C = label_channels;
+        g->capacity = capacity ? capacity : (1u << 21);  // grid.hpp:107
+        g->V = block_res * block_res * block_res;
+        *out = g;
+    });
+}
+void svro_grid_destroy(svro_grid* g) { delete g; }
+uint64_t svro_block_count(const svro_grid* g) { return g->coords.size(); }
+uint64_t svro_capacity(const svro_grid* g) { return g->capacity; }
+void svro_coords(const svro_grid* g, int32_t* out) {
+    for (size_t i = 0; i < g->coords.size(); ++i) {
+        out[3 * i] = g->coords[i].x;
+        out[3 * i + 1] = g->coords[i].y;
+        out[3 * i + 2] = g->coords[i].z;
+    }
+}
+int svro_bounds(const svro_grid* g, int32_t* lo3, int32_t* hi3) {
+    lo3[0] = g->lo.x, lo3[1] = g->lo.y, lo3[2] = g->lo.z;
+    hi3[0] = g->hi.x, hi3[1] = g->hi.y, hi3[2] = g->hi.z;
+    return g->coords.empty() ? kData : 0;
+}
+
+int svro_allocate_blocks(svro_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out) {
+    return guarded([&] {
+        for (uint64_t i = 0; i < n; ++i) {
+            const uint32_t idx =
+                g->allocate_block(BlockCoord{coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]});
+            if (idx_out) idx_out[i] = idx;
+        }
+    });
+}
+
+// allocate_for_points (allocation.cpp:45-54)
+int svro_allocate_points(svro_grid* g, const double* xyz, uint64_t n, int dilation,
+                         svro_report* rep) {
+    svro_report r{};
+    const int st = guarded([&] {
+        if (dilation < 0) throw Status(kConfig, "allocate: dilation must be >= 0");
+        std::unordered_set<uint64_t, KeyHash> base;
+        base.reserve(n);
+        for (uint64_t i = 0; i < n; ++i) {
+            const BlockCoord c = g->block_of_point(xyz + 3 * i);
+            if (!packable(c)) throw Status(kConfig, "allocate: block outside +-2^20");
+            base.insert(pack_key(c));
+        }
+        r.pixels_used = n;
+        commit(*g, base, dilation, r);
+    });
+    if (rep) *rep = r;
+    return st;
+}
+
+// allocate_for_frames (allocation.cpp:56-83)
+int svro_allocate_frames(svro_grid* g, const float* depth, const svro_camera* cams,
+                         uint32_t n_frames, const double* scales, int sf_rows, int sf_cols,
+                         int dilation, svro_report* rep) {
+    svro_report r{};
+    const int st = guarded([&] {
+        if (dilation < 0) throw Status(kConfig, "allocate: dilation must be >= 0");
+        if (n_frames == 0) {
+            std::unordered_set<uint64_t, KeyHash> none;
+            commit(*g, none, dilation, r);
+            return;
+        }
+        const int W = cams[0].width, H = cams[0].height;
+        for (uint32_t f = 0; f < n_frames; ++f)
+            if (cams[f].width != W || cams[f].height != H)
+                throw Status(kConfig, "allocate: all frames must share one size");
+        if (scales && (sf_rows < 2 || sf_cols < 2))
+            throw Status(kConfig, "scale field needs at least a 2x2 grid");
+        std::unordered_set<uint64_t, KeyHash> base;
+        uint64_t pixels = 0;
+        for (uint32_t f = 0; f < n_frames; ++f) {
+            const float* dm = depth + static_cast<size_t>(f) * W * H;
+            const double* sf = scales ? scales + static_cast<size_t>(f) * sf_rows * sf_cols : nullptr;
+            for (int y = 0; y < H; ++y)
+                for (int x = 0; x < W; ++x) {
+                    const float d = dm[static_cast<size_t>(y) * W + x];
+                    if (!(d > 0.0f)) continue;
+                    const double scale =
+                        sf ? scale_value(sf, sf_rows, sf_cols, W, H, x, y) : 1.0;
+                    if (!(scale > 0.0)) continue;
+                    double p[3];
+                    unproject(cams[f], static_cast<double>(x), static_cast<double>(y), d * scale, p);
+                    const BlockCoord c = g->block_of_point(p);
+                    if (!packable(c)) throw Status(kConfig, "allocate: block outside +-2^20");
+                    base.insert(pack_key(c));
+                    ++pixels;
+                }
+        }
+        r.pixels_used = pixels;
+        commit(*g, base, dilation, r);
+    });
+    if (rep) *rep = r;
+    return st;
+}
+
+void svro_find(const svro_grid* g, const int32_t* coords, uint64_t n, uint32_t* out) {
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = g->map.find(BlockCoord{coords[3 * i], coords[3 * i + 1], coords[3 * i + 2]});
+}
+
+int svro_set_payload(svro_grid* g, uint32_t first, uint32_t n, const float* sdf,
+                     const float* weight, const float* rgb, const float* logits) {
+    return guarded([&] {
+        if (static_cast<size_t>(first) + n > g->coords.size())
+            throw Status(kData, "payload: block range out of bounds");
+        const size_t V = g->V, o = static_cast<size_t>(first) * V, m = static_cast<size_t>(n) * V;
+        if (sdf) std::memcpy(&g->sdf[o], sdf, m * 4);
+        if (weight) std::memcpy(&g->weight[o], weight, m * 4);
+        if (rgb) std::memcpy(&g->rgb[3 * o], rgb, 3 * m * 4);
+        if (logits) std::memcpy(&g->logits[g->C * o], logits, g->C * m * 4);
+    });
+}
+int svro_get_payload(const svro_grid* g, uint32_t first, uint32_t n, float* sdf, float* weight,
+                     float* rgb, float* logits) {
+    return guarded([&] {
+        if (static_cast<size_t>(first) + n > g->coords.size())
+            throw Status(kData, "payload: block range out of bounds");
+        const size_t V = g->V, o = static_cast<size_t>(first) * V, m = static_cast<size_t>(n) * V;
+        if (sdf) std::memcpy(sdf, &g->sdf[o], m * 4);
+        if (weight) std::memcpy(weight, &g->weight[o], m * 4);
+        if (rgb) std::memcpy(rgb, &g->rgb[3 * o], 3 * m * 4);
+        if (logits) std::memcpy(logits, &g->logits[g->C * o], g->C * m * 4);
+    });
+}
+
+// query_sdf_with_gradient + color_at + logits_at over CornerCacheD
+// (grid.cpp:157-261): invalid -> zeros and valid = 0.
+void svro_query(const svro_grid* g, const double* x, uint64_t n, double* sdf, double* grad,
+                double* rgb, double* logits, uint8_t* valid) {
+    parallel_chunks(n, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            Corners cc;
+            const bool ok = !g->coords.empty() && gather(*g, x + 3 * i, cc);
+            Interp it{};
+            if (ok) interpolate(*g, cc, it);
+            if (sdf) sdf[i] = ok ? it.s : 0.0;
+            for (int a = 0; a < 3; ++a) {
+                if (grad) grad[3 * i + a] = ok ? it.grad[a] : 0.0;
+                if (rgb) rgb[3 * i + a] = ok ? it.rgb[a] : 0.0;
+            }
+            if (logits) {  // logits_at(CornerCacheD) grid.cpp:230-238
+                double* out = logits + static_cast<size_t>(g->C) * i;
+                for (int k = 0; k < g->C; ++k) out[k] = 0.0;
+                if (ok)
+                    for (int j = 0; j < 8; ++j) {
+                        const float* l =
+                            &g->logits[static_cast<size_t>(g->C) *
+                                       (static_cast<size_t>(cc.block[j]) * g->V + cc.voxel[j])];
+                        for (int k = 0; k < g->C; ++k) out[k] += cc.w[j] * l[k];
+                    }
+            }
+            if (valid) valid[i] = ok ? 1 : 0;
+        }
+    });
+}
+
+void svro_march(const svro_grid* g, const double* o, const double* d, uint64_t n, double step,
+                uint32_t max_samples, uint32_t* counts, double* t, double* delta) {
+    parallel_chunks(n, [&](size_t b, size_t e) {
+        std::vector<Sample> s;
+        for (size_t i = b; i < e; ++i) {
+            march_ray(*g, o + 3 * i, d + 3 * i, step, max_samples, s);
+            counts[i] = static_cast<uint32_t>(s.size());
+            for (size_t k = 0; k < s.size(); ++k) {
+                if (t) t[i * max_samples + k] = s[k].t;
+                if (delta) delta[i * max_samples + k] = s[k].delta;
+            }
+        }
+    });
+}
+
+double svro_sdf_to_density(double s, double beta) { return density(s, beta); }
+
+// render_ray forward:
+//   x_k = o + t_k d; invalid samples contribute tau = 0 (builder decision, SPEC.md:281
+//   leaves them undefined); w_k = T_k (1 - exp(-sigma_k delta_k)), T_{k+1} = T_k exp(-tau_k);
+//   C = sum w c, D = sum w t, N = sum w grad(sdf) (world, un-normalised), W = sum w.
+int svro_render_forward(const svro_grid* g, const double* o, const double* d, uint64_t n,
+                        double step, uint32_t max_samples, double beta, double* rgb,
+                        double* depth, double* normal, double* wsum, uint32_t* nsamples) {
+    return guarded([&] {
+        if (!(beta > 0.0)) throw Status(kConfig, "render: beta must be positive");
+        if (!(step > 0.0)) throw Status(kConfig, "render: step must be positive");
+        parallel_chunks(n, [&](size_t b, size_t e) {
+            std::vector<Sample> s;
+            for (size_t i = b; i < e; ++i) {
+                march_ray(*g, o + 3 * i, d + 3 * i, step, max_samples, s);
+                double T = 1.0, C[3] = {0, 0, 0}, D = 0, N[3] = {0, 0, 0}, W = 0;
+                for (const Sample& sm : s) {
+                    double x[3];
+                    for (int a = 0; a < 3; ++a) x[a] = o[3 * i + a] + sm.t * d[3 * i + a];
+                    Corners cc;
+                    if (!gather(*g, x, cc)) continue;
+                    Interp it;
+                    interpolate(*g, cc, it);
+                    const double tau = density(it.s, beta) * sm.delta;
+                    const double w = T * (1.0 - std::exp(-tau));
+                    for (int a = 0; a < 3; ++a) {
+                        C[a] += w * it.rgb[a];
+                        N[a] += w * it.grad[a];
+                    }
+                    D += w * sm.t;
+                    W += w;
+                    T *= std::exp(-tau);
+                }
+                for (int a = 0; a < 3; ++a) {
+                    if (rgb) rgb[3 * i + a] = C[a];
+                    if (normal) normal[3 * i + a] = N[a];
+                }
+                if (depth) depth[i] = D;
+                if (wsum) wsum[i] = W;
+                if (nsamples) nsamples[i] = static_cast<uint32_t>(s.size());
+            }
+        });
+    });
+}
+
+// backward_step, render part: with v_k = dC.c_k + dD t_k + dN.n_k
+// and S_k = sum_{m>k} w_m v_m:  dL/dtau_k = T_{k+1} v_k - S_k,
+// dL/ds_k = delta_k sigma'(s_k) dL/dtau_k, and per corner c of sample k
+//   g_sdf[c] += w_c dL/ds_k + dw_c . (w_k dN),   g_rgb[c] += w_c w_k dC.
+// Accumulates into grad_sdf[A*V] / grad_rgb[A*V*3] (caller zeroes); `active[A]`
+// (optional) gets 1 for every block owning a corner of a valid sample.
+int svro_render_backward(const svro_grid* g, const double* o, const double* d, uint64_t n,
+                         double step, uint32_t max_samples, double beta, const double* d_rgb,
+                         const double* d_depth, const double* d_normal, double* grad_sdf,
+                         double* grad_rgb, uint8_t* active) {
+    return guarded([&] {
+        if (!(beta > 0.0)) throw Status(kConfig, "render: beta must be positive");
+        if (!(step > 0.0)) throw Status(kConfig, "render: step must be positive");
+        const bool atomic = g_threads > 1;
+        auto add = [atomic](double& dst, double v) {
+            if (atomic)
+                std::atomic_ref<double>(dst).fetch_add(v, std::memory_order_relaxed);
+            else
+                dst += v;
+        };
+        parallel_chunks(n, [&](size_t b, size_t e) {
+            std::vector<Sample> s;
+            struct Rec {
+                Corners cc;
+                Interp it;
+                double t, delta, w, Tn, v;
+                bool valid;
+            };
+            std::vector<Rec> rec;
+            for (size_t i = b; i < e; ++i) {
+                march_ray(*g, o + 3 * i, d + 3 * i, step, max_samples, s);
+                rec.resize(s.size());
+                const double* dC = d_rgb + 3 * i;
+                const double dD = d_depth[i];
+                const double* dN = d_normal + 3 * i;
+                double T = 1.0;
+                for (size_t k = 0; k < s.size(); ++k) {
+                    Rec& r = rec[k];
+                    r.t = s[k].t;
+                    r.delta = s[k].delta;
+                    double x[3];
+                    for (int a = 0; a < 3; ++a) x[a] = o[3 * i + a] + r.t * d[3 * i + a];
+                    r.valid = gather(*g, x, r.cc);
+                    if (!r.valid) {
+                        r.w = 0.0;
+                        r.Tn = T;
+                        r.v = 0.0;
+                        continue;
+                    }
+                    interpolate(*g, r.cc, r.it);
+                    const double tau = density(r.it.s, beta) * r.delta;
+                    r.w = T * (1.0 - std::exp(-tau));
+                    T *= std::exp(-tau);
+                    r.Tn = T;
+                    r.v = dC[0] * r.it.rgb[0] + dC[1] * r.it.rgb[1] + dC[2] * r.it.rgb[2] +
+                          dD * r.t + dN[0] * r.it.grad[0] + dN[1] * r.it.grad[1] +
+                          dN[2] * r.it.grad[2];
+                }
+                double S = 0.0;
+                for (size_t kk = s.size(); kk-- > 0;) {
+                    const Rec& r = rec[kk];
+                    if (!r.valid) continue;
+                    const double sigma = density(r.it.s, beta);
+                    const double dtau = r.Tn * r.v - S;
+                    const double ds = r.delta * density_ds(r.it.s, sigma, beta) * dtau;
+                    const double wn[3] = {r.w * dN[0], r.w * dN[1], r.w * dN[2]};
+                    for (int c = 0; c < 8; ++c) {
+                        const size_t vx = static_cast<size_t>(r.cc.block[c]) * g->V + r.cc.voxel[c];
+                        const double gs = r.cc.w[c] * ds + (r.cc.dw[c][0] * wn[0] +
+                                                            r.cc.dw[c][1] * wn[1] +
+                                                            r.cc.dw[c][2] * wn[2]);
+                        add(grad_sdf[vx], gs);
+                        const double wc = r.cc.w[c] * r.w;
+                        for (int a = 0; a < 3; ++a) add(grad_rgb[3 * vx + a], wc * dC[a]);
+                        if (active)
+                            std::atomic_ref<uint8_t>(active[r.cc.block[c]])
+                                .store(1, std::memory_order_relaxed);
+                    }
+                    S += r.w * r.v;
+                }
+            }
+        });
+    });
+}
+
+// save_grid / load_grid (grid_io.cpp:37-97), SDGV v1 little-endian.
+int svro_save_sdgv(const svro_grid* g, const char* path) {
+    return guarded([&] {
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw Status(kData, std::string("save_grid: cannot open ") + path);
+        const uint32_t ver = 1, B = g->B, C = g->C;
+        const uint64_t n = g->coords.size();
+        os.write("SDGV", 4);
+        os.write(reinterpret_cast<const char*>(&ver), 4);
+        os.write(reinterpret_cast<const char*>(&g->h), 8);
+        os.write(reinterpret_cast<const char*>(&B), 4);
+        os.write(reinterpret_cast<const char*>(&n), 8);
+        os.write(reinterpret_cast<const char*>(&C), 4);
+        const size_t V = g->V;
+        for (size_t i = 0; i < n; ++i) {
+            os.write(reinterpret_cast<const char*>(&g->coords[i]), 12);
+            os.write(reinterpret_cast<const char*>(&g->sdf[i * V]), V * 4);
+            os.write(reinterpret_cast<const char*>(&g->weight[i * V]), V * 4);
+            os.write(reinterpret_cast<const char*>(&g->rgb[3 * i * V]), 3 * V * 4);
+            os.write(reinterpret_cast<const char*>(&g->logits[g->C * i * V]), g->C * V * 4);
+        }
+        if (!os) throw Status(kData, std::string("save_grid: write failed for ") + path);
+    });
+}
+
+int svro_load_sdgv(const char* path, svro_grid** out) {
+    return guarded([&] {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw Status(kData, std::string("load_grid: cannot open ") + path);
+        char magic[4];
+        is.read(magic, 4);
+        if (!is || std::memcmp(magic, "SDGV", 4) != 0) throw Status(kData, "load_grid: bad magic");
+        uint32_t ver = 0, B = 0, C = 0;
+        double h = 0;
+        uint64_t n = 0;
+        is.read(reinterpret_cast<char*>(&ver), 4);
+        if (ver != 1) throw Status(kData, "load_grid: unsupported version");
+        is.read(reinterpret_cast<char*>(&h), 8);
+        is.read(reinterpret_cast<char*>(&B), 4);
+        is.read(reinterpret_cast<char*>(&n), 8);
+        is.read(reinterpret_cast<char*>(&C), 4);
+        if (!is) throw Status(kData, "load_grid: truncated header");
+        svro_grid* g = nullptr;
+        const int st = svro_grid_create(h, static_cast<int>(B), static_cast<int>(C),
+                                        std::max<uint64_t>(1u << 21, n), &g);
+        if (st) throw Status(st, g_err);
+        std::unique_ptr<svro_grid> hold(g);
+        const size_t V = g->V;
+        for (uint64_t i = 0; i < n; ++i) {
+            BlockCoord c;
+            is.read(reinterpret_cast<char*>(&c), 12);
+            const uint32_t idx = g->allocate_block(c);
+            is.read(reinterpret_cast<char*>(&g->sdf[idx * V]), V * 4);
+            is.read(reinterpret_cast<char*>(&g->weight[idx * V]), V * 4);
+            is.read(reinterpret_cast<char*>(&g->rgb[3 * idx * V]), 3 * V * 4);
+            is.read(reinterpret_cast<char*>(&g->logits[g->C * idx * V]), g->C * V * 4);
+            if (!is) throw Status(kData, "load_grid: truncated block data");
+        }
+        *out = hold.release();
+    });
+}
+
+}  // extern "C"

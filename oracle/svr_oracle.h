@@ -1,0 +1,91 @@
+/* TEST INFRASTRUCTURE ONLY -- CPU oracle for the sparse-dense SDF rendering path.
+ *
+ * A plain C++ (no Eigen, no CUDA) restatement of the reference `svrecon` grid code
+ * (/root/reference/proj/src/core/grid.{hpp,cpp}, allocation.cpp, camera.cpp,
+ * scale_field.cpp, grid_io.cpp) plus the renderer that the reference only specifies
+ * (SPEC.md:268-319).  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg load this library, as the CHECKER.  The product path
+ * (paper_2305_13220_b200/, libsvr_b200.so) never links or calls it.
+ *
+ * Parity pins: grid/march/gather/activation are validated against the reference's
+ * own sources compiled verbatim (oracle/_ref, see Makefile) and against the golden
+ * vectors in tests/golden/.  The renderer has no reference code: it is pinned only by
+ * the SPEC known-answer tests and finite differences (tests/test_oracle_render.py).
+ * All arithmetic is IEEE double; built with -ffp-contract=off (no FMA), like the
+ * reference's Release build (proj/CMakeLists.txt:9-11).
+ */
+#ifndef SVR_ORACLE_H
+#define SVR_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct svro_grid svro_grid;
+
+typedef struct {
+    uint64_t blocks_added;     /* allocation.hpp:14 */
+    uint64_t blocks_requested; /* allocation.hpp:15 */
+    uint64_t pixels_used;      /* allocation.hpp:16 */
+    uint64_t unallocated;      /* errors.hpp:27-31 CapacityError::unallocated_blocks */
+} svro_report;
+
+/* Pinhole camera, camera-to-world pose x_w = R x_c + t (camera.hpp:16-29).
+ * R is row-major. */
+typedef struct {
+    double fx, fy, cx, cy;
+    int32_t width, height;
+    double R[9];
+    double t[3];
+} svro_camera;
+
+/* status codes mirror errors.hpp:12-31: 0 ok, 2 config, 3 data, 5 capacity */
+const char* svro_last_error(void);
+void svro_set_threads(int n);
+
+int svro_grid_create(double voxel_size, int block_res, int label_channels, uint64_t capacity,
+                     svro_grid** out);
+void svro_grid_destroy(svro_grid* g);
+uint64_t svro_block_count(const svro_grid* g);
+uint64_t svro_capacity(const svro_grid* g);
+void svro_coords(const svro_grid* g, int32_t* out);
+int svro_bounds(const svro_grid* g, int32_t* lo3, int32_t* hi3);
+
+int svro_allocate_blocks(svro_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out);
+int svro_allocate_points(svro_grid* g, const double* xyz, uint64_t n, int dilation,
+                         svro_report* rep);
+int svro_allocate_frames(svro_grid* g, const float* depth, const svro_camera* cams,
+                         uint32_t n_frames, const double* scales, int sf_rows, int sf_cols,
+                         int dilation, svro_report* rep);
+void svro_find(const svro_grid* g, const int32_t* coords, uint64_t n, uint32_t* out);
+
+int svro_set_payload(svro_grid* g, uint32_t first, uint32_t n, const float* sdf,
+                     const float* weight, const float* rgb, const float* logits);
+int svro_get_payload(const svro_grid* g, uint32_t first, uint32_t n, float* sdf, float* weight,
+                     float* rgb, float* logits);
+
+void svro_query(const svro_grid* g, const double* x, uint64_t n, double* sdf, double* grad,
+                double* rgb, double* logits, uint8_t* valid);
+void svro_march(const svro_grid* g, const double* o, const double* d, uint64_t n, double step,
+                uint32_t max_samples, uint32_t* counts, double* t, double* delta);
+
+int svro_render_forward(const svro_grid* g, const double* o, const double* d, uint64_t n,
+                        double step, uint32_t max_samples, double beta, double* rgb,
+                        double* depth, double* normal, double* wsum, uint32_t* nsamples);
+int svro_render_backward(const svro_grid* g, const double* o, const double* d, uint64_t n,
+                         double step, uint32_t max_samples, double beta, const double* d_rgb,
+                         const double* d_depth, const double* d_normal, double* grad_sdf,
+                         double* grad_rgb, uint8_t* active);
+
+double svro_sdf_to_density(double s, double beta);
+
+int svro_save_sdgv(const svro_grid* g, const char* path);
+int svro_load_sdgv(const char* path, svro_grid** out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

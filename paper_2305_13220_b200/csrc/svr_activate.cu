@@ -1,0 +1,331 @@
+// sm_100a kernels for block activation and the block hash table:
+//   K1 hash insert / find over 64-bit packed keys (grid.cpp:28-67, 88-108)
+//   K3 depth / points -> base block keys -> L-inf dilation -> new-key filter
+//      (allocation.cpp:19-83).  Dedup uses device key sets (open addressing, CAS);
+//      warps first collapse equal keys with __match_any_sync so a run of pixels that
+//      land in one block costs one probe.
+// All discrete math (unproject, floor(x / L)) is fp64 with explicit _rn intrinsics.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "svr_internal.h"
+
+namespace svr_dev {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// Insert into a key set; returns true if this call added the key.
+__device__ __forceinline__ bool keyset_insert(unsigned long long* slots, unsigned long long mask,
+                                              unsigned long long key) {
+    unsigned long long i = mix64(key) & mask;
+    for (unsigned long long probes = 0; probes <= mask; ++probes) {
+        const unsigned long long cur = slots[i];
+        if (cur == key) return false;
+        if (cur == kEmptyKey) {
+            const unsigned long long prev = atomicCAS(slots + i, kEmptyKey, key);
+            if (prev == kEmptyKey) return true;
+            if (prev == key) return false;
+        }
+        i = (i + 1) & mask;
+    }
+    return false;  // full; caller detects via the count
+}
+
+__device__ __forceinline__ void append_key(unsigned long long key, bool add,
+                                           const svr_internal::KeySet& ks,
+                                           unsigned long long* count) {
+    if (!add) return;
+    const unsigned long long pos = atomicAdd(count, 1ull);
+    if (pos < ks.cap) ks.list[pos] = key;
+}
+
+// Warp-collapse equal keys, then one leader per distinct key probes the set.
+__device__ __forceinline__ void warp_insert(bool have, unsigned long long key,
+                                            const svr_internal::KeySet& ks,
+                                            unsigned long long* count) {
+    const unsigned active = __ballot_sync(kFull, have);
+    if (!have) return;
+    const unsigned peers = __match_any_sync(active, key);
+    const int lane = threadIdx.x & 31;
+    if (lane == __ffs(peers) - 1) append_key(key, keyset_insert(ks.slots, ks.mask, key), ks, count);
+}
+
+// block_of_point (grid.hpp:136-141): floor(x / L), a true division.
+__device__ __forceinline__ bool block_of_point(const double p[3], double L, int32_t b[3]) {
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double f = floor(__ddiv_rn(p[a], L));
+        ok = ok && f >= -static_cast<double>(kCoordLim) && f < static_cast<double>(kCoordLim);
+        b[a] = ok ? static_cast<int32_t>(f) : 0;
+    }
+    return ok;
+}
+
+__global__ void k_keyset_clear(unsigned long long* slots, unsigned long long n) {
+    for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        slots[i] = kEmptyKey;
+}
+
+__global__ void k_points_to_keys(const double* __restrict__ xyz, uint64_t n, double L,
+                                 svr_internal::KeySet ks, unsigned long long* count,
+                                 uint32_t* flags) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool have = i < n;
+    unsigned long long key = 0;
+    if (have) {
+        const double p[3] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+        int32_t b[3];
+        if (block_of_point(p, L, b)) {
+            key = pack_key(b[0], b[1], b[2]);
+        } else {
+            atomicOr(flags, 1u);
+            have = false;
+        }
+    }
+    warp_insert(have, key, ks, count);
+}
+
+// allocate_for_frames pixel loop (allocation.cpp:63-79): valid depth, optional
+// ScaleField::value (scale_field.cpp:15-60), Camera::unproject (camera.cpp:20-25) with
+// R x_c evaluated row-wise left to right, then block_of_point.
+__global__ void k_depth_to_keys(const float* __restrict__ depth, const svr_camera* __restrict__ cams,
+                                uint32_t n_frames, int32_t W, int32_t H,
+                                const double* __restrict__ scales, int32_t rows, int32_t cols,
+                                double L, svr_internal::KeySet ks, unsigned long long* count,
+                                unsigned long long* pixels, uint32_t* flags) {
+    const uint64_t npx = static_cast<uint64_t>(W) * H;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool have = i < npx * n_frames;
+    unsigned long long key = 0;
+    if (have) {
+        const uint32_t f = static_cast<uint32_t>(i / npx);
+        const uint64_t pix = i - static_cast<uint64_t>(f) * npx;
+        const int x = static_cast<int>(pix % W), y = static_cast<int>(pix / W);
+        const float dv = depth[i];
+        have = dv > 0.0f;
+        double scale = 1.0;
+        if (have && scales) {
+            const double* grid = scales + static_cast<size_t>(f) * rows * cols;
+            const double sx = __ddiv_rn(static_cast<double>(cols - 1), static_cast<double>(W - 1));
+            const double sy = __ddiv_rn(static_cast<double>(rows - 1), static_cast<double>(H - 1));
+            double gx = __dmul_rn(static_cast<double>(x), sx);
+            double gy = __dmul_rn(static_cast<double>(y), sy);
+            const double cmax = static_cast<double>(cols - 1), rmax = static_cast<double>(rows - 1);
+            gx = gx < 0.0 ? 0.0 : (cmax < gx ? cmax : gx);
+            gy = gy < 0.0 ? 0.0 : (rmax < gy ? rmax : gy);
+            const int c0 = min(static_cast<int>(gx), cols - 2);
+            const int r0 = min(static_cast<int>(gy), rows - 2);
+            const double fx = __dsub_rn(gx, static_cast<double>(c0));
+            const double fy = __dsub_rn(gy, static_cast<double>(r0));
+            const int b = r0 * cols + c0;
+            const double w[4] = {__dmul_rn(__dsub_rn(1.0, fx), __dsub_rn(1.0, fy)),
+                                 __dmul_rn(fx, __dsub_rn(1.0, fy)),
+                                 __dmul_rn(__dsub_rn(1.0, fx), fy), __dmul_rn(fx, fy)};
+            const int idx[4] = {b, b + 1, b + cols, b + cols + 1};
+            double v = 0.0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v = __dadd_rn(v, __dmul_rn(w[k], grid[idx[k]]));
+            scale = v;
+            have = scale > 0.0;
+        }
+        if (have) {
+            const svr_camera& c = cams[f];
+            const double dep = __dmul_rn(static_cast<double>(dv), scale);
+            const double xc[3] = {
+                __dmul_rn(__ddiv_rn(__dsub_rn(static_cast<double>(x), c.cx), c.fx), dep),
+                __dmul_rn(__ddiv_rn(__dsub_rn(static_cast<double>(y), c.cy), c.fy), dep), dep};
+            double p[3];
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                double acc = __dmul_rn(c.R[3 * r], xc[0]);
+                acc = __dadd_rn(acc, __dmul_rn(c.R[3 * r + 1], xc[1]));
+                acc = __dadd_rn(acc, __dmul_rn(c.R[3 * r + 2], xc[2]));
+                p[r] = __dadd_rn(acc, c.t[r]);
+            }
+            int32_t b[3];
+            if (block_of_point(p, L, b)) {
+                key = pack_key(b[0], b[1], b[2]);
+            } else {
+                atomicOr(flags, 1u);
+                have = false;
+            }
+        }
+    }
+    const unsigned used = __ballot_sync(kFull, have);
+    if ((threadIdx.x & 31) == 0 && used) atomicAdd(pixels, static_cast<unsigned long long>(__popc(used)));
+    warp_insert(have, key, ks, count);
+}
+
+// commit's dilation (allocation.cpp:22-26): base x (2R+1)^3 offsets into `wanted`.
+__global__ void k_dilate(const unsigned long long* __restrict__ base, uint64_t nbase, int32_t R,
+                         svr_internal::KeySet ks, unsigned long long* count, uint32_t* flags) {
+    const uint64_t side = 2 * static_cast<uint64_t>(R) + 1, per = side * side * side;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    bool have = i < nbase * per;
+    unsigned long long key = 0;
+    if (have) {
+        const uint64_t bi = i / per, off = i - bi * per;
+        int32_t x, y, z;
+        unpack_key(base[bi], x, y, z);
+        x += static_cast<int32_t>(off % side) - R;
+        y += static_cast<int32_t>((off / side) % side) - R;
+        z += static_cast<int32_t>(off / (side * side)) - R;
+        if (packable(x, y, z)) {
+            key = pack_key(x, y, z);
+        } else {
+            atomicOr(flags, 1u);
+            have = false;
+        }
+    }
+    warp_insert(have, key, ks, count);
+}
+
+// commit's "already allocated?" test (allocation.cpp:31).
+__global__ void k_filter_fresh(GridView g, const unsigned long long* __restrict__ keys, uint64_t n,
+                               unsigned long long* fresh, unsigned long long* nfresh) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = keys[i];
+    const bool is_new = g.n_blocks == 0 || hash_find(g, k) == kInvalid;
+    if (is_new) fresh[atomicAdd(nfresh, 1ull)] = k;
+}
+
+// Inserts keys[i] -> first_index + i.  Keys are unique and absent (filtered above), so
+// a CAS on the empty marker is the only synchronisation needed.  coords4 gets (x,y,z,0).
+__global__ void k_hash_insert(HashSlot* slots, unsigned long long mask,
+                              const unsigned long long* __restrict__ keys, uint64_t n,
+                              uint32_t first, int32_t* coords4) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long k = keys[i];
+    unsigned long long s = mix64(k) & mask;
+    for (;;) {
+        const unsigned long long prev = atomicCAS(&slots[s].key, kEmptyKey, k);
+        if (prev == kEmptyKey || prev == k) {
+            slots[s].val = first + static_cast<uint32_t>(i);
+            break;
+        }
+        s = (s + 1) & mask;
+    }
+    int32_t x, y, z;
+    unpack_key(k, x, y, z);
+    reinterpret_cast<int4*>(coords4)[first + i] = make_int4(x, y, z, 0);
+}
+
+// Warp-cooperative find: 8 lanes probe one 128 B line (8 slots) per step.
+__global__ void k_hash_find(const HashSlot* __restrict__ slots, unsigned long long mask,
+                            const int32_t* __restrict__ coords3, uint64_t n, uint32_t* out) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t q = tid >> 3;
+    const int sub = threadIdx.x & 7;
+    const unsigned group = 0xFFu << (threadIdx.x & 24);
+    const bool have = q < n;
+    unsigned long long key = 0;
+    bool ok = have;
+    if (have) {
+        const int32_t x = coords3[3 * q], y = coords3[3 * q + 1], z = coords3[3 * q + 2];
+        ok = packable(x, y, z);
+        key = ok ? pack_key(x, y, z) : 0;
+    }
+    uint32_t result = kInvalid;
+    bool done = !ok;
+    unsigned long long start = ok ? (mix64(key) & mask) : 0;
+    for (unsigned long long step = 0; !__all_sync(kFull, done); step += 8) {
+        if (!done) {
+            const unsigned long long s = (start + step + sub) & mask;
+            const HashSlot hs = slots[s];
+            const unsigned hit = __ballot_sync(group, hs.key == key) & group;
+            const unsigned empty = __ballot_sync(group, hs.key == kEmptyKey) & group;
+            // first empty or hit in probe order decides
+            const unsigned shift = threadIdx.x & 24;
+            const unsigned h8 = (hit >> shift) & 0xFFu, e8 = (empty >> shift) & 0xFFu;
+            const int fh = h8 ? __ffs(h8) - 1 : 8, fe = e8 ? __ffs(e8) - 1 : 8;
+            if (fh < 8 && fh < fe) {
+                result = __shfl_sync(group, hs.val, (threadIdx.x & 24) + fh);
+                done = true;
+            } else if (fe < 8) {
+                done = true;
+            } else if (step > mask) {
+                done = true;
+            }
+        }
+    }
+    if (have && sub == 0) out[q] = result;
+}
+
+}  // namespace
+}  // namespace svr_dev
+
+namespace svr_internal {
+using namespace svr_dev;
+
+static inline unsigned grid_for(uint64_t n, unsigned per_block) {
+    return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+void launch_keyset_clear(KeySet& ks, cudaStream_t s) {
+    k_keyset_clear<<<1184, 256, 0, s>>>(ks.slots, ks.mask + 1);
+}
+
+void launch_points_to_keys(const double* xyz, uint64_t n, double L, KeySet ks,
+                           unsigned long long* count, uint32_t* flags, cudaStream_t s) {
+    if (!n) return;
+    k_points_to_keys<<<grid_for(n, 256), 256, 0, s>>>(xyz, n, L, ks, count, flags);
+}
+
+void launch_depth_to_keys(const float* depth, const svr_camera* cams, uint32_t n_frames, int32_t W,
+                          int32_t H, const double* scales, int32_t rows, int32_t cols, double L,
+                          KeySet ks, unsigned long long* count, unsigned long long* pixels,
+                          uint32_t* flags, cudaStream_t s) {
+    const uint64_t n = static_cast<uint64_t>(W) * H * n_frames;
+    if (!n) return;
+    k_depth_to_keys<<<grid_for(n, 256), 256, 0, s>>>(depth, cams, n_frames, W, H, scales, rows,
+                                                     cols, L, ks, count, pixels, flags);
+}
+
+void launch_dilate(const unsigned long long* base, uint64_t nbase, int32_t R, KeySet ks,
+                   unsigned long long* count, uint32_t* flags, cudaStream_t s) {
+    const uint64_t side = 2 * static_cast<uint64_t>(R) + 1;
+    const uint64_t n = nbase * side * side * side;
+    if (!n) return;
+    k_dilate<<<grid_for(n, 256), 256, 0, s>>>(base, nbase, R, ks, count, flags);
+}
+
+void launch_filter_fresh(const GridView& g, const unsigned long long* keys, uint64_t n,
+                         unsigned long long* fresh, unsigned long long* nfresh, cudaStream_t s) {
+    if (!n) return;
+    k_filter_fresh<<<grid_for(n, 256), 256, 0, s>>>(g, keys, n, fresh, nfresh);
+}
+
+void launch_sort_keys(unsigned long long* keys, uint64_t n, void** tmp, size_t* tmp_bytes,
+                      cudaStream_t s) {
+    if (n < 2) return;
+    // sort in place through a double buffer placed after the keys in tmp
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, keys, keys, static_cast<int>(n), 0, 63, s);
+    const size_t total = need + n * sizeof(unsigned long long) + 256;
+    if (*tmp_bytes < total) {
+        if (*tmp) cudaFree(*tmp);
+        cudaMalloc(tmp, total);
+        *tmp_bytes = total;
+    }
+    auto* alt = reinterpret_cast<unsigned long long*>(static_cast<char*>(*tmp) + ((need + 255) / 256) * 256);
+    cudaMemcpyAsync(alt, keys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s);
+    cub::DeviceRadixSort::SortKeys(*tmp, need, alt, keys, static_cast<int>(n), 0, 63, s);
+}
+
+void launch_hash_insert(HashSlot* slots, unsigned long long mask, const unsigned long long* keys,
+                        uint64_t n, uint32_t first, int32_t* coords4, cudaStream_t s) {
+    if (!n) return;
+    k_hash_insert<<<grid_for(n, 256), 256, 0, s>>>(slots, mask, keys, n, first, coords4);
+}
+
+void launch_hash_find(const HashSlot* slots, unsigned long long mask, const int32_t* coords3,
+                      uint64_t n, uint32_t* out, cudaStream_t s) {
+    if (!n) return;
+    k_hash_find<<<grid_for(n * 8, 256), 256, 0, s>>>(slots, mask, coords3, n, out);
+}
+
+}  // namespace svr_internal

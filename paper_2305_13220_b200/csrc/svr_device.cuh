@@ -1,0 +1,135 @@
+// Device-side views and helpers shared by the sm_100a kernels.
+//
+// HBM layout:
+//   slots   : HashSlot[pow2 >= 2*capacity]  {u64 packed key, u32 block index, u32 pad}
+//   pay     : float4[A*512]  (sdf, r, g, b) per voxel, x fastest (grid.hpp:142-147)
+//   weight  : float[A*512]   (kept for get_payload / SDGV round trips)
+//   logits  : float[A*512*C] interleaved like the reference (grid.hpp:66)
+//   vmask   : u32[A*16]      512-bit "weight > 0" mask per block (grid.hpp:58-59)
+//   meta    : u32[A]         bit0 = every voxel of the block is valid
+//   grad    : float4[A*512]  (g_sdf, g_r, g_g, g_b) -- one 16 B red.global.add.v4 per corner
+//   active  : u8[A]          block received a scatter since the last grad zero
+//   dense   : u32[dx*dy*dz]  block index (| 1<<31 when all-valid) over the block AABB,
+//                            0xFFFFFFFF = unallocated; occ: bit per AABB cell
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace svr_dev {
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+constexpr uint32_t kFullBit = 0x80000000u;
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int kRes = 8;        // block resolution
+constexpr int kVox = 512;      // voxels per block
+constexpr int32_t kCoordLim = 1 << 20;
+
+struct __align__(16) HashSlot {
+    unsigned long long key;
+    uint32_t val;
+    uint32_t pad;
+};
+
+__host__ __device__ inline bool packable(int32_t x, int32_t y, int32_t z) {
+    return x >= -kCoordLim && x < kCoordLim && y >= -kCoordLim && y < kCoordLim &&
+           z >= -kCoordLim && z < kCoordLim;
+}
+// (z, y, x) lexicographic order == numeric order of the packed key.
+__host__ __device__ inline unsigned long long pack_key(int32_t x, int32_t y, int32_t z) {
+    return (static_cast<unsigned long long>(z + kCoordLim) << 42) |
+           (static_cast<unsigned long long>(y + kCoordLim) << 21) |
+           static_cast<unsigned long long>(x + kCoordLim);
+}
+__host__ __device__ inline void unpack_key(unsigned long long k, int32_t& x, int32_t& y, int32_t& z) {
+    const unsigned long long m = (1ull << 21) - 1;
+    x = static_cast<int32_t>(k & m) - kCoordLim;
+    y = static_cast<int32_t>((k >> 21) & m) - kCoordLim;
+    z = static_cast<int32_t>((k >> 42) & m) - kCoordLim;
+}
+// splitmix64 finaliser: slot positions are not observable, only
+// find() results are, so the device table uses its own mixer and a power-of-two size.
+__host__ __device__ inline unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    x ^= x >> 31;
+    return x;
+}
+
+struct GridView {
+    const HashSlot* slots;
+    unsigned long long slot_mask;
+    const uint32_t* dense;
+    const uint32_t* occ;
+    const float4* pay;
+    const uint32_t* vmask;
+    const uint32_t* meta;
+    const float* logits;
+    float4* grad;
+    uint8_t* active;
+    int32_t lo[3], hi[3];   // block AABB (grid.hpp:222)
+    int32_t dim[3];         // hi - lo + 1
+    int use_dense;
+    uint32_t n_blocks;
+    int32_t C;
+    double h, inv_h, L;
+};
+
+__device__ __forceinline__ uint32_t hash_find(const GridView& g, unsigned long long key) {
+    unsigned long long i = mix64(key) & g.slot_mask;
+    for (;;) {
+        const HashSlot s = g.slots[i];
+        if (s.key == key) return s.val;
+        if (s.key == kEmptyKey) return kInvalid;
+        i = (i + 1) & g.slot_mask;
+    }
+}
+
+// Block index (| kFullBit when the block is fully observed) or kInvalid.
+__device__ __forceinline__ uint32_t lookup_block(const GridView& g, int32_t bx, int32_t by,
+                                                 int32_t bz) {
+    const uint32_t x = static_cast<uint32_t>(bx - g.lo[0]);
+    const uint32_t y = static_cast<uint32_t>(by - g.lo[1]);
+    const uint32_t z = static_cast<uint32_t>(bz - g.lo[2]);
+    if (x >= static_cast<uint32_t>(g.dim[0]) || y >= static_cast<uint32_t>(g.dim[1]) ||
+        z >= static_cast<uint32_t>(g.dim[2]))
+        return kInvalid;
+    if (g.use_dense)
+        return __ldg(g.dense + (static_cast<size_t>(z) * g.dim[1] + y) * g.dim[0] + x);
+    const uint32_t idx = hash_find(g, pack_key(bx, by, bz));
+    if (idx == kInvalid) return kInvalid;
+    return idx | ((__ldg(g.meta + idx) & 1u) ? kFullBit : 0u);
+}
+
+// allocated? (DDA test, grid.cpp:317-318)
+__device__ __forceinline__ bool block_allocated(const GridView& g, int32_t bx, int32_t by,
+                                                int32_t bz) {
+    const uint32_t x = static_cast<uint32_t>(bx - g.lo[0]);
+    const uint32_t y = static_cast<uint32_t>(by - g.lo[1]);
+    const uint32_t z = static_cast<uint32_t>(bz - g.lo[2]);
+    if (x >= static_cast<uint32_t>(g.dim[0]) || y >= static_cast<uint32_t>(g.dim[1]) ||
+        z >= static_cast<uint32_t>(g.dim[2]))
+        return false;
+    if (g.use_dense) {
+        const size_t cell = (static_cast<size_t>(z) * g.dim[1] + y) * g.dim[0] + x;
+        return (__ldg(g.occ + (cell >> 5)) >> (cell & 31)) & 1u;
+    }
+    return hash_find(g, pack_key(bx, by, bz)) != kInvalid;
+}
+
+__device__ __forceinline__ bool voxel_valid(const GridView& g, uint32_t entry, uint32_t local) {
+    if (entry & kFullBit) return true;
+    const uint32_t blk = entry & ~kFullBit;
+    return (__ldg(g.vmask + blk * 16u + (local >> 5)) >> (local & 31)) & 1u;
+}
+
+// std::min / std::max argument semantics (ties and NaN return the first argument).
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+
+// floor_div by 8 (grid.hpp:207-210) == arithmetic shift.
+__device__ __forceinline__ int32_t fdiv8(int32_t v) { return v >> 3; }
+
+}  // namespace svr_dev

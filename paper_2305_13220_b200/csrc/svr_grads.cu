@@ -1,0 +1,256 @@
+// sm_100a kernels around the payload and gradient planes:
+//   payload in/out (reference per-block layout <-> float4 (sdf,r,g,b) planes + validity
+//   bitmask), dense AABB index build, gradient readback, K7 active-block compaction,
+//   and the pack / unpack / zero kernels of the multi-GPU active-block reduction (K8's
+//   device side; the collective itself is NCCL through torch.distributed).
+#include "svr_internal.h"
+
+namespace svr_dev {
+namespace {
+
+// One CTA of 512 threads per block: thread v handles voxel v (coalesced float4 stores).
+__global__ void __launch_bounds__(512) k_payload_in(float4* pay, float* weight, float* logits,
+                                                    uint32_t* vmask, uint32_t* meta, uint32_t first,
+                                                    int32_t C, const float* __restrict__ sdf,
+                                                    const float* __restrict__ w,
+                                                    const float* __restrict__ rgb,
+                                                    const float* __restrict__ lg) {
+    const uint32_t b = blockIdx.x, v = threadIdx.x;
+    const size_t src = static_cast<size_t>(b) * kVox + v;
+    const size_t dst = static_cast<size_t>(first + b) * kVox + v;
+    if (sdf || rgb) {
+        float4 p = pay[dst];
+        if (sdf) p.x = sdf[src];
+        if (rgb) p.y = rgb[3 * src], p.z = rgb[3 * src + 1], p.w = rgb[3 * src + 2];
+        pay[dst] = p;
+    }
+    if (lg)
+        for (int k = 0; k < C; ++k) logits[dst * C + k] = lg[src * C + k];
+    if (w) {
+        const float wv = w[src];
+        weight[dst] = wv;
+        const unsigned bits = __ballot_sync(0xFFFFFFFFu, wv > 0.0f);  // grid.cpp:142
+        __shared__ unsigned words[16];
+        if ((v & 31) == 0) {
+            words[v >> 5] = bits;
+            vmask[static_cast<size_t>(first + b) * 16 + (v >> 5)] = bits;
+        }
+        __syncthreads();
+        if (v == 0) {
+            unsigned all = 0xFFFFFFFFu;
+            for (int i = 0; i < 16; ++i) all &= words[i];
+            meta[first + b] = (all == 0xFFFFFFFFu) ? 1u : 0u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(512) k_payload_out(const float4* __restrict__ pay,
+                                                     const float* __restrict__ weight,
+                                                     const float* __restrict__ logits,
+                                                     uint32_t first, int32_t C, float* sdf,
+                                                     float* w, float* rgb, float* lg) {
+    const uint32_t b = blockIdx.x, v = threadIdx.x;
+    const size_t dst = static_cast<size_t>(b) * kVox + v;
+    const size_t src = static_cast<size_t>(first + b) * kVox + v;
+    const float4 p = pay[src];
+    if (sdf) sdf[dst] = p.x;
+    if (rgb) rgb[3 * dst] = p.y, rgb[3 * dst + 1] = p.z, rgb[3 * dst + 2] = p.w;
+    if (w) w[dst] = weight[src];
+    if (lg)
+        for (int k = 0; k < C; ++k) lg[dst * C + k] = logits[src * C + k];
+}
+
+__global__ void k_dense_build(const int4* __restrict__ coords, const uint32_t* __restrict__ meta,
+                              uint32_t n, int32_t lx, int32_t ly, int32_t lz, int32_t dx,
+                              int32_t dy, uint32_t* dense, uint32_t* occ) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    const size_t cell = (static_cast<size_t>(c.z - lz) * dy + (c.y - ly)) * dx + (c.x - lx);
+    dense[cell] = i | ((meta[i] & 1u) ? kFullBit : 0u);
+    atomicOr(occ + (cell >> 5), 1u << (cell & 31));
+}
+
+__global__ void k_grad_out(const float4* __restrict__ grad, uint64_t nvox, float* g_sdf,
+                           float* g_rgb) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nvox) return;
+    const float4 g = grad[i];
+    if (g_sdf) g_sdf[i] = g.x;
+    if (g_rgb) g_rgb[3 * i] = g.y, g_rgb[3 * i + 1] = g.z, g_rgb[3 * i + 2] = g.w;
+}
+
+// K7: ascending compaction of the active mask. Each CTA scans 1024 flags, takes a
+// base offset with one atomic, and the final list is made ascending by a sort-free
+// two-pass scheme: pass 1 counts per CTA, pass 2 (below) writes at exclusive offsets.
+__global__ void __launch_bounds__(1024) k_active_count(const uint8_t* __restrict__ active,
+                                                       uint32_t n, uint32_t* per_cta) {
+    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
+    const bool a = i < n && active[i];
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, a);
+    __shared__ uint32_t warp_tot[32];
+    if ((threadIdx.x & 31) == 0) warp_tot[threadIdx.x >> 5] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int w = 0; w < 32; ++w) s += warp_tot[w];
+        per_cta[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_active_scan(uint32_t* per_cta, uint32_t nctas, unsigned long long* count) {
+    // single-CTA exclusive scan over <= a few thousand CTA totals
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < nctas; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        uint32_t v = i < nctas ? per_cta[i] : 0;
+        // block-wide inclusive scan
+        __shared__ uint32_t tmp[1024];
+        tmp[threadIdx.x] = v;
+        __syncthreads();
+        for (uint32_t off = 1; off < 1024; off <<= 1) {
+            const uint32_t add = threadIdx.x >= off ? tmp[threadIdx.x - off] : 0;
+            __syncthreads();
+            tmp[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < nctas) per_cta[i] = carry + tmp[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += tmp[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void __launch_bounds__(1024) k_active_write(const uint8_t* __restrict__ active,
+                                                       uint32_t n,
+                                                       const uint32_t* __restrict__ per_cta,
+                                                       uint32_t* list) {
+    const uint32_t i = blockIdx.x * 1024 + threadIdx.x;
+    const bool a = i < n && active[i];
+    const unsigned bal = __ballot_sync(0xFFFFFFFFu, a);
+    __shared__ uint32_t warp_off[32];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) warp_off[w] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t s = 0;
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t t = warp_off[k];
+            warp_off[k] = s;
+            s += t;
+        }
+    }
+    __syncthreads();
+    if (a) list[per_cta[blockIdx.x] + warp_off[w] + __popc(bal & ((1u << lane) - 1))] = i;
+}
+
+__global__ void k_set_active(uint8_t* active, const uint8_t* __restrict__ mask, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) active[i] = mask[i] ? 1 : 0;
+}
+
+// pack / unpack: one CTA of 128 threads moves one block (512 float4 = 8 KB).
+__global__ void __launch_bounds__(128) k_grad_pack(const float4* __restrict__ grad,
+                                                   const uint32_t* __restrict__ blocks,
+                                                   float4* out) {
+    const size_t src = static_cast<size_t>(blocks[blockIdx.x]) * kVox;
+    const size_t dst = static_cast<size_t>(blockIdx.x) * kVox;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[dst + threadIdx.x + 128 * k] = grad[src + threadIdx.x + 128 * k];
+}
+__global__ void __launch_bounds__(128) k_grad_unpack(float4* grad, const uint32_t* __restrict__ blocks,
+                                                     const float4* __restrict__ in) {
+    const size_t dst = static_cast<size_t>(blocks[blockIdx.x]) * kVox;
+    const size_t src = static_cast<size_t>(blockIdx.x) * kVox;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) grad[dst + threadIdx.x + 128 * k] = in[src + threadIdx.x + 128 * k];
+}
+// zero active blocks' gradients (grid-stride over the device-side count)
+__global__ void __launch_bounds__(128) k_grad_zero_active(float4* grad, uint8_t* active,
+                                                          const uint32_t* __restrict__ list,
+                                                          const unsigned long long* count) {
+    const unsigned long long n = *count;
+    for (unsigned long long j = blockIdx.x; j < n; j += gridDim.x) {
+        const uint32_t b = list[j];
+        const size_t base = static_cast<size_t>(b) * kVox;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) grad[base + threadIdx.x + 128 * k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (threadIdx.x == 0) active[b] = 0;
+    }
+}
+
+}  // namespace
+}  // namespace svr_dev
+
+namespace svr_internal {
+using namespace svr_dev;
+
+void launch_payload_in(float4* pay, float* weight, float* logits, uint32_t* vmask, uint32_t* meta,
+                       uint32_t first, uint32_t n, int32_t C, const float* sdf, const float* w,
+                       const float* rgb, const float* lg, cudaStream_t s) {
+    if (!n) return;
+    k_payload_in<<<n, 512, 0, s>>>(pay, weight, logits, vmask, meta, first, C, sdf, w, rgb, lg);
+}
+
+void launch_payload_out(const float4* pay, const float* weight, const float* logits,
+                        uint32_t first, uint32_t n, int32_t C, float* sdf, float* w, float* rgb,
+                        float* lg, cudaStream_t s) {
+    if (!n) return;
+    k_payload_out<<<n, 512, 0, s>>>(pay, weight, logits, first, C, sdf, w, rgb, lg);
+}
+
+void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n, const int32_t* lo,
+                        const int32_t* dim, uint32_t* dense, uint32_t* occ, cudaStream_t s) {
+    if (!n) return;
+    k_dense_build<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), meta, n,
+                                                  lo[0], lo[1], lo[2], dim[0], dim[1], dense, occ);
+}
+
+void launch_grad_out(const float4* grad, uint32_t n, float* g_sdf, float* g_rgb, cudaStream_t s) {
+    const uint64_t nvox = static_cast<uint64_t>(n) * kVox;
+    if (!nvox) return;
+    k_grad_out<<<static_cast<unsigned>((nvox + 255) / 256), 256, 0, s>>>(grad, nvox, g_sdf, g_rgb);
+}
+
+void launch_active_list(const uint8_t* active, uint32_t n, uint32_t* list,
+                        unsigned long long* count, cudaStream_t s) {
+    // per_cta scratch lives right after the count (caller provides >= nctas+2 words there)
+    const uint32_t nctas = (n + 1023) / 1024;
+    uint32_t* per_cta = reinterpret_cast<uint32_t*>(count + 1);
+    if (nctas == 0) {
+        cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+        return;
+    }
+    k_active_count<<<nctas, 1024, 0, s>>>(active, n, per_cta);
+    k_active_scan<<<1, 1024, 0, s>>>(per_cta, nctas, count);
+    k_active_write<<<nctas, 1024, 0, s>>>(active, n, per_cta, list);
+}
+
+void launch_set_active(uint8_t* active, const uint8_t* mask, uint32_t n, cudaStream_t s) {
+    if (!n) return;
+    k_set_active<<<(n + 255) / 256, 256, 0, s>>>(active, mask, n);
+}
+
+void launch_grad_pack(const float4* grad, const uint32_t* blocks, uint64_t n, float4* out,
+                      cudaStream_t s) {
+    if (!n) return;
+    k_grad_pack<<<static_cast<unsigned>(n), 128, 0, s>>>(grad, blocks, out);
+}
+
+void launch_grad_unpack(float4* grad, const uint32_t* blocks, uint64_t n, const float4* in,
+                        cudaStream_t s) {
+    if (!n) return;
+    k_grad_unpack<<<static_cast<unsigned>(n), 128, 0, s>>>(grad, blocks, in);
+}
+
+void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list,
+                             const unsigned long long* count, uint32_t n_max, cudaStream_t s) {
+    if (!n_max) return;
+    const unsigned grid = n_max < 148u * 16u ? n_max : 148u * 16u;
+    k_grad_zero_active<<<grid, 128, 0, s>>>(grad, active, list, count);
+}
+
+}  // namespace svr_internal

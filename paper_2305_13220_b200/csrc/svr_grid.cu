@@ -1,0 +1,1077 @@
+// Host C++ side of libsvr_b200.so: the svr_grid handle (one device + one stream) and
+// every C-ABI entry point of include/svr.h.  It owns all device memory, stages host
+// arrays, keeps the host mirror of block coordinates (grid.hpp:219-222) and rebuilds
+// the dense AABB lookup index lazily.  There is no CPU compute fallback: every
+// numerical result comes from the sm_100a kernels in svr_render.cu / svr_activate.cu /
+// svr_grads.cu, and a missing or failing device surfaces as SVR_ERR_CUDA.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "svr_internal.h"
+#include "svr_synth.h"
+
+using namespace svr_dev;
+
+namespace svr_internal {
+thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace svr_internal
+
+using svr_internal::set_error;
+
+namespace {
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define SVR_CK(expr)                                                                        \
+    do {                                                                                    \
+        const cudaError_t e_ = (expr);                                                      \
+        if (e_ != cudaSuccess)                                                              \
+            throw Fail{SVR_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)};   \
+    } while (0)
+#define SVR_LAUNCHED() SVR_CK(cudaGetLastError())
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return SVR_OK;
+    } catch (const Fail& f) {
+        set_error(f.msg);
+        return f.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return SVR_ERR_DATA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return SVR_ERR_DATA;
+    }
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        SVR_CK(cudaGetDevice(&prev));
+        if (prev != dev) SVR_CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t need) {
+        if (need <= bytes) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        SVR_CK(cudaMalloc(&p, need));
+        bytes = need;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// Host <-> device staging for one API call.  Device pointers pass through; host
+// arrays are copied through stream-ordered temporaries, and the call synchronises
+// before returning if any host array was involved.
+struct Stage {
+    cudaStream_t s;
+    std::vector<void*> tmp;
+    struct Out {
+        void* host;
+        void* dev;
+        size_t bytes;
+    };
+    std::vector<Out> outs;
+    bool host_involved = false;
+    explicit Stage(cudaStream_t st) : s(st) {}
+    void* alloc(size_t bytes) {
+        void* d = nullptr;
+        SVR_CK(cudaMallocAsync(&d, bytes, s));
+        tmp.push_back(d);
+        return d;
+    }
+    template <typename T>
+    const T* in(const T* p, size_t n) {
+        if (!p || n == 0 || is_device_ptr(p)) return p;
+        host_involved = true;
+        void* d = alloc(n * sizeof(T));
+        SVR_CK(cudaMemcpyAsync(d, p, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        return static_cast<const T*>(d);
+    }
+    template <typename T>
+    T* out(T* p, size_t n) {
+        if (!p || n == 0 || is_device_ptr(p)) return p;
+        host_involved = true;
+        void* d = alloc(n * sizeof(T));
+        outs.push_back({p, d, n * sizeof(T)});
+        return static_cast<T*>(d);
+    }
+    void finish() {
+        SVR_LAUNCHED();
+        for (const Out& o : outs)
+            SVR_CK(cudaMemcpyAsync(o.host, o.dev, o.bytes, cudaMemcpyDeviceToHost, s));
+        outs.clear();
+        for (void* p : tmp) cudaFreeAsync(p, s);
+        tmp.clear();
+        if (host_involved) SVR_CK(cudaStreamSynchronize(s));
+    }
+    ~Stage() {
+        for (void* p : tmp) cudaFreeAsync(p, s);
+    }
+};
+
+uint64_t next_pow2(uint64_t v) {
+    uint64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+struct svr_grid {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double h = 0, inv_h = 0, L = 0;
+    int32_t C = 1;
+    uint64_t capacity = 0;
+    std::vector<int32_t> coords;  // host mirror, 3 per block
+    int32_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+
+    HashSlot* slots = nullptr;
+    uint64_t nslots = 0;
+
+    uint64_t cap_blocks = 0;  // rows allocated in the per-block arrays
+    int32_t* coords4 = nullptr;
+    float4* pay = nullptr;
+    float* weight = nullptr;
+    float* logits = nullptr;
+    uint32_t* vmask = nullptr;
+    uint32_t* meta = nullptr;
+    float4* grad = nullptr;
+    uint8_t* active = nullptr;
+
+    int lookup_pref = SVR_LOOKUP_AUTO;
+    bool dense_dirty = true;
+    int use_dense = 0;
+    int32_t dim[3] = {0, 0, 0};
+    DevBuf dense, occ;
+
+    // render context
+    DevBuf ray_o, ray_d, counts, tbuf, nvalid;
+    const double* ctx_o = nullptr;
+    const double* ctx_d = nullptr;
+    uint64_t ctx_n = 0;
+    uint32_t ctx_S = 0;
+    double ctx_step = 0, ctx_beta = 0;
+    bool ctx_valid = false;
+
+    DevBuf active_list, active_count;  // count: u64 + per-CTA scratch
+    DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
+    void* sort_tmp_p = nullptr;
+    size_t sort_tmp_bytes = 0;
+
+    uint64_t n() const { return coords.size() / 3; }
+
+    ~svr_grid() {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (void* p : {static_cast<void*>(slots), static_cast<void*>(coords4), static_cast<void*>(pay),
+                        static_cast<void*>(weight), static_cast<void*>(logits), static_cast<void*>(vmask),
+                        static_cast<void*>(meta), static_cast<void*>(grad), static_cast<void*>(active),
+                        sort_tmp_p})
+            if (p) cudaFree(p);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+
+    GridView view() {
+        GridView v{};
+        v.slots = slots;
+        v.slot_mask = nslots - 1;
+        v.dense = dense.as<uint32_t>();
+        v.occ = occ.as<uint32_t>();
+        v.pay = pay;
+        v.vmask = vmask;
+        v.meta = meta;
+        v.logits = logits;
+        v.grad = grad;
+        v.active = active;
+        for (int a = 0; a < 3; ++a) {
+            v.lo[a] = lo[a];
+            v.hi[a] = hi[a];
+            v.dim[a] = n() ? hi[a] - lo[a] + 1 : 0;
+        }
+        v.use_dense = use_dense;
+        v.n_blocks = static_cast<uint32_t>(n());
+        v.C = C;
+        v.h = h;
+        v.inv_h = inv_h;
+        v.L = L;
+        return v;
+    }
+
+    // Grow the per-block arrays to hold `need` blocks (contents preserved).
+    void ensure_blocks(uint64_t need) {
+        if (need <= cap_blocks) return;
+        uint64_t nc = std::max<uint64_t>(need, std::min<uint64_t>(capacity, cap_blocks * 2));
+        nc = std::max<uint64_t>(nc, 64);
+        nc = std::min<uint64_t>(std::max(nc, need), std::max<uint64_t>(capacity, need));
+        auto grow = [&](auto*& ptr, size_t per_block) {
+            using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
+            T* np = nullptr;
+            SVR_CK(cudaMalloc(&np, nc * per_block * sizeof(T)));
+            if (ptr) {
+                SVR_CK(cudaMemcpyAsync(np, ptr, cap_blocks * per_block * sizeof(T),
+                                       cudaMemcpyDeviceToDevice, stream));
+                SVR_CK(cudaStreamSynchronize(stream));
+                cudaFree(ptr);
+            }
+            ptr = np;
+        };
+        grow(coords4, 4);
+        grow(pay, kVox);
+        grow(weight, kVox);
+        grow(logits, static_cast<size_t>(kVox) * C);
+        grow(vmask, 16);
+        grow(meta, 1);
+        grow(grad, kVox);
+        grow(active, 1);
+        cap_blocks = nc;
+    }
+
+    // Zero-initialise blocks [first, first+count) (grid.cpp:69-75).
+    void zero_blocks(uint64_t first, uint64_t count) {
+        if (!count) return;
+        SVR_CK(cudaMemsetAsync(pay + first * kVox, 0, count * kVox * sizeof(float4), stream));
+        SVR_CK(cudaMemsetAsync(weight + first * kVox, 0, count * kVox * sizeof(float), stream));
+        SVR_CK(cudaMemsetAsync(logits + first * kVox * C, 0, count * kVox * C * sizeof(float), stream));
+        SVR_CK(cudaMemsetAsync(vmask + first * 16, 0, count * 16 * sizeof(uint32_t), stream));
+        SVR_CK(cudaMemsetAsync(meta + first, 0, count * sizeof(uint32_t), stream));
+        SVR_CK(cudaMemsetAsync(grad + first * kVox, 0, count * kVox * sizeof(float4), stream));
+        SVR_CK(cudaMemsetAsync(active + first, 0, count, stream));
+    }
+
+    // Host mirror + AABB after blocks [first, first+count) got coords (grid.cpp:96-106).
+    void pull_coords(uint64_t first, uint64_t count) {
+        std::vector<int32_t> c4(count * 4);
+        SVR_CK(cudaMemcpyAsync(c4.data(), coords4 + first * 4, count * 16, cudaMemcpyDeviceToHost, stream));
+        SVR_CK(cudaStreamSynchronize(stream));
+        for (uint64_t i = 0; i < count; ++i) push_coord(c4[4 * i], c4[4 * i + 1], c4[4 * i + 2]);
+    }
+    void push_coord(int32_t x, int32_t y, int32_t z) {
+        if (coords.empty()) {
+            lo[0] = hi[0] = x, lo[1] = hi[1] = y, lo[2] = hi[2] = z;
+        } else {
+            lo[0] = std::min(lo[0], x), lo[1] = std::min(lo[1], y), lo[2] = std::min(lo[2], z);
+            hi[0] = std::max(hi[0], x), hi[1] = std::max(hi[1], y), hi[2] = std::max(hi[2], z);
+        }
+        coords.push_back(x), coords.push_back(y), coords.push_back(z);
+        dense_dirty = true;
+    }
+
+    // Dense AABB index (rebuilt lazily): used when the block AABB volume is modest.
+    void ensure_lookup() {
+        if (!dense_dirty) return;
+        dense_dirty = false;
+        use_dense = 0;
+        if (n() == 0 || lookup_pref == SVR_LOOKUP_HASH) return;
+        uint64_t cells = 1;
+        for (int a = 0; a < 3; ++a) {
+            dim[a] = hi[a] - lo[a] + 1;
+            cells *= static_cast<uint64_t>(dim[a]);
+        }
+        const bool fits = cells <= (1ull << 28) && cells <= 64 * n() + (1ull << 22);
+        if (!fits) {
+            if (lookup_pref == SVR_LOOKUP_DENSE)
+                throw Fail{SVR_ERR_CONFIG, "lookup: block AABB too large for the dense index"};
+            return;
+        }
+        dense.ensure(cells * 4);
+        occ.ensure(((cells + 31) / 32) * 4);
+        SVR_CK(cudaMemsetAsync(dense.p, 0xFF, cells * 4, stream));
+        SVR_CK(cudaMemsetAsync(occ.p, 0, ((cells + 31) / 32) * 4, stream));
+        svr_internal::launch_dense_build(coords4, meta, static_cast<uint32_t>(n()), lo, dim,
+                                         dense.as<uint32_t>(), occ.as<uint32_t>(), stream);
+        SVR_LAUNCHED();
+        use_dense = 1;
+    }
+
+    // Insert `keys` (unique, absent) with indices n().. in order.
+    void insert_new(const unsigned long long* d_keys, uint64_t count) {
+        if (!count) return;
+        const uint64_t first = n();
+        ensure_blocks(first + count);
+        zero_blocks(first, count);
+        svr_internal::launch_hash_insert(slots, nslots - 1, d_keys, count, static_cast<uint32_t>(first),
+                                         coords4, stream);
+        SVR_LAUNCHED();
+        pull_coords(first, count);
+    }
+
+    // commit (allocation.cpp:19-43) on a device list of unique base keys.
+    void commit(const unsigned long long* d_base, uint64_t nbase, int32_t R, svr_alloc_report& rep) {
+        const uint64_t side = 2 * static_cast<uint64_t>(R) + 1;
+        const uint64_t ncand = nbase * side * side * side;
+        svr_internal::KeySet ks;
+        const uint64_t slots_n = next_pow2(std::max<uint64_t>(2 * ncand, 1024));
+        scratch_b.ensure(slots_n * 8 + ncand * 8 + 64);
+        ks.slots = scratch_b.as<unsigned long long>();
+        ks.mask = slots_n - 1;
+        ks.list = ks.slots + slots_n;
+        ks.cap = ncand;
+        unsigned long long* counters = reinterpret_cast<unsigned long long*>(ks.list + ncand);
+        SVR_CK(cudaMemsetAsync(counters, 0, 32, stream));
+        svr_internal::launch_keyset_clear(ks, stream);
+        uint32_t* flags = reinterpret_cast<uint32_t*>(counters + 3);
+        svr_internal::launch_dilate(d_base, nbase, R, ks, counters, flags, stream);
+        SVR_LAUNCHED();
+        unsigned long long hc[4];
+        SVR_CK(cudaMemcpyAsync(hc, counters, 32, cudaMemcpyDeviceToHost, stream));
+        SVR_CK(cudaStreamSynchronize(stream));
+        if (reinterpret_cast<uint32_t*>(&hc[3])[0] & 1u)
+            throw Fail{SVR_ERR_CONFIG, "allocate: block coordinate outside +-2^20"};
+        const uint64_t nwanted = hc[0];
+        rep.blocks_requested = nwanted;
+        // filter out the allocated ones
+        scratch_c.ensure(nwanted * 8 + 64);
+        unsigned long long* fresh = scratch_c.as<unsigned long long>();
+        unsigned long long* nfresh_d = counters + 1;
+        svr_internal::launch_filter_fresh(view(), ks.list, nwanted, fresh, nfresh_d, stream);
+        SVR_LAUNCHED();
+        unsigned long long nfresh = 0;
+        SVR_CK(cudaMemcpyAsync(&nfresh, nfresh_d, 8, cudaMemcpyDeviceToHost, stream));
+        SVR_CK(cudaStreamSynchronize(stream));
+        svr_internal::launch_sort_keys(fresh, nfresh, &sort_tmp_p, &sort_tmp_bytes, stream);
+        SVR_LAUNCHED();
+        const uint64_t room = capacity > n() ? capacity - n() : 0;
+        const uint64_t take = std::min<uint64_t>(nfresh, room);
+        insert_new(fresh, take);
+        rep.blocks_added = take;
+        rep.unallocated = nfresh - take;
+        if (rep.unallocated > 0)
+            throw Fail{SVR_ERR_CAPACITY, "allocate: grid capacity exceeded"};
+    }
+
+    void ensure_rays(uint64_t nr, uint32_t S) {
+        counts.ensure(nr * 4);
+        nvalid.ensure(nr * 4);
+        tbuf.ensure(nr * S * 8);
+    }
+};
+
+namespace {
+
+svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t device) {
+    if (!(h > 0.0)) throw Fail{SVR_ERR_CONFIG, "grid: voxel_size must be positive"};  // grid.cpp:83
+    if (B < 2) throw Fail{SVR_ERR_CONFIG, "grid: block_res must be >= 2"};
+    if (B != kRes) throw Fail{SVR_ERR_CONFIG, "grid: this build specialises block_res = 8"};
+    if (C < 1) throw Fail{SVR_ERR_CONFIG, "grid: label_channels must be >= 1"};
+    int ndev = 0;
+    SVR_CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Fail{SVR_ERR_CUDA, "grid: no such CUDA device"};
+    DeviceGuard dg(device);
+    auto g = std::make_unique<svr_grid>();
+    g->device = device;
+    g->h = h;
+    g->inv_h = 1.0 / h;  // grid.cpp:116
+    g->L = h * kRes;     // grid.hpp:112
+    g->C = C;
+    g->capacity = capacity ? capacity : (1ull << 21);  // grid.hpp:107
+    SVR_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->own_stream = true;
+    g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
+    SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
+    SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
+    SVR_CK(cudaStreamSynchronize(g->stream));
+    return g.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* svr_last_error(void) { return svr_internal::g_err.c_str(); }
+int svr_abi_version(void) { return SVR_ABI_VERSION; }
+
+int svr_device_count(int32_t* n) {
+    return guarded([&] {
+        int c = 0;
+        SVR_CK(cudaGetDeviceCount(&c));
+        *n = c;
+    });
+}
+
+int svr_grid_create(double voxel_size, int32_t block_res, int32_t label_channels, uint64_t capacity,
+                    int32_t device, svr_grid** out) {
+    return guarded([&] { *out = make_grid(voxel_size, block_res, label_channels, capacity, device); });
+}
+
+int svr_grid_destroy(svr_grid* g) {
+    delete g;
+    return SVR_OK;
+}
+
+int svr_grid_set_stream(svr_grid* g, void* s) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        if (g->own_stream) cudaStreamDestroy(g->stream);
+        g->stream = static_cast<cudaStream_t>(s);
+        g->own_stream = false;
+        if (!s) {
+            SVR_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            g->own_stream = true;
+        }
+    });
+}
+
+int svr_grid_synchronize(svr_grid* g) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        SVR_CK(cudaStreamSynchronize(g->stream));
+    });
+}
+
+int svr_grid_get_info(svr_grid* g, svr_grid_info* out) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        g->ensure_lookup();
+        svr_grid_info i{};
+        i.voxel_size = g->h;
+        i.block_res = kRes;
+        i.label_channels = g->C;
+        i.capacity = g->capacity;
+        i.block_count = g->n();
+        i.hash_slots = g->nslots;
+        for (int a = 0; a < 3; ++a) i.bounds_lo[a] = g->lo[a], i.bounds_hi[a] = g->hi[a];
+        i.lookup_mode = g->use_dense ? SVR_LOOKUP_DENSE : SVR_LOOKUP_HASH;
+        i.device = g->device;
+        const uint64_t per_block = 16 + kVox * (16 + 4 + 4ull * g->C + 16) + 64 + 4 + 1;
+        i.device_bytes = g->nslots * sizeof(HashSlot) + g->cap_blocks * per_block + g->dense.bytes +
+                         g->occ.bytes + g->tbuf.bytes + g->counts.bytes + g->nvalid.bytes;
+        *out = i;
+    });
+}
+
+int svr_grid_set_lookup(svr_grid* g, int32_t mode) {
+    return guarded([&] {
+        if (mode < SVR_LOOKUP_AUTO || mode > SVR_LOOKUP_DENSE)
+            throw Fail{SVR_ERR_CONFIG, "lookup: unknown mode"};
+        DeviceGuard dg(g->device);
+        g->lookup_pref = mode;
+        g->dense_dirty = true;
+        g->ensure_lookup();
+    });
+}
+
+int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        if (n == 0) return;
+        std::vector<int32_t> hc(3 * n);
+        if (is_device_ptr(coords)) {
+            SVR_CK(cudaMemcpy(hc.data(), coords, 12 * n, cudaMemcpyDeviceToHost));
+        } else {
+            std::memcpy(hc.data(), coords, 12 * n);
+        }
+        std::vector<uint32_t> existing(n, kInvalid);
+        if (g->n()) {
+            Stage st(g->stream);
+            const int32_t* dc = st.in(hc.data(), 3 * n);
+            uint32_t* dout = st.out(existing.data(), n);
+            svr_internal::launch_hash_find(g->slots, g->nslots - 1, dc, n, dout, g->stream);
+            st.finish();
+        }
+        std::unordered_map<unsigned long long, uint32_t> fresh_idx;
+        std::vector<unsigned long long> fresh;
+        std::vector<uint32_t> idx(n, kInvalid);
+        bool full = false;
+        int code = SVR_OK;
+        std::string msg;
+        for (uint64_t i = 0; i < n; ++i) {
+            const int32_t x = hc[3 * i], y = hc[3 * i + 1], z = hc[3 * i + 2];
+            if (existing[i] != kInvalid) {
+                idx[i] = existing[i];
+                continue;
+            }
+            if (!packable(x, y, z)) {
+                code = SVR_ERR_CONFIG;
+                msg = "grid: block coordinate outside +-2^20";
+                break;
+            }
+            const unsigned long long k = pack_key(x, y, z);
+            auto it = fresh_idx.find(k);
+            if (it != fresh_idx.end()) {
+                idx[i] = it->second;
+                continue;
+            }
+            if (g->n() + fresh.size() >= g->capacity) {  // grid.cpp:91-92
+                full = true;
+                code = SVR_ERR_CAPACITY;
+                msg = "grid: block capacity exceeded";
+                break;
+            }
+            const uint32_t v = static_cast<uint32_t>(g->n() + fresh.size());
+            fresh_idx.emplace(k, v);
+            fresh.push_back(k);
+            idx[i] = v;
+        }
+        (void)full;
+        if (!fresh.empty()) {
+            g->scratch_a.ensure(fresh.size() * 8);
+            SVR_CK(cudaMemcpyAsync(g->scratch_a.p, fresh.data(), fresh.size() * 8,
+                                   cudaMemcpyHostToDevice, g->stream));
+            g->insert_new(g->scratch_a.as<unsigned long long>(), fresh.size());
+        }
+        if (idx_out) {
+            if (is_device_ptr(idx_out)) {
+                SVR_CK(cudaMemcpy(idx_out, idx.data(), 4 * n, cudaMemcpyHostToDevice));
+            } else {
+                std::memcpy(idx_out, idx.data(), 4 * n);
+            }
+        }
+        if (code != SVR_OK) throw Fail{code, msg};
+    });
+}
+
+int svr_grid_activate_points(svr_grid* g, const double* xyz, uint64_t n, int32_t dilation,
+                             svr_alloc_report* report) {
+    svr_alloc_report rep{};
+    const int st = guarded([&] {
+        if (dilation < 0) throw Fail{SVR_ERR_CONFIG, "allocate: dilation must be >= 0"};
+        DeviceGuard dg(g->device);
+        Stage stg(g->stream);
+        const double* dx = stg.in(xyz, 3 * n);
+        svr_internal::KeySet ks;
+        const uint64_t slots_n = next_pow2(std::max<uint64_t>(2 * n, 1024));
+        g->scratch_a.ensure(slots_n * 8 + n * 8 + 64);
+        ks.slots = g->scratch_a.as<unsigned long long>();
+        ks.mask = slots_n - 1;
+        ks.list = ks.slots + slots_n;
+        ks.cap = n;
+        unsigned long long* counters = ks.list + n;
+        SVR_CK(cudaMemsetAsync(counters, 0, 16, g->stream));
+        svr_internal::launch_keyset_clear(ks, g->stream);
+        svr_internal::launch_points_to_keys(dx, n, g->L, ks, counters,
+                                            reinterpret_cast<uint32_t*>(counters + 1), g->stream);
+        stg.finish();
+        unsigned long long hc[2];
+        SVR_CK(cudaMemcpyAsync(hc, counters, 16, cudaMemcpyDeviceToHost, g->stream));
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        if (reinterpret_cast<uint32_t*>(&hc[1])[0] & 1u)
+            throw Fail{SVR_ERR_CONFIG, "allocate: block coordinate outside +-2^20"};
+        rep.pixels_used = n;  // allocation.cpp:85
+        g->commit(ks.list, hc[0], dilation, rep);
+    });
+    if (report) *report = rep;
+    return st;
+}
+
+int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* cams,
+                            uint32_t n_frames, const double* scales, int32_t sf_rows,
+                            int32_t sf_cols, int32_t dilation, svr_alloc_report* report) {
+    svr_alloc_report rep{};
+    const int st = guarded([&] {
+        if (dilation < 0) throw Fail{SVR_ERR_CONFIG, "allocate: dilation must be >= 0"};
+        DeviceGuard dg(g->device);
+        if (n_frames == 0) {
+            g->commit(nullptr, 0, dilation, rep);
+            return;
+        }
+        std::vector<svr_camera> hcams(n_frames);
+        if (is_device_ptr(cams)) {
+            SVR_CK(cudaMemcpy(hcams.data(), cams, n_frames * sizeof(svr_camera), cudaMemcpyDeviceToHost));
+        } else {
+            std::memcpy(hcams.data(), cams, n_frames * sizeof(svr_camera));
+        }
+        const int32_t W = hcams[0].width, H = hcams[0].height;
+        for (uint32_t f = 0; f < n_frames; ++f)
+            if (hcams[f].width != W || hcams[f].height != H)
+                throw Fail{SVR_ERR_CONFIG, "allocate: all frames must share one size"};
+        if (scales && (sf_rows < 2 || sf_cols < 2))
+            throw Fail{SVR_ERR_CONFIG, "scale field needs at least a 2x2 grid"};
+        if (W < 1 || H < 1) throw Fail{SVR_ERR_CONFIG, "allocate: empty frames"};
+        const uint64_t npx = static_cast<uint64_t>(W) * H * n_frames;
+        Stage stg(g->stream);
+        const float* dd = stg.in(depth, npx);
+        const svr_camera* dc = stg.in(hcams.data(), n_frames);
+        const double* ds = scales ? stg.in(scales, static_cast<uint64_t>(n_frames) * sf_rows * sf_cols)
+                                  : nullptr;
+        // base-key set: start at 2^22 slots and double on overflow
+        uint64_t slots_n = 1ull << 22;
+        unsigned long long hc[3];
+        svr_internal::KeySet ks;
+        for (;;) {
+            const uint64_t cap = slots_n / 2;
+            g->scratch_a.ensure(slots_n * 8 + cap * 8 + 64);
+            ks.slots = g->scratch_a.as<unsigned long long>();
+            ks.mask = slots_n - 1;
+            ks.list = ks.slots + slots_n;
+            ks.cap = cap;
+            unsigned long long* counters = ks.list + cap;
+            SVR_CK(cudaMemsetAsync(counters, 0, 24, g->stream));
+            svr_internal::launch_keyset_clear(ks, g->stream);
+            svr_internal::launch_depth_to_keys(dd, dc, n_frames, W, H, ds, sf_rows, sf_cols, g->L, ks,
+                                               counters, counters + 1,
+                                               reinterpret_cast<uint32_t*>(counters + 2), g->stream);
+            SVR_LAUNCHED();
+            SVR_CK(cudaMemcpyAsync(hc, counters, 24, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            if (hc[0] <= cap) break;
+            slots_n *= 2;
+        }
+        stg.finish();
+        if (reinterpret_cast<uint32_t*>(&hc[2])[0] & 1u)
+            throw Fail{SVR_ERR_CONFIG, "allocate: block coordinate outside +-2^20"};
+        rep.pixels_used = hc[1];
+        // keep the base list alive while commit reuses scratch_a? copy it out first
+        DevBuf base;
+        base.ensure(std::max<uint64_t>(hc[0], 1) * 8);
+        SVR_CK(cudaMemcpyAsync(base.p, ks.list, hc[0] * 8, cudaMemcpyDeviceToDevice, g->stream));
+        g->commit(base.as<unsigned long long>(), hc[0], dilation, rep);
+        SVR_CK(cudaStreamSynchronize(g->stream));
+    });
+    if (report) *report = rep;
+    return st;
+}
+
+int svr_grid_find(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        if (!n) return;
+        Stage st(g->stream);
+        const int32_t* dc = st.in(coords, 3 * n);
+        uint32_t* dout = st.out(idx_out, n);
+        svr_internal::launch_hash_find(g->slots, g->nslots - 1, dc, n, dout, g->stream);
+        st.finish();
+    });
+}
+
+int svr_grid_coords(svr_grid* g, int32_t* out) {
+    return guarded([&] {
+        if (g->coords.empty()) return;
+        if (is_device_ptr(out)) {
+            DeviceGuard dg(g->device);
+            SVR_CK(cudaMemcpy(out, g->coords.data(), g->coords.size() * 4, cudaMemcpyHostToDevice));
+        } else {
+            std::memcpy(out, g->coords.data(), g->coords.size() * 4);
+        }
+    });
+}
+
+int svr_grid_set_payload(svr_grid* g, uint32_t first, uint32_t n, const float* sdf,
+                         const float* weight, const float* rgb, const float* logits) {
+    return guarded([&] {
+        if (static_cast<uint64_t>(first) + n > g->n())
+            throw Fail{SVR_ERR_DATA, "payload: block range out of bounds"};
+        if (!n) return;
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        const uint64_t V = static_cast<uint64_t>(n) * kVox;
+        const float* a = st.in(sdf, V);
+        const float* b = st.in(weight, V);
+        const float* c = st.in(rgb, 3 * V);
+        const float* d = st.in(logits, V * g->C);
+        svr_internal::launch_payload_in(g->pay, g->weight, g->logits, g->vmask, g->meta, first, n,
+                                        g->C, a, b, c, d, g->stream);
+        st.finish();
+        if (weight) g->dense_dirty = true;
+    });
+}
+
+int svr_grid_get_payload(svr_grid* g, uint32_t first, uint32_t n, float* sdf, float* weight,
+                         float* rgb, float* logits) {
+    return guarded([&] {
+        if (static_cast<uint64_t>(first) + n > g->n())
+            throw Fail{SVR_ERR_DATA, "payload: block range out of bounds"};
+        if (!n) return;
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        const uint64_t V = static_cast<uint64_t>(n) * kVox;
+        float* a = st.out(sdf, V);
+        float* b = st.out(weight, V);
+        float* c = st.out(rgb, 3 * V);
+        float* d = st.out(logits, V * g->C);
+        svr_internal::launch_payload_out(g->pay, g->weight, g->logits, first, n, g->C, a, b, c, d,
+                                         g->stream);
+        st.finish();
+    });
+}
+
+int svr_query(svr_grid* g, const double* x, uint64_t n, double* sdf, double* grad, double* rgb,
+              double* logits, uint8_t* valid) {
+    return guarded([&] {
+        if (!n) return;
+        DeviceGuard dg(g->device);
+        g->ensure_lookup();
+        Stage st(g->stream);
+        const double* dx = st.in(x, 3 * n);
+        double* a = st.out(sdf, n);
+        double* b = st.out(grad, 3 * n);
+        double* c = st.out(rgb, 3 * n);
+        double* d = st.out(logits, n * g->C);
+        uint8_t* e = st.out(valid, n);
+        svr_internal::launch_query(g->view(), dx, n, a, b, c, d, e, g->stream);
+        st.finish();
+    });
+}
+
+int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double step,
+              uint32_t max_samples, uint32_t* counts, double* t, double* delta) {
+    return guarded([&] {
+        if (!(step > 0.0)) throw Fail{SVR_ERR_CONFIG, "march: step must be positive"};
+        if (!n) return;
+        DeviceGuard dg(g->device);
+        g->ensure_lookup();
+        Stage st(g->stream);
+        const double* dO = st.in(o, 3 * n);
+        const double* dD = st.in(d, 3 * n);
+        uint32_t* dc = st.out(counts, n);
+        if (!dc) dc = static_cast<uint32_t*>(st.alloc(4 * n));
+        const uint64_t nt = n * static_cast<uint64_t>(max_samples);
+        double* dt = st.out(t, nt);
+        if (!dt && nt) dt = static_cast<double*>(st.alloc(8 * nt));
+        double* dl = st.out(delta, nt);
+        svr_internal::launch_march(g->view(), dO, dD, n, step, max_samples, dc, dt, dl, g->stream);
+        st.finish();
+    });
+}
+
+int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n, double step,
+                       uint32_t max_samples, double beta, float* rgb, float* depth, float* normal,
+                       float* wsum, uint32_t* n_samples) {
+    return guarded([&] {
+        if (!(beta > 0.0)) throw Fail{SVR_ERR_CONFIG, "render: beta must be positive"};
+        if (!(step > 0.0)) throw Fail{SVR_ERR_CONFIG, "render: step must be positive"};
+        if (max_samples < 1 || max_samples > 2048)
+            throw Fail{SVR_ERR_CONFIG, "render: max_samples must be in [1, 2048]"};
+        DeviceGuard dg(g->device);
+        g->ensure_lookup();
+        g->ctx_valid = false;
+        Stage st(g->stream);
+        // retain rays for the backward pass: device arrays by pointer, host arrays copied
+        const double* dO = o;
+        const double* dD = d;
+        if (n && !is_device_ptr(o)) {
+            g->ray_o.ensure(24 * n);
+            SVR_CK(cudaMemcpyAsync(g->ray_o.p, o, 24 * n, cudaMemcpyHostToDevice, g->stream));
+            dO = g->ray_o.as<double>();
+            st.host_involved = true;
+        }
+        if (n && !is_device_ptr(d)) {
+            g->ray_d.ensure(24 * n);
+            SVR_CK(cudaMemcpyAsync(g->ray_d.p, d, 24 * n, cudaMemcpyHostToDevice, g->stream));
+            dD = g->ray_d.as<double>();
+            st.host_involved = true;
+        }
+        g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
+        float* a = st.out(rgb, 3 * n);
+        float* b = st.out(depth, n);
+        float* c = st.out(normal, 3 * n);
+        float* e = st.out(wsum, n);
+        if (n) {
+            const GridView v = g->view();
+            svr_internal::launch_march(v, dO, dD, n, step, max_samples, g->counts.as<uint32_t>(),
+                                       g->tbuf.as<double>(), nullptr, g->stream);
+            svr_internal::launch_render_forward(v, dO, dD, n, g->counts.as<uint32_t>(),
+                                                g->tbuf.as<double>(), max_samples, step, beta, a, b,
+                                                c, e, nullptr, g->stream);
+            if (n_samples) {
+                uint32_t* ns = st.out(n_samples, n);
+                SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));
+            }
+        }
+        st.finish();
+        g->ctx_o = dO;
+        g->ctx_d = dD;
+        g->ctx_n = n;
+        g->ctx_S = max_samples;
+        g->ctx_step = step;
+        g->ctx_beta = beta;
+        g->ctx_valid = true;
+    });
+}
+
+int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, const float* d_normal) {
+    return guarded([&] {
+        if (!g->ctx_valid) throw Fail{SVR_ERR_DATA, "render_backward: no retained forward context"};
+        if (!d_rgb || !d_depth || !d_normal)
+            throw Fail{SVR_ERR_DATA, "render_backward: upstream gradients required"};
+        DeviceGuard dg(g->device);
+        const uint64_t n = g->ctx_n;
+        if (!n) return;
+        Stage st(g->stream);
+        const float* a = st.in(d_rgb, 3 * n);
+        const float* b = st.in(d_depth, n);
+        const float* c = st.in(d_normal, 3 * n);
+        svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->counts.as<uint32_t>(),
+                                             g->tbuf.as<double>(), g->ctx_S, g->ctx_step, g->ctx_beta,
+                                             a, b, c, g->stream);
+        st.finish();
+    });
+}
+
+int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        svr_render_stats s{};
+        s.rays = g->ctx_valid ? g->ctx_n : 0;
+        if (g->ctx_valid && g->ctx_n) {
+            // re-run the forward's validity count on the retained context (not on the hot path)
+            std::vector<uint32_t> cnt(g->ctx_n);
+            SVR_CK(cudaMemcpyAsync(cnt.data(), g->counts.p, 4 * g->ctx_n, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            for (uint32_t c : cnt) s.samples += c;
+            DevBuf vc;
+            vc.ensure(8);
+            SVR_CK(cudaMemsetAsync(vc.p, 0, 8, g->stream));
+            svr_internal::launch_render_forward(g->view(), g->ctx_o, g->ctx_d, g->ctx_n,
+                                                g->counts.as<uint32_t>(), g->tbuf.as<double>(),
+                                                g->ctx_S, g->ctx_step, g->ctx_beta, nullptr, nullptr,
+                                                nullptr, nullptr, vc.as<unsigned long long>(), g->stream);
+            SVR_LAUNCHED();
+            unsigned long long v = 0;
+            SVR_CK(cudaMemcpyAsync(&v, vc.p, 8, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            s.valid_samples = v;
+        }
+        *out = s;
+    });
+}
+
+int svr_grad_zero(svr_grid* g) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        if (!g->n()) return;
+        SVR_CK(cudaMemsetAsync(g->grad, 0, g->n() * kVox * sizeof(float4), g->stream));
+        SVR_CK(cudaMemsetAsync(g->active, 0, g->n(), g->stream));
+    });
+}
+
+int svr_grad_get(svr_grid* g, float* g_sdf, float* g_rgb) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        if (!g->n()) return;
+        Stage st(g->stream);
+        const uint64_t V = g->n() * kVox;
+        float* a = st.out(g_sdf, V);
+        float* b = st.out(g_rgb, 3 * V);
+        svr_internal::launch_grad_out(g->grad, static_cast<uint32_t>(g->n()), a, b, g->stream);
+        st.finish();
+    });
+}
+
+int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* count) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint32_t nb = static_cast<uint32_t>(g->n());
+        Stage st(g->stream);
+        if (mask && nb) {
+            uint8_t* m = st.out(mask, nb);
+            SVR_CK(cudaMemcpyAsync(m, g->active, nb, cudaMemcpyDeviceToDevice, g->stream));
+        }
+        if (list || count) {
+            g->active_list.ensure(std::max<uint32_t>(nb, 1) * 4);
+            g->active_count.ensure(8 + 4 * ((nb + 1023) / 1024 + 2));
+            auto* dcount = g->active_count.as<unsigned long long>();
+            svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
+            SVR_LAUNCHED();
+            unsigned long long c = 0;
+            SVR_CK(cudaMemcpyAsync(&c, dcount, 8, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            if (count) {
+                if (is_device_ptr(count)) {
+                    SVR_CK(cudaMemcpyAsync(count, dcount, 8, cudaMemcpyDeviceToDevice, g->stream));
+                } else {
+                    *count = c;
+                }
+            }
+            if (list && c) {
+                uint32_t* l = st.out(list, c);
+                SVR_CK(cudaMemcpyAsync(l, g->active_list.p, 4 * c, cudaMemcpyDeviceToDevice, g->stream));
+            }
+        }
+        st.finish();
+    });
+}
+
+int svr_active_set_mask(svr_grid* g, const uint8_t* mask) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint32_t nb = static_cast<uint32_t>(g->n());
+        Stage st(g->stream);
+        const uint8_t* m = st.in(mask, nb);
+        svr_internal::launch_set_active(g->active, m, nb, g->stream);
+        st.finish();
+    });
+}
+
+int svr_grad_pack(svr_grid* g, const uint32_t* blocks, uint64_t n, float* out) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        const uint32_t* b = st.in(blocks, n);
+        float* o = st.out(out, n * kVox * 4);
+        svr_internal::launch_grad_pack(g->grad, b, n, reinterpret_cast<float4*>(o), g->stream);
+        st.finish();
+    });
+}
+
+int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float* in) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        const uint32_t* b = st.in(blocks, n);
+        const float* i = st.in(in, n * kVox * 4);
+        svr_internal::launch_grad_unpack(g->grad, b, n, reinterpret_cast<const float4*>(i), g->stream);
+        st.finish();
+    });
+}
+
+int svr_grad_zero_active(svr_grid* g) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint32_t nb = static_cast<uint32_t>(g->n());
+        if (!nb) return;
+        g->active_list.ensure(nb * 4);
+        g->active_count.ensure(8 + 4 * ((nb + 1023) / 1024 + 2));
+        auto* dcount = g->active_count.as<unsigned long long>();
+        svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
+        svr_internal::launch_grad_zero_active(g->grad, g->active, g->active_list.as<uint32_t>(), dcount,
+                                              nb, g->stream);
+        SVR_LAUNCHED();
+    });
+}
+
+// ---------------------------------------------------------------------------
+// SDGV v1 snapshots (grid_io.cpp:37-97), streamed in chunks of blocks.
+// ---------------------------------------------------------------------------
+int svr_grid_save_sdgv(svr_grid* g, const char* path) {
+    return guarded([&] {
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("save_grid: cannot open ") + path};
+        const uint32_t ver = 1, B = kRes, C = static_cast<uint32_t>(g->C);
+        const uint64_t nb = g->n();
+        os.write("SDGV", 4);
+        os.write(reinterpret_cast<const char*>(&ver), 4);
+        os.write(reinterpret_cast<const char*>(&g->h), 8);
+        os.write(reinterpret_cast<const char*>(&B), 4);
+        os.write(reinterpret_cast<const char*>(&nb), 8);
+        os.write(reinterpret_cast<const char*>(&C), 4);
+        const uint32_t chunk = 4096;
+        std::vector<float> sdf, w, rgb, lg;
+        for (uint64_t f = 0; f < nb; f += chunk) {
+            const uint32_t m = static_cast<uint32_t>(std::min<uint64_t>(chunk, nb - f));
+            sdf.resize(static_cast<size_t>(m) * kVox);
+            w.resize(static_cast<size_t>(m) * kVox);
+            rgb.resize(static_cast<size_t>(m) * kVox * 3);
+            lg.resize(static_cast<size_t>(m) * kVox * C);
+            const int st = svr_grid_get_payload(g, static_cast<uint32_t>(f), m, sdf.data(), w.data(),
+                                                rgb.data(), lg.data());
+            if (st) throw Fail{st, svr_internal::g_err};
+            for (uint32_t i = 0; i < m; ++i) {
+                os.write(reinterpret_cast<const char*>(&g->coords[3 * (f + i)]), 12);
+                os.write(reinterpret_cast<const char*>(&sdf[static_cast<size_t>(i) * kVox]), kVox * 4);
+                os.write(reinterpret_cast<const char*>(&w[static_cast<size_t>(i) * kVox]), kVox * 4);
+                os.write(reinterpret_cast<const char*>(&rgb[static_cast<size_t>(i) * kVox * 3]), kVox * 12);
+                os.write(reinterpret_cast<const char*>(&lg[static_cast<size_t>(i) * kVox * C]),
+                         static_cast<std::streamsize>(kVox) * 4 * C);
+            }
+        }
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("save_grid: write failed for ") + path};
+    });
+}
+
+int svr_grid_load_sdgv(const char* path, int32_t device, svr_grid** out) {
+    return guarded([&] {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw Fail{SVR_ERR_DATA, std::string("load_grid: cannot open ") + path};
+        char magic[4];
+        is.read(magic, 4);
+        if (!is || std::memcmp(magic, "SDGV", 4) != 0) throw Fail{SVR_ERR_DATA, "load_grid: bad magic"};
+        uint32_t ver = 0, B = 0, C = 0;
+        double h = 0;
+        uint64_t nb = 0;
+        is.read(reinterpret_cast<char*>(&ver), 4);
+        if (ver != 1) throw Fail{SVR_ERR_DATA, "load_grid: unsupported version"};
+        is.read(reinterpret_cast<char*>(&h), 8);
+        is.read(reinterpret_cast<char*>(&B), 4);
+        is.read(reinterpret_cast<char*>(&nb), 8);
+        is.read(reinterpret_cast<char*>(&C), 4);
+        if (!is) throw Fail{SVR_ERR_DATA, "load_grid: truncated header"};
+        std::unique_ptr<svr_grid> g(make_grid(h, static_cast<int32_t>(B), static_cast<int32_t>(C),
+                                              std::max<uint64_t>(1ull << 21, nb), device));
+        const uint32_t chunk = 4096;
+        std::vector<int32_t> cc;
+        std::vector<float> sdf, w, rgb, lg;
+        std::vector<uint32_t> idx;
+        for (uint64_t f = 0; f < nb; f += chunk) {
+            const uint32_t m = static_cast<uint32_t>(std::min<uint64_t>(chunk, nb - f));
+            cc.resize(3 * m);
+            sdf.resize(static_cast<size_t>(m) * kVox);
+            w.resize(sdf.size());
+            rgb.resize(sdf.size() * 3);
+            lg.resize(sdf.size() * C);
+            for (uint32_t i = 0; i < m; ++i) {
+                is.read(reinterpret_cast<char*>(&cc[3 * i]), 12);
+                is.read(reinterpret_cast<char*>(&sdf[static_cast<size_t>(i) * kVox]), kVox * 4);
+                is.read(reinterpret_cast<char*>(&w[static_cast<size_t>(i) * kVox]), kVox * 4);
+                is.read(reinterpret_cast<char*>(&rgb[static_cast<size_t>(i) * kVox * 3]), kVox * 12);
+                is.read(reinterpret_cast<char*>(&lg[static_cast<size_t>(i) * kVox * C]),
+                        static_cast<std::streamsize>(kVox) * 4 * C);
+                if (!is) throw Fail{SVR_ERR_DATA, "load_grid: truncated block data"};
+            }
+            idx.resize(m);
+            int st = svr_grid_allocate_blocks(g.get(), cc.data(), m, idx.data());
+            if (st) throw Fail{st, svr_internal::g_err};
+            bool contiguous = true;
+            for (uint32_t i = 0; i < m; ++i) contiguous = contiguous && idx[i] == idx[0] + i;
+            if (contiguous) {
+                st = svr_grid_set_payload(g.get(), idx[0], m, sdf.data(), w.data(), rgb.data(), lg.data());
+                if (st) throw Fail{st, svr_internal::g_err};
+            } else {  // duplicate records: later records overwrite (grid_io.cpp:90-95)
+                for (uint32_t i = 0; i < m; ++i) {
+                    const size_t o = static_cast<size_t>(i) * kVox;
+                    st = svr_grid_set_payload(g.get(), idx[i], 1, &sdf[o], &w[o], &rgb[3 * o], &lg[C * o]);
+                    if (st) throw Fail{st, svr_internal::g_err};
+                }
+            }
+        }
+        *out = g.release();
+    });
+}
+
+}  // extern "C"

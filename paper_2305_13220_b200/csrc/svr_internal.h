@@ -1,0 +1,85 @@
+// Host-side internals shared by the C-ABI (svr_grid.cu) and the kernel launchers.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "svr.h"
+#include "svr_device.cuh"
+
+namespace svr_internal {
+
+void set_error(const std::string& msg);
+
+struct Status {
+    int code;
+    std::string msg;
+};
+
+// Launchers (svr_render.cu)
+void launch_query(const svr_dev::GridView& g, const double* x, uint64_t n, double* sdf,
+                  double* grad, double* rgb, double* logits, uint8_t* valid, cudaStream_t s);
+void launch_march(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
+                  double step, uint32_t max_samples, uint32_t* counts, double* t, double* delta,
+                  cudaStream_t s);
+void launch_render_forward(const svr_dev::GridView& g, const double* o, const double* d,
+                           uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
+                           double step, double beta, float* rgb, float* depth, float* normal,
+                           float* wsum, unsigned long long* valid_counter, cudaStream_t s);
+void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
+                            uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
+                            double step, double beta, const float* d_rgb, const float* d_depth,
+                            const float* d_normal, cudaStream_t s);
+
+// Launchers (svr_activate.cu)
+struct KeySet {
+    unsigned long long* slots = nullptr;  // open addressing, kEmptyKey = free
+    unsigned long long mask = 0;
+    unsigned long long* list = nullptr;   // unique keys in insertion order
+    unsigned long long cap = 0;           // capacity of `list` (== slots/2)
+};
+void launch_keyset_clear(KeySet& ks, cudaStream_t s);
+// points -> base block keys; flags[0] |= 1 on an unpackable coordinate
+void launch_points_to_keys(const double* xyz, uint64_t n, double L, KeySet ks,
+                           unsigned long long* count, uint32_t* flags, cudaStream_t s);
+void launch_depth_to_keys(const float* depth, const svr_camera* cams, uint32_t n_frames,
+                          int32_t W, int32_t H, const double* scales, int32_t rows, int32_t cols,
+                          double L, KeySet ks, unsigned long long* count,
+                          unsigned long long* pixels, uint32_t* flags, cudaStream_t s);
+void launch_dilate(const unsigned long long* base, uint64_t nbase, int32_t R, KeySet ks,
+                   unsigned long long* count, uint32_t* flags, cudaStream_t s);
+void launch_filter_fresh(const svr_dev::GridView& g, const unsigned long long* keys, uint64_t n,
+                         unsigned long long* fresh, unsigned long long* nfresh, cudaStream_t s);
+void launch_sort_keys(unsigned long long* keys, uint64_t n, void** tmp, size_t* tmp_bytes,
+                      cudaStream_t s);
+void launch_hash_insert(svr_dev::HashSlot* slots, unsigned long long mask,
+                        const unsigned long long* keys, uint64_t n, uint32_t first_index,
+                        int32_t* coords4, cudaStream_t s);
+void launch_hash_find(const svr_dev::HashSlot* slots, unsigned long long mask,
+                      const int32_t* coords3, uint64_t n, uint32_t* out, cudaStream_t s);
+
+// Launchers (svr_grads.cu)
+void launch_payload_in(float4* pay, float* weight, float* logits, uint32_t* vmask,
+                       uint32_t* meta, uint32_t first, uint32_t n, int32_t C, const float* sdf,
+                       const float* w, const float* rgb, const float* lg, cudaStream_t s);
+void launch_payload_out(const float4* pay, const float* weight, const float* logits,
+                        uint32_t first, uint32_t n, int32_t C, float* sdf, float* w, float* rgb,
+                        float* lg, cudaStream_t s);
+void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n,
+                        const int32_t* lo, const int32_t* dim, uint32_t* dense, uint32_t* occ,
+                        cudaStream_t s);
+void launch_grad_out(const float4* grad, uint32_t n, float* g_sdf, float* g_rgb, cudaStream_t s);
+void launch_active_list(const uint8_t* active, uint32_t n, uint32_t* list,
+                        unsigned long long* count, cudaStream_t s);
+void launch_set_active(uint8_t* active, const uint8_t* mask, uint32_t n, cudaStream_t s);
+void launch_grad_pack(const float4* grad, const uint32_t* blocks, uint64_t n, float4* out,
+                      cudaStream_t s);
+void launch_grad_unpack(float4* grad, const uint32_t* blocks, uint64_t n, const float4* in,
+                        cudaStream_t s);
+void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list,
+                             const unsigned long long* count, uint32_t n_max, cudaStream_t s);
+
+}  // namespace svr_internal

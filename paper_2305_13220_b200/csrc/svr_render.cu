@@ -1,0 +1,574 @@
+// sm_100a kernels of the rendering hot path:
+//   K2 k_query     -- fp64 trilinear query, bit-exact with grid.cpp:112-261
+//   K4 k_march     -- ray-block DDA + fixed-step sampling, bit-exact with grid.cpp:263-353
+//   K5 k_forward   -- fused gather/interpolate/Laplace density/compositing, warp per ray
+//   K6 k_backward  -- compositing adjoint (warp suffix scan) + trilinear adjoint +
+//                     red.global.add.v4.f32 scatter into the float4 gradient planes
+// Discrete decisions (which block/cell, sample t) use fp64 with explicit _rn
+// intrinsics so nvcc cannot contract them into FMA (the reference's x86-64 Release
+// build has no FMA, proj/CMakeLists.txt:9-11).  Continuous interpolation and
+// compositing run in fp32 (tolerance in tests/test_gpu_render.py).
+#include <cfloat>
+#include <cstdint>
+
+#include "svr_internal.h"
+
+namespace svr_dev {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------
+// K2: query_sdf_with_gradient + color_at + logits_at (grid.cpp:112-261), fp64 with the
+// reference's association order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_query(GridView g, const double* __restrict__ x,
+                                               uint64_t n, double* sdf, double* grad,
+                                               double* rgb, double* logits, uint8_t* valid) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double fx[3];
+    int base[3];
+    for (int a = 0; a < 3; ++a) {
+        const double gg = __dmul_rn(x[3 * i + a], g.inv_h);
+        const double fl = floor(gg);
+        base[a] = static_cast<int>(fl);
+        fx[a] = __dsub_rn(gg, fl);
+    }
+    const double w0[3] = {__dsub_rn(1.0, fx[0]), __dsub_rn(1.0, fx[1]), __dsub_rn(1.0, fx[2])};
+    bool ok = g.n_blocks > 0;
+    uint32_t gidx[8];
+    double w[8], dw[8][3];
+    int32_t lbx = INT32_MIN, lby = 0, lbz = 0;
+    uint32_t le = kInvalid;
+    for (int c = 0; c < 8 && ok; ++c) {
+        const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+        const int vx = base[0] + cx, vy = base[1] + cy, vz = base[2] + cz;
+        const int32_t bx = fdiv8(vx), by = fdiv8(vy), bz = fdiv8(vz);
+        if (bx != lbx || by != lby || bz != lbz) {
+            lbx = bx, lby = by, lbz = bz;
+            le = lookup_block(g, bx, by, bz);
+        }
+        if (le == kInvalid) {
+            ok = false;
+            break;
+        }
+        const uint32_t local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
+        if (!voxel_valid(g, le, local)) {
+            ok = false;
+            break;
+        }
+        gidx[c] = (le & ~kFullBit) * kVox + local;
+        const double wx = cx ? fx[0] : w0[0];
+        const double wy = cy ? fx[1] : w0[1];
+        const double wz = cz ? fx[2] : w0[2];
+        w[c] = __dmul_rn(__dmul_rn(wx, wy), wz);
+        dw[c][0] = __dmul_rn(__dmul_rn(__dmul_rn(cx ? 1.0 : -1.0, g.inv_h), wy), wz);
+        dw[c][1] = __dmul_rn(__dmul_rn(__dmul_rn(cy ? 1.0 : -1.0, g.inv_h), wx), wz);
+        dw[c][2] = __dmul_rn(__dmul_rn(__dmul_rn(cz ? 1.0 : -1.0, g.inv_h), wx), wy);
+    }
+    if (!ok) {
+        if (sdf) sdf[i] = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            if (grad) grad[3 * i + a] = 0.0;
+            if (rgb) rgb[3 * i + a] = 0.0;
+        }
+        if (logits)
+            for (int k = 0; k < g.C; ++k) logits[static_cast<uint64_t>(g.C) * i + k] = 0.0;
+        if (valid) valid[i] = 0;
+        return;
+    }
+    float4 p[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + gidx[c]);
+    double s = 0.0, gr[3] = {0.0, 0.0, 0.0}, col[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s = __dadd_rn(s, __dmul_rn(w[c], static_cast<double>(p[c].x)));
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const double v = p[c].x;
+        gr[0] = __dadd_rn(gr[0], __dmul_rn(dw[c][0], v));
+        gr[1] = __dadd_rn(gr[1], __dmul_rn(dw[c][1], v));
+        gr[2] = __dadd_rn(gr[2], __dmul_rn(dw[c][2], v));
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        col[0] = __dadd_rn(col[0], __dmul_rn(w[c], static_cast<double>(p[c].y)));
+        col[1] = __dadd_rn(col[1], __dmul_rn(w[c], static_cast<double>(p[c].z)));
+        col[2] = __dadd_rn(col[2], __dmul_rn(w[c], static_cast<double>(p[c].w)));
+    }
+    if (sdf) sdf[i] = s;
+    for (int a = 0; a < 3; ++a) {
+        if (grad) grad[3 * i + a] = gr[a];
+        if (rgb) rgb[3 * i + a] = col[a];
+    }
+    if (logits) {  // logits_at(CornerCacheD) grid.cpp:230-238
+        for (int k = 0; k < g.C; ++k) {
+            double acc = 0.0;
+            for (int c = 0; c < 8; ++c)
+                acc = __dadd_rn(acc, __dmul_rn(w[c], static_cast<double>(__ldg(
+                                                         g.logits + static_cast<size_t>(gidx[c]) * g.C + k))));
+            logits[static_cast<uint64_t>(g.C) * i + k] = acc;
+        }
+    }
+    if (valid) valid[i] = 1;
+}
+
+// ---------------------------------------------------------------------------
+// K4: march_intervals + march_ray (grid.cpp:263-353) fused into one DDA walk that
+// emits samples per allocated block (equivalence argued in oracle/svr_oracle.cpp).
+// Crossing times are recomputed from plane equations exactly as the reference does;
+// only the stepped axis' crossing changes per step, so the other two are cached.
+// ---------------------------------------------------------------------------
+template <typename Emit>
+__device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[3],
+                                              const double d[3], double step, uint32_t S,
+                                              Emit&& emit) {
+    if (g.n_blocks == 0 || S == 0) return 0;
+    const double L = g.L;
+    double t0 = 0.0, t1 = DBL_MAX;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double box_lo = __dmul_rn(static_cast<double>(g.lo[a]), L);
+        const double box_hi = __dmul_rn(static_cast<double>(g.hi[a] + 1), L);
+        if (d[a] == 0.0) {
+            if (o[a] < box_lo || o[a] >= box_hi) return 0;
+            continue;
+        }
+        const double ta = __ddiv_rn(__dsub_rn(box_lo, o[a]), d[a]);
+        const double tb = __ddiv_rn(__dsub_rn(box_hi, o[a]), d[a]);
+        t0 = smax(t0, smin(ta, tb));
+        t1 = smin(t1, smax(ta, tb));
+    }
+    if (!(t0 < t1)) return 0;
+    const double t_eps = __dmul_rn(1e-12, smax(1.0, fabs(t0)));
+    const double ts = __dadd_rn(t0, t_eps);
+    int32_t b[3], inc[3];
+    double cross[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double start = __dadd_rn(o[a], __dmul_rn(ts, d[a]));
+        int32_t v = static_cast<int32_t>(floor(__ddiv_rn(start, L)));
+        v = v < g.lo[a] ? g.lo[a] : (g.hi[a] < v ? g.hi[a] : v);  // std::clamp
+        b[a] = v;
+        inc[a] = d[a] > 0.0 ? 1 : -1;
+        cross[a] = d[a] == 0.0
+                       ? __longlong_as_double(0x7ff0000000000000ll)
+                       : __ddiv_rn(__dsub_rn(__dmul_rn(static_cast<double>(b[a] + (d[a] > 0.0 ? 1 : 0)), L),
+                                             o[a]),
+                                   d[a]);
+    }
+    const double half_step = __dmul_rn(0.5, step);
+    double t = t0, cursor = -__longlong_as_double(0x7ff0000000000000ll);
+    bool open = false;
+    uint32_t cnt = 0;
+    while (t < t1) {
+        double t_exit = t1;
+        int axis = -1;
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            if (cross[a] < t_exit) {
+                t_exit = cross[a];
+                axis = a;
+            }
+        const bool alloc = block_allocated(g, b[0], b[1], b[2]);
+        if (alloc && !open) {
+            open = true;
+            if (cursor < t) cursor = __dadd_rn(t, half_step);
+        } else if (!alloc && open) {
+            open = false;
+        }
+        if (alloc) {
+            while (cursor < t_exit && cnt < S) {
+                emit(cnt, cursor);
+                ++cnt;
+                cursor = __dadd_rn(cursor, step);
+            }
+            if (cnt >= S) break;
+        }
+        if (axis < 0) break;
+        b[axis] += inc[axis];
+        t = t_exit;
+        if (b[axis] < g.lo[axis] || b[axis] > g.hi[axis]) break;
+        cross[axis] = __ddiv_rn(
+            __dsub_rn(__dmul_rn(static_cast<double>(b[axis] + (d[axis] > 0.0 ? 1 : 0)), L), o[axis]),
+            d[axis]);
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(128) k_march(GridView g, const double* __restrict__ O,
+                                               const double* __restrict__ D, uint64_t n,
+                                               double step, uint32_t S, uint32_t* counts,
+                                               double* T, double* delta) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    double* tr = T + r * S;
+    const uint32_t cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+    counts[r] = cnt;
+    if (delta) {
+        double* dr = delta + r * S;
+        for (uint32_t k = 0; k < cnt; ++k)
+            dr[k] = (k + 1 < cnt) ? __dsub_rn(tr[k + 1], tr[k]) : step;  // grid.cpp:352
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Per-sample gather + interpolation (fp32 payload math, fp64 cell decision).
+// ---------------------------------------------------------------------------
+struct SampleVal {
+    uint32_t gidx[8];
+    float fx, fy, fz;
+    float s, gx, gy, gz, r, gc, b;
+};
+
+__device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
+                                            double t, SampleVal& v) {
+    int base[3];
+    float fr[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = __dadd_rn(o[a], __dmul_rn(t, d[a]));
+        const double gg = __dmul_rn(x, g.inv_h);
+        const double fl = floor(gg);
+        base[a] = static_cast<int>(fl);
+        fr[a] = static_cast<float>(__dsub_rn(gg, fl));
+    }
+    v.fx = fr[0], v.fy = fr[1], v.fz = fr[2];
+    bool ok = true;
+    int32_t lbx = INT32_MIN, lby = 0, lbz = 0;
+    uint32_t le = kInvalid;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const int vx = base[0] + (c & 1), vy = base[1] + ((c >> 1) & 1), vz = base[2] + (c >> 2);
+        const int32_t bx = fdiv8(vx), by = fdiv8(vy), bz = fdiv8(vz);
+        if (bx != lbx || by != lby || bz != lbz) {
+            lbx = bx, lby = by, lbz = bz;
+            le = lookup_block(g, bx, by, bz);
+        }
+        const uint32_t local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
+        if (le == kInvalid) {
+            ok = false;
+            v.gidx[c] = 0;
+        } else {
+            ok = ok && voxel_valid(g, le, local);
+            v.gidx[c] = (le & ~kFullBit) * kVox + local;
+        }
+    }
+    if (!ok) return false;
+    float4 p[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + v.gidx[c]);
+    const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
+    const float w[8] = {x0 * y0 * z0, x1 * y0 * z0, x0 * y1 * z0, x1 * y1 * z0,
+                        x0 * y0 * z1, x1 * y0 * z1, x0 * y1 * z1, x1 * y1 * z1};
+    float s = 0.f, r = 0.f, gc = 0.f, b = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        s = fmaf(w[c], p[c].x, s);
+        r = fmaf(w[c], p[c].y, r);
+        gc = fmaf(w[c], p[c].z, gc);
+        b = fmaf(w[c], p[c].w, b);
+    }
+    const float ih = static_cast<float>(g.inv_h);
+    v.s = s, v.r = r, v.gc = gc, v.b = b;
+    v.gx = ih * ((y0 * z0) * (p[1].x - p[0].x) + (y1 * z0) * (p[3].x - p[2].x) +
+                 (y0 * z1) * (p[5].x - p[4].x) + (y1 * z1) * (p[7].x - p[6].x));
+    v.gy = ih * ((x0 * z0) * (p[2].x - p[0].x) + (x1 * z0) * (p[3].x - p[1].x) +
+                 (x0 * z1) * (p[6].x - p[4].x) + (x1 * z1) * (p[7].x - p[5].x));
+    v.gz = ih * ((x0 * y0) * (p[4].x - p[0].x) + (x1 * y0) * (p[5].x - p[1].x) +
+                 (x0 * y1) * (p[6].x - p[2].x) + (x1 * y1) * (p[7].x - p[3].x));
+    return true;
+}
+
+// Laplace density and its derivative.
+__device__ __forceinline__ float density(float s, float ib) {
+    return s > 0.f ? ib * (0.5f * expf(-s * ib)) : ib * (1.f - 0.5f * expf(s * ib));
+}
+__device__ __forceinline__ float density_ds(float s, float sigma, float ib) {
+    return s > 0.f ? -sigma * ib : -(ib - sigma) * ib;
+}
+
+__device__ __forceinline__ float warp_incl_scan(float v, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float n = __shfl_up_sync(kFull, v, off);
+        if (lane >= off) v += n;
+    }
+    return v;
+}
+__device__ __forceinline__ float warp_incl_suffix(float v, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const float n = __shfl_down_sync(kFull, v, off);
+        if (lane + off < 32) v += n;
+    }
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+}
+
+// Sample k's t and delta (delta_k = t_{k+1} - t_k, last = step: grid.cpp:352) for the
+// lane's two consecutive samples k0 = base + 2 lane, k1 = k0 + 1.
+struct PairT {
+    double t0, t1;
+    float d0, d1;
+    bool in0, in1;
+};
+__device__ __forceinline__ PairT load_pair(const double* tr, uint32_t cnt, uint32_t base, int lane,
+                                           double step) {
+    PairT p;
+    const uint32_t k0 = base + 2 * lane, k1 = k0 + 1;
+    p.in0 = k0 < cnt;
+    p.in1 = k1 < cnt;
+    p.t0 = p.in0 ? tr[k0] : 0.0;
+    p.t1 = p.in1 ? tr[k1] : 0.0;
+    double tn = __shfl_down_sync(kFull, p.t0, 1);
+    if (lane == 31 && k1 + 1 < cnt) tn = tr[k1 + 1];
+    p.d0 = p.in1 ? static_cast<float>(__dsub_rn(p.t1, p.t0)) : static_cast<float>(step);
+    p.d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn, p.t1)) : static_cast<float>(step);
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
+// chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_forward(GridView g, const double* __restrict__ O,
+                                                 const double* __restrict__ D, uint64_t n,
+                                                 const uint32_t* __restrict__ counts,
+                                                 const double* __restrict__ T, uint32_t S,
+                                                 double step, float ib, float* rgb, float* depth,
+                                                 float* normal, float* wsum,
+                                                 unsigned long long* valid_counter) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (r >= n) return;
+    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    const uint32_t cnt = counts[r];
+    const double* tr = T + r * S;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
+    float tau_base = 0.f;
+    uint32_t nvalid = 0;
+    for (uint32_t base = 0; base < cnt; base += 64) {
+        const PairT p = load_pair(tr, cnt, base, lane, step);
+        SampleVal v0, v1;
+        const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
+        const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+        const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
+        const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
+        const float incl = warp_incl_scan(tau0 + tau1, lane);
+        float excl = __shfl_up_sync(kFull, incl, 1);
+        if (lane == 0) excl = 0.f;
+        const float P0 = tau_base + excl, P1 = P0 + tau0;
+        const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
+        const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
+        if (ok0) {
+            acc[0] += w0 * v0.r, acc[1] += w0 * v0.gc, acc[2] += w0 * v0.b;
+            acc[3] += w0 * static_cast<float>(p.t0);
+            acc[4] += w0 * v0.gx, acc[5] += w0 * v0.gy, acc[6] += w0 * v0.gz;
+            acc[7] += w0;
+        }
+        if (ok1) {
+            acc[0] += w1 * v1.r, acc[1] += w1 * v1.gc, acc[2] += w1 * v1.b;
+            acc[3] += w1 * static_cast<float>(p.t1);
+            acc[4] += w1 * v1.gx, acc[5] += w1 * v1.gy, acc[6] += w1 * v1.gz;
+            acc[7] += w1;
+        }
+        nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
+        tau_base += __shfl_sync(kFull, incl, 31);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = warp_sum(acc[i]);
+    if (lane == 0) {
+        if (rgb) rgb[3 * r] = acc[0], rgb[3 * r + 1] = acc[1], rgb[3 * r + 2] = acc[2];
+        if (depth) depth[r] = acc[3];
+        if (normal) normal[3 * r] = acc[4], normal[3 * r + 1] = acc[5], normal[3 * r + 2] = acc[6];
+        if (wsum) wsum[r] = acc[7];
+        if (valid_counter && nvalid) atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+    }
+}
+
+// Per-corner gradient of one sample: (g_sdf, g_r, g_g, g_b).
+__device__ __forceinline__ void corner_grads(const SampleVal& v, float ds, float wk,
+                                             const float dC[3], const float dN[3], float ih,
+                                             float4 out[8]) {
+    const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
+    const float wn0 = wk * dN[0] * ih, wn1 = wk * dN[1] * ih, wn2 = wk * dN[2] * ih;
+    const float wc0 = wk * dC[0], wc1 = wk * dC[1], wc2 = wk * dC[2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const float wx = (c & 1) ? x1 : x0, wy = (c & 2) ? y1 : y0, wz = (c & 4) ? z1 : z0;
+        const float sx = (c & 1) ? 1.f : -1.f, sy = (c & 2) ? 1.f : -1.f, sz = (c & 4) ? 1.f : -1.f;
+        const float w = wx * wy * wz;
+        const float gs = w * ds + sx * (wy * wz) * wn0 + sy * (wx * wz) * wn1 + sz * (wx * wy) * wn2;
+        out[c] = make_float4(gs, w * wc0, w * wc1, w * wc2);
+    }
+}
+
+__device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& v) {
+    uint32_t prev = kInvalid;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t blk = v.gidx[c] >> 9;
+        if (blk != prev) {
+            if (!g.active[blk]) g.active[blk] = 1;
+            prev = blk;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: backward.  Chunks of 64 samples are visited back to front; within a chunk the
+// suffix S_k = sum_{m>k} w_m v_m comes from a warp suffix scan (no cancellation-prone
+// "total minus prefix").  dL/dtau_k = T_{k+1} v_k - S_k, dL/ds_k = delta_k sigma' dL/dtau_k.
+// A lane whose two samples share a cell sums them before the 8 vector atomics.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_backward(GridView g, const double* __restrict__ O,
+                                                  const double* __restrict__ D, uint64_t n,
+                                                  const uint32_t* __restrict__ counts,
+                                                  const double* __restrict__ T, uint32_t S,
+                                                  double step, float ib,
+                                                  const float* __restrict__ d_rgb,
+                                                  const float* __restrict__ d_depth,
+                                                  const float* __restrict__ d_normal) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (r >= n) return;
+    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    const uint32_t cnt = counts[r];
+    if (cnt == 0) return;
+    const double* tr = T + r * S;
+    const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
+    const float dD = d_depth[r];
+    const float dN[3] = {d_normal[3 * r], d_normal[3 * r + 1], d_normal[3 * r + 2]};
+    const float ih = static_cast<float>(g.inv_h);
+    const uint32_t nch = (cnt + 63) / 64;
+
+    // Exclusive tau prefix of each chunk (lane c holds chunk c's); only for long rays.
+    float my_prefix = 0.f;
+    if (nch > 1) {
+        float run = 0.f;
+        for (uint32_t ch = 0; ch < nch; ++ch) {
+            const PairT p = load_pair(tr, cnt, ch * 64, lane, step);
+            SampleVal v0, v1;
+            const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
+            const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+            const float tau = (ok0 ? density(v0.s, ib) * p.d0 : 0.f) +
+                              (ok1 ? density(v1.s, ib) * p.d1 : 0.f);
+            const float incl = warp_incl_scan(tau, lane);
+            if (lane == static_cast<int>(ch)) my_prefix = run;
+            run += __shfl_sync(kFull, incl, 31);
+        }
+    }
+
+    float S_after = 0.f;
+    for (int ch = static_cast<int>(nch) - 1; ch >= 0; --ch) {
+        const float tau_base = __shfl_sync(kFull, my_prefix, ch & 31);
+        const PairT p = load_pair(tr, cnt, static_cast<uint32_t>(ch) * 64, lane, step);
+        SampleVal v0, v1;
+        const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
+        const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+        const float sg0 = ok0 ? density(v0.s, ib) : 0.f, sg1 = ok1 ? density(v1.s, ib) : 0.f;
+        const float tau0 = sg0 * p.d0, tau1 = sg1 * p.d1;
+        const float incl = warp_incl_scan(tau0 + tau1, lane);
+        float excl = __shfl_up_sync(kFull, incl, 1);
+        if (lane == 0) excl = 0.f;
+        const float P0 = tau_base + excl, P1 = P0 + tau0;
+        const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
+        const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
+        const float Tn0 = expf(-P1), Tn1 = expf(-(P1 + tau1));
+        const float vv0 = ok0 ? dC[0] * v0.r + dC[1] * v0.gc + dC[2] * v0.b +
+                                    dD * static_cast<float>(p.t0) + dN[0] * v0.gx + dN[1] * v0.gy +
+                                    dN[2] * v0.gz
+                              : 0.f;
+        const float vv1 = ok1 ? dC[0] * v1.r + dC[1] * v1.gc + dC[2] * v1.b +
+                                    dD * static_cast<float>(p.t1) + dN[0] * v1.gx + dN[1] * v1.gy +
+                                    dN[2] * v1.gz
+                              : 0.f;
+        const float u0 = w0 * vv0, u1 = w1 * vv1;
+        const float sinc = warp_incl_suffix(u0 + u1, lane);
+        float sexc = __shfl_down_sync(kFull, sinc, 1);
+        if (lane == 31) sexc = 0.f;
+        const float S1 = S_after + sexc, S0 = S1 + u1;
+        float4 g0[8], g1[8];
+        if (ok0) {
+            const float ds = p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0);
+            corner_grads(v0, ds, w0, dC, dN, ih, g0);
+            mark_blocks(g, v0);
+        }
+        if (ok1) {
+            const float ds = p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1);
+            corner_grads(v1, ds, w1, dC, dN, ih, g1);
+            mark_blocks(g, v1);
+        }
+        if (ok0 && ok1 && v0.gidx[0] == v1.gidx[0]) {  // same cell: one atomic per corner
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                atomicAdd(g.grad + v0.gidx[c],
+                          make_float4(g0[c].x + g1[c].x, g0[c].y + g1[c].y, g0[c].z + g1[c].z,
+                                      g0[c].w + g1[c].w));
+        } else {
+            if (ok0) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) atomicAdd(g.grad + v0.gidx[c], g0[c]);
+            }
+            if (ok1) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) atomicAdd(g.grad + v1.gidx[c], g1[c]);
+            }
+        }
+        S_after += __shfl_sync(kFull, sinc, 0);
+    }
+}
+
+}  // namespace
+}  // namespace svr_dev
+
+namespace svr_internal {
+using namespace svr_dev;
+
+static inline unsigned grid_for(uint64_t n, unsigned per_block) {
+    return static_cast<unsigned>((n + per_block - 1) / per_block);
+}
+
+void launch_query(const GridView& g, const double* x, uint64_t n, double* sdf, double* grad,
+                  double* rgb, double* logits, uint8_t* valid, cudaStream_t s) {
+    if (!n) return;
+    k_query<<<grid_for(n, 256), 256, 0, s>>>(g, x, n, sdf, grad, rgb, logits, valid);
+}
+
+void launch_march(const GridView& g, const double* o, const double* d, uint64_t n, double step,
+                  uint32_t S, uint32_t* counts, double* t, double* delta, cudaStream_t s) {
+    if (!n) return;
+    k_march<<<grid_for(n, 128), 128, 0, s>>>(g, o, d, n, step, S, counts, t, delta);
+}
+
+void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
+                           const uint32_t* counts, const double* t, uint32_t S, double step,
+                           double beta, float* rgb, float* depth, float* normal, float* wsum,
+                           unsigned long long* valid_counter, cudaStream_t s) {
+    if (!n) return;
+    k_forward<<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, step,
+                                                    static_cast<float>(1.0 / beta), rgb, depth,
+                                                    normal, wsum, valid_counter);
+}
+
+void launch_render_backward(const GridView& g, const double* o, const double* d, uint64_t n,
+                            const uint32_t* counts, const double* t, uint32_t S, double step,
+                            double beta, const float* d_rgb, const float* d_depth,
+                            const float* d_normal, cudaStream_t s) {
+    if (!n) return;
+    k_backward<<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, step,
+                                                     static_cast<float>(1.0 / beta), d_rgb,
+                                                     d_depth, d_normal);
+}
+
+}  // namespace svr_internal

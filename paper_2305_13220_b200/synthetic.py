@@ -1,0 +1,92 @@
+"""Synthetic analytic-SDF scene fixtures (include/svr_synth.h; host-only, no GPU needed).
+
+Restates the reference's SyntheticScene (proj/src/core/synthetic.cpp:42-192) and the
+input recipes of SURVEY.md 8(d): GT depth frames for activation, clamped-SDF payloads,
+random-pixel rays from ring poses and U(-1,1) upstream gradients.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import Camera, SceneSpec, check
+
+
+class SyntheticScene:
+    def __init__(self, **spec):
+        self._lib = _lib.load()
+        s = SceneSpec()
+        self._lib.svr_scene_spec_default(ctypes.byref(s))
+        for k, v in spec.items():
+            if not hasattr(s, k):
+                raise TypeError(f"unknown SceneSpec field {k}")
+            setattr(s, k, v)
+        self.spec = s
+        h = ctypes.c_void_p()
+        check(self._lib.svr_scene_create(ctypes.byref(s), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h.value:
+                self._lib.svr_scene_destroy(self._h)
+        except Exception:
+            pass
+
+    def camera_for_frame(self, frame: int) -> Camera:
+        c = Camera()
+        check(self._lib.svr_scene_camera(self._h, frame, ctypes.byref(c)))
+        return c
+
+    def cameras(self, n: int | None = None) -> list[Camera]:
+        n = self.spec.n_frames if n is None else n
+        return [self.camera_for_frame(f) for f in range(n)]
+
+    def depth(self, cams: list[Camera], threads: int = 0) -> np.ndarray:
+        arr = (Camera * len(cams))(*cams)
+        out = np.empty((len(cams), self.spec.height, self.spec.width), np.float32)
+        check(self._lib.svr_scene_depth(self._h, ctypes.addressof(arr), len(cams), out.ctypes.data,
+                                        threads))
+        return out
+
+    def sdf(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
+        out = np.empty(len(x), np.float64)
+        check(self._lib.svr_scene_sdf(self._h, x.ctypes.data, len(x), out.ctypes.data))
+        return out
+
+    def fill_payload(self, voxel_size: float, coords, trunc: float, label_channels: int,
+                     block_res: int = 8, threads: int = 0) -> dict:
+        c = np.ascontiguousarray(coords, np.int32).reshape(-1, 3)
+        n, V = len(c), block_res ** 3
+        out = {"sdf": np.empty((n, V), np.float32), "weight": np.empty((n, V), np.float32),
+               "rgb": np.empty((n, V, 3), np.float32),
+               "logits": np.empty((n, V, label_channels), np.float32)}
+        check(self._lib.svr_scene_fill_payload(
+            self._h, voxel_size, block_res, label_channels, trunc, c.ctypes.data, n,
+            out["sdf"].ctypes.data, out["weight"].ctypes.data, out["rgb"].ctypes.data,
+            out["logits"].ctypes.data, threads))
+        return out
+
+    def rays(self, n_poses: int, rays_per_pose: int, seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
+        n = n_poses * rays_per_pose
+        o = np.empty((n, 3), np.float64)
+        d = np.empty((n, 3), np.float64)
+        check(self._lib.svr_scene_rays(self._h, n_poses, rays_per_pose, seed, o.ctypes.data,
+                                       d.ctypes.data))
+        return o, d
+
+    def image_rays(self, frame: int) -> tuple[np.ndarray, np.ndarray]:
+        n = self.spec.width * self.spec.height
+        o = np.empty((n, 3), np.float64)
+        d = np.empty((n, 3), np.float64)
+        check(self._lib.svr_scene_image_rays(self._h, frame, o.ctypes.data, d.ctypes.data))
+        return o, d
+
+
+def uniform_floats(n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    check(_lib.load().svr_uniform_floats(n, seed, lo, hi, out.ctypes.data))
+    return out
