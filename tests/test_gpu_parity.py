@@ -1,0 +1,185 @@
+"""GPU parity: libsvr_b200.so (through the C-ABI) vs the CPU oracle on identical inputs.
+
+Integer / index / fp64-decision outputs are compared bit-exactly; fp32 rendering outputs
+and gradients within the tolerance stated in tests/common.py (RTOL=1e-4 relative plus an
+atomic-order floor of 1e-6 x max|oracle|).
+"""
+import numpy as np
+import pytest
+
+from common import assert_close, gpu_grid_from, scene_case
+from oracle import OracleGrid
+
+pytestmark = pytest.mark.gpu
+
+LOOKUPS = [1, 2]  # SVR_LOOKUP_HASH, SVR_LOOKUP_DENSE
+
+
+@pytest.fixture(scope="module")
+def case():
+    return scene_case()
+
+
+def test_hash_insert_find_roundtrip():
+    """test_grid.cpp:33 at 1e5 coords in [-4000,4000]^3 plus 1000 far misses."""
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    rng = np.random.default_rng(42)
+    coords = rng.integers(-4000, 4001, size=(100000, 3), dtype=np.int32)
+    g = SparseDenseGrid(0.015, 8, 2, capacity=200000)
+    og = OracleGrid(0.015, 8, 2, capacity=200000)
+    idx = g.allocate_blocks(coords)
+    oidx = og.allocate_blocks(coords)
+    assert np.array_equal(idx, oidx)
+    assert np.array_equal(g.coords(), og.coords())
+    assert np.array_equal(g.find(coords), oidx)
+    far = rng.integers(10000, 20001, size=(1000, 3), dtype=np.int32)
+    assert (g.find(far) == 0xFFFFFFFF).all()
+
+
+def test_activation_points_matches_oracle():
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    rng = np.random.default_rng(1)
+    pts = rng.uniform(-0.5, 0.5, size=(2000, 3))
+    for R in (0, 1, 2):
+        g = SparseDenseGrid(0.015, 8, 2)
+        og = OracleGrid(0.015, 8, 2)
+        r = g.allocate_for_points(pts, R)
+        ro = og.allocate_points(pts, R)
+        assert (r.blocks_added, r.blocks_requested, r.pixels_used) == \
+               (ro.blocks_added, ro.blocks_requested, ro.pixels_used)
+        assert np.array_equal(g.coords(), og.coords())  # same deterministic order
+        again = g.allocate_for_points(pts, R)  # idempotent (test_grid.cpp:76)
+        assert again.blocks_added == 0 and g.block_count() == og.block_count()
+
+
+def test_activation_capacity_error():
+    """test_grid.cpp:89: capacity 10, 20 distinct blocks -> 10 allocated, 10 unallocated."""
+    from paper_2305_13220_b200 import CapacityError, SparseDenseGrid
+
+    g = SparseDenseGrid(0.015, 8, 2, capacity=10)
+    pts = np.array([[0.13 * i, 0.0, 0.0] for i in range(20)])
+    with pytest.raises(CapacityError) as e:
+        g.allocate_for_points(pts, 0)
+    assert e.value.unallocated_blocks == 10
+    assert g.block_count() == 10
+
+
+def test_activation_depth_matches_oracle(case):
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    g = SparseDenseGrid(case["h"], 8, case["C"])
+    r = g.allocate_for_frames(case["depth"], case["cams"], 1)
+    og = OracleGrid(case["h"], 8, case["C"])
+    ro = og.allocate_frames(case["depth"], case["cams"], 1)
+    assert (r.blocks_added, r.blocks_requested, r.pixels_used) == \
+           (ro.blocks_added, ro.blocks_requested, ro.pixels_used)
+    assert np.array_equal(g.coords(), og.coords())
+
+
+@pytest.mark.parametrize("lookup", LOOKUPS)
+def test_query_bit_exact(case, lookup):
+    g = gpu_grid_from(case, lookup)
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1.3, 1.3, size=(20000, 3))
+    q = g.query(x, logits=True)
+    qo = case["oracle"].query(x, logits=True)
+    assert q["valid"].sum() > 1000
+    for k in ("sdf", "grad", "rgb", "logits", "valid"):
+        assert np.array_equal(q[k], qo[k]), k
+
+
+@pytest.mark.parametrize("lookup", LOOKUPS)
+def test_march_bit_exact(case, lookup):
+    g = gpu_grid_from(case, lookup)
+    m = g.march(case["o"], case["d"], case["step"], 64)
+    mo = case["oracle"].march(case["o"], case["d"], case["step"], 64)
+    assert np.array_equal(m["counts"], mo["counts"])
+    for r in range(len(m["counts"])):
+        k = int(m["counts"][r])
+        assert np.array_equal(m["t"][r, :k], mo["t"][r, :k])
+        assert np.array_equal(m["delta"][r, :k], mo["delta"][r, :k])
+
+
+@pytest.mark.parametrize("lookup", LOOKUPS)
+def test_render_forward_matches_oracle(case, lookup):
+    g = gpu_grid_from(case, lookup)
+    out = g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    ref = case["oracle"].render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    assert np.array_equal(out["n_samples"], ref["n_samples"])
+    for k in ("rgb", "depth", "normal", "wsum"):
+        assert_close(out[k], ref[k], what=k)
+
+
+@pytest.mark.parametrize("lookup", LOOKUPS)
+def test_render_backward_matches_oracle(case, lookup):
+    g = gpu_grid_from(case, lookup)
+    g.grad_zero()
+    g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    g.render_backward(case["dC"], case["dD"], case["dN"])
+    gs, gr = g.grads()
+    os_, or_, act = case["oracle"].render_backward(case["o"], case["d"], case["step"], 64, case["beta"],
+                                                   case["dC"], case["dD"], case["dN"])
+    assert_close(gs, os_, what="grad_sdf")
+    assert_close(gr, or_, what="grad_rgb")
+    assert np.array_equal(g.active_mask(), act)
+    assert np.array_equal(g.active_blocks(), np.nonzero(act)[0].astype(np.uint32))
+
+
+def test_grad_zero_active_and_pack_roundtrip(case):
+    import torch
+
+    g = gpu_grid_from(case)
+    g.grad_zero()
+    g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    g.render_backward(case["dC"], case["dD"], case["dN"])
+    gs, gr = g.grads()
+    blocks = torch.from_numpy(g.active_blocks().astype(np.int32)).cuda()
+    packed = torch.empty((blocks.numel(), 512, 4), dtype=torch.float32, device="cuda")
+    g.grad_pack(blocks, packed)
+    g.synchronize()
+    b = blocks.cpu().numpy()
+    p = packed.cpu().numpy()
+    assert np.array_equal(p[..., 0], gs[b])
+    assert np.array_equal(p[..., 1:], gr[b])
+    g.grad_zero_active()
+    gs2, gr2 = g.grads()
+    assert not gs2.any() and not gr2.any() and not g.active_mask().any()
+    g.grad_unpack(blocks, packed)
+    g.synchronize()
+    gs3, gr3 = g.grads()
+    assert np.array_equal(gs3, gs) and np.array_equal(gr3, gr)
+
+
+def test_sdgv_roundtrip_with_oracle(case, tmp_path):
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    g = gpu_grid_from(case)
+    path = tmp_path / "g.sdgv"
+    g.save(path)
+    og = OracleGrid.load(path, case["C"])
+    assert np.array_equal(og.coords(), case["coords"])
+    p = og.get_payload()
+    for k in ("sdf", "weight", "rgb", "logits"):
+        assert np.array_equal(p[k], case["pay"][k]), k
+    path2 = tmp_path / "o.sdgv"
+    case["oracle"].save(path2)
+    g2 = SparseDenseGrid.load(path2)
+    assert np.array_equal(g2.coords(), case["coords"])
+    p2 = g2.get_payload()
+    for k in ("sdf", "weight", "rgb", "logits"):
+        assert np.array_equal(p2[k], case["pay"][k]), k
+
+
+def test_device_resident_path_matches_host_path(case):
+    import torch
+
+    g = gpu_grid_from(case)
+    host = g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    o = torch.from_numpy(case["o"]).cuda()
+    d = torch.from_numpy(case["d"]).cuda()
+    dev = g.render_forward(o, d, case["step"], 64, case["beta"])
+    g.synchronize()
+    for k in ("rgb", "depth", "normal", "wsum"):
+        assert np.array_equal(dev[k].cpu().numpy(), host[k]), k
