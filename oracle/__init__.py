@@ -193,7 +193,7 @@ class OracleGrid(_Base):
         "bounds": (c_int, [c_void_p, P, P]),
         "get_payload": (c_int, [c_void_p, c_uint32, c_uint32, P, P, P, P]),
         "query": (None, [c_void_p, P, c_uint64, P, P, P, P, P]),
-        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P]),
+        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P, P]),
         "render_backward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P, P]),
         "sdf_to_density": (c_double, [c_double, c_double]),
     })
@@ -255,19 +255,22 @@ class OracleGrid(_Base):
         o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
         n = len(o)
         out = {"rgb": np.empty((n, 3)), "depth": np.empty(n), "normal": np.empty((n, 3)),
-               "wsum": np.empty(n), "n_samples": np.empty(n, np.uint32)}
+               "wsum": np.empty(n), "n_samples": np.empty(n, np.uint32), "n_valid": np.empty(n, np.uint32)}
         self._check(self.lib().svro_render_forward(self._h, _ptr(o), _ptr(d), n, step, max_samples, beta,
                                                    _ptr(out["rgb"]), _ptr(out["depth"]), _ptr(out["normal"]),
-                                                   _ptr(out["wsum"]), _ptr(out["n_samples"])))
+                                                   _ptr(out["wsum"]), _ptr(out["n_samples"]),
+                                                   _ptr(out["n_valid"])))
         return out
 
-    def render_backward(self, o, d, step, max_samples, beta, d_rgb, d_depth, d_normal):
+    def grad_buffers(self):
+        A, V = self.block_count(), self.B ** 3
+        return np.zeros((A, V)), np.zeros((A, V, 3)), np.zeros(A, np.uint8)
+
+    def render_backward(self, o, d, step, max_samples, beta, d_rgb, d_depth, d_normal, out=None):
+        """Accumulates into `out` = (grad_sdf, grad_rgb, active) if given, else fresh zeros."""
         o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
         n = len(o)
-        A, V = self.block_count(), self.B ** 3
-        gs = np.zeros((A, V))
-        gr = np.zeros((A, V, 3))
-        active = np.zeros(A, np.uint8)
+        gs, gr, active = self.grad_buffers() if out is None else out
         up = [_f64(d_rgb, (-1, 3)), _f64(d_depth, (-1,)), _f64(d_normal, (-1, 3))]
         self._check(self.lib().svro_render_backward(
             self._h, _ptr(o), _ptr(d), n, step, max_samples, beta, _ptr(up[0]), _ptr(up[1]),
@@ -285,7 +288,7 @@ class RefGrid(_Base):
         "worker_count": (c_int, []),
         "bounds": (c_int, [c_void_p, P, P]),
         "query": (None, [c_void_p, P, c_uint64, P, P, P, P]),
-        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P]),
+        "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P]),
         "render_backward": (c_int, [c_void_p, P, P, P]),
         "grad_get": (c_int, [c_void_p, P, P]),
     })
@@ -329,10 +332,11 @@ class RefGrid(_Base):
         o, d = _f64(o, (-1, 3)), _f64(d, (-1, 3))
         n = len(o)
         out = {"rgb": np.empty((n, 3), np.float32), "depth": np.empty(n, np.float32),
-               "normal": np.empty((n, 3), np.float32), "wsum": np.empty(n, np.float32)}
+               "normal": np.empty((n, 3), np.float32), "wsum": np.empty(n, np.float32),
+               "n_valid": np.empty(n, np.uint32)}
         self._check(self.lib().svrr_render_forward(self._h, _ptr(o), _ptr(d), n, step, max_samples, beta,
                                                    _ptr(out["rgb"]), _ptr(out["depth"]), _ptr(out["normal"]),
-                                                   _ptr(out["wsum"])))
+                                                   _ptr(out["wsum"]), _ptr(out["n_valid"])))
         return out
 
     def render_backward(self, d_rgb, d_depth, d_normal):

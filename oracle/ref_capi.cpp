@@ -251,7 +251,7 @@ void svrr_march(const svrr_grid* w, const double* o, const double* d, uint64_t n
 // Forward: per sample gather into a retained float CornerCache (grid.hpp:76-86).
 int svrr_render_forward(svrr_grid* w, const double* o, const double* d, uint64_t n, double step,
                         uint32_t max_samples, double beta, float* rgb, float* depth,
-                        float* normal, float* wsum) {
+                        float* normal, float* wsum, uint32_t* nvalid) {
     return guarded([&] {
         if (!(beta > 0.0)) throw ConfigError("render: beta must be positive");
         w->rays.resize(n);
@@ -265,12 +265,14 @@ int svrr_render_forward(svrr_grid* w, const double* o, const double* d, uint64_t
                 std::vector<Retained>& rec = w->rays[i];
                 rec.resize(s.size());
                 double T = 1.0, C[3] = {0, 0, 0}, D = 0, N[3] = {0, 0, 0}, W = 0;
+                uint32_t nv = 0;
                 for (size_t k = 0; k < s.size(); ++k) {
                     Retained& r = rec[k];
                     r.t = s[k].t;
                     r.delta = s[k].delta;
                     r.valid = w->g->gather_corners(ro + s[k].t * rd, r.cc);
                     if (!r.valid) continue;
+                    ++nv;
                     r.s = w->g->sdf_at(r.cc);
                     const Eigen::Vector3f gr = w->g->sdf_gradient_at(r.cc);
                     const Eigen::Vector3f col = w->g->color_at(r.cc);
@@ -288,6 +290,7 @@ int svrr_render_forward(svrr_grid* w, const double* o, const double* d, uint64_t
                 }
                 if (depth) depth[i] = static_cast<float>(D);
                 if (wsum) wsum[i] = static_cast<float>(W);
+                if (nvalid) nvalid[i] = nv;
             }
         });
     });

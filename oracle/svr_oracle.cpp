@@ -670,7 +670,8 @@ double svro_sdf_to_density(double s, double beta) { return density(s, beta); }
 //   C = sum w c, D = sum w t, N = sum w grad(sdf) (world, un-normalised), W = sum w.
 int svro_render_forward(const svro_grid* g, const double* o, const double* d, uint64_t n,
                         double step, uint32_t max_samples, double beta, double* rgb,
-                        double* depth, double* normal, double* wsum, uint32_t* nsamples) {
+                        double* depth, double* normal, double* wsum, uint32_t* nsamples,
+                        uint32_t* nvalid) {
     return guarded([&] {
         if (!(beta > 0.0)) throw Status(kConfig, "render: beta must be positive");
         if (!(step > 0.0)) throw Status(kConfig, "render: step must be positive");
@@ -679,11 +680,13 @@ int svro_render_forward(const svro_grid* g, const double* o, const double* d, ui
             for (size_t i = b; i < e; ++i) {
                 march_ray(*g, o + 3 * i, d + 3 * i, step, max_samples, s);
                 double T = 1.0, C[3] = {0, 0, 0}, D = 0, N[3] = {0, 0, 0}, W = 0;
+                uint32_t nv = 0;
                 for (const Sample& sm : s) {
                     double x[3];
                     for (int a = 0; a < 3; ++a) x[a] = o[3 * i + a] + sm.t * d[3 * i + a];
                     Corners cc;
                     if (!gather(*g, x, cc)) continue;
+                    ++nv;
                     Interp it;
                     interpolate(*g, cc, it);
                     const double tau = density(it.s, beta) * sm.delta;
@@ -703,6 +706,7 @@ int svro_render_forward(const svro_grid* g, const double* o, const double* d, ui
                 if (depth) depth[i] = D;
                 if (wsum) wsum[i] = W;
                 if (nsamples) nsamples[i] = static_cast<uint32_t>(s.size());
+                if (nvalid) nvalid[i] = nv;
             }
         });
     });

@@ -73,7 +73,8 @@ void svro_march(const svro_grid* g, const double* o, const double* d, uint64_t n
 
 int svro_render_forward(const svro_grid* g, const double* o, const double* d, uint64_t n,
                         double step, uint32_t max_samples, double beta, double* rgb,
-                        double* depth, double* normal, double* wsum, uint32_t* nsamples);
+                        double* depth, double* normal, double* wsum, uint32_t* nsamples,
+                        uint32_t* nvalid);
 int svro_render_backward(const svro_grid* g, const double* o, const double* d, uint64_t n,
                          double step, uint32_t max_samples, double beta, const double* d_rgb,
                          const double* d_depth, const double* d_normal, double* grad_sdf,
