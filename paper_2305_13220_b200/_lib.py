@@ -100,6 +100,7 @@ _PROTOS = {
     "svr_grid_synchronize": (_I, [c_void_p]),
     "svr_grid_get_info": (_I, [c_void_p, POINTER(GridInfo)]),
     "svr_grid_set_lookup": (_I, [c_void_p, c_int32]),
+    "svr_grid_set_tuning": (_I, [c_void_p, c_char_p, ctypes.c_int64]),
     "svr_grid_load_sdgv": (_I, [c_char_p, c_int32, POINTER(c_void_p)]),
     "svr_grid_save_sdgv": (_I, [c_void_p, c_char_p]),
     "svr_grid_allocate_blocks": (_I, [c_void_p, P, c_uint64, P]),

@@ -6,6 +6,7 @@
 // svr_grads.cu, and a missing or failing device surfaces as SVR_ERR_CUDA.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -189,6 +190,12 @@ struct svr_grid {
 
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
+    DevBuf ord_keys, ord_ids, ord_tmp;  // ray ordering (Morton key of the first sample block)
+    uint32_t* ctx_order = nullptr;
+    // tuning knobs (svr_grid_set_tuning)
+    bool ray_sort = true;
+    int fwd_min_blocks = 4;
+    int bwd_min_blocks = 4;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
     uint64_t ctx_n = 0;
@@ -412,6 +419,7 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
     g->capacity = capacity ? capacity : (1ull << 21);  // grid.hpp:107
     SVR_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     g->own_stream = true;
+    if (const char* e = std::getenv("SVR_RAY_SORT")) g->ray_sort = std::atoi(e) != 0;
     g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
     SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
     SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
@@ -486,6 +494,21 @@ int svr_grid_get_info(svr_grid* g, svr_grid_info* out) {
     });
 }
 
+int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
+    return guarded([&] {
+        const std::string k = key ? key : "";
+        if (k == "ray_sort") {
+            g->ray_sort = value != 0;
+        } else if (k == "fwd_min_blocks") {
+            g->fwd_min_blocks = static_cast<int>(value);
+        } else if (k == "bwd_min_blocks") {
+            g->bwd_min_blocks = static_cast<int>(value);
+        } else {
+            throw Fail{SVR_ERR_CONFIG, "tuning: unknown key " + k};
+        }
+    });
+}
+
 int svr_grid_set_lookup(svr_grid* g, int32_t mode) {
     return guarded([&] {
         if (mode < SVR_LOOKUP_AUTO || mode > SVR_LOOKUP_DENSE)
@@ -518,7 +541,6 @@ int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uin
         std::unordered_map<unsigned long long, uint32_t> fresh_idx;
         std::vector<unsigned long long> fresh;
         std::vector<uint32_t> idx(n, kInvalid);
-        bool full = false;
         int code = SVR_OK;
         std::string msg;
         for (uint64_t i = 0; i < n; ++i) {
@@ -539,7 +561,6 @@ int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uin
                 continue;
             }
             if (g->n() + fresh.size() >= g->capacity) {  // grid.cpp:91-92
-                full = true;
                 code = SVR_ERR_CAPACITY;
                 msg = "grid: block capacity exceeded";
                 break;
@@ -549,7 +570,6 @@ int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uin
             fresh.push_back(k);
             idx[i] = v;
         }
-        (void)full;
         if (!fresh.empty()) {
             g->scratch_a.ensure(fresh.size() * 8);
             SVR_CK(cudaMemcpyAsync(g->scratch_a.p, fresh.data(), fresh.size() * 8,
@@ -806,9 +826,21 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
             const GridView v = g->view();
             svr_internal::launch_march(v, dO, dD, n, step, max_samples, g->counts.as<uint32_t>(),
                                        g->tbuf.as<double>(), nullptr, g->stream);
-            svr_internal::launch_render_forward(v, dO, dD, n, g->counts.as<uint32_t>(),
+            g->ctx_order = nullptr;
+            if (g->ray_sort && n > 1) {
+                g->ord_keys.ensure(8 * n);
+                g->ord_ids.ensure(8 * n);
+                const size_t tb = svr_internal::ray_order_tmp_bytes(n);
+                g->ord_tmp.ensure(std::max<size_t>(tb, 16));
+                uint32_t* k = g->ord_keys.as<uint32_t>();
+                uint32_t* id = g->ord_ids.as<uint32_t>();
+                svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
+                                               max_samples, k, id, k + n, id + n, g->ord_tmp.p,
+                                               g->ord_tmp.bytes, &g->ctx_order, g->stream);
+            }
+            svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
                                                 g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                c, e, nullptr, g->stream);
+                                                c, e, nullptr, g->stream, g->fwd_min_blocks);
             if (n_samples) {
                 uint32_t* ns = st.out(n_samples, n);
                 SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));
@@ -837,9 +869,10 @@ int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, c
         const float* a = st.in(d_rgb, 3 * n);
         const float* b = st.in(d_depth, n);
         const float* c = st.in(d_normal, 3 * n);
-        svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->counts.as<uint32_t>(),
+        svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
+                                             g->counts.as<uint32_t>(),
                                              g->tbuf.as<double>(), g->ctx_S, g->ctx_step, g->ctx_beta,
-                                             a, b, c, g->stream);
+                                             a, b, c, g->stream, g->bwd_min_blocks);
         st.finish();
     });
 }
@@ -858,10 +891,11 @@ int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
             DevBuf vc;
             vc.ensure(8);
             SVR_CK(cudaMemsetAsync(vc.p, 0, 8, g->stream));
-            svr_internal::launch_render_forward(g->view(), g->ctx_o, g->ctx_d, g->ctx_n,
+            svr_internal::launch_render_forward(g->view(), g->ctx_o, g->ctx_d, g->ctx_n, g->ctx_order,
                                                 g->counts.as<uint32_t>(), g->tbuf.as<double>(),
                                                 g->ctx_S, g->ctx_step, g->ctx_beta, nullptr, nullptr,
-                                                nullptr, nullptr, vc.as<unsigned long long>(), g->stream);
+                                                nullptr, nullptr, vc.as<unsigned long long>(), g->stream,
+                                                g->fwd_min_blocks);
             SVR_LAUNCHED();
             unsigned long long v = 0;
             SVR_CK(cudaMemcpyAsync(&v, vc.p, 8, cudaMemcpyDeviceToHost, g->stream));

@@ -26,13 +26,22 @@ void launch_march(const svr_dev::GridView& g, const double* o, const double* d, 
                   double step, uint32_t max_samples, uint32_t* counts, double* t, double* delta,
                   cudaStream_t s);
 void launch_render_forward(const svr_dev::GridView& g, const double* o, const double* d,
-                           uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
-                           double step, double beta, float* rgb, float* depth, float* normal,
-                           float* wsum, unsigned long long* valid_counter, cudaStream_t s);
+                           uint64_t n, const uint32_t* order, const uint32_t* counts,
+                           const double* t, uint32_t S, double step, double beta, float* rgb,
+                           float* depth, float* normal, float* wsum,
+                           unsigned long long* valid_counter, cudaStream_t s, int min_blocks);
 void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
-                            uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
-                            double step, double beta, const float* d_rgb, const float* d_depth,
-                            const float* d_normal, cudaStream_t s);
+                            uint64_t n, const uint32_t* order, const uint32_t* counts,
+                            const double* t, uint32_t S, double step, double beta,
+                            const float* d_rgb, const float* d_depth, const float* d_normal,
+                            cudaStream_t s, int min_blocks);
+// Sort rays by the Morton code of their first sample's block; *sorted_ids points into
+// ids or ids_alt.
+void launch_ray_order(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
+                      const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
+                      uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
+                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s);
+size_t ray_order_tmp_bytes(uint64_t n);
 
 // Launchers (svr_activate.cu)
 struct KeySet {

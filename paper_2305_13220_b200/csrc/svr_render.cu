@@ -11,6 +11,8 @@
 #include <cfloat>
 #include <cstdint>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "svr_internal.h"
 
 namespace svr_dev {
@@ -336,19 +338,61 @@ __device__ __forceinline__ PairT load_pair(const double* tr, uint32_t cnt, uint3
 }
 
 // ---------------------------------------------------------------------------
+// Ray ordering for L2 locality: key = Morton code of the block holding the ray's first
+// sample (10 bits per axis, relative to the AABB); rays without samples sort last.
+// The forward / backward warps then visit rays in key order, so concurrently resident
+// warps touch the same blocks and the same gradient lines.  Outputs stay in caller order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {
+    v &= 0x3FF;
+    v = (v | (v << 16)) & 0x030000FF;
+    v = (v | (v << 8)) & 0x0300F00F;
+    v = (v | (v << 4)) & 0x030C30C3;
+    v = (v | (v << 2)) & 0x09249249;
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_ray_keys(GridView g, const double* __restrict__ O,
+                                                  const double* __restrict__ D, uint64_t n,
+                                                  const uint32_t* __restrict__ counts,
+                                                  const double* __restrict__ T, uint32_t S,
+                                                  uint32_t* keys, uint32_t* ids) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    uint32_t key = 0xFFFFFFFFu;
+    if (counts[r]) {
+        const double t = T[r * S];
+        uint32_t b[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double x = O[3 * r + a] + t * D[3 * r + a];
+            int32_t v = static_cast<int32_t>(floor(x / g.L)) - g.lo[a];
+            v = v < 0 ? 0 : (v > 1023 ? 1023 : v);
+            b[a] = static_cast<uint32_t>(v);
+        }
+        key = spread3(b[0]) | (spread3(b[1]) << 1) | (spread3(b[2]) << 2);
+    }
+    keys[r] = key;
+    ids[r] = static_cast<uint32_t>(r);
+}
+
+// ---------------------------------------------------------------------------
 // K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
 // chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_forward(GridView g, const double* __restrict__ O,
-                                                 const double* __restrict__ D, uint64_t n,
-                                                 const uint32_t* __restrict__ counts,
-                                                 const double* __restrict__ T, uint32_t S,
-                                                 double step, float ib, float* rgb, float* depth,
-                                                 float* normal, float* wsum,
-                                                 unsigned long long* valid_counter) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const double* __restrict__ O,
+                                                    const double* __restrict__ D, uint64_t n,
+                                                    const uint32_t* __restrict__ order,
+                                                    const uint32_t* __restrict__ counts,
+                                                    const double* __restrict__ T, uint32_t S,
+                                                    double step, float ib, float* rgb, float* depth,
+                                                    float* normal, float* wsum,
+                                                    unsigned long long* valid_counter) {
     const int lane = threadIdx.x & 31;
-    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (r >= n) return;
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const uint64_t r = order ? order[w] : w;
     const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
     const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
     const uint32_t cnt = counts[r];
@@ -395,21 +439,27 @@ __global__ void __launch_bounds__(256) k_forward(GridView g, const double* __res
     }
 }
 
-// Per-corner gradient of one sample: (g_sdf, g_r, g_g, g_b).
-__device__ __forceinline__ void corner_grads(const SampleVal& v, float ds, float wk,
-                                             const float dC[3], const float dN[3], float ih,
-                                             float4 out[8]) {
-    const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
-    const float wn0 = wk * dN[0] * ih, wn1 = wk * dN[1] * ih, wn2 = wk * dN[2] * ih;
-    const float wc0 = wk * dC[0], wc1 = wk * dC[1], wc2 = wk * dC[2];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const float wx = (c & 1) ? x1 : x0, wy = (c & 2) ? y1 : y0, wz = (c & 4) ? z1 : z0;
-        const float sx = (c & 1) ? 1.f : -1.f, sy = (c & 2) ? 1.f : -1.f, sz = (c & 4) ? 1.f : -1.f;
-        const float w = wx * wy * wz;
-        const float gs = w * ds + sx * (wy * wz) * wn0 + sy * (wx * wz) * wn1 + sz * (wx * wy) * wn2;
-        out[c] = make_float4(gs, w * wc0, w * wc1, w * wc2);
-    }
+// Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
+//   g_sdf = w_c dL/ds + dw_c . (w_k dN),  g_rgb = w_c w_k dC.
+struct CornerCoef {
+    float x0, x1, y0, y1, z0, z1, ds, wn0, wn1, wn2, wc0, wc1, wc2;
+};
+__device__ __forceinline__ CornerCoef make_coef(const SampleVal& v, float ds, float wk,
+                                                const float dC[3], const float dN[3], float ih) {
+    CornerCoef k;
+    k.x1 = v.fx, k.x0 = 1.f - v.fx, k.y1 = v.fy, k.y0 = 1.f - v.fy, k.z1 = v.fz, k.z0 = 1.f - v.fz;
+    k.ds = ds;
+    k.wn0 = wk * dN[0] * ih, k.wn1 = wk * dN[1] * ih, k.wn2 = wk * dN[2] * ih;
+    k.wc0 = wk * dC[0], k.wc1 = wk * dC[1], k.wc2 = wk * dC[2];
+    return k;
+}
+template <int c>
+__device__ __forceinline__ float4 corner_grad(const CornerCoef& k) {
+    const float wx = (c & 1) ? k.x1 : k.x0, wy = (c & 2) ? k.y1 : k.y0, wz = (c & 4) ? k.z1 : k.z0;
+    const float sx = (c & 1) ? 1.f : -1.f, sy = (c & 2) ? 1.f : -1.f, sz = (c & 4) ? 1.f : -1.f;
+    const float w = wx * wy * wz;
+    const float gs = w * k.ds + sx * (wy * wz) * k.wn0 + sy * (wx * wz) * k.wn1 + sz * (wx * wy) * k.wn2;
+    return make_float4(gs, w * k.wc0, w * k.wc1, w * k.wc2);
 }
 
 __device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& v) {
@@ -424,27 +474,44 @@ __device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& 
     }
 }
 
+template <int c>
+__device__ __forceinline__ void scatter_corner(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                               const CornerCoef& k0, const CornerCoef& k1, bool ok0,
+                                               bool ok1, bool same) {
+    if (same) {
+        const float4 a = corner_grad<c>(k0), b = corner_grad<c>(k1);
+        atomicAdd(grad + v0.gidx[c], make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
+    } else {
+        if (ok0) atomicAdd(grad + v0.gidx[c], corner_grad<c>(k0));
+        if (ok1) atomicAdd(grad + v1.gidx[c], corner_grad<c>(k1));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K6: backward.  Chunks of 64 samples are visited back to front; within a chunk the
 // suffix S_k = sum_{m>k} w_m v_m comes from a warp suffix scan (no cancellation-prone
 // "total minus prefix").  dL/dtau_k = T_{k+1} v_k - S_k, dL/ds_k = delta_k sigma' dL/dtau_k.
-// A lane whose two samples share a cell sums them before the 8 vector atomics.
+// Corner gradients are produced and issued one corner at a time (red.global.add.v4.f32);
+// a lane whose two samples share a cell sums them first.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_backward(GridView g, const double* __restrict__ O,
-                                                  const double* __restrict__ D, uint64_t n,
-                                                  const uint32_t* __restrict__ counts,
-                                                  const double* __restrict__ T, uint32_t S,
-                                                  double step, float ib,
-                                                  const float* __restrict__ d_rgb,
-                                                  const float* __restrict__ d_depth,
-                                                  const float* __restrict__ d_normal) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const double* __restrict__ O,
+                                                     const double* __restrict__ D, uint64_t n,
+                                                     const uint32_t* __restrict__ order,
+                                                     const uint32_t* __restrict__ counts,
+                                                     const double* __restrict__ T, uint32_t S,
+                                                     double step, float ib,
+                                                     const float* __restrict__ d_rgb,
+                                                     const float* __restrict__ d_depth,
+                                                     const float* __restrict__ d_normal) {
     const int lane = threadIdx.x & 31;
-    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (r >= n) return;
-    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const uint64_t r = order ? order[w] : w;
     const uint32_t cnt = counts[r];
     if (cnt == 0) return;
+    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
     const double* tr = T + r * S;
     const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
     const float dD = d_depth[r];
@@ -498,33 +565,21 @@ __global__ void __launch_bounds__(256) k_backward(GridView g, const double* __re
         float sexc = __shfl_down_sync(kFull, sinc, 1);
         if (lane == 31) sexc = 0.f;
         const float S1 = S_after + sexc, S0 = S1 + u1;
-        float4 g0[8], g1[8];
-        if (ok0) {
-            const float ds = p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0);
-            corner_grads(v0, ds, w0, dC, dN, ih, g0);
-            mark_blocks(g, v0);
-        }
-        if (ok1) {
-            const float ds = p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1);
-            corner_grads(v1, ds, w1, dC, dN, ih, g1);
-            mark_blocks(g, v1);
-        }
-        if (ok0 && ok1 && v0.gidx[0] == v1.gidx[0]) {  // same cell: one atomic per corner
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-                atomicAdd(g.grad + v0.gidx[c],
-                          make_float4(g0[c].x + g1[c].x, g0[c].y + g1[c].y, g0[c].z + g1[c].z,
-                                      g0[c].w + g1[c].w));
-        } else {
-            if (ok0) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) atomicAdd(g.grad + v0.gidx[c], g0[c]);
-            }
-            if (ok1) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) atomicAdd(g.grad + v1.gidx[c], g1[c]);
-            }
-        }
+        const CornerCoef k0 = make_coef(v0, ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f,
+                                        w0, dC, dN, ih);
+        const CornerCoef k1 = make_coef(v1, ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f,
+                                        w1, dC, dN, ih);
+        if (ok0) mark_blocks(g, v0);
+        if (ok1) mark_blocks(g, v1);
+        const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
+        scatter_corner<0>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<1>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<2>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<3>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<4>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<5>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<6>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<7>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
         S_after += __shfl_sync(kFull, sinc, 0);
     }
 }
@@ -552,23 +607,60 @@ void launch_march(const GridView& g, const double* o, const double* d, uint64_t 
 }
 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
-                           const uint32_t* counts, const double* t, uint32_t S, double step,
-                           double beta, float* rgb, float* depth, float* normal, float* wsum,
-                           unsigned long long* valid_counter, cudaStream_t s) {
+                           const uint32_t* order, const uint32_t* counts, const double* t, uint32_t S,
+                           double step, double beta, float* rgb, float* depth, float* normal,
+                           float* wsum, unsigned long long* valid_counter, cudaStream_t s,
+                           int min_blocks) {
     if (!n) return;
-    k_forward<<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, step,
-                                                    static_cast<float>(1.0 / beta), rgb, depth,
-                                                    normal, wsum, valid_counter);
+    const float ib = static_cast<float>(1.0 / beta);
+    const unsigned grid = grid_for(n * 32, 256);
+#define SVR_FWD(MB) k_forward<MB><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, rgb, \
+                                                       depth, normal, wsum, valid_counter)
+    switch (min_blocks) {
+        case 1: SVR_FWD(1); break;
+        case 2: SVR_FWD(2); break;
+        case 3: SVR_FWD(3); break;
+        default: SVR_FWD(4); break;
+    }
+#undef SVR_FWD
 }
 
 void launch_render_backward(const GridView& g, const double* o, const double* d, uint64_t n,
-                            const uint32_t* counts, const double* t, uint32_t S, double step,
-                            double beta, const float* d_rgb, const float* d_depth,
-                            const float* d_normal, cudaStream_t s) {
+                            const uint32_t* order, const uint32_t* counts, const double* t,
+                            uint32_t S, double step, double beta, const float* d_rgb,
+                            const float* d_depth, const float* d_normal, cudaStream_t s,
+                            int min_blocks) {
     if (!n) return;
-    k_backward<<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, step,
-                                                     static_cast<float>(1.0 / beta), d_rgb,
-                                                     d_depth, d_normal);
+    const float ib = static_cast<float>(1.0 / beta);
+    const unsigned grid = grid_for(n * 32, 256);
+#define SVR_BWD(MB) k_backward<MB><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
+                                                        d_rgb, d_depth, d_normal)
+    switch (min_blocks) {
+        case 1: SVR_BWD(1); break;
+        case 2: SVR_BWD(2); break;
+        case 3: SVR_BWD(3); break;
+        default: SVR_BWD(4); break;
+    }
+#undef SVR_BWD
+}
+
+void launch_ray_order(const GridView& g, const double* o, const double* d, uint64_t n,
+                      const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
+                      uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
+                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s) {
+    if (!n) return;
+    k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids);
+    cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
+    size_t bytes = tmp_bytes;
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, 30, s);
+    *sorted_ids = vb.Current();
+}
+
+size_t ray_order_tmp_bytes(uint64_t n) {
+    size_t bytes = 0;
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int>(n), 0, 30);
+    return bytes;
 }
 
 }  // namespace svr_internal

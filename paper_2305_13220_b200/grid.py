@@ -124,6 +124,9 @@ class SparseDenseGrid:
     def set_lookup(self, mode: int) -> None:
         check(self._lib.svr_grid_set_lookup(self._h, mode))
 
+    def set_tuning(self, key: str, value: int) -> None:
+        check(self._lib.svr_grid_set_tuning(self._h, key.encode(), int(value)))
+
     # --- metadata (grid.hpp:109-120) -----------------------------------------
     def info(self) -> GridInfo:
         i = GridInfo()

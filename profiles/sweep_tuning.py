@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Sweep the renderer's performance knobs (results unaffected) on the cfg3 workload in one
+process: ray_sort, fwd_min_blocks, bwd_min_blocks.  Prints per-config device times of the
+forward call (march + sort + forward) and the backward kernel, CUDA events, mean of K."""
+import itertools
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2305_13220_b200 import SparseDenseGrid  # noqa: E402
+
+
+def main():
+    cfg = dict(bench.CFG3)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    scene = bench.make_scene(cfg)
+    cams, depth = bench.activation_frames(scene, cfg)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22)
+    g.set_stream(stream)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    bench.fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    o, d, dC, dD, dN = (torch.from_numpy(a).to(dev) for a in bench.rays_for_rank(scene, cfg, 0, 1))
+    n = o.shape[0]
+    outs = {k: torch.empty(s, dtype=torch.float32, device=dev)
+            for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
+    outs["n_samples"] = None
+    S, step, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
+    sorts = [int(x) for x in os.environ.get("SWEEP_SORT", "0,1").split(",")]
+    fwds = [int(x) for x in os.environ.get("SWEEP_FWD", "1,2,3,4").split(",")]
+    bwds = [int(x) for x in os.environ.get("SWEEP_BWD", "1,2,3,4").split(",")]
+    print(f"blocks={g.block_count()} rays={n}", flush=True)
+    for srt, fb, bb in itertools.product(sorts, fwds, bwds):
+        g.set_tuning("ray_sort", srt)
+        g.set_tuning("fwd_min_blocks", fb)
+        g.set_tuning("bwd_min_blocks", bb)
+        f_ms, b_ms = [], []
+        for it in range(6):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record(stream)
+            g.render_forward(o, d, step, S, beta, out=outs)
+            e[1].record(stream)
+            g.render_backward(dC, dD, dN)
+            e[2].record(stream)
+            g.grad_zero_active()
+            torch.cuda.synchronize()
+            if it >= 2:
+                f_ms.append(e[0].elapsed_time(e[1]))
+                b_ms.append(e[1].elapsed_time(e[2]))
+        print(f"sort={srt} fwd_minb={fb} bwd_minb={bb}: fwd {statistics.mean(f_ms):7.3f} ms  "
+              f"bwd {statistics.mean(b_ms):7.3f} ms  total {statistics.mean(f_ms) + statistics.mean(b_ms):7.3f}",
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()
