@@ -96,6 +96,9 @@ int svr_device_count(int32_t* n);
 int svr_grid_create(double voxel_size, int32_t block_res, int32_t label_channels,
                     uint64_t capacity, int32_t device, svr_grid** out);
 int svr_grid_destroy(svr_grid* g);
+/* Bind the handle to a CUDA stream (cudaStream_t; cudaStreamLegacy = (void*)1 selects the
+ * legacy default stream).  NULL restores a private non-blocking stream.  Device inputs must
+ * be complete in the order of this stream when a call is issued. */
 int svr_grid_set_stream(svr_grid* g, void* cuda_stream);
 int svr_grid_synchronize(svr_grid* g);
 int svr_grid_get_info(svr_grid* g, svr_grid_info* out);

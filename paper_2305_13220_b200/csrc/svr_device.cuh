@@ -11,6 +11,8 @@
 //   active  : u8[A]          block received a scatter since the last grad zero
 //   dense   : u32[dx*dy*dz]  block index (| 1<<31 when all-valid) over the block AABB,
 //                            0xFFFFFFFF = unallocated; occ: bit per AABB cell
+//   nbr     : u32[A*8]       entries of the +x/+y/+z neighbour blocks (trilinear corners
+//                            that cross a block face resolve with one L1-resident load)
 #pragma once
 
 #include <cstdint>
@@ -67,6 +69,7 @@ struct GridView {
     const uint32_t* vmask;
     const uint32_t* meta;
     const float* logits;
+    const uint32_t* nbr;    // [A][8]: entry of block + (k&1, k>>1&1, k>>2), k = 0..7
     float4* grad;
     uint8_t* active;
     int32_t lo[3], hi[3];   // block AABB (grid.hpp:222)

@@ -71,6 +71,20 @@ __global__ void k_dense_build(const int4* __restrict__ coords, const uint32_t* _
     atomicOr(occ + (cell >> 5), 1u << (cell & 31));
 }
 
+// Per-block table of the 8 blocks a trilinear cell can touch: entry k = lookup of
+// coord + (k & 1, (k >> 1) & 1, k >> 2) (k = 0 is the block itself), with the all-valid bit.
+__global__ void k_nbr_build(GridView g, const int4* __restrict__ coords, uint32_t n, uint32_t* nbr) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    uint32_t e[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = lookup_block(g, c.x + (k & 1), c.y + ((k >> 1) & 1), c.z + (k >> 2));
+    uint4* out = reinterpret_cast<uint4*>(nbr + static_cast<size_t>(i) * 8);
+    out[0] = make_uint4(e[0], e[1], e[2], e[3]);
+    out[1] = make_uint4(e[4], e[5], e[6], e[7]);
+}
+
 __global__ void k_grad_out(const float4* __restrict__ grad, uint64_t nvox, float* g_sdf,
                            float* g_rgb) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -207,6 +221,12 @@ void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n
     if (!n) return;
     k_dense_build<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), meta, n,
                                                   lo[0], lo[1], lo[2], dim[0], dim[1], dense, occ);
+}
+
+void launch_nbr_build(const GridView& g, const int32_t* coords4, uint32_t n, uint32_t* nbr,
+                      cudaStream_t s) {
+    if (!n) return;
+    k_nbr_build<<<(n + 255) / 256, 256, 0, s>>>(g, reinterpret_cast<const int4*>(coords4), n, nbr);
 }
 
 void launch_grad_out(const float4* grad, uint32_t n, float* g_sdf, float* g_rgb, cudaStream_t s) {

@@ -186,7 +186,7 @@ struct svr_grid {
     bool dense_dirty = true;
     int use_dense = 0;
     int32_t dim[3] = {0, 0, 0};
-    DevBuf dense, occ;
+    DevBuf dense, occ, nbr;
 
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
@@ -195,7 +195,7 @@ struct svr_grid {
     // tuning knobs (svr_grid_set_tuning)
     bool ray_sort = true;
     int fwd_min_blocks = 4;
-    int bwd_min_blocks = 4;
+    int bwd_min_blocks = 3;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
     uint64_t ctx_n = 0;
@@ -234,6 +234,7 @@ struct svr_grid {
         v.vmask = vmask;
         v.meta = meta;
         v.logits = logits;
+        v.nbr = nbr.as<uint32_t>();
         v.grad = grad;
         v.active = active;
         for (int a = 0; a < 3; ++a) {
@@ -309,31 +310,35 @@ struct svr_grid {
         dense_dirty = true;
     }
 
-    // Dense AABB index (rebuilt lazily): used when the block AABB volume is modest.
+    // Lookup structures, rebuilt lazily after blocks or validity change: the dense AABB
+    // index (when the AABB volume is modest) and the per-block neighbour table.
     void ensure_lookup() {
         if (!dense_dirty) return;
         dense_dirty = false;
         use_dense = 0;
-        if (n() == 0 || lookup_pref == SVR_LOOKUP_HASH) return;
+        if (n() == 0) return;
         uint64_t cells = 1;
         for (int a = 0; a < 3; ++a) {
             dim[a] = hi[a] - lo[a] + 1;
             cells *= static_cast<uint64_t>(dim[a]);
         }
         const bool fits = cells <= (1ull << 28) && cells <= 64 * n() + (1ull << 22);
-        if (!fits) {
-            if (lookup_pref == SVR_LOOKUP_DENSE)
-                throw Fail{SVR_ERR_CONFIG, "lookup: block AABB too large for the dense index"};
-            return;
+        if (lookup_pref == SVR_LOOKUP_DENSE && !fits)
+            throw Fail{SVR_ERR_CONFIG, "lookup: block AABB too large for the dense index"};
+        if (fits && lookup_pref != SVR_LOOKUP_HASH) {
+            dense.ensure(cells * 4);
+            occ.ensure(((cells + 31) / 32) * 4);
+            SVR_CK(cudaMemsetAsync(dense.p, 0xFF, cells * 4, stream));
+            SVR_CK(cudaMemsetAsync(occ.p, 0, ((cells + 31) / 32) * 4, stream));
+            svr_internal::launch_dense_build(coords4, meta, static_cast<uint32_t>(n()), lo, dim,
+                                             dense.as<uint32_t>(), occ.as<uint32_t>(), stream);
+            SVR_LAUNCHED();
+            use_dense = 1;
         }
-        dense.ensure(cells * 4);
-        occ.ensure(((cells + 31) / 32) * 4);
-        SVR_CK(cudaMemsetAsync(dense.p, 0xFF, cells * 4, stream));
-        SVR_CK(cudaMemsetAsync(occ.p, 0, ((cells + 31) / 32) * 4, stream));
-        svr_internal::launch_dense_build(coords4, meta, static_cast<uint32_t>(n()), lo, dim,
-                                         dense.as<uint32_t>(), occ.as<uint32_t>(), stream);
+        nbr.ensure(n() * 32);
+        svr_internal::launch_nbr_build(view(), coords4, static_cast<uint32_t>(n()), nbr.as<uint32_t>(),
+                                       stream);
         SVR_LAUNCHED();
-        use_dense = 1;
     }
 
     // Insert `keys` (unique, absent) with indices n().. in order.

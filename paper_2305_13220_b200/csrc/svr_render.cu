@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
     const double L = g.L;
     double t0 = 0.0, t1 = DBL_MAX;
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
+    for (int a = 0; a < 3; ++a) {  // grid.cpp:270-285
         const double box_lo = __dmul_rn(static_cast<double>(g.lo[a]), L);
         const double box_hi = __dmul_rn(static_cast<double>(g.hi[a] + 1), L);
         if (d[a] == 0.0) {
@@ -143,45 +143,49 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         t1 = smin(t1, smax(ta, tb));
     }
     if (!(t0 < t1)) return 0;
-    const double t_eps = __dmul_rn(1e-12, smax(1.0, fabs(t0)));
+    const double t_eps = __dmul_rn(1e-12, smax(1.0, fabs(t0)));  // grid.cpp:289-296
     const double ts = __dadd_rn(t0, t_eps);
-    int32_t b[3], inc[3];
-    double cross[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const double start = __dadd_rn(o[a], __dmul_rn(ts, d[a]));
-        int32_t v = static_cast<int32_t>(floor(__ddiv_rn(start, L)));
-        v = v < g.lo[a] ? g.lo[a] : (g.hi[a] < v ? g.hi[a] : v);  // std::clamp
-        b[a] = v;
-        inc[a] = d[a] > 0.0 ? 1 : -1;
-        cross[a] = d[a] == 0.0
-                       ? __longlong_as_double(0x7ff0000000000000ll)
-                       : __ddiv_rn(__dsub_rn(__dmul_rn(static_cast<double>(b[a] + (d[a] > 0.0 ? 1 : 0)), L),
-                                             o[a]),
-                                   d[a]);
-    }
+    const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+    // Scalar per-axis state (no local-memory arrays): block coordinate, step, crossing.
+    int32_t b0, b1, b2;
+    double c0, c1, c2;
+    auto start_block = [&](int a) {
+        const double st = __dadd_rn(o[a], __dmul_rn(ts, d[a]));
+        int32_t v = static_cast<int32_t>(floor(__ddiv_rn(st, L)));
+        return v < g.lo[a] ? g.lo[a] : (g.hi[a] < v ? g.hi[a] : v);  // std::clamp
+    };
+    auto crossing = [&](int a, int32_t bv) {  // grid.cpp:298-302, recomputed exactly
+        if (d[a] == 0.0) return kInf;
+        return __ddiv_rn(__dsub_rn(__dmul_rn(static_cast<double>(bv + (d[a] > 0.0 ? 1 : 0)), L), o[a]),
+                         d[a]);
+    };
+    b0 = start_block(0), b1 = start_block(1), b2 = start_block(2);
+    c0 = crossing(0, b0), c1 = crossing(1, b1), c2 = crossing(2, b2);
+    const int32_t s0 = d[0] > 0.0 ? 1 : -1, s1 = d[1] > 0.0 ? 1 : -1, s2 = d[2] > 0.0 ? 1 : -1;
+    // dense mode: occupancy bit index of (b0,b1,b2), updated incrementally per step
+    const int64_t dx = g.dim[0], dxy = static_cast<int64_t>(g.dim[0]) * g.dim[1];
+    int64_t cell = (static_cast<int64_t>(b2 - g.lo[2]) * g.dim[1] + (b1 - g.lo[1])) * dx + (b0 - g.lo[0]);
     const double half_step = __dmul_rn(0.5, step);
-    double t = t0, cursor = -__longlong_as_double(0x7ff0000000000000ll);
+    double t = t0, cursor = -kInf;
     bool open = false;
     uint32_t cnt = 0;
-    while (t < t1) {
+    while (t < t1) {  // grid.cpp:306-333
         double t_exit = t1;
         int axis = -1;
-#pragma unroll
-        for (int a = 0; a < 3; ++a)
-            if (cross[a] < t_exit) {
-                t_exit = cross[a];
-                axis = a;
-            }
-        const bool alloc = block_allocated(g, b[0], b[1], b[2]);
+        if (c0 < t_exit) t_exit = c0, axis = 0;
+        if (c1 < t_exit) t_exit = c1, axis = 1;
+        if (c2 < t_exit) t_exit = c2, axis = 2;
+        const bool alloc = g.use_dense
+                               ? ((__ldg(g.occ + (cell >> 5)) >> (cell & 31)) & 1u) != 0
+                               : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
         if (alloc && !open) {
             open = true;
-            if (cursor < t) cursor = __dadd_rn(t, half_step);
+            if (cursor < t) cursor = __dadd_rn(t, half_step);  // grid.cpp:345
         } else if (!alloc && open) {
             open = false;
         }
         if (alloc) {
-            while (cursor < t_exit && cnt < S) {
+            while (cursor < t_exit && cnt < S) {  // grid.cpp:346-349
                 emit(cnt, cursor);
                 ++cnt;
                 cursor = __dadd_rn(cursor, step);
@@ -189,12 +193,23 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
             if (cnt >= S) break;
         }
         if (axis < 0) break;
-        b[axis] += inc[axis];
         t = t_exit;
-        if (b[axis] < g.lo[axis] || b[axis] > g.hi[axis]) break;
-        cross[axis] = __ddiv_rn(
-            __dsub_rn(__dmul_rn(static_cast<double>(b[axis] + (d[axis] > 0.0 ? 1 : 0)), L), o[axis]),
-            d[axis]);
+        if (axis == 0) {
+            b0 += s0;
+            if (b0 < g.lo[0] || b0 > g.hi[0]) break;
+            cell += s0;
+            c0 = crossing(0, b0);
+        } else if (axis == 1) {
+            b1 += s1;
+            if (b1 < g.lo[1] || b1 > g.hi[1]) break;
+            cell += s1 * dx;
+            c1 = crossing(1, b1);
+        } else {
+            b2 += s2;
+            if (b2 < g.lo[2] || b2 > g.hi[2]) break;
+            cell += s2 * dxy;
+            c2 = crossing(2, b2);
+        }
     }
     return cnt;
 }
@@ -219,11 +234,15 @@ __global__ void __launch_bounds__(128) k_march(GridView g, const double* __restr
 
 // ---------------------------------------------------------------------------
 // Per-sample gather + interpolation (fp32 payload math, fp64 cell decision).
+// Corner c of the cell at base voxel v lies in block (v + bits(c)) >> 3; only axes with
+// local coordinate 7 cross a face (smask), and those corners take their block entry from
+// the per-block neighbour table -- no extra hash / dense-index lookups.
 // ---------------------------------------------------------------------------
 struct SampleVal {
     uint32_t gidx[8];
     float fx, fy, fz;
     float s, gx, gy, gz, r, gc, b;
+    uint32_t smask;
 };
 
 __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
@@ -233,33 +252,41 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double x = __dadd_rn(o[a], __dmul_rn(t, d[a]));
-        const double gg = __dmul_rn(x, g.inv_h);
+        const double gg = __dmul_rn(x, g.inv_h);  // grid.cpp:116-121
         const double fl = floor(gg);
         base[a] = static_cast<int>(fl);
         fr[a] = static_cast<float>(__dsub_rn(gg, fl));
     }
     v.fx = fr[0], v.fy = fr[1], v.fz = fr[2];
-    bool ok = true;
-    int32_t lbx = INT32_MIN, lby = 0, lbz = 0;
-    uint32_t le = kInvalid;
+    const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
+    const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
+    v.smask = (lx == 7 ? 1u : 0u) | (ly == 7 ? 2u : 0u) | (lz == 7 ? 4u : 0u);
+    bool ok = e0 != kInvalid;
+    const uint32_t blk0 = e0 & ~kFullBit;
+    // local index pieces of the two layers per axis
+    const uint32_t X[2] = {lx, (lx + 1) & 7}, Y[2] = {ly * 8, ((ly + 1) & 7) * 8},
+                   Z[2] = {lz * 64, ((lz + 1) & 7) * 64};
+    uint32_t full = e0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-        const int vx = base[0] + (c & 1), vy = base[1] + ((c >> 1) & 1), vz = base[2] + (c >> 2);
-        const int32_t bx = fdiv8(vx), by = fdiv8(vy), bz = fdiv8(vz);
-        if (bx != lbx || by != lby || bz != lbz) {
-            lbx = bx, lby = by, lbz = bz;
-            le = lookup_block(g, bx, by, bz);
-        }
-        const uint32_t local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
-        if (le == kInvalid) {
-            ok = false;
-            v.gidx[c] = 0;
-        } else {
-            ok = ok && voxel_valid(g, le, local);
-            v.gidx[c] = (le & ~kFullBit) * kVox + local;
+        const uint32_t k = static_cast<uint32_t>(c) & v.smask;
+        uint32_t ec = e0;
+        if (k && ok) ec = __ldg(g.nbr + static_cast<size_t>(blk0) * 8 + k);
+        ok = ok && ec != kInvalid;
+        full &= ec;
+        v.gidx[c] = (ec & ~kFullBit) * kVox + (X[c & 1] + Y[(c >> 1) & 1] + Z[c >> 2]);
+    }
+    if (ok && !(full & kFullBit)) {  // some corner block is partially observed
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const uint32_t gi = v.gidx[c];
+            ok = ok && ((__ldg(g.vmask + (gi >> 5)) >> (gi & 31)) & 1u);
         }
     }
-    if (!ok) return false;
+    if (!ok) {
+        v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
+        return false;
+    }
     float4 p[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + v.gidx[c]);
@@ -413,18 +440,14 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const d
         const float P0 = tau_base + excl, P1 = P0 + tau0;
         const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
         const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
-        if (ok0) {
-            acc[0] += w0 * v0.r, acc[1] += w0 * v0.gc, acc[2] += w0 * v0.b;
-            acc[3] += w0 * static_cast<float>(p.t0);
-            acc[4] += w0 * v0.gx, acc[5] += w0 * v0.gy, acc[6] += w0 * v0.gz;
-            acc[7] += w0;
-        }
-        if (ok1) {
-            acc[0] += w1 * v1.r, acc[1] += w1 * v1.gc, acc[2] += w1 * v1.b;
-            acc[3] += w1 * static_cast<float>(p.t1);
-            acc[4] += w1 * v1.gx, acc[5] += w1 * v1.gy, acc[6] += w1 * v1.gz;
-            acc[7] += w1;
-        }
+        acc[0] += w0 * v0.r + w1 * v1.r;
+        acc[1] += w0 * v0.gc + w1 * v1.gc;
+        acc[2] += w0 * v0.b + w1 * v1.b;
+        acc[3] += w0 * static_cast<float>(p.t0) + w1 * static_cast<float>(p.t1);
+        acc[4] += w0 * v0.gx + w1 * v1.gx;
+        acc[5] += w0 * v0.gy + w1 * v1.gy;
+        acc[6] += w0 * v0.gz + w1 * v1.gz;
+        acc[7] += w0 + w1;
         nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
         tau_base += __shfl_sync(kFull, incl, 31);
     }
@@ -462,15 +485,15 @@ __device__ __forceinline__ float4 corner_grad(const CornerCoef& k) {
     return make_float4(gs, w * k.wc0, w * k.wc1, w * k.wc2);
 }
 
+__device__ __forceinline__ void mark_block(const GridView& g, uint32_t blk) {
+    if (!g.active[blk]) g.active[blk] = 1;
+}
 __device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& v) {
-    uint32_t prev = kInvalid;
+    mark_block(g, v.gidx[0] >> 9);
+    if (v.smask) {  // corners in neighbour blocks: every other corner slot may differ
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const uint32_t blk = v.gidx[c] >> 9;
-        if (blk != prev) {
-            if (!g.active[blk]) g.active[blk] = 1;
-            prev = blk;
-        }
+        for (int c = 1; c < 8; ++c)
+            if (c & v.smask) mark_block(g, v.gidx[c] >> 9);
     }
 }
 

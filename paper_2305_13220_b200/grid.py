@@ -114,9 +114,15 @@ class SparseDenseGrid:
         check(self._lib.svr_grid_save_sdgv(self._h, str(path).encode()))
 
     def set_stream(self, stream) -> None:
-        """Launch on a CUDA stream (torch.cuda.Stream or raw handle); None = own stream."""
+        """Launch on a CUDA stream (torch.cuda.Stream or raw handle); None = own stream.
+
+        Torch's legacy default stream (handle 0) maps to cudaStreamLegacy so that device
+        inputs produced by torch on it are ordered before the library's kernels."""
+        if stream is None:
+            check(self._lib.svr_grid_set_stream(self._h, None))
+            return
         handle = getattr(stream, "cuda_stream", stream)
-        check(self._lib.svr_grid_set_stream(self._h, ctypes.c_void_p(handle or 0)))
+        check(self._lib.svr_grid_set_stream(self._h, ctypes.c_void_p(handle if handle else 1)))
 
     def synchronize(self) -> None:
         check(self._lib.svr_grid_synchronize(self._h))

@@ -131,6 +131,7 @@ def test_grad_zero_active_and_pack_roundtrip(case):
     import torch
 
     g = gpu_grid_from(case)
+    g.set_stream(torch.cuda.current_stream())
     g.grad_zero()
     g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
     g.render_backward(case["dC"], case["dD"], case["dN"])
@@ -176,6 +177,7 @@ def test_device_resident_path_matches_host_path(case):
     import torch
 
     g = gpu_grid_from(case)
+    g.set_stream(torch.cuda.current_stream())  # order after torch's H2D copies
     host = g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
     o = torch.from_numpy(case["o"]).cuda()
     d = torch.from_numpy(case["d"]).cuda()
