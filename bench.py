@@ -324,7 +324,11 @@ def run_ours(args, cfg, rank, world, local_rank):
             reduce_active_grads(grid, dev)  # K7 mask union + K8 NCCL all-reduce
         grid.grad_zero_active()
 
-    launches_per_step = 2 + 1 + 4 + (5 if world > 1 else 0)
+    # ours per step: k_ray_keys_dir, k_march, k_ray_keys, k_forward, k_backward,
+    # k_active_count/scan/write, k_grad_zero_active (+ k_active_* / pack / unpack for N > 1);
+    # plus 2 CUB radix sorts (5 library kernels each) that only reorder rays
+    launches_per_step = 9 + (5 if world > 1 else 0)
+    library_launches_per_step = 10
     for _ in range(max(args.warmup, 3)):
         step(False)
     torch.cuda.synchronize(dev)
@@ -437,6 +441,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                 "path": "SparseDenseGrid.render_forward/backward via C-ABI with pinned host buffers"},
         "gpu_launches": launches_per_step * args.steps,
+        "library_launches": {"cub_radix_sort": library_launches_per_step * args.steps},
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -103,7 +103,9 @@ int svr_grid_set_stream(svr_grid* g, void* cuda_stream);
 int svr_grid_synchronize(svr_grid* g);
 int svr_grid_get_info(svr_grid* g, svr_grid_info* out);
 int svr_grid_set_lookup(svr_grid* g, int32_t mode);
-/* Performance knobs (results are unaffected): "ray_sort" (0/1, Morton ray ordering),
+/* Performance knobs (results are unaffected): "ray_sort" (bit 1: order the march by origin +
+ * octahedral direction; bit 0: order forward/backward by the Morton code of each ray's
+ * first-sample block; default 3 = both),
  * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for). */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 

@@ -193,8 +193,10 @@ struct svr_grid {
     DevBuf ord_keys, ord_ids, ord_tmp;  // ray ordering (Morton key of the first sample block)
     uint32_t* ctx_order = nullptr;
     // tuning knobs (svr_grid_set_tuning)
-    bool ray_sort = true;
-    int fwd_min_blocks = 4;
+    // bit 1: order the march by origin + direction; bit 0: order forward/backward by the
+    // block of each ray's first sample (3 = both)
+    int ray_sort = 3;
+    int fwd_min_blocks = 3;
     int bwd_min_blocks = 3;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
@@ -424,7 +426,7 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
     g->capacity = capacity ? capacity : (1ull << 21);  // grid.hpp:107
     SVR_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     g->own_stream = true;
-    if (const char* e = std::getenv("SVR_RAY_SORT")) g->ray_sort = std::atoi(e) != 0;
+    if (const char* e = std::getenv("SVR_RAY_SORT")) g->ray_sort = std::atoi(e);
     g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
     SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
     SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
@@ -503,7 +505,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
     return guarded([&] {
         const std::string k = key ? key : "";
         if (k == "ray_sort") {
-            g->ray_sort = value != 0;
+            if (value < 0 || value > 3) throw Fail{SVR_ERR_CONFIG, "tuning: ray_sort is 0..3"};
+            g->ray_sort = static_cast<int>(value);
         } else if (k == "fwd_min_blocks") {
             g->fwd_min_blocks = static_cast<int>(value);
         } else if (k == "bwd_min_blocks") {
@@ -790,7 +793,7 @@ int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double 
         double* dt = st.out(t, nt);
         if (!dt && nt) dt = static_cast<double*>(st.alloc(8 * nt));
         double* dl = st.out(delta, nt);
-        svr_internal::launch_march(g->view(), dO, dD, n, step, max_samples, dc, dt, dl, g->stream);
+        svr_internal::launch_march(g->view(), dO, dD, n, nullptr, step, max_samples, dc, dt, dl, g->stream);
         st.finish();
     });
 }
@@ -829,20 +832,25 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
         float* e = st.out(wsum, n);
         if (n) {
             const GridView v = g->view();
-            svr_internal::launch_march(v, dO, dD, n, step, max_samples, g->counts.as<uint32_t>(),
-                                       g->tbuf.as<double>(), nullptr, g->stream);
             g->ctx_order = nullptr;
-            if (g->ray_sort && n > 1) {
+            const bool sort = g->ray_sort != 0 && n > 1;
+            if (sort) {
                 g->ord_keys.ensure(8 * n);
                 g->ord_ids.ensure(8 * n);
-                const size_t tb = svr_internal::ray_order_tmp_bytes(n);
-                g->ord_tmp.ensure(std::max<size_t>(tb, 16));
-                uint32_t* k = g->ord_keys.as<uint32_t>();
-                uint32_t* id = g->ord_ids.as<uint32_t>();
+                g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
+            }
+            uint32_t* k = g->ord_keys.as<uint32_t>();
+            uint32_t* id = g->ord_ids.as<uint32_t>();
+            if (sort && (g->ray_sort & 2))  // pre-march: origin + direction
+                svr_internal::launch_ray_order(v, dO, dD, n, nullptr, nullptr, max_samples, k, id, k + n,
+                                               id + n, g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order,
+                                               g->stream);
+            svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples,
+                                       g->counts.as<uint32_t>(), g->tbuf.as<double>(), nullptr, g->stream);
+            if (sort && (g->ray_sort & 1))  // post-march: first-sample block
                 svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
                                                max_samples, k, id, k + n, id + n, g->ord_tmp.p,
                                                g->ord_tmp.bytes, &g->ctx_order, g->stream);
-            }
             svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
                                                 g->tbuf.as<double>(), max_samples, step, beta, a, b,
                                                 c, e, nullptr, g->stream, g->fwd_min_blocks);

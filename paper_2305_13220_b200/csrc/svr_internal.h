@@ -23,8 +23,8 @@ struct Status {
 void launch_query(const svr_dev::GridView& g, const double* x, uint64_t n, double* sdf,
                   double* grad, double* rgb, double* logits, uint8_t* valid, cudaStream_t s);
 void launch_march(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
-                  double step, uint32_t max_samples, uint32_t* counts, double* t, double* delta,
-                  cudaStream_t s);
+                  const uint32_t* order, double step, uint32_t max_samples, uint32_t* counts,
+                  double* t, double* delta, cudaStream_t s);
 void launch_render_forward(const svr_dev::GridView& g, const double* o, const double* d,
                            uint64_t n, const uint32_t* order, const uint32_t* counts,
                            const double* t, uint32_t S, double step, double beta, float* rgb,
@@ -35,8 +35,9 @@ void launch_render_backward(const svr_dev::GridView& g, const double* o, const d
                             const double* t, uint32_t S, double step, double beta,
                             const float* d_rgb, const float* d_depth, const float* d_normal,
                             cudaStream_t s, int min_blocks);
-// Sort rays by the Morton code of their first sample's block; *sorted_ids points into
-// ids or ids_alt.
+// Sort rays for locality; *sorted_ids points into ids or ids_alt.  counts != NULL: key =
+// Morton code of the first sample's block (after the march); counts == NULL: key = origin
+// hash + octahedral-direction Morton code (before the march).
 void launch_ray_order(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
                       const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,

@@ -162,9 +162,11 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
     b0 = start_block(0), b1 = start_block(1), b2 = start_block(2);
     c0 = crossing(0, b0), c1 = crossing(1, b1), c2 = crossing(2, b2);
     const int32_t s0 = d[0] > 0.0 ? 1 : -1, s1 = d[1] > 0.0 ? 1 : -1, s2 = d[2] > 0.0 ? 1 : -1;
+    const int32_t p0 = d[0] > 0.0 ? 1 : 0, p1 = d[1] > 0.0 ? 1 : 0, p2 = d[2] > 0.0 ? 1 : 0;
     // dense mode: occupancy bit index of (b0,b1,b2), updated incrementally per step
-    const int64_t dx = g.dim[0], dxy = static_cast<int64_t>(g.dim[0]) * g.dim[1];
-    int64_t cell = (static_cast<int64_t>(b2 - g.lo[2]) * g.dim[1] + (b1 - g.lo[1])) * dx + (b0 - g.lo[0]);
+    // (the dense index is only built when the AABB has <= 2^28 cells)
+    const int32_t st0 = s0, st1 = s1 * g.dim[0], st2 = s2 * g.dim[0] * g.dim[1];
+    int32_t cell = ((b2 - g.lo[2]) * g.dim[1] + (b1 - g.lo[1])) * g.dim[0] + (b0 - g.lo[0]);
     const double half_step = __dmul_rn(0.5, step);
     double t = t0, cursor = -kInf;
     bool open = false;
@@ -176,7 +178,7 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         if (c1 < t_exit) t_exit = c1, axis = 1;
         if (c2 < t_exit) t_exit = c2, axis = 2;
         const bool alloc = g.use_dense
-                               ? ((__ldg(g.occ + (cell >> 5)) >> (cell & 31)) & 1u) != 0
+                               ? ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0
                                : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
         if (alloc && !open) {
             open = true;
@@ -194,32 +196,31 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         }
         if (axis < 0) break;
         t = t_exit;
-        if (axis == 0) {
-            b0 += s0;
-            if (b0 < g.lo[0] || b0 > g.hi[0]) break;
-            cell += s0;
-            c0 = crossing(0, b0);
-        } else if (axis == 1) {
-            b1 += s1;
-            if (b1 < g.lo[1] || b1 > g.hi[1]) break;
-            cell += s1 * dx;
-            c1 = crossing(1, b1);
-        } else {
-            b2 += s2;
-            if (b2 < g.lo[2] || b2 > g.hi[2]) break;
-            cell += s2 * dxy;
-            c2 = crossing(2, b2);
-        }
+        // step the chosen axis; one exactly-rounded division for its next crossing
+        const bool a0 = axis == 0, a1 = axis == 1;
+        const int32_t nb = (a0 ? b0 : (a1 ? b1 : b2)) + (a0 ? s0 : (a1 ? s1 : s2));
+        const int32_t lo_a = a0 ? g.lo[0] : (a1 ? g.lo[1] : g.lo[2]);
+        const int32_t hi_a = a0 ? g.hi[0] : (a1 ? g.hi[1] : g.hi[2]);
+        if (nb < lo_a || nb > hi_a) break;
+        cell += a0 ? st0 : (a1 ? st1 : st2);
+        const double oa = a0 ? o[0] : (a1 ? o[1] : o[2]);
+        const double da = a0 ? d[0] : (a1 ? d[1] : d[2]);
+        const int32_t pa = a0 ? p0 : (a1 ? p1 : p2);
+        const double c = __ddiv_rn(__dsub_rn(__dmul_rn(static_cast<double>(nb + pa), L), oa), da);
+        if (a0) b0 = nb, c0 = c;
+        else if (a1) b1 = nb, c1 = c;
+        else b2 = nb, c2 = c;
     }
     return cnt;
 }
 
 __global__ void __launch_bounds__(128) k_march(GridView g, const double* __restrict__ O,
                                                const double* __restrict__ D, uint64_t n,
-                                               double step, uint32_t S, uint32_t* counts,
-                                               double* T, double* delta) {
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= n) return;
+                                               const uint32_t* __restrict__ order, double step,
+                                               uint32_t S, uint32_t* counts, double* T, double* delta) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t r = order ? order[i] : i;
     const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
     const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
     double* tr = T + r * S;
@@ -244,6 +245,19 @@ struct SampleVal {
     float s, gx, gy, gz, r, gc, b;
     uint32_t smask;
 };
+
+__device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
+                                            double t, SampleVal& v);
+
+// A lane slot past the ray's sample count: well-defined zeros (accumulated with w = 0).
+__device__ __forceinline__ bool eval_slot(const GridView& g, const double o[3], const double d[3],
+                                          bool in, double t, SampleVal& v) {
+    if (in) return eval_sample(g, o, d, t, v);
+    v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
+    v.fx = v.fy = v.fz = 0.f;
+    v.smask = 0;
+    return false;
+}
 
 __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
                                             double t, SampleVal& v) {
@@ -403,6 +417,34 @@ __global__ void __launch_bounds__(256) k_ray_keys(GridView g, const double* __re
     ids[r] = static_cast<uint32_t>(r);
 }
 
+// Pre-march ordering: 10-bit hash of the origin (1 mm cells) above a 22-bit Morton code of
+// the octahedral direction, so rays from one camera with nearby pixels march together.
+__global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__ O,
+                                                      const double* __restrict__ D, uint64_t n,
+                                                      uint32_t* keys, uint32_t* ids) {
+    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const double dx = D[3 * r], dy = D[3 * r + 1], dz = D[3 * r + 2];
+    const double l1 = fabs(dx) + fabs(dy) + fabs(dz);
+    double u = dx / l1, v = dy / l1;
+    if (dz < 0.0) {
+        const double uu = (1.0 - fabs(v)) * (u >= 0.0 ? 1.0 : -1.0);
+        const double vv = (1.0 - fabs(u)) * (v >= 0.0 ? 1.0 : -1.0);
+        u = uu, v = vv;
+    }
+    const uint32_t qu = min(2047u, static_cast<uint32_t>((u * 0.5 + 0.5) * 2048.0));
+    const uint32_t qv = min(2047u, static_cast<uint32_t>((v * 0.5 + 0.5) * 2048.0));
+    uint32_t m = 0;
+#pragma unroll
+    for (int b = 0; b < 11; ++b) m |= (((qu >> b) & 1u) << (2 * b)) | (((qv >> b) & 1u) << (2 * b + 1));
+    unsigned long long h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+        h = mix64(h ^ static_cast<unsigned long long>(llrint(O[3 * r + a] * 1000.0)));
+    keys[r] = (static_cast<uint32_t>(h >> 54) << 22) | m;
+    ids[r] = static_cast<uint32_t>(r);
+}
+
 // ---------------------------------------------------------------------------
 // K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
 // chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
@@ -430,8 +472,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const d
     for (uint32_t base = 0; base < cnt; base += 64) {
         const PairT p = load_pair(tr, cnt, base, lane, step);
         SampleVal v0, v1;
-        const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
-        const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+        const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
+        const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
         const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
         const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
         const float incl = warp_incl_scan(tau0 + tau1, lane);
@@ -549,8 +591,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const PairT p = load_pair(tr, cnt, ch * 64, lane, step);
             SampleVal v0, v1;
-            const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
-            const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+            const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
+            const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
             const float tau = (ok0 ? density(v0.s, ib) * p.d0 : 0.f) +
                               (ok1 ? density(v1.s, ib) * p.d1 : 0.f);
             const float incl = warp_incl_scan(tau, lane);
@@ -564,8 +606,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
         const float tau_base = __shfl_sync(kFull, my_prefix, ch & 31);
         const PairT p = load_pair(tr, cnt, static_cast<uint32_t>(ch) * 64, lane, step);
         SampleVal v0, v1;
-        const bool ok0 = p.in0 && eval_sample(g, o, d, p.t0, v0);
-        const bool ok1 = p.in1 && eval_sample(g, o, d, p.t1, v1);
+        const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
+        const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
         const float sg0 = ok0 ? density(v0.s, ib) : 0.f, sg1 = ok1 ? density(v1.s, ib) : 0.f;
         const float tau0 = sg0 * p.d0, tau1 = sg1 * p.d1;
         const float incl = warp_incl_scan(tau0 + tau1, lane);
@@ -623,10 +665,11 @@ void launch_query(const GridView& g, const double* x, uint64_t n, double* sdf, d
     k_query<<<grid_for(n, 256), 256, 0, s>>>(g, x, n, sdf, grad, rgb, logits, valid);
 }
 
-void launch_march(const GridView& g, const double* o, const double* d, uint64_t n, double step,
-                  uint32_t S, uint32_t* counts, double* t, double* delta, cudaStream_t s) {
+void launch_march(const GridView& g, const double* o, const double* d, uint64_t n,
+                  const uint32_t* order, double step, uint32_t S, uint32_t* counts, double* t,
+                  double* delta, cudaStream_t s) {
     if (!n) return;
-    k_march<<<grid_for(n, 128), 128, 0, s>>>(g, o, d, n, step, S, counts, t, delta);
+    k_march<<<grid_for(n, 128), 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta);
 }
 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
@@ -672,17 +715,20 @@ void launch_ray_order(const GridView& g, const double* o, const double* d, uint6
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
                       size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s) {
     if (!n) return;
-    k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids);
+    if (counts)  // post-march: first-sample block
+        k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids);
+    else         // pre-march: origin + direction
+        k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
     cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
     size_t bytes = tmp_bytes;
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, 30, s);
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, 32, s);
     *sorted_ids = vb.Current();
 }
 
 size_t ray_order_tmp_bytes(uint64_t n) {
     size_t bytes = 0;
     cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int>(n), 0, 30);
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int>(n), 0, 32);
     return bytes;
 }
 
