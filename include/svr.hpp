@@ -1,0 +1,208 @@
+// svr.hpp -- header-only C++ host mirror of the reference grid / renderer interface over
+// the C-ABI in svr.h.  Names, argument meaning and error behaviour follow the reference
+// (/root/reference/proj/src/core/grid.hpp:100-223, allocation.hpp:13-29, grid_io.hpp:14-15,
+// errors.hpp:8-31; renderer ops per SPEC.md:268-319), so code written against
+// svr::SparseDenseGrid switches to the B200 build by changing the include and namespace:
+//
+//     #include "svr.hpp"                       // instead of "core/grid.hpp" + friends
+//     svr::b200::SparseDenseGrid grid(0.015, 8, 4);
+//     svr::b200::allocate_for_frames(grid, frames, nullptr, 2);
+//     grid.render_forward(o, d, n, step, 64, beta, out);  grid.render_backward(dC, dD, dN);
+//
+// Status codes become the reference's exception types.  Arrays are plain pointers (host or
+// device), so there is no Eigen in the interface.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "svr.h"
+
+namespace svr::b200 {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ConfigError : Error {  // errors.hpp:12-15
+    using Error::Error;
+};
+struct DataError : Error {  // errors.hpp:17-20
+    using Error::Error;
+};
+struct DivergedError : Error {  // errors.hpp:22-25
+    using Error::Error;
+};
+struct CapacityError : Error {  // errors.hpp:27-31
+    CapacityError(const std::string& what, std::size_t unallocated)
+        : Error(what), unallocated_blocks(unallocated) {}
+    std::size_t unallocated_blocks = 0;
+};
+struct CudaError : Error {
+    using Error::Error;
+};
+
+inline void check(int status, const svr_alloc_report* rep = nullptr) {
+    if (status == SVR_OK) return;
+    const std::string msg = svr_last_error();
+    switch (status) {
+        case SVR_ERR_CONFIG: throw ConfigError(msg);
+        case SVR_ERR_DATA: throw DataError(msg);
+        case SVR_ERR_DIVERGED: throw DivergedError(msg);
+        case SVR_ERR_CAPACITY: throw CapacityError(msg, rep ? rep->unallocated : 0);
+        default: throw CudaError(msg);
+    }
+}
+
+struct BlockCoord {  // grid.hpp:11-14
+    std::int32_t x = 0, y = 0, z = 0;
+};
+
+using AllocationReport = svr_alloc_report;  // allocation.hpp:13-17
+using Camera = svr_camera;                  // camera.hpp:16-29 (row-major R, camera-to-world)
+
+struct RenderOutputs {  // render_ray outputs per ray
+    float* rgb = nullptr;     // [n][3]
+    float* depth = nullptr;   // [n]
+    float* normal = nullptr;  // [n][3], world frame, un-normalised
+    float* wsum = nullptr;    // [n]
+    std::uint32_t* n_samples = nullptr;
+};
+
+class SparseDenseGrid {
+public:
+    static constexpr std::uint32_t kInvalidBlock = SVR_INVALID_BLOCK;
+    static constexpr std::size_t kDefaultCapacity = std::size_t(1) << 21;
+
+    SparseDenseGrid(double voxel_size, int block_res, int label_channels,
+                    std::size_t capacity = kDefaultCapacity, int device = 0) {
+        check(svr_grid_create(voxel_size, block_res, label_channels, capacity, device, &g_));
+    }
+    explicit SparseDenseGrid(svr_grid* adopt) : g_(adopt) {}
+    SparseDenseGrid(const SparseDenseGrid&) = delete;
+    SparseDenseGrid& operator=(const SparseDenseGrid&) = delete;
+    SparseDenseGrid(SparseDenseGrid&& o) noexcept : g_(std::exchange(o.g_, nullptr)) {}
+    ~SparseDenseGrid() {
+        if (g_) svr_grid_destroy(g_);
+    }
+
+    svr_grid* handle() const { return g_; }
+    svr_grid_info info() const {
+        svr_grid_info i{};
+        check(svr_grid_get_info(g_, &i));
+        return i;
+    }
+    double voxel_size() const { return info().voxel_size; }
+    int block_res() const { return info().block_res; }
+    int label_channels() const { return info().label_channels; }
+    double block_extent() const { return voxel_size() * block_res(); }
+    std::size_t capacity() const { return info().capacity; }
+    std::size_t block_count() const { return info().block_count; }
+    bool empty() const { return block_count() == 0; }
+
+    // find_block / allocate_block (grid.hpp:156-159)
+    std::uint32_t find_block(const BlockCoord& c) const {
+        std::uint32_t idx = kInvalidBlock;
+        check(svr_grid_find(g_, &c.x, 1, &idx));
+        return idx;
+    }
+    std::uint32_t allocate_block(const BlockCoord& c) {
+        std::uint32_t idx = kInvalidBlock;
+        check(svr_grid_allocate_blocks(g_, &c.x, 1, &idx));
+        return idx;
+    }
+    std::vector<BlockCoord> coords() const {
+        std::vector<BlockCoord> out(block_count());
+        if (!out.empty()) check(svr_grid_coords(g_, &out[0].x));
+        return out;
+    }
+
+    // payload in the reference's VoxelBlock layout (grid.hpp:62-66)
+    void set_payload(std::uint32_t first, std::uint32_t n, const float* sdf, const float* weight,
+                     const float* rgb, const float* logits) {
+        check(svr_grid_set_payload(g_, first, n, sdf, weight, rgb, logits));
+    }
+    void get_payload(std::uint32_t first, std::uint32_t n, float* sdf, float* weight, float* rgb,
+                     float* logits) const {
+        check(svr_grid_get_payload(g_, first, n, sdf, weight, rgb, logits));
+    }
+
+    // query_sdf / query_sdf_with_gradient (grid.hpp:177-179), batched; fp64 like CornerCacheD
+    bool query_sdf_with_gradient(const double x[3], double& sdf, double grad[3]) const {
+        std::uint8_t valid = 0;
+        check(svr_query(g_, x, 1, &sdf, grad, nullptr, nullptr, &valid));
+        return valid != 0;
+    }
+    bool query_sdf(const double x[3], double& sdf) const {
+        std::uint8_t valid = 0;
+        check(svr_query(g_, x, 1, &sdf, nullptr, nullptr, nullptr, &valid));
+        return valid != 0;
+    }
+    void query(const double* x, std::size_t n, double* sdf, double* grad, double* rgb,
+               double* logits, std::uint8_t* valid) const {
+        check(svr_query(g_, x, n, sdf, grad, rgb, logits, valid));
+    }
+
+    // march_ray (grid.hpp:190-198), batched
+    void march(const double* o, const double* d, std::size_t n, double step,
+               std::uint32_t max_samples, std::uint32_t* counts, double* t, double* delta) const {
+        check(svr_march(g_, o, d, n, step, max_samples, counts, t, delta));
+    }
+
+    // renderer
+    void render_forward(const double* o, const double* d, std::size_t n, double step,
+                        std::uint32_t max_samples, double beta, const RenderOutputs& out) {
+        check(svr_render_forward(g_, o, d, n, step, max_samples, beta, out.rgb, out.depth, out.normal,
+                                 out.wsum, out.n_samples));
+    }
+    void render_backward(const float* d_rgb, const float* d_depth, const float* d_normal) {
+        check(svr_render_backward(g_, d_rgb, d_depth, d_normal));
+    }
+    void zero_grad() { check(svr_grad_zero(g_)); }
+    void grads(float* g_sdf, float* g_rgb) const { check(svr_grad_get(g_, g_sdf, g_rgb)); }
+    std::vector<std::uint32_t> active_blocks() const {
+        std::vector<std::uint32_t> list(block_count() ? block_count() : 1);
+        std::uint64_t count = 0;
+        check(svr_active_blocks(g_, nullptr, list.data(), &count));
+        list.resize(count);
+        return list;
+    }
+
+    void set_stream(void* cuda_stream) { check(svr_grid_set_stream(g_, cuda_stream)); }
+    void synchronize() const { check(svr_grid_synchronize(g_)); }
+
+private:
+    svr_grid* g_ = nullptr;
+};
+
+// allocate_for_points / allocate_for_frames (allocation.hpp:22-29)
+inline AllocationReport allocate_for_points(SparseDenseGrid& grid, const double* xyz, std::size_t n,
+                                            int dilation) {
+    AllocationReport r{};
+    check(svr_grid_activate_points(grid.handle(), xyz, n, dilation, &r), &r);
+    return r;
+}
+inline AllocationReport allocate_for_frames(SparseDenseGrid& grid, const float* depth,
+                                            const Camera* cams, std::uint32_t n_frames,
+                                            const double* scales, int sf_rows, int sf_cols,
+                                            int dilation) {
+    AllocationReport r{};
+    check(svr_grid_activate_depth(grid.handle(), depth, cams, n_frames, scales, sf_rows, sf_cols,
+                                  dilation, &r),
+          &r);
+    return r;
+}
+
+// save_grid / load_grid (grid_io.hpp:14-15)
+inline void save_grid(const SparseDenseGrid& grid, const std::string& path) {
+    check(svr_grid_save_sdgv(grid.handle(), path.c_str()));
+}
+inline SparseDenseGrid load_grid(const std::string& path, int device = 0) {
+    svr_grid* g = nullptr;
+    check(svr_grid_load_sdgv(path.c_str(), device, &g));
+    return SparseDenseGrid(g);
+}
+
+}  // namespace svr::b200
