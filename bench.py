@@ -218,11 +218,13 @@ def run_reference(args, cfg, rank, world):
         render = lambda n: (g.render_forward(o[:n], d[:n], cfg["h"] / 2, cfg["max_samples"], 2 * cfg["h"]),  # noqa: E731
                             g.render_backward(o[:n], d[:n], cfg["h"] / 2, cfg["max_samples"], 2 * cfg["h"],
                                               dC[:n], dD[:n], dN[:n]))
-    # size one step's ray sample so a step takes ~3 s of host time
+    # size one step's ray sample so a step takes ~3 s of host time (after a first call
+    # that allocates the reference's gradient shadow buffers)
+    render(1024)
     t0 = time.perf_counter()
-    f, _ = render(1024)
+    f, _ = render(8192)
     dt = time.perf_counter() - t0
-    n = int(min(len(o), max(1024, 1024 * 3.0 / max(dt, 1e-3))))
+    n = int(min(len(o), max(8192, 8192 * 3.0 / max(dt, 1e-3))))
     for _ in range(args.warmup):
         render(n)
     times, nvalid = [], 0
