@@ -106,7 +106,8 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
 /* Performance knobs (results are unaffected): "ray_sort" (bit 1: order the march by origin +
  * octahedral direction; bit 0: order forward/backward by the Morton code of each ray's
  * first-sample block; default 3 = both),
- * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for). */
+ * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for),
+ * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather). */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 
 /* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */

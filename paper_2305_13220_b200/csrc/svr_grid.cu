@@ -191,12 +191,18 @@ struct svr_grid {
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
     DevBuf ord_keys, ord_ids, ord_tmp;  // ray ordering (Morton key of the first sample block)
+    DevBuf rec;                         // per-sample forward records for the backward
+    bool ctx_rec = false;
     uint32_t* ctx_order = nullptr;
     // tuning knobs (svr_grid_set_tuning)
     // bit 1: order the march by origin + direction; bit 0: order forward/backward by the
     // block of each ray's first sample (3 = both)
     int ray_sort = 3;
     int fwd_min_blocks = 3;
+    bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
+    bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
+    int pipe_min_blocks = 3;
+    int num_sms = 148;
     int bwd_min_blocks = 3;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
@@ -427,6 +433,7 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
     SVR_CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     g->own_stream = true;
     if (const char* e = std::getenv("SVR_RAY_SORT")) g->ray_sort = std::atoi(e);
+    SVR_CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
     g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
     SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
     SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
@@ -509,6 +516,12 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->ray_sort = static_cast<int>(value);
         } else if (k == "fwd_min_blocks") {
             g->fwd_min_blocks = static_cast<int>(value);
+        } else if (k == "bwd_pipe") {
+            g->bwd_pipe = value != 0;
+        } else if (k == "pipe_min_blocks") {
+            g->pipe_min_blocks = static_cast<int>(value);
+        } else if (k == "records") {
+            g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
         } else {
@@ -851,9 +864,13 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
                 svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
                                                max_samples, k, id, k + n, id + n, g->ord_tmp.p,
                                                g->ord_tmp.bytes, &g->ctx_order, g->stream);
+            g->ctx_rec = g->use_records;
+            if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
             svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
                                                 g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                c, e, nullptr, g->stream, g->fwd_min_blocks);
+                                                c, e, nullptr,
+                                                g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream,
+                                                g->fwd_min_blocks);
             if (n_samples) {
                 uint32_t* ns = st.out(n_samples, n);
                 SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));
@@ -882,10 +899,19 @@ int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, c
         const float* a = st.in(d_rgb, 3 * n);
         const float* b = st.in(d_depth, n);
         const float* c = st.in(d_normal, 3 * n);
+        const bool piped =
+            g->bwd_pipe && g->ctx_rec &&
+            svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
+                                                      g->counts.as<uint32_t>(), g->tbuf.as<double>(),
+                                                      g->ctx_S, g->ctx_step, g->ctx_beta, a, b, c,
+                                                      g->rec.as<float4>(), g->stream,
+                                                      g->pipe_min_blocks, g->num_sms);
+        if (!piped)
         svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                              g->counts.as<uint32_t>(),
                                              g->tbuf.as<double>(), g->ctx_S, g->ctx_step, g->ctx_beta,
-                                             a, b, c, g->stream, g->bwd_min_blocks);
+                                             a, b, c, g->ctx_rec ? g->rec.as<float4>() : nullptr,
+                                             g->stream, g->bwd_min_blocks);
         st.finish();
     });
 }
@@ -907,8 +933,8 @@ int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
             svr_internal::launch_render_forward(g->view(), g->ctx_o, g->ctx_d, g->ctx_n, g->ctx_order,
                                                 g->counts.as<uint32_t>(), g->tbuf.as<double>(),
                                                 g->ctx_S, g->ctx_step, g->ctx_beta, nullptr, nullptr,
-                                                nullptr, nullptr, vc.as<unsigned long long>(), g->stream,
-                                                g->fwd_min_blocks);
+                                                nullptr, nullptr, vc.as<unsigned long long>(), nullptr,
+                                                g->stream, g->fwd_min_blocks);
             SVR_LAUNCHED();
             unsigned long long v = 0;
             SVR_CK(cudaMemcpyAsync(&v, vc.p, 8, cudaMemcpyDeviceToHost, g->stream));

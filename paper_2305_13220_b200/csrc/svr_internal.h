@@ -29,12 +29,13 @@ void launch_render_forward(const svr_dev::GridView& g, const double* o, const do
                            uint64_t n, const uint32_t* order, const uint32_t* counts,
                            const double* t, uint32_t S, double step, double beta, float* rgb,
                            float* depth, float* normal, float* wsum,
-                           unsigned long long* valid_counter, cudaStream_t s, int min_blocks);
+                           unsigned long long* valid_counter, float4* rec, cudaStream_t s,
+                           int min_blocks);
 void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
                             uint64_t n, const uint32_t* order, const uint32_t* counts,
                             const double* t, uint32_t S, double step, double beta,
                             const float* d_rgb, const float* d_depth, const float* d_normal,
-                            cudaStream_t s, int min_blocks);
+                            const float4* rec, cudaStream_t s, int min_blocks);
 // Sort rays for locality; *sorted_ids points into ids or ids_alt.  counts != NULL: key =
 // Morton code of the first sample's block (after the march); counts == NULL: key = origin
 // hash + octahedral-direction Morton code (before the march).
@@ -43,6 +44,12 @@ void launch_ray_order(const svr_dev::GridView& g, const double* o, const double*
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
                       size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s);
 size_t ray_order_tmp_bytes(uint64_t n);
+// Pipelined backward (records, max_samples <= 64, even); returns false if not applicable.
+bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
+                                 uint64_t n, const uint32_t* order, const uint32_t* counts,
+                                 const double* t, uint32_t S, double step, double beta,
+                                 const float* d_rgb, const float* d_depth, const float* d_normal,
+                                 const float4* rec, cudaStream_t s, int min_blocks, int num_sms);
 
 // Launchers (svr_activate.cu)
 struct KeySet {

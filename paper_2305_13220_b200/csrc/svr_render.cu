@@ -244,40 +244,42 @@ struct SampleVal {
     float fx, fy, fz;
     float s, gx, gy, gz, r, gc, b;
     uint32_t smask;
+    uint32_t e0;  // block entry of the base voxel (kInvalid: invalid sample)
 };
 
-__device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
-                                            double t, SampleVal& v);
-
-// A lane slot past the ray's sample count: well-defined zeros (accumulated with w = 0).
-__device__ __forceinline__ bool eval_slot(const GridView& g, const double o[3], const double d[3],
-                                          bool in, double t, SampleVal& v) {
-    if (in) return eval_sample(g, o, d, t, v);
+__device__ __forceinline__ void zero_sample(SampleVal& v) {
     v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
     v.fx = v.fy = v.fz = 0.f;
     v.smask = 0;
-    return false;
+    v.e0 = kInvalid;
 }
 
-__device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
-                                            double t, SampleVal& v) {
-    int base[3];
+// fp64 cell decision: x = o + t d, g = x * (1/h), base = floor(g) (grid.cpp:116-121).
+__device__ __forceinline__ void cell_geom(const GridView& g, const double o[3], const double d[3],
+                                          double t, int base[3], SampleVal& v) {
     float fr[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         const double x = __dadd_rn(o[a], __dmul_rn(t, d[a]));
-        const double gg = __dmul_rn(x, g.inv_h);  // grid.cpp:116-121
+        const double gg = __dmul_rn(x, g.inv_h);
         const double fl = floor(gg);
         base[a] = static_cast<int>(fl);
         fr[a] = static_cast<float>(__dsub_rn(gg, fl));
     }
     v.fx = fr[0], v.fy = fr[1], v.fz = fr[2];
     const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
-    const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
     v.smask = (lx == 7 ? 1u : 0u) | (ly == 7 ? 2u : 0u) | (lz == 7 ? 4u : 0u);
+}
+
+// Corner c of the cell lies in block (base + bits(c)) >> 3; only axes with local
+// coordinate 7 cross a face (smask), and those corners take their block entry from the
+// per-block neighbour table.  kCheck: verify presence + validity (weight > 0).
+template <bool kCheck>
+__device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3], uint32_t e0,
+                                             SampleVal& v) {
+    const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
     bool ok = e0 != kInvalid;
     const uint32_t blk0 = e0 & ~kFullBit;
-    // local index pieces of the two layers per axis
     const uint32_t X[2] = {lx, (lx + 1) & 7}, Y[2] = {ly * 8, ((ly + 1) & 7) * 8},
                    Z[2] = {lz * 64, ((lz + 1) & 7) * 64};
     uint32_t full = e0;
@@ -286,21 +288,33 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
         const uint32_t k = static_cast<uint32_t>(c) & v.smask;
         uint32_t ec = e0;
         if (k && ok) ec = __ldg(g.nbr + static_cast<size_t>(blk0) * 8 + k);
-        ok = ok && ec != kInvalid;
+        if (kCheck) ok = ok && ec != kInvalid;
         full &= ec;
         v.gidx[c] = (ec & ~kFullBit) * kVox + (X[c & 1] + Y[(c >> 1) & 1] + Z[c >> 2]);
     }
-    if (ok && !(full & kFullBit)) {  // some corner block is partially observed
+    if (kCheck && ok && !(full & kFullBit)) {  // some corner block is partially observed
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const uint32_t gi = v.gidx[c];
             ok = ok && ((__ldg(g.vmask + (gi >> 5)) >> (gi & 31)) & 1u);
         }
     }
+    return ok;
+}
+
+// Full gather + trilinear interpolation of sdf, grad(sdf) and rgb (fp32 payload math).
+__device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
+                                            double t, SampleVal& v) {
+    int base[3];
+    cell_geom(g, o, d, t, base, v);
+    const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
+    const bool ok = corner_addrs<true>(g, base, e0, v);
     if (!ok) {
         v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
+        v.e0 = kInvalid;
         return false;
     }
+    v.e0 = e0;
     float4 p[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + v.gidx[c]);
@@ -323,6 +337,47 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
                  (x0 * z1) * (p[6].x - p[4].x) + (x1 * z1) * (p[7].x - p[5].x));
     v.gz = ih * ((x0 * y0) * (p[4].x - p[0].x) + (x1 * y0) * (p[5].x - p[1].x) +
                  (x0 * y1) * (p[6].x - p[2].x) + (x1 * y1) * (p[7].x - p[3].x));
+    return true;
+}
+
+// A lane slot past the ray's sample count: well-defined zeros (accumulated with w = 0).
+__device__ __forceinline__ bool eval_slot(const GridView& g, const double o[3], const double d[3],
+                                          bool in, double t, SampleVal& v) {
+    if (in) return eval_sample(g, o, d, t, v);
+    zero_sample(v);
+    return false;
+}
+
+// Per-sample record the forward leaves for the backward (32 B, two float4):
+//   {sdf, r, g, b}, {d sdf/dx, d sdf/dy, d sdf/dz, bits(block entry of the base voxel)}.
+// The backward re-derives the cell geometry from t (fp64, identical decision) and the
+// corner addresses from the entry + neighbour table: no dense-index lookup, no payload.
+__device__ __forceinline__ void store_record(float4* rec, const SampleVal& v) {
+    rec[0] = make_float4(v.s, v.r, v.gc, v.b);
+    rec[1] = make_float4(v.gx, v.gy, v.gz, __uint_as_float(v.e0));
+}
+
+// `rec` may point to global memory (k_backward) or shared memory (k_backward_pipe):
+// generic loads only.
+__device__ __forceinline__ bool eval_from_record(const GridView& g, const double o[3],
+                                                 const double d[3], bool in, double t,
+                                                 const float4* rec, SampleVal& v) {
+    if (!in) {
+        zero_sample(v);
+        return false;
+    }
+    const float4 a = rec[0], b = rec[1];
+    const uint32_t e0 = __float_as_uint(b.w);
+    if (e0 == kInvalid) {
+        zero_sample(v);
+        return false;
+    }
+    int base[3];
+    cell_geom(g, o, d, t, base, v);
+    corner_addrs<false>(g, base, e0, v);
+    v.e0 = e0;
+    v.s = a.x, v.r = a.y, v.gc = a.z, v.b = a.w;
+    v.gx = b.x, v.gy = b.y, v.gz = b.z;
     return true;
 }
 
@@ -457,7 +512,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const d
                                                     const double* __restrict__ T, uint32_t S,
                                                     double step, float ib, float* rgb, float* depth,
                                                     float* normal, float* wsum,
-                                                    unsigned long long* valid_counter) {
+                                                    unsigned long long* valid_counter, float4* rec) {
     const int lane = threadIdx.x & 31;
     const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
@@ -474,6 +529,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const d
         SampleVal v0, v1;
         const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
         const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
+        if (rec) {  // per-sample record for the backward (coalesced: 64 B per lane)
+            float4* rr = rec + (r * S + base + 2 * lane) * 2;
+            if (p.in0) store_record(rr, v0);
+            if (p.in1) store_record(rr + 2, v1);
+        }
         const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
         const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
         const float incl = warp_incl_scan(tau0 + tau1, lane);
@@ -539,10 +599,20 @@ __device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& 
     }
 }
 
-template <int c>
+template <int c, int kMode = 0>
 __device__ __forceinline__ void scatter_corner(float4* grad, const SampleVal& v0, const SampleVal& v1,
                                                const CornerCoef& k0, const CornerCoef& k1, bool ok0,
                                                bool ok1, bool same) {
+    if (kMode == 1) {  // diagnostic: same arithmetic, plain stores instead of atomics
+        if (ok0) grad[v0.gidx[c]] = corner_grad<c>(k0);
+        if (ok1) grad[v1.gidx[c]] = corner_grad<c>(k1);
+        return;
+    }
+    if (kMode == 2) {  // diagnostic: arithmetic only, no memory traffic
+        const float4 a = corner_grad<c>(k0), b = corner_grad<c>(k1);
+        if (a.x == 1234.5f && b.y == 1234.5f) grad[0] = a;
+        return;
+    }
     if (same) {
         const float4 a = corner_grad<c>(k0), b = corner_grad<c>(k1);
         atomicAdd(grad + v0.gidx[c], make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
@@ -559,7 +629,7 @@ __device__ __forceinline__ void scatter_corner(float4* grad, const SampleVal& v0
 // Corner gradients are produced and issued one corner at a time (red.global.add.v4.f32);
 // a lane whose two samples share a cell sums them first.
 // ---------------------------------------------------------------------------
-template <int kMinBlocks>
+template <int kMinBlocks, int kMode, bool kRec>
 __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const double* __restrict__ O,
                                                      const double* __restrict__ D, uint64_t n,
                                                      const uint32_t* __restrict__ order,
@@ -568,7 +638,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
                                                      double step, float ib,
                                                      const float* __restrict__ d_rgb,
                                                      const float* __restrict__ d_depth,
-                                                     const float* __restrict__ d_normal) {
+                                                     const float* __restrict__ d_normal,
+                                                     const float4* __restrict__ rec) {
     const int lane = threadIdx.x & 31;
     const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
@@ -591,8 +662,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
         for (uint32_t ch = 0; ch < nch; ++ch) {
             const PairT p = load_pair(tr, cnt, ch * 64, lane, step);
             SampleVal v0, v1;
-            const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
-            const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
+            const float4* rr = rec + (r * S + ch * 64 + 2 * lane) * 2;
+            const bool ok0 = kRec ? eval_from_record(g, o, d, p.in0, p.t0, rr, v0) : eval_slot(g, o, d, p.in0, p.t0, v0);
+            const bool ok1 = kRec ? eval_from_record(g, o, d, p.in1, p.t1, rr + 2, v1) : eval_slot(g, o, d, p.in1, p.t1, v1);
             const float tau = (ok0 ? density(v0.s, ib) * p.d0 : 0.f) +
                               (ok1 ? density(v1.s, ib) * p.d1 : 0.f);
             const float incl = warp_incl_scan(tau, lane);
@@ -606,8 +678,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
         const float tau_base = __shfl_sync(kFull, my_prefix, ch & 31);
         const PairT p = load_pair(tr, cnt, static_cast<uint32_t>(ch) * 64, lane, step);
         SampleVal v0, v1;
-        const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
-        const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
+        const float4* rr = rec + (r * S + static_cast<uint32_t>(ch) * 64 + 2 * lane) * 2;
+        const bool ok0 = kRec ? eval_from_record(g, o, d, p.in0, p.t0, rr, v0) : eval_slot(g, o, d, p.in0, p.t0, v0);
+        const bool ok1 = kRec ? eval_from_record(g, o, d, p.in1, p.t1, rr + 2, v1) : eval_slot(g, o, d, p.in1, p.t1, v1);
         const float sg0 = ok0 ? density(v0.s, ib) : 0.f, sg1 = ok1 ? density(v1.s, ib) : 0.f;
         const float tau0 = sg0 * p.d0, tau1 = sg1 * p.d1;
         const float incl = warp_incl_scan(tau0 + tau1, lane);
@@ -637,15 +710,164 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
         if (ok0) mark_blocks(g, v0);
         if (ok1) mark_blocks(g, v1);
         const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-        scatter_corner<0>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<1>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<2>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<3>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<4>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<5>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<6>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<7>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<0, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<1, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<2, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<3, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<4, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<5, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<6, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        scatter_corner<7, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
         S_after += __shfl_sync(kFull, sinc, 0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6p: pipelined backward (records required, max_samples <= 64).  Persistent warps;
+// each warp owns a ring of kStages shared-memory slots and streams the t row and the
+// record row of the rays it will process next with cp.async.bulk (TMA bulk copy,
+// completion on an mbarrier), so the per-ray load latency overlaps the compositing
+// adjoint and the atomic scatter of the current ray.
+// ---------------------------------------------------------------------------
+constexpr int kPipeStages = 3;
+constexpr int kPipeWarps = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+struct PipeSlot {
+    double t[64];
+    float4 rec[128];
+};
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
+    k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
+                    const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
+                    const double* __restrict__ T, uint32_t S, double step, float ib,
+                    const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
+                    const float* __restrict__ d_normal, const float4* __restrict__ rec,
+                    uint64_t warps_total) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    PipeSlot* slots = reinterpret_cast<PipeSlot*>(smem_raw) + wib * kPipeStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(PipeSlot) * kPipeStages * kPipeWarps) +
+                     wib * kPipeStages;
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
+    const uint32_t tbytes = S * 8, rbytes = S * 32;
+    if (lane == 0) {
+        for (int st = 0; st < kPipeStages; ++st) mbar_init(bars + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
+    auto issue = [&](uint64_t i, int st) {  // lane 0: stream ray i's t + record rows
+        const uint64_t r = ray_of(i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bars + st, tbytes + rbytes);
+        bulk_g2s(slots[st].t, T + r * S, tbytes, bars + st);
+        bulk_g2s(slots[st].rec, rec + r * S * 2, rbytes, bars + st);
+    };
+    // prologue
+    if (lane == 0)
+        for (int st = 0; st < kPipeStages - 1; ++st) {
+            const uint64_t i = w0 + st * warps_total;
+            if (i < n) issue(i, st);
+        }
+    const float ih = static_cast<float>(g.inv_h);
+    uint32_t phase = 0;  // bit st = parity of stage st
+    int st = 0;
+    for (uint64_t i = w0; i < n; i += warps_total) {
+        {  // keep kStages-1 rays in flight: refill the stage released last iteration
+            const uint64_t nxt = i + (kPipeStages - 1) * warps_total;
+            const int nst = (st + kPipeStages - 1) % kPipeStages;
+            if (lane == 0 && nxt < n) issue(nxt, nst);
+        }
+        const uint64_t r = ray_of(i);
+        const uint32_t cnt = counts[r];
+        const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+        const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+        const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
+        const float dD = d_depth[r];
+        const float dN[3] = {d_normal[3 * r], d_normal[3 * r + 1], d_normal[3 * r + 2]};
+        mbar_wait(bars + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const PipeSlot& sl = slots[st];
+        if (cnt) {
+            const uint32_t k0 = 2 * lane, k1 = k0 + 1;
+            PairT p;
+            p.in0 = k0 < cnt;
+            p.in1 = k1 < cnt;
+            p.t0 = p.in0 ? sl.t[k0] : 0.0;
+            p.t1 = p.in1 ? sl.t[k1] : 0.0;
+            p.d0 = p.in1 ? static_cast<float>(__dsub_rn(p.t1, p.t0)) : static_cast<float>(step);
+            p.d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(sl.t[k1 + 1], p.t1)) : static_cast<float>(step);
+            SampleVal v0, v1;
+            const bool ok0 = eval_from_record(g, o, d, p.in0, p.t0, sl.rec + 2 * k0, v0);
+            const bool ok1 = eval_from_record(g, o, d, p.in1, p.t1, sl.rec + 2 * k1, v1);
+            const float sg0 = ok0 ? density(v0.s, ib) : 0.f, sg1 = ok1 ? density(v1.s, ib) : 0.f;
+            const float tau0 = sg0 * p.d0, tau1 = sg1 * p.d1;
+            const float incl = warp_incl_scan(tau0 + tau1, lane);
+            float excl = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) excl = 0.f;
+            const float P0 = excl, P1 = P0 + tau0;
+            const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
+            const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
+            const float Tn0 = expf(-P1), Tn1 = expf(-(P1 + tau1));
+            const float vv0 = ok0 ? dC[0] * v0.r + dC[1] * v0.gc + dC[2] * v0.b + dD * static_cast<float>(p.t0) +
+                                        dN[0] * v0.gx + dN[1] * v0.gy + dN[2] * v0.gz
+                                  : 0.f;
+            const float vv1 = ok1 ? dC[0] * v1.r + dC[1] * v1.gc + dC[2] * v1.b + dD * static_cast<float>(p.t1) +
+                                        dN[0] * v1.gx + dN[1] * v1.gy + dN[2] * v1.gz
+                                  : 0.f;
+            const float u0 = w0 * vv0, u1 = w1 * vv1;
+            const float sinc = warp_incl_suffix(u0 + u1, lane);
+            float sexc = __shfl_down_sync(kFull, sinc, 1);
+            if (lane == 31) sexc = 0.f;
+            const float S1 = sexc, S0 = S1 + u1;
+            const CornerCoef c0 = make_coef(v0, ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f,
+                                            w0, dC, dN, ih);
+            const CornerCoef c1 = make_coef(v1, ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f,
+                                            w1, dC, dN, ih);
+            if (ok0) mark_blocks(g, v0);
+            if (ok1) mark_blocks(g, v1);
+            const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
+            scatter_corner<0>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<1>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<2>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<3>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<4>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<5>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<6>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<7>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+        }
+        __syncwarp();  // every lane is done reading slot st before it is refilled
+        st = (st + 1) % kPipeStages;
     }
 }
 
@@ -675,13 +897,13 @@ void launch_march(const GridView& g, const double* o, const double* d, uint64_t 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
                            const uint32_t* order, const uint32_t* counts, const double* t, uint32_t S,
                            double step, double beta, float* rgb, float* depth, float* normal,
-                           float* wsum, unsigned long long* valid_counter, cudaStream_t s,
-                           int min_blocks) {
+                           float* wsum, unsigned long long* valid_counter, float4* rec,
+                           cudaStream_t s, int min_blocks) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
     const unsigned grid = grid_for(n * 32, 256);
 #define SVR_FWD(MB) k_forward<MB><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, rgb, \
-                                                       depth, normal, wsum, valid_counter)
+                                                       depth, normal, wsum, valid_counter, rec)
     switch (min_blocks) {
         case 1: SVR_FWD(1); break;
         case 2: SVR_FWD(2); break;
@@ -694,20 +916,28 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
 void launch_render_backward(const GridView& g, const double* o, const double* d, uint64_t n,
                             const uint32_t* order, const uint32_t* counts, const double* t,
                             uint32_t S, double step, double beta, const float* d_rgb,
-                            const float* d_depth, const float* d_normal, cudaStream_t s,
-                            int min_blocks) {
+                            const float* d_depth, const float* d_normal, const float4* rec,
+                            cudaStream_t s, int min_blocks) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
     const unsigned grid = grid_for(n * 32, 256);
-#define SVR_BWD(MB) k_backward<MB><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
-                                                        d_rgb, d_depth, d_normal)
+#define SVR_COMMA(a, b, c) a, b, c
+#define SVR_BWD(...) k_backward<__VA_ARGS__><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
+                                                                d_rgb, d_depth, d_normal, rec)
+    const bool r = rec != nullptr;
     switch (min_blocks) {
-        case 1: SVR_BWD(1); break;
-        case 2: SVR_BWD(2); break;
-        case 3: SVR_BWD(3); break;
-        default: SVR_BWD(4); break;
+        case 2: r ? SVR_BWD(2, 0, true) : SVR_BWD(2, 0, false); break;
+        case 4: r ? SVR_BWD(4, 0, true) : SVR_BWD(4, 0, false); break;
+        case 103:  // diagnostics (wrong gradients): plain stores / arithmetic only
+            r ? SVR_BWD(3, 1, true) : SVR_BWD(3, 1, false);
+            break;
+        case 203:
+            r ? SVR_BWD(3, 2, true) : SVR_BWD(3, 2, false);
+            break;
+        default: r ? SVR_BWD(3, 0, true) : SVR_BWD(3, 0, false); break;
     }
 #undef SVR_BWD
+#undef SVR_COMMA
 }
 
 void launch_ray_order(const GridView& g, const double* o, const double* d, uint64_t n,
@@ -723,6 +953,35 @@ void launch_ray_order(const GridView& g, const double* o, const double* d, uint6
     size_t bytes = tmp_bytes;
     cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, 32, s);
     *sorted_ids = vb.Current();
+}
+
+bool launch_render_backward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
+                                 const uint32_t* order, const uint32_t* counts, const double* t,
+                                 uint32_t S, double step, double beta, const float* d_rgb,
+                                 const float* d_depth, const float* d_normal, const float4* rec,
+                                 cudaStream_t s, int min_blocks, int num_sms) {
+    if (!n) return true;
+    if (!rec || S > 64 || (S & 1)) return false;
+    const size_t smem = sizeof(PipeSlot) * kPipeStages * kPipeWarps + 8 * kPipeStages * kPipeWarps;
+    const float ib = static_cast<float>(1.0 / beta);
+    uint64_t ctas = static_cast<uint64_t>(num_sms) * min_blocks;
+    const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
+    if (ctas > need) ctas = need;
+    const uint64_t warps_total = ctas * kPipeWarps;
+#define SVR_PIPE(MB)                                                                              \
+    do {                                                                                          \
+        cudaFuncSetAttribute(k_backward_pipe<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                             static_cast<int>(smem));                                             \
+        k_backward_pipe<MB><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(           \
+            g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
+    } while (0)
+    switch (min_blocks) {
+        case 1: SVR_PIPE(1); break;
+        case 2: SVR_PIPE(2); break;
+        default: SVR_PIPE(3); break;
+    }
+#undef SVR_PIPE
+    return true;
 }
 
 size_t ray_order_tmp_bytes(uint64_t n) {

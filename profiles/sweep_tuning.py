@@ -1,7 +1,9 @@
 #!/usr/bin/env python
-"""Sweep the renderer's performance knobs (results unaffected) on the cfg3 workload in one
-process: ray_sort, fwd_min_blocks, bwd_min_blocks.  Prints per-config device times of the
-forward call (march + sort + forward) and the backward kernel, CUDA events, mean of K."""
+"""Sweep the renderer's performance knobs (svr_grid_set_tuning; results unaffected) on the
+cfg3 workload in one process.  Knobs and values come from SWEEP, e.g.
+    SWEEP="ray_sort=1,3;bwd_pipe=0,1;pipe_min_blocks=2,3" python profiles/sweep_tuning.py
+Prints per-config device times (CUDA events, mean of 4 after 2 warm-up steps) of the
+forward call (sort + march + sort + forward) and the backward call."""
 import itertools
 import os
 import statistics
@@ -17,6 +19,12 @@ from paper_2305_13220_b200 import SparseDenseGrid  # noqa: E402
 
 
 def main():
+    spec = os.environ.get("SWEEP", "ray_sort=3")
+    knobs = []
+    for part in spec.split(";"):
+        if part.strip():
+            k, vals = part.split("=")
+            knobs.append((k.strip(), [int(v) for v in vals.split(",")]))
     cfg = dict(bench.CFG3)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
@@ -33,14 +41,10 @@ def main():
             for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
     outs["n_samples"] = None
     S, step, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
-    sorts = [int(x) for x in os.environ.get("SWEEP_SORT", "0,1").split(",")]
-    fwds = [int(x) for x in os.environ.get("SWEEP_FWD", "1,2,3,4").split(",")]
-    bwds = [int(x) for x in os.environ.get("SWEEP_BWD", "1,2,3,4").split(",")]
     print(f"blocks={g.block_count()} rays={n}", flush=True)
-    for srt, fb, bb in itertools.product(sorts, fwds, bwds):
-        g.set_tuning("ray_sort", srt)
-        g.set_tuning("fwd_min_blocks", fb)
-        g.set_tuning("bwd_min_blocks", bb)
+    for combo in itertools.product(*[v for _, v in knobs]):
+        for (k, _), v in zip(knobs, combo):
+            g.set_tuning(k, v)
         f_ms, b_ms = [], []
         for it in range(6):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -54,9 +58,9 @@ def main():
             if it >= 2:
                 f_ms.append(e[0].elapsed_time(e[1]))
                 b_ms.append(e[1].elapsed_time(e[2]))
-        print(f"sort={srt} fwd_minb={fb} bwd_minb={bb}: fwd {statistics.mean(f_ms):7.3f} ms  "
-              f"bwd {statistics.mean(b_ms):7.3f} ms  total {statistics.mean(f_ms) + statistics.mean(b_ms):7.3f}",
-              flush=True)
+        tag = " ".join(f"{k}={v}" for (k, _), v in zip(knobs, combo))
+        print(f"{tag}: fwd {statistics.mean(f_ms):7.3f} ms  bwd {statistics.mean(b_ms):7.3f} ms  "
+              f"total {statistics.mean(f_ms) + statistics.mean(b_ms):7.3f}", flush=True)
 
 
 if __name__ == "__main__":
