@@ -434,6 +434,13 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
     g->own_stream = true;
     if (const char* e = std::getenv("SVR_RAY_SORT")) g->ray_sort = std::atoi(e);
     SVR_CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+    {  // host-array staging uses stream-ordered temporaries: keep freed pool memory mapped
+        // across synchronisations instead of returning it to the OS (threshold 0 default)
+        cudaMemPool_t pool;
+        SVR_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = ~0ull;
+        SVR_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
     SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
     SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
