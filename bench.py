@@ -446,12 +446,107 @@ def run_ours(args, cfg, rank, world, local_rank):
         "library_launches": {"cub_radix_sort": library_launches_per_step * args.steps},
         "clocks": clk,
     }
+    del grid
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_extra:
+        try:
+            line["extra_configs"] = {"cfg2_image_forward": bench_cfg2(dev, stream),
+                                     "cfg4_activation_and_query": bench_cfg4(dev, stream)}
+        except Exception as e:  # pragma: no cover
+            line["extra_configs"] = {"error": str(e)}
     if world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline_port(coords, lambda: chunks, o, d, dC, dD, dN, cfg)
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line), flush=True)
+
+
+def _events_ms(stream, fn, reps):
+    import torch
+
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_cfg2(dev, stream):
+    """configs[1]: 5x5x3 m room, 2 cm voxels (R=2 from 24 ring frames), one full 640x480
+    image from camera_for_frame(0), forward only (color/depth/normal)."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    cfg = dict(CFG3, room=(5.0, 5.0, 3.0), h=0.02, act_frames=24, ray_poses=24)
+    scene = make_scene(cfg)
+    cams, depth = activation_frames(scene, cfg)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
+    g.set_stream(stream)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    o, d = scene.image_rays(0)
+    od, dd = torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev)
+    n = len(o)
+    outs = {k: torch.empty(s, dtype=torch.float32, device=dev)
+            for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
+    outs["n_samples"] = None
+    g.set_tuning("records", 0)  # inference: no backward context needed
+    ms = _events_ms(stream, lambda: g.render_forward(od, dd, cfg["h"] / 2, 64, 2 * cfg["h"], out=outs), 20)
+    st = g.render_stats()
+    return {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),
+            "ms_per_image": ms, "rays_per_s": n / (ms * 1e-3),
+            "samples_per_s": st.valid_samples / (ms * 1e-3)}
+
+
+def bench_cfg4(dev, stream, n_frames=300, k=256):
+    """configs[3]: block activation + hash insert from 300 GT depth frames (640x480) into an
+    empty 1 cm grid (R=2), then a k^3 query_sdf_with_gradient sweep over the bounds."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    cfg = dict(CFG3, ray_poses=n_frames)
+    scene = make_scene(cfg)
+    cams = scene.cameras(n_frames)
+    depth = scene.depth(cams)
+    depth_d = torch.from_numpy(depth).to(dev)
+    times = []
+    for _ in range(3):
+        g = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22, device=dev.index)
+        g.set_stream(stream)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = g.allocate_for_frames(depth_d, cams, cfg["dilation"])
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    act_s = min(times)
+    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    info = g.info()
+    L = cfg["h"] * 8
+    lo = np.array(info.bounds_lo) * L
+    hi = (np.array(info.bounds_hi) + 1) * L
+    ax = [np.linspace(lo[a], hi[a], k, endpoint=False) + (hi[a] - lo[a]) / (2 * k) for a in range(3)]
+    pts = np.stack(np.meshgrid(*ax, indexing="ij"), -1).reshape(-1, 3)
+    x = torch.from_numpy(pts).to(dev)
+    sdf = torch.empty(len(pts), dtype=torch.float64, device=dev)
+    grad = torch.empty((len(pts), 3), dtype=torch.float64, device=dev)
+    valid = torch.empty(len(pts), dtype=torch.uint8, device=dev)
+    from paper_2305_13220_b200._lib import check
+
+    ms = _events_ms(stream, lambda: check(g._lib.svr_query(g._h, x.data_ptr(), len(pts), sdf.data_ptr(),
+                                                           grad.data_ptr(), None, None, valid.data_ptr())), 5)
+    return {"frames": n_frames, "pixels": int(rep.pixels_used), "blocks": int(rep.blocks_added),
+            "activation_ms": act_s * 1e3, "pixels_per_s": rep.pixels_used / act_s,
+            "blocks_per_s": rep.blocks_added / act_s, "query_points": len(pts),
+            "query_valid": int(valid.sum().item()), "query_ms": ms,
+            "query_points_per_s": len(pts) / (ms * 1e-3)}
 
 
 def main():
@@ -461,6 +556,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 side measurements")
     ap.add_argument("--rays-per-pose", type=int, default=CFG3["rays_per_pose"])
     ap.add_argument("--act-frames", type=int, default=CFG3["act_frames"])
     args = ap.parse_args()
