@@ -201,6 +201,8 @@ struct svr_grid {
     int fwd_min_blocks = 3;
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
+    bool fwd_pipe = false;    // persistent forward streaming t rows (measured slower: off)
+    int fwd_pipe_min_blocks = 3;
     int pipe_min_blocks = 3;
     int num_sms = 148;
     int bwd_min_blocks = 3;
@@ -523,6 +525,10 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->ray_sort = static_cast<int>(value);
         } else if (k == "fwd_min_blocks") {
             g->fwd_min_blocks = static_cast<int>(value);
+        } else if (k == "fwd_pipe") {
+            g->fwd_pipe = value != 0;
+        } else if (k == "fwd_pipe_min_blocks") {
+            g->fwd_pipe_min_blocks = static_cast<int>(value);
         } else if (k == "bwd_pipe") {
             g->bwd_pipe = value != 0;
         } else if (k == "pipe_min_blocks") {
@@ -873,11 +879,17 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
                                                g->ord_tmp.bytes, &g->ctx_order, g->stream);
             g->ctx_rec = g->use_records;
             if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
-            svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
-                                                g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                c, e, nullptr,
-                                                g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream,
-                                                g->fwd_min_blocks);
+            float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;
+            const bool piped =
+                g->fwd_pipe &&
+                svr_internal::launch_render_forward_pipe(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
+                                                         g->tbuf.as<double>(), max_samples, step, beta, a, b,
+                                                         c, e, recp, g->stream, g->fwd_pipe_min_blocks,
+                                                         g->num_sms);
+            if (!piped)
+                svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
+                                                    g->tbuf.as<double>(), max_samples, step, beta, a, b,
+                                                    c, e, nullptr, recp, g->stream, g->fwd_min_blocks);
             if (n_samples) {
                 uint32_t* ns = st.out(n_samples, n);
                 SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));

@@ -44,6 +44,12 @@ void launch_ray_order(const svr_dev::GridView& g, const double* o, const double*
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
                       size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s);
 size_t ray_order_tmp_bytes(uint64_t n);
+// Pipelined forward (max_samples <= 64, even); returns false if not applicable.
+bool launch_render_forward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
+                                uint64_t n, const uint32_t* order, const uint32_t* counts,
+                                const double* t, uint32_t S, double step, double beta, float* rgb,
+                                float* depth, float* normal, float* wsum, float4* rec,
+                                cudaStream_t s, int min_blocks, int num_sms);
 // Pipelined backward (records, max_samples <= 64, even); returns false if not applicable.
 bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
                                  uint64_t n, const uint32_t* order, const uint32_t* counts,

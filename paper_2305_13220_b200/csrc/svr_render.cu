@@ -871,6 +871,188 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     }
 }
 
+// ---------------------------------------------------------------------------
+// K5p: pipelined forward (max_samples <= 64, even).  Persistent warps, 3-stage ring of
+// t rows streamed with cp.async.bulk; while ray i is gathered and composited, ray i+1's
+// t row is already resident and its base-voxel block lookups are in flight, and ray i+2's
+// t row is being copied.  Per-ray scalars (o, d) ride in lanes 0-5 and are broadcast.
+// ---------------------------------------------------------------------------
+constexpr int kFwdStages = 3;
+
+struct RayPrep {  // state of the next ray, prepared one iteration ahead
+    uint64_t r;
+    uint32_t cnt;
+    double od;          // lane k < 6 holds o[k] (k < 3) or d[k-3]
+    uint32_t e0a, e0b;  // block entries of the base voxels of this lane's two samples
+};
+
+__device__ __forceinline__ void bcast_od(double od, double o[3], double d[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        o[k] = __shfl_sync(kFull, od, k);
+        d[k] = __shfl_sync(kFull, od, k + 3);
+    }
+}
+
+__device__ __forceinline__ uint32_t base_lookup(const GridView& g, const double o[3], const double d[3],
+                                                double t) {
+    int base[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = __dadd_rn(o[a], __dmul_rn(t, d[a]));
+        base[a] = static_cast<int>(floor(__dmul_rn(x, g.inv_h)));
+    }
+    return lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
+}
+
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
+    k_forward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
+                   const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
+                   const double* __restrict__ T, uint32_t S, double step, float ib, float* rgb,
+                   float* depth, float* normal, float* wsum, float4* rec, uint64_t warps_total) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double(*trow)[64] = reinterpret_cast<double(*)[64]>(smem_raw) + wib * kFwdStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double) * 64 * kFwdStages * kPipeWarps) +
+                     wib * kFwdStages;
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
+    const uint32_t tbytes = S * 8;
+    if (lane == 0) {
+        for (int st = 0; st < kFwdStages; ++st) mbar_init(bars + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
+    auto issue = [&](uint64_t i, int st) {
+        const uint64_t r = ray_of(i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bars + st, tbytes);
+        bulk_g2s(trow[st], T + r * S, tbytes, bars + st);
+    };
+    uint32_t phase = 0;
+    auto prep = [&](uint64_t i, int st, RayPrep& p) {  // scalars + base lookups of ray i
+        p.r = ray_of(i);
+        p.cnt = counts[p.r];
+        p.od = lane < 3 ? O[3 * p.r + lane] : (lane < 6 ? D[3 * p.r + lane - 3] : 0.0);
+        double o[3], d[3];
+        bcast_od(p.od, o, d);
+        mbar_wait(bars + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const uint32_t k0 = 2 * lane, k1 = k0 + 1;
+        p.e0a = k0 < p.cnt ? base_lookup(g, o, d, trow[st][k0]) : kInvalid;
+        p.e0b = k1 < p.cnt ? base_lookup(g, o, d, trow[st][k1]) : kInvalid;
+    };
+    if (w0 >= n) return;
+    if (lane == 0) {
+        issue(w0, 0);
+        if (w0 + warps_total < n) issue(w0 + warps_total, 1);
+    }
+    RayPrep cur;
+    prep(w0, 0, cur);
+    int st = 0;
+    const float ih = static_cast<float>(g.inv_h);
+    for (uint64_t i = w0; i < n; i += warps_total) {
+        const uint64_t i1 = i + warps_total, i2 = i + 2 * warps_total;
+        const int st1 = (st + 1) % kFwdStages, st2 = (st + 2) % kFwdStages;
+        if (lane == 0 && i2 < n) issue(i2, st2);
+        RayPrep nxt;
+        nxt.cnt = 0;
+        if (i1 < n) prep(i1, st1, nxt);  // its lookups are in flight during this ray
+        // ---- gather + composite ray i (t row in stage st) ----
+        double o[3], d[3];
+        bcast_od(cur.od, o, d);
+        const uint64_t r = cur.r;
+        const uint32_t cnt = cur.cnt;
+        const double* tr = trow[st];
+        const uint32_t k0 = 2 * lane, k1 = k0 + 1;
+        PairT p;
+        p.in0 = k0 < cnt;
+        p.in1 = k1 < cnt;
+        p.t0 = p.in0 ? tr[k0] : 0.0;
+        p.t1 = p.in1 ? tr[k1] : 0.0;
+        p.d0 = p.in1 ? static_cast<float>(__dsub_rn(p.t1, p.t0)) : static_cast<float>(step);
+        p.d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(tr[k1 + 1], p.t1)) : static_cast<float>(step);
+        SampleVal v0, v1;
+        bool ok0 = false, ok1 = false;
+        float4 p0[8], p1[8];
+        {
+            int b0[3], b1[3];
+            zero_sample(v0);
+            zero_sample(v1);
+            if (p.in0) {
+                cell_geom(g, o, d, p.t0, b0, v0);
+                ok0 = corner_addrs<true>(g, b0, cur.e0a, v0);
+            }
+            if (p.in1) {
+                cell_geom(g, o, d, p.t1, b1, v1);
+                ok1 = corner_addrs<true>(g, b1, cur.e0b, v1);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                p0[c] = ok0 ? __ldg(g.pay + v0.gidx[c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                p1[c] = ok1 ? __ldg(g.pay + v1.gidx[c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        auto interp = [&](SampleVal& v, const float4* pp, bool ok, uint32_t e0) {
+            const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
+            const float w[8] = {x0 * y0 * z0, x1 * y0 * z0, x0 * y1 * z0, x1 * y1 * z0,
+                                x0 * y0 * z1, x1 * y0 * z1, x0 * y1 * z1, x1 * y1 * z1};
+            float sv = 0.f, rv = 0.f, gv = 0.f, bv = 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                sv = fmaf(w[c], pp[c].x, sv);
+                rv = fmaf(w[c], pp[c].y, rv);
+                gv = fmaf(w[c], pp[c].z, gv);
+                bv = fmaf(w[c], pp[c].w, bv);
+            }
+            v.s = sv, v.r = rv, v.gc = gv, v.b = bv;
+            v.gx = ih * ((y0 * z0) * (pp[1].x - pp[0].x) + (y1 * z0) * (pp[3].x - pp[2].x) +
+                         (y0 * z1) * (pp[5].x - pp[4].x) + (y1 * z1) * (pp[7].x - pp[6].x));
+            v.gy = ih * ((x0 * z0) * (pp[2].x - pp[0].x) + (x1 * z0) * (pp[3].x - pp[1].x) +
+                         (x0 * z1) * (pp[6].x - pp[4].x) + (x1 * z1) * (pp[7].x - pp[5].x));
+            v.gz = ih * ((x0 * y0) * (pp[4].x - pp[0].x) + (x1 * y0) * (pp[5].x - pp[1].x) +
+                         (x0 * y1) * (pp[6].x - pp[2].x) + (x1 * y1) * (pp[7].x - pp[3].x));
+            v.e0 = ok ? e0 : kInvalid;
+        };
+        interp(v0, p0, ok0, cur.e0a);
+        interp(v1, p1, ok1, cur.e0b);
+        if (rec) {
+            float4* rr = rec + (r * S + 2 * lane) * 2;
+            if (p.in0) store_record(rr, v0);
+            if (p.in1) store_record(rr + 2, v1);
+        }
+        const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
+        const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
+        const float incl = warp_incl_scan(tau0 + tau1, lane);
+        float excl = __shfl_up_sync(kFull, incl, 1);
+        if (lane == 0) excl = 0.f;
+        const float P0 = excl, P1 = P0 + tau0;
+        const float w0v = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
+        const float w1v = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
+        float acc[8];
+        acc[0] = w0v * v0.r + w1v * v1.r;
+        acc[1] = w0v * v0.gc + w1v * v1.gc;
+        acc[2] = w0v * v0.b + w1v * v1.b;
+        acc[3] = w0v * static_cast<float>(p.t0) + w1v * static_cast<float>(p.t1);
+        acc[4] = w0v * v0.gx + w1v * v1.gx;
+        acc[5] = w0v * v0.gy + w1v * v1.gy;
+        acc[6] = w0v * v0.gz + w1v * v1.gz;
+        acc[7] = w0v + w1v;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = warp_sum(acc[k]);
+        if (lane == 0) {
+            if (rgb) rgb[3 * r] = acc[0], rgb[3 * r + 1] = acc[1], rgb[3 * r + 2] = acc[2];
+            if (depth) depth[r] = acc[3];
+            if (normal) normal[3 * r] = acc[4], normal[3 * r + 1] = acc[5], normal[3 * r + 2] = acc[6];
+            if (wsum) wsum[r] = acc[7];
+        }
+        __syncwarp();  // stage st is free for refilling
+        cur = nxt;
+        st = st1;
+    }
+}
+
 }  // namespace
 }  // namespace svr_dev
 
@@ -981,6 +1163,32 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
         default: SVR_PIPE(3); break;
     }
 #undef SVR_PIPE
+    return true;
+}
+
+bool launch_render_forward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
+                                const uint32_t* order, const uint32_t* counts, const double* t,
+                                uint32_t S, double step, double beta, float* rgb, float* depth,
+                                float* normal, float* wsum, float4* rec, cudaStream_t s,
+                                int min_blocks, int num_sms) {
+    if (!n) return true;
+    if (S > 64 || (S & 1)) return false;
+    const size_t smem = sizeof(double) * 64 * kFwdStages * kPipeWarps + 8 * kFwdStages * kPipeWarps;
+    const float ib = static_cast<float>(1.0 / beta);
+    uint64_t ctas = static_cast<uint64_t>(num_sms) * min_blocks;
+    const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
+    if (ctas > need) ctas = need;
+    const uint64_t warps_total = ctas * kPipeWarps;
+#define SVR_FPIPE(MB)                                                                                 \
+    k_forward_pipe<MB><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(                  \
+        g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, rec, warps_total)
+    switch (min_blocks) {
+        case 1: SVR_FPIPE(1); break;
+        case 2: SVR_FPIPE(2); break;
+        case 4: SVR_FPIPE(4); break;
+        default: SVR_FPIPE(3); break;
+    }
+#undef SVR_FPIPE
     return true;
 }
 
