@@ -198,6 +198,7 @@ struct svr_grid {
     // bit 1: order the march by origin + direction; bit 0: order forward/backward by the
     // block of each ray's first sample (3 = both)
     int ray_sort = 3;
+    int sort_impl = 1;  // 1: CUB radix sort (default, best order), 0: in-house bucketed counting sort
     int fwd_min_blocks = 3;
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
@@ -525,6 +526,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->ray_sort = static_cast<int>(value);
         } else if (k == "fwd_min_blocks") {
             g->fwd_min_blocks = static_cast<int>(value);
+        } else if (k == "sort_impl") {
+            g->sort_impl = static_cast<int>(value);
         } else if (k == "fwd_pipe") {
             g->fwd_pipe = value != 0;
         } else if (k == "fwd_pipe_min_blocks") {
@@ -860,23 +863,31 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
             const GridView v = g->view();
             g->ctx_order = nullptr;
             const bool sort = g->ray_sort != 0 && n > 1;
-            if (sort) {
+            const bool cub_sort = sort && g->sort_impl == 1;
+            if (cub_sort) {
                 g->ord_keys.ensure(8 * n);
                 g->ord_ids.ensure(8 * n);
                 g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
+            } else if (sort) {
+                g->ord_ids.ensure(4 * svr_internal::ray_order_scratch_words(n));
             }
             uint32_t* k = g->ord_keys.as<uint32_t>();
             uint32_t* id = g->ord_ids.as<uint32_t>();
-            if (sort && (g->ray_sort & 2))  // pre-march: origin + direction
-                svr_internal::launch_ray_order(v, dO, dD, n, nullptr, nullptr, max_samples, k, id, k + n,
-                                               id + n, g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order,
-                                               g->stream);
+            auto order_rays = [&](bool post_march) {
+                const uint32_t* cnt = post_march ? g->counts.as<uint32_t>() : nullptr;
+                const double* tt = post_march ? g->tbuf.as<double>() : nullptr;
+                if (cub_sort) {
+                    svr_internal::launch_ray_order(v, dO, dD, n, cnt, tt, max_samples, k, id, k + n, id + n,
+                                                   g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream);
+                } else {
+                    svr_internal::launch_ray_bucket_order(v, dO, dD, n, cnt, tt, max_samples, id, g->stream);
+                    g->ctx_order = id;
+                }
+            };
+            if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
             svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples,
                                        g->counts.as<uint32_t>(), g->tbuf.as<double>(), nullptr, g->stream);
-            if (sort && (g->ray_sort & 1))  // post-march: first-sample block
-                svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
-                                               max_samples, k, id, k + n, id + n, g->ord_tmp.p,
-                                               g->ord_tmp.bytes, &g->ctx_order, g->stream);
+            if (sort && (g->ray_sort & 1)) order_rays(true);   // post-march: first-sample block
             g->ctx_rec = g->use_records;
             if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
             float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;

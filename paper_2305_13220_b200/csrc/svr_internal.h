@@ -44,6 +44,12 @@ void launch_ray_order(const svr_dev::GridView& g, const double* o, const double*
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
                       size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s);
 size_t ray_order_tmp_bytes(uint64_t n);
+// In-house bucketed counting sort (svr_sort.cu): order = scratch[0, n).  counts == NULL:
+// origin + direction buckets (pre-march); else first-sample block buckets (post-march).
+size_t ray_order_scratch_words(uint64_t n);
+void launch_ray_bucket_order(const svr_dev::GridView& g, const double* o, const double* d,
+                             uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
+                             uint32_t* scratch, cudaStream_t s);
 // Pipelined forward (max_samples <= 64, even); returns false if not applicable.
 bool launch_render_forward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
                                 uint64_t n, const uint32_t* order, const uint32_t* counts,
