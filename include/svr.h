@@ -108,7 +108,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * first-sample block; default 3 = both),
  * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for),
  * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather),
-  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
+ * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
  * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
  * "pipe_min_blocks". */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
