@@ -180,6 +180,26 @@ int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float
 /* Zero the gradients of the active blocks only and clear the active mask. */
 int svr_grad_zero_active(svr_grid* g);
 
+/* --- the losses / update around the rendering path ---------- */
+
+/* sample_uniform (grid.cpp:355-370): n points uniform over the union of
+ * allocated block volumes (uniform block, then uniform inside it), deterministic for a
+ * seed.  The device uses a counter-based splitmix64 stream, NOT the reference's
+ * mt19937_64 + libstdc++ distributions (whose stream is library-specific).
+ * out[n][3]; SVR_ERR_DATA on an empty grid (grid.cpp:358). */
+int svr_sample_uniform(svr_grid* g, uint64_t n, uint64_t seed, double* out);
+/* Eikonal regulariser (Eq. 16/18): over the valid points of
+ * x[n][3], loss = mean (|grad f(x)| - 1)^2 with f the fp64 trilinear interpolant; adds
+ * scale * dloss/dsdf to the sdf gradient plane through the analytic trilinear weight
+ * derivatives and marks active blocks.  *loss (mean) and *n_valid are returned. */
+int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* loss,
+                uint64_t* n_valid);
+/* RMSProp on the active blocks (SPEC.md:320-327 refine, grid.hpp:70 rms_* buffers):
+ * v = alpha v + (1 - alpha) g^2,  theta -= lr g / (sqrt(v) + eps)  for sdf and rgb, then the
+ * active gradients are zeroed and the active mask cleared (fused).  State lives in the
+ * handle (allocated on first use). */
+int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
+
 #ifdef __cplusplus
 }
 #endif

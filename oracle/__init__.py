@@ -196,6 +196,8 @@ class OracleGrid(_Base):
         "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P, P]),
         "render_backward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P, P]),
         "sdf_to_density": (c_double, [c_double, c_double]),
+        "eikonal": (c_int, [c_void_p, P, c_uint64, c_double, P, P, POINTER(c_double), POINTER(c_uint64)]),
+        "rmsprop": (c_int, [c_void_p, P, P, P, c_float, c_float, c_float, P]),
     })
 
     def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
@@ -276,6 +278,28 @@ class OracleGrid(_Base):
             self._h, _ptr(o), _ptr(d), n, step, max_samples, beta, _ptr(up[0]), _ptr(up[1]),
             _ptr(up[2]), _ptr(gs), _ptr(gr), _ptr(active)))
         return gs, gr, active
+
+
+def _eikonal(self, x, scale=1.0):
+    """(loss, n_valid, grad_sdf[A,V], active[A]) of the restated Eikonal regulariser."""
+    x = _f64(x, (-1, 3))
+    A, V = self.block_count(), self.B ** 3
+    gs = np.zeros((A, V))
+    act = np.zeros(A, np.uint8)
+    loss, nv = c_double(), c_uint64()
+    self._check(self.lib().svro_eikonal(self._h, _ptr(x), len(x), scale, _ptr(gs), _ptr(act),
+                                        ctypes.byref(loss), ctypes.byref(nv)))
+    return loss.value, nv.value, gs, act
+
+
+def _rmsprop(self, grad_sdf, grad_rgb, active, lr, alpha, eps, rms_state):
+    arrs = [np.ascontiguousarray(grad_sdf, np.float64), np.ascontiguousarray(grad_rgb, np.float64),
+            np.ascontiguousarray(active, np.uint8)]
+    self._check(self.lib().svro_rmsprop(self._h, *[_ptr(a) for a in arrs], lr, alpha, eps, _ptr(rms_state)))
+
+
+OracleGrid.eikonal = _eikonal
+OracleGrid.rmsprop = _rmsprop
 
 
 class RefGrid(_Base):

@@ -797,6 +797,75 @@ int svro_render_backward(const svro_grid* g, const double* o, const double* d, u
     });
 }
 
+// eikonal_loss (Eq. 16/18): mean over valid points of
+// (|grad f(x)| - 1)^2, gradient (2 scale / N) (1 - 1/|g|) (g . dw_c) into grad_sdf.
+int svro_eikonal(const svro_grid* g, const double* x, uint64_t n, double scale, double* grad_sdf,
+                 uint8_t* active, double* loss, uint64_t* n_valid) {
+    return guarded([&] {
+        struct P {
+            Corners cc;
+            double gr[3];
+            bool ok;
+        };
+        std::vector<P> pts(n);
+        double sum = 0.0;
+        uint64_t cnt = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            P& p = pts[i];
+            p.ok = !g->coords.empty() && gather(*g, x + 3 * i, p.cc);
+            if (!p.ok) continue;
+            Interp it;
+            interpolate(*g, p.cc, it);
+            for (int a = 0; a < 3; ++a) p.gr[a] = it.grad[a];
+            const double nrm = std::sqrt(p.gr[0] * p.gr[0] + p.gr[1] * p.gr[1] + p.gr[2] * p.gr[2]);
+            sum += (nrm - 1.0) * (nrm - 1.0);
+            ++cnt;
+        }
+        if (loss) *loss = cnt ? sum / static_cast<double>(cnt) : 0.0;
+        if (n_valid) *n_valid = cnt;
+        if (!cnt || !grad_sdf) return;
+        const double coef = 2.0 * scale / static_cast<double>(cnt);
+        for (uint64_t i = 0; i < n; ++i) {
+            const P& p = pts[i];
+            if (!p.ok) continue;
+            const double nrm = std::sqrt(p.gr[0] * p.gr[0] + p.gr[1] * p.gr[1] + p.gr[2] * p.gr[2]);
+            if (!(nrm > 0.0)) continue;
+            const double k = coef * (1.0 - 1.0 / nrm);
+            for (int c = 0; c < 8; ++c) {
+                grad_sdf[static_cast<size_t>(p.cc.block[c]) * g->V + p.cc.voxel[c]] +=
+                    k * (p.gr[0] * p.cc.dw[c][0] + p.gr[1] * p.cc.dw[c][1] + p.gr[2] * p.cc.dw[c][2]);
+                if (active) active[p.cc.block[c]] = 1;
+            }
+        }
+    });
+}
+
+// RMSProp over the active blocks, fp32 like the device:
+//   v = alpha v + (1 - alpha) g^2,  theta -= lr g / (sqrt(v) + eps)   for sdf and rgb.
+// rms_state is [A][V][4] (sdf, r, g, b), caller-owned.
+int svro_rmsprop(svro_grid* g, const double* grad_sdf, const double* grad_rgb, const uint8_t* active,
+                 float lr, float alpha, float eps, float* rms_state) {
+    return guarded([&] {
+        const size_t V = g->V;
+        const float beta = 1.f - alpha;
+        for (size_t b = 0; b < g->coords.size(); ++b) {
+            if (!active[b]) continue;
+            for (size_t v = 0; v < V; ++v) {
+                const size_t i = b * V + v;
+                float* r = rms_state + 4 * i;
+                const float gv[4] = {static_cast<float>(grad_sdf[i]), static_cast<float>(grad_rgb[3 * i]),
+                                     static_cast<float>(grad_rgb[3 * i + 1]),
+                                     static_cast<float>(grad_rgb[3 * i + 2])};
+                float* th[4] = {&g->sdf[i], &g->rgb[3 * i], &g->rgb[3 * i + 1], &g->rgb[3 * i + 2]};
+                for (int k = 0; k < 4; ++k) {
+                    r[k] = alpha * r[k] + beta * gv[k] * gv[k];
+                    *th[k] -= lr * gv[k] / (std::sqrt(r[k]) + eps);
+                }
+            }
+        }
+    });
+}
+
 // save_grid / load_grid (grid_io.cpp:37-97), SDGV v1 little-endian.
 int svro_save_sdgv(const svro_grid* g, const char* path) {
     return guarded([&] {

@@ -81,6 +81,10 @@ int svro_render_backward(const svro_grid* g, const double* o, const double* d, u
                          double* grad_rgb, uint8_t* active);
 
 double svro_sdf_to_density(double s, double beta);
+int svro_eikonal(const svro_grid* g, const double* x, uint64_t n, double scale, double* grad_sdf,
+                 uint8_t* active, double* loss, uint64_t* n_valid);
+int svro_rmsprop(svro_grid* g, const double* grad_sdf, const double* grad_rgb, const uint8_t* active,
+                 float lr, float alpha, float eps, float* rms_state);
 
 int svro_save_sdgv(const svro_grid* g, const char* path);
 int svro_load_sdgv(const char* path, svro_grid** out);

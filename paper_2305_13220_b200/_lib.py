@@ -124,6 +124,9 @@ _PROTOS = {
     "svr_grad_pack": (_I, [c_void_p, P, c_uint64, P]),
     "svr_grad_unpack": (_I, [c_void_p, P, c_uint64, P]),
     "svr_grad_zero_active": (_I, [c_void_p]),
+    "svr_sample_uniform": (_I, [c_void_p, c_uint64, c_uint64, P]),
+    "svr_eikonal": (_I, [c_void_p, P, c_uint64, c_double, POINTER(c_double), POINTER(c_uint64)]),
+    "svr_rmsprop_step": (_I, [c_void_p, c_float, c_float, c_float]),
     # svr_synth.h (host-only fixtures)
     "svr_scene_spec_default": (None, [POINTER(SceneSpec)]),
     "svr_scene_create": (_I, [POINTER(SceneSpec), POINTER(c_void_p)]),

@@ -128,6 +128,48 @@ __device__ __forceinline__ bool voxel_valid(const GridView& g, uint32_t entry, u
     return (__ldg(g.vmask + blk * 16u + (local >> 5)) >> (local & 31)) & 1u;
 }
 
+// gather_impl over CornerCacheD (grid.cpp:112-155) in fp64 with the reference's operation
+// order (explicit _rn so nothing is contracted): corner c takes bit a of c on axis a,
+// w_c = (wx wy) wz, dw_c[a] = ((+-1 inv_h) w_other1) w_other2.  False when a corner's block
+// is missing or its voxel unobserved.
+__device__ __forceinline__ bool gather_fp64(const GridView& g, const double x[3], uint32_t gidx[8],
+                                            double w[8], double dw[8][3]) {
+    double fx[3];
+    int base[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double gg = __dmul_rn(x[a], g.inv_h);
+        const double fl = floor(gg);
+        base[a] = static_cast<int>(fl);
+        fx[a] = __dsub_rn(gg, fl);
+    }
+    const double w0[3] = {__dsub_rn(1.0, fx[0]), __dsub_rn(1.0, fx[1]), __dsub_rn(1.0, fx[2])};
+    if (g.n_blocks == 0) return false;
+    int32_t lbx = INT32_MIN, lby = 0, lbz = 0;
+    uint32_t le = kInvalid;
+    for (int c = 0; c < 8; ++c) {
+        const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
+        const int vx = base[0] + cx, vy = base[1] + cy, vz = base[2] + cz;
+        const int32_t bx = vx >> 3, by = vy >> 3, bz = vz >> 3;
+        if (bx != lbx || by != lby || bz != lbz) {
+            lbx = bx, lby = by, lbz = bz;
+            le = lookup_block(g, bx, by, bz);
+        }
+        if (le == kInvalid) return false;
+        const uint32_t local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
+        if (!voxel_valid(g, le, local)) return false;
+        gidx[c] = (le & ~kFullBit) * 512u + local;
+        const double wx = cx ? fx[0] : w0[0];
+        const double wy = cy ? fx[1] : w0[1];
+        const double wz = cz ? fx[2] : w0[2];
+        w[c] = __dmul_rn(__dmul_rn(wx, wy), wz);
+        dw[c][0] = __dmul_rn(__dmul_rn(__dmul_rn(cx ? 1.0 : -1.0, g.inv_h), wy), wz);
+        dw[c][1] = __dmul_rn(__dmul_rn(__dmul_rn(cy ? 1.0 : -1.0, g.inv_h), wx), wz);
+        dw[c][2] = __dmul_rn(__dmul_rn(__dmul_rn(cz ? 1.0 : -1.0, g.inv_h), wx), wy);
+    }
+    return true;
+}
+
 // std::min / std::max argument semantics (ties and NaN return the first argument).
 __device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
 __device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }

@@ -215,6 +215,8 @@ struct svr_grid {
     bool ctx_valid = false;
 
     DevBuf active_list, active_count;  // count: u64 + per-CTA scratch
+    DevBuf rms;                        // RMSProp state float4 [rms_blocks][512]
+    uint64_t rms_blocks = 0;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
     void* sort_tmp_p = nullptr;
     size_t sort_tmp_bytes = 0;
@@ -1075,6 +1077,70 @@ int svr_grad_zero_active(svr_grid* g) {
         svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
         svr_internal::launch_grad_zero_active(g->grad, g->active, g->active_list.as<uint32_t>(), dcount,
                                               nb, g->stream);
+        SVR_LAUNCHED();
+    });
+}
+
+int svr_sample_uniform(svr_grid* g, uint64_t n, uint64_t seed, double* out) {
+    return guarded([&] {
+        if (g->n() == 0) throw Fail{SVR_ERR_DATA, "sample_uniform: empty grid"};  // grid.cpp:358
+        if (!n) return;
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        double* o = st.out(out, 3 * n);
+        svr_internal::launch_sample_uniform(g->coords4, static_cast<uint32_t>(g->n()), g->L, n, seed, o,
+                                            g->stream);
+        st.finish();
+    });
+}
+
+int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* loss, uint64_t* n_valid) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        double sums[2] = {0.0, 0.0};
+        if (n && g->n()) {
+            g->ensure_lookup();
+            Stage st(g->stream);
+            const double* dx = st.in(x, 3 * n);
+            double* dsum = static_cast<double*>(st.alloc(16));
+            SVR_CK(cudaMemsetAsync(dsum, 0, 16, g->stream));
+            const GridView v = g->view();
+            svr_internal::launch_eikonal_stats(v, dx, n, dsum, g->stream);
+            SVR_LAUNCHED();
+            SVR_CK(cudaMemcpyAsync(sums, dsum, 16, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            if (sums[1] > 0.0 && scale != 0.0)
+                svr_internal::launch_eikonal_scatter(v, dx, n, 2.0 * scale / sums[1], g->stream);
+            st.finish();
+        }
+        if (loss) *loss = sums[1] > 0.0 ? sums[0] / sums[1] : 0.0;
+        if (n_valid) *n_valid = static_cast<uint64_t>(sums[1]);
+    });
+}
+
+int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint32_t nb = static_cast<uint32_t>(g->n());
+        if (!nb) return;
+        if (g->rms_blocks < nb) {  // grow the state, new rows start at zero
+            DevBuf fresh;
+            fresh.ensure(static_cast<size_t>(nb) * kVox * sizeof(float4));
+            SVR_CK(cudaMemsetAsync(fresh.p, 0, static_cast<size_t>(nb) * kVox * sizeof(float4), g->stream));
+            if (g->rms_blocks)
+                SVR_CK(cudaMemcpyAsync(fresh.p, g->rms.p, g->rms_blocks * kVox * sizeof(float4),
+                                       cudaMemcpyDeviceToDevice, g->stream));
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            std::swap(g->rms.p, fresh.p);
+            std::swap(g->rms.bytes, fresh.bytes);
+            g->rms_blocks = nb;
+        }
+        g->active_list.ensure(nb * 4);
+        g->active_count.ensure(8 + 4 * ((nb + 1023) / 1024 + 2));
+        auto* dcount = g->active_count.as<unsigned long long>();
+        svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
+        svr_internal::launch_rmsprop(g->pay, g->grad, g->rms.as<float4>(), g->active,
+                                     g->active_list.as<uint32_t>(), dcount, nb, lr, alpha, eps, g->stream);
         SVR_LAUNCHED();
     });
 }

@@ -113,4 +113,15 @@ void launch_grad_unpack(float4* grad, const uint32_t* blocks, uint64_t n, const 
 void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list,
                              const unsigned long long* count, uint32_t n_max, cudaStream_t s);
 
+// Launchers (svr_regularize.cu)
+void launch_sample_uniform(const int32_t* coords4, uint32_t A, double L, uint64_t n, uint64_t seed,
+                           double* out, cudaStream_t s);
+void launch_eikonal_stats(const svr_dev::GridView& g, const double* x, uint64_t n, double* sums,
+                          cudaStream_t s);
+void launch_eikonal_scatter(const svr_dev::GridView& g, const double* x, uint64_t n, double coef,
+                            cudaStream_t s);
+void launch_rmsprop(float4* pay, float4* grad, float4* rms, uint8_t* active, const uint32_t* list,
+                    const unsigned long long* count, uint32_t n_max, float lr, float alpha, float eps,
+                    cudaStream_t s);
+
 }  // namespace svr_internal

@@ -29,46 +29,10 @@ __global__ void __launch_bounds__(256) k_query(GridView g, const double* __restr
                                                double* rgb, double* logits, uint8_t* valid) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double fx[3];
-    int base[3];
-    for (int a = 0; a < 3; ++a) {
-        const double gg = __dmul_rn(x[3 * i + a], g.inv_h);
-        const double fl = floor(gg);
-        base[a] = static_cast<int>(fl);
-        fx[a] = __dsub_rn(gg, fl);
-    }
-    const double w0[3] = {__dsub_rn(1.0, fx[0]), __dsub_rn(1.0, fx[1]), __dsub_rn(1.0, fx[2])};
-    bool ok = g.n_blocks > 0;
+    const double xp[3] = {x[3 * i], x[3 * i + 1], x[3 * i + 2]};
     uint32_t gidx[8];
     double w[8], dw[8][3];
-    int32_t lbx = INT32_MIN, lby = 0, lbz = 0;
-    uint32_t le = kInvalid;
-    for (int c = 0; c < 8 && ok; ++c) {
-        const int cx = c & 1, cy = (c >> 1) & 1, cz = (c >> 2) & 1;
-        const int vx = base[0] + cx, vy = base[1] + cy, vz = base[2] + cz;
-        const int32_t bx = fdiv8(vx), by = fdiv8(vy), bz = fdiv8(vz);
-        if (bx != lbx || by != lby || bz != lbz) {
-            lbx = bx, lby = by, lbz = bz;
-            le = lookup_block(g, bx, by, bz);
-        }
-        if (le == kInvalid) {
-            ok = false;
-            break;
-        }
-        const uint32_t local = (vx & 7) + 8 * ((vy & 7) + 8 * (vz & 7));
-        if (!voxel_valid(g, le, local)) {
-            ok = false;
-            break;
-        }
-        gidx[c] = (le & ~kFullBit) * kVox + local;
-        const double wx = cx ? fx[0] : w0[0];
-        const double wy = cy ? fx[1] : w0[1];
-        const double wz = cz ? fx[2] : w0[2];
-        w[c] = __dmul_rn(__dmul_rn(wx, wy), wz);
-        dw[c][0] = __dmul_rn(__dmul_rn(__dmul_rn(cx ? 1.0 : -1.0, g.inv_h), wy), wz);
-        dw[c][1] = __dmul_rn(__dmul_rn(__dmul_rn(cy ? 1.0 : -1.0, g.inv_h), wx), wz);
-        dw[c][2] = __dmul_rn(__dmul_rn(__dmul_rn(cz ? 1.0 : -1.0, g.inv_h), wx), wy);
-    }
+    const bool ok = gather_fp64(g, xp, gidx, w, dw);
     if (!ok) {
         if (sdf) sdf[i] = 0.0;
         for (int a = 0; a < 3; ++a) {

@@ -343,6 +343,28 @@ class SparseDenseGrid:
         check(self._lib.svr_active_blocks(self._h, None, lst.ctypes.data, ctypes.addressof(cnt)))
         return lst[: cnt.value].copy()
 
+    # --- losses / update around the path ------------------------------
+    def sample_uniform(self, n: int, seed: int) -> np.ndarray:
+        """sample_uniform (grid.cpp:355-370); counter-based device RNG, not mt19937_64."""
+        out = np.empty((n, 3), np.float64)
+        check(self._lib.svr_sample_uniform(self._h, n, seed, out.ctypes.data if n else None))
+        return out
+
+    def eikonal(self, points, scale: float = 1.0) -> tuple[float, int]:
+        """Eikonal loss mean (|grad f| - 1)^2 over valid points; adds scale * dL/dsdf to the
+        gradient plane.  Returns (loss, n_valid)."""
+        keep: list = []
+        loss = ctypes.c_double()
+        nv = ctypes.c_uint64()
+        n = points.shape[0]
+        check(self._lib.svr_eikonal(self._h, _in(points, np.float64, keep), n, scale, ctypes.byref(loss),
+                                    ctypes.byref(nv)))
+        return loss.value, nv.value
+
+    def rmsprop_step(self, lr: float, alpha: float = 0.99, eps: float = 1e-8) -> None:
+        """RMSProp on active blocks, then zero their gradients."""
+        check(self._lib.svr_rmsprop_step(self._h, lr, alpha, eps))
+
     # device-pointer plumbing for the multi-GPU reduction (paper_2305_13220_b200.distributed)
     def active_set_mask(self, mask) -> None:
         keep: list = []
