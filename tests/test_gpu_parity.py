@@ -185,3 +185,31 @@ def test_device_resident_path_matches_host_path(case):
     g.synchronize()
     for k in ("rgb", "depth", "normal", "wsum"):
         assert np.array_equal(dev[k].cpu().numpy(), host[k]), k
+
+
+@pytest.mark.parametrize("lookup", LOOKUPS)
+def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup):
+    """200k rays from random origins (inside and outside the AABB) with random and nearly
+    axis-parallel directions (components down to 1e-300) -- counts, t, delta bit-exact."""
+    rng = np.random.default_rng(99)
+    n = 200_000
+    o = rng.uniform(-2.0, 2.0, size=(n, 3))
+    d = rng.normal(size=(n, 3))
+    k = n // 8
+    for j, tiny in enumerate((1e-9, 1e-17, 1e-200, 1e-300)):
+        sl = slice(j * k, (j + 1) * k)
+        d[sl, j % 3] = tiny * np.sign(d[sl, j % 3])
+    d[4 * k:5 * k, 1] = 0.0
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    g = gpu_grid_from(case, lookup)
+    m = g.march(o, d, case["step"], 48)
+    OracleGrid.set_threads(8)
+    try:
+        mo = case["oracle"].march(o, d, case["step"], 48)
+    finally:
+        OracleGrid.set_threads(1)
+    assert np.array_equal(m["counts"], mo["counts"])
+    mask = np.arange(48)[None, :] < m["counts"][:, None]
+    assert np.array_equal(m["t"][mask], mo["t"][mask])
+    assert np.array_equal(m["delta"][mask], mo["delta"][mask])
+    assert mask.sum() > 500_000
