@@ -375,6 +375,43 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
+// Reduce 8 per-lane values over the warp with 9 shuffles (reduce-scatter then butterfly):
+// afterwards lane 4 v (v = 0..7) holds the warp total of value v; returns this lane's.
+__device__ __forceinline__ float warp_sum8(const float a[8], int lane) {
+    const bool hi4 = lane & 16, hi3 = lane & 8, hi2 = lane & 4;
+    float b[4], c[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float send = hi4 ? a[k] : a[k + 4];
+        b[k] = (hi4 ? a[k + 4] : a[k]) + __shfl_xor_sync(kFull, send, 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const float send = hi3 ? b[k] : b[k + 2];
+        c[k] = (hi3 ? b[k + 2] : b[k]) + __shfl_xor_sync(kFull, send, 8);
+    }
+    float v = (hi2 ? c[1] : c[0]) + __shfl_xor_sync(kFull, hi2 ? c[0] : c[1], 4);
+    v += __shfl_xor_sync(kFull, v, 2);
+    v += __shfl_xor_sync(kFull, v, 1);
+    return v;
+}
+
+// Ray outputs from warp_sum8's layout: lane 4v writes value v (C.rgb, D, N.xyz, W).
+__device__ __forceinline__ void write_ray_outputs(float v, int lane, uint64_t r, float* rgb, float* depth,
+                                                  float* normal, float* wsum) {
+    if (lane & 3) return;
+    const int k = lane >> 2;
+    if (k < 3) {
+        if (rgb) rgb[3 * r + k] = v;
+    } else if (k == 3) {
+        if (depth) depth[r] = v;
+    } else if (k < 7) {
+        if (normal) normal[3 * r + (k - 4)] = v;
+    } else {
+        if (wsum) wsum[r] = v;
+    }
+}
+
 // Sample k's t and delta (delta_k = t_{k+1} - t_k, last = step: grid.cpp:352) for the
 // lane's two consecutive samples k0 = base + 2 lane, k1 = k0 + 1.
 struct PairT {
@@ -517,15 +554,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const d
         nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
         tau_base += __shfl_sync(kFull, incl, 31);
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = warp_sum(acc[i]);
-    if (lane == 0) {
-        if (rgb) rgb[3 * r] = acc[0], rgb[3 * r + 1] = acc[1], rgb[3 * r + 2] = acc[2];
-        if (depth) depth[r] = acc[3];
-        if (normal) normal[3 * r] = acc[4], normal[3 * r + 1] = acc[5], normal[3 * r + 2] = acc[6];
-        if (wsum) wsum[r] = acc[7];
-        if (valid_counter && nvalid) atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
-    }
+    write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
+    if (lane == 0 && valid_counter && nvalid)
+        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
 }
 
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
@@ -1003,14 +1034,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
         acc[5] = w0v * v0.gy + w1v * v1.gy;
         acc[6] = w0v * v0.gz + w1v * v1.gz;
         acc[7] = w0v + w1v;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = warp_sum(acc[k]);
-        if (lane == 0) {
-            if (rgb) rgb[3 * r] = acc[0], rgb[3 * r + 1] = acc[1], rgb[3 * r + 2] = acc[2];
-            if (depth) depth[r] = acc[3];
-            if (normal) normal[3 * r] = acc[4], normal[3 * r + 1] = acc[5], normal[3 * r + 2] = acc[6];
-            if (wsum) wsum[r] = acc[7];
-        }
+        write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
         __syncwarp();  // stage st is free for refilling
         cur = nxt;
         st = st1;
