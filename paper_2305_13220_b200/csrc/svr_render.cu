@@ -505,8 +505,8 @@ __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__
 // K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
 // chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
 // ---------------------------------------------------------------------------
-template <int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks) k_forward(GridView g, const double* __restrict__ O,
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, const double* __restrict__ O,
                                                     const double* __restrict__ D, uint64_t n,
                                                     const uint32_t* __restrict__ order,
                                                     const uint32_t* __restrict__ counts,
@@ -760,7 +760,7 @@ struct PipeSlot {
     float4 rec[128];
 };
 
-template <int kMinBlocks>
+template <int kMinBlocks, int kMode = 0>
 __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
@@ -852,14 +852,14 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
             if (ok0) mark_blocks(g, v0);
             if (ok1) mark_blocks(g, v1);
             const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-            scatter_corner<0>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<1>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<2>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<3>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<4>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<5>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<6>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<7>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<0, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<1, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<2, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<3, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<4, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<5, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<6, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            scatter_corner<7, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
         st = (st + 1) % kPipeStages;
@@ -1071,14 +1071,17 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
                            cudaStream_t s, int min_blocks) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
-    const unsigned grid = grid_for(n * 32, 256);
-#define SVR_FWD(MB) k_forward<MB><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, rgb, \
-                                                       depth, normal, wsum, valid_counter, rec)
+#define SVR_FWD(TH, MB)                                                                         \
+    k_forward<TH, MB><<<grid_for(n * 32, TH), TH, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
+                                                          rgb, depth, normal, wsum, valid_counter, rec)
     switch (min_blocks) {
-        case 1: SVR_FWD(1); break;
-        case 2: SVR_FWD(2); break;
-        case 3: SVR_FWD(3); break;
-        default: SVR_FWD(4); break;
+        case 1: SVR_FWD(256, 1); break;
+        case 2: SVR_FWD(256, 2); break;
+        case 4: SVR_FWD(256, 4); break;
+        case 11: SVR_FWD(768, 1); break;  // one 24-warp CTA per SM: concurrent warps = adjacent rays
+        case 12: SVR_FWD(512, 1); break;
+        case 13: SVR_FWD(1024, 1); break;
+        default: SVR_FWD(256, 3); break;
     }
 #undef SVR_FWD
 }
@@ -1134,23 +1137,26 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     if (!rec || S > 64 || (S & 1)) return false;
     const size_t smem = sizeof(PipeSlot) * kPipeStages * kPipeWarps + 8 * kPipeStages * kPipeWarps;
     const float ib = static_cast<float>(1.0 / beta);
-    uint64_t ctas = static_cast<uint64_t>(num_sms) * min_blocks;
+    uint64_t ctas = static_cast<uint64_t>(num_sms) * (min_blocks % 100);
     const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
     if (ctas > need) ctas = need;
     const uint64_t warps_total = ctas * kPipeWarps;
-#define SVR_PIPE(MB)                                                                              \
+#define SVR_COMMA2(a, b) a, b
+#define SVR_PIPE(...)                                                                             \
     do {                                                                                          \
-        cudaFuncSetAttribute(k_backward_pipe<MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+        cudaFuncSetAttribute(k_backward_pipe<__VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              static_cast<int>(smem));                                             \
-        k_backward_pipe<MB><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(           \
+        k_backward_pipe<__VA_ARGS__><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(  \
             g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
     } while (0)
     switch (min_blocks) {
         case 1: SVR_PIPE(1); break;
         case 2: SVR_PIPE(2); break;
+        case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
         default: SVR_PIPE(3); break;
     }
 #undef SVR_PIPE
+#undef SVR_COMMA2
     return true;
 }
 
