@@ -200,6 +200,46 @@ int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* 
  * handle (allocated on first use). */
 int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
 
+/* ---- fusion + de-noising (SPEC.md:207-233 module "fusion", PAPER Eq. 9-11, sec. 3.4.3) ----
+ * The reference declares the state (VoxelBlock::sum_*, grid.hpp:59-68) but ships no code;
+ * the contract is the SPEC's:
+ *   association  voxel centre v*h -> Camera::project (camera.cpp:7-18) -> nearest pixel
+ *                floor(p + 0.5) inside the image; depth > 0 and ScaleField value > 0
+ *   distance     d = D(p) * phi(p) - z_v (positive in front of the surface), rejected when
+ *                d < -mu, integrated as psi = min(d, mu)
+ *   running mean sums in 32.32 fixed point + counts: any frame order gives bit-identical
+ *                results; |rgb|, |semantic| * frames must stay < 2^31
+ *   finalize     sdf/rgb/logits = sum / count, logits scaled to unit L2 norm (Eq. 11),
+ *                weight = count (grid.hpp:57-58), voxels never associated keep their
+ *                payload with weight 0 (unobserved)
+ * Images: depth [n][H][W] (<= 0 invalid), rgb [n][H][W][3], semantic [n][H][W][C] (the
+ * reference ImageF32 interleave, frame.hpp:60-67), all frames one size; optional ScaleField
+ * grids scales [n][rows][cols] as in svr_grid_activate_depth. */
+#define SVR_FUSE_COLOR 1
+#define SVR_FUSE_SEMANTIC 2
+typedef struct {
+    uint64_t frames;
+    uint64_t in_view;    /* voxel-frame pairs projecting on a pixel with depth > 0, scale > 0 */
+    uint64_t integrated; /* in_view pairs with d >= -mu */
+    uint64_t rejected;   /* in_view pairs with d < -mu: behind the surface beyond the band */
+} svr_fuse_report;
+/* Open a fusion session (zeroed sums over the current blocks; blocks allocated later join
+ * with zero sums).  flags = SVR_FUSE_COLOR | SVR_FUSE_SEMANTIC selects the fused channels;
+ * the sdf is always fused.  Re-opening discards an open session. */
+int svr_fuse_begin(svr_grid* g, int32_t flags);
+/* fuse_frame over n_frames frames (fuse_all = begin + frames + finalize).  rgb / semantic
+ * must be given exactly when the session's flags select them.  mu in (0, 2^20). */
+int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const float* semantic,
+                    const svr_camera* cams, uint32_t n_frames, const double* scales,
+                    int32_t sf_rows, int32_t sf_cols, double mu, svr_fuse_report* report);
+/* Write the means into the payload and close the session (sums released). */
+int svr_fuse_finalize(svr_grid* g);
+/* denoise(grid, sigma_vox, radius): every property of every valid voxel
+ * (sdf, rgb, logits) becomes the Gaussian-weighted mean over the valid voxels of its
+ * (2r+1)^3 neighbourhood, g(d) = exp(-d^2 / (2 sigma^2)) per axis, weights renormalised over
+ * the valid set; weights / validity unchanged.  radius in [0, 4], sigma_vox > 0. */
+int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius);
+
 #ifdef __cplusplus
 }
 #endif

@@ -148,6 +148,32 @@ class _Base:
                                                     _ptr(counts), _ptr(t), _ptr(delta))
         return {"counts": counts, "t": t, "delta": delta}
 
+    def get_payload(self, first=0, n=None):
+        n = self.block_count() - first if n is None else n
+        V = self.B ** 3
+        out = {"sdf": np.empty((n, V), np.float32), "weight": np.empty((n, V), np.float32),
+               "rgb": np.empty((n, V, 3), np.float32), "logits": np.empty((n, V, self.C), np.float32)}
+        self._check(getattr(self.lib(), self._prefix + "get_payload")(self._h, first, n, *[_ptr(out[k]) for k in
+                                                                     ("sdf", "weight", "rgb", "logits")]))
+        return out
+
+
+    def fuse_begin(self, color=True, semantic=True):
+        self._check(getattr(self.lib(), self._prefix + "fuse_begin")(self._h, int(color) | (int(semantic) << 1)))
+
+    def _fuse_args(self, depth, cams, rgb, sem, scales):
+        d = np.ascontiguousarray(depth, np.float32)
+        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float32)  # noqa: E731
+        arr = (_Cam * len(cams))(*[_Cam.from_any(c) for c in cams])
+        sc = None if scales is None else np.ascontiguousarray(scales, np.float64)
+        rows, cols = (0, 0) if sc is None else (sc.shape[-2], sc.shape[-1])
+        keep = (d, f(rgb), f(sem), sc, arr)
+        return keep, [_ptr(d), _ptr(keep[1]), _ptr(keep[2]), ctypes.addressof(arr), len(cams), _ptr(sc),
+                      rows, cols]
+
+    def fuse_finalize(self):
+        self._check(getattr(self.lib(), self._prefix + "fuse_finalize")(self._h))
+
     def save(self, path):
         self._check(getattr(self.lib(), self._prefix + "save_sdgv")(self._h, str(path).encode()))
 
@@ -180,7 +206,15 @@ _COMMON = {
     "march": (None, [c_void_p, P, P, c_uint64, c_double, c_uint32, P, P, P]),
     "save_sdgv": (c_int, [c_void_p, c_char_p]),
     "load_sdgv": (c_int, [c_char_p, POINTER(c_void_p)]),
+    "get_payload": (c_int, [c_void_p, c_uint32, c_uint32, P, P, P, P]),
+    "fuse_begin": (c_int, [c_void_p, c_int]),
+    "fuse_finalize": (c_int, [c_void_p]),
 }
+
+
+class FuseReport(ctypes.Structure):
+    _fields_ = [("frames", c_uint64), ("in_view", c_uint64), ("integrated", c_uint64),
+                ("rejected", c_uint64)]
 
 
 class OracleGrid(_Base):
@@ -198,6 +232,8 @@ class OracleGrid(_Base):
         "sdf_to_density": (c_double, [c_double, c_double]),
         "eikonal": (c_int, [c_void_p, P, c_uint64, c_double, P, P, POINTER(c_double), POINTER(c_uint64)]),
         "rmsprop": (c_int, [c_void_p, P, P, P, c_float, c_float, c_float, P]),
+        "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double, POINTER(FuseReport)]),
+        "denoise": (c_int, [c_void_p, c_double, c_int]),
     })
 
     def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
@@ -231,15 +267,6 @@ class OracleGrid(_Base):
         hi = np.zeros(3, np.int32)
         st = self.lib().svro_bounds(self._h, _ptr(lo), _ptr(hi))
         return (lo, hi) if st == 0 else None
-
-    def get_payload(self, first=0, n=None):
-        n = self.block_count() - first if n is None else n
-        V = self.B ** 3
-        out = {"sdf": np.empty((n, V), np.float32), "weight": np.empty((n, V), np.float32),
-               "rgb": np.empty((n, V, 3), np.float32), "logits": np.empty((n, V, self.C), np.float32)}
-        self._check(self.lib().svro_get_payload(self._h, first, n, *[_ptr(out[k]) for k in
-                                                                     ("sdf", "weight", "rgb", "logits")]))
-        return out
 
     def query(self, x, logits=False):
         x = _f64(x, (-1, 3))
@@ -298,6 +325,20 @@ def _rmsprop(self, grad_sdf, grad_rgb, active, lr, alpha, eps, rms_state):
     self._check(self.lib().svro_rmsprop(self._h, *[_ptr(a) for a in arrs], lr, alpha, eps, _ptr(rms_state)))
 
 
+def _o_fuse_frames(self, depth, cams, mu, rgb=None, sem=None, scales=None) -> FuseReport:
+    keep, args = self._fuse_args(depth, cams, rgb, sem, scales)
+    rep = FuseReport()
+    self._check(self.lib().svro_fuse_frames(self._h, *args, mu, ctypes.byref(rep)))
+    del keep
+    return rep
+
+
+def _o_denoise(self, sigma_vox=1.0, radius=1):
+    self._check(self.lib().svro_denoise(self._h, sigma_vox, radius))
+
+
+OracleGrid.fuse_frames = _o_fuse_frames
+OracleGrid.denoise = _o_denoise
 OracleGrid.eikonal = _eikonal
 OracleGrid.rmsprop = _rmsprop
 
@@ -315,7 +356,13 @@ class RefGrid(_Base):
         "render_forward": (c_int, [c_void_p, P, P, c_uint64, c_double, c_uint32, c_double, P, P, P, P, P]),
         "render_backward": (c_int, [c_void_p, P, P, P]),
         "grad_get": (c_int, [c_void_p, P, P]),
+        "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double]),
     })
+
+    def fuse_frames(self, depth, cams, mu, rgb=None, sem=None, scales=None):
+        keep, args = self._fuse_args(depth, cams, rgb, sem, scales)
+        self._check(self.lib().svrr_fuse_frames(self._h, *args, mu))
+        del keep
 
     def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
         self.C = label_channels

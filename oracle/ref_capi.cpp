@@ -43,6 +43,10 @@ struct svrr_grid {
     // retained forward context for svrr_render_backward
     std::vector<std::vector<Retained>> rays;
     double beta = 0.0;
+    // fusion session: 32.32 fixed-point sums [voxel][4 + C] + counts (see svr_oracle.cpp)
+    int fuse_flags = -1;
+    std::vector<int64_t> fsum;
+    std::vector<uint32_t> fcount;
 };
 
 typedef struct {
@@ -383,6 +387,124 @@ int svrr_load_sdgv(const char* path, svrr_grid** out) {
         w->g = std::make_unique<SparseDenseGrid>(load_grid(path));
         *out = w;
     });
+}
+
+}  // extern "C"
+
+// Fusion restated ON the reference's own primitives: voxel_to_world
+// (grid.hpp:124), Camera::project + pixel_in_frame (camera.cpp:7-18), ScaleField::value
+// (scale_field.cpp:56-60).  Same association / fixed-point rules as svr_oracle.cpp, so a
+// bit-exact match pins the oracle's projection arithmetic to the reference's.
+extern "C" {
+
+int svrr_fuse_begin(svrr_grid* w, int flags) {
+    return guarded([&] {
+        const size_t V = w->g->voxels_per_block(), nb = w->g->block_count();
+        w->fuse_flags = flags;
+        w->fsum.assign(nb * V * (4 + w->g->label_channels()), 0);
+        w->fcount.assign(nb * V, 0);
+    });
+}
+
+int svrr_fuse_frames(svrr_grid* w, const float* depth, const float* rgb, const float* sem,
+                     const svrr_camera* cams, uint32_t n_frames, const double* scales, int rows,
+                     int cols, double mu) {
+    return guarded([&] {
+        const SparseDenseGrid& g = *w->g;
+        const int B = g.block_res(), C = g.label_channels();
+        const size_t V = g.voxels_per_block(), K = 4 + C, nb = g.block_count();
+        w->fsum.resize(nb * V * K, 0);
+        w->fcount.resize(nb * V, 0);
+        for (uint32_t f = 0; f < n_frames; ++f) {
+            const Camera cam = to_camera(cams[f]);
+            const int W = cam.width, H = cam.height;
+            std::unique_ptr<ScaleField> sf;
+            if (scales) {
+                sf = std::make_unique<ScaleField>(rows, cols, W, H);
+                std::memcpy(sf->values().data(), scales + static_cast<size_t>(f) * rows * cols,
+                            static_cast<size_t>(rows) * cols * 8);
+            }
+            parallel_chunks(nb, [&](std::size_t b0, std::size_t b1, int) {
+                for (std::size_t b = b0; b < b1; ++b) {
+                    const BlockCoord bc = g.block_coord(static_cast<uint32_t>(b));
+                    for (size_t v = 0; v < V; ++v) {
+                        const Eigen::Vector3i vox(bc.x * B + static_cast<int>(v % B),
+                                                  bc.y * B + static_cast<int>((v / B) % B),
+                                                  bc.z * B + static_cast<int>(v / (B * B)));
+                        const Projection pr = cam.project(g.voxel_to_world(vox));
+                        if (pr.behind || !pr.in_frame) continue;
+                        const int ix = static_cast<int>(std::floor(pr.pixel.x() + 0.5));
+                        const int iy = static_cast<int>(std::floor(pr.pixel.y() + 0.5));
+                        const size_t pix = (static_cast<size_t>(f) * H + iy) * W + ix;
+                        const float D = depth[pix];
+                        if (!(D > 0.0f)) continue;
+                        const double phi = sf ? sf->value(ix, iy) : 1.0;
+                        if (!(phi > 0.0)) continue;
+                        const double d = static_cast<double>(D) * phi - pr.depth;
+                        if (d < -mu) continue;
+                        const size_t i = b * V + v;
+                        int64_t* s = &w->fsum[i * K];
+                        auto fix = [](double x) {
+                            return static_cast<int64_t>(std::nearbyint(x * 4294967296.0));
+                        };
+                        s[0] += fix(std::min(d, mu));
+                        if (rgb)
+                            for (int c = 0; c < 3; ++c) s[1 + c] += fix(rgb[3 * pix + c]);
+                        if (sem)
+                            for (int k = 0; k < C; ++k) s[4 + k] += fix(sem[C * pix + k]);
+                        ++w->fcount[i];
+                    }
+                }
+            });
+        }
+    });
+}
+
+int svrr_fuse_finalize(svrr_grid* w) {
+    return guarded([&] {
+        SparseDenseGrid& g = *w->g;
+        const size_t V = g.voxels_per_block(), C = g.label_channels(), K = 4 + C;
+        for (uint32_t b = 0; b < g.block_count(); ++b) {
+            VoxelBlock& blk = g.block(b);
+            for (size_t v = 0; v < V; ++v) {
+                const size_t i = b * V + v;
+                const uint32_t n = i < w->fcount.size() ? w->fcount[i] : 0;
+                blk.weight[v] = static_cast<float>(n);
+                if (!n) continue;
+                const double dn = n;
+                const int64_t* s = &w->fsum[i * K];
+                blk.sdf[v] = static_cast<float>(static_cast<double>(s[0]) * 0x1p-32 / dn);
+                if (w->fuse_flags & 1)
+                    for (int c = 0; c < 3; ++c)
+                        blk.color[3 * v + c] = static_cast<float>(static_cast<double>(s[1 + c]) * 0x1p-32 / dn);
+                if (w->fuse_flags & 2) {
+                    std::vector<double> mm(C);
+                    double n2 = 0.0;
+                    for (size_t k = 0; k < C; ++k) {
+                        mm[k] = static_cast<double>(s[4 + k]) * 0x1p-32 / dn;
+                        n2 = n2 + mm[k] * mm[k];
+                    }
+                    const double nrm = std::sqrt(n2);
+                    for (size_t k = 0; k < C; ++k)
+                        blk.logits[C * v + k] = nrm > 0.0 ? static_cast<float>(mm[k] / nrm) : 0.0f;
+                }
+            }
+        }
+        w->fuse_flags = -1;
+    });
+}
+
+int svrr_get_payload(const svrr_grid* w, uint32_t first, uint32_t n, float* sdf, float* weight,
+                     float* rgb, float* logits) {
+    const size_t V = w->g->voxels_per_block(), C = w->g->label_channels();
+    for (uint32_t i = 0; i < n; ++i) {
+        const VoxelBlock& b = w->g->block(first + i);
+        if (sdf) std::memcpy(sdf + i * V, b.sdf.data(), V * 4);
+        if (weight) std::memcpy(weight + i * V, b.weight.data(), V * 4);
+        if (rgb) std::memcpy(rgb + 3 * i * V, b.color.data(), 3 * V * 4);
+        if (logits) std::memcpy(logits + C * i * V, b.logits.data(), C * V * 4);
+    }
+    return 0;
 }
 
 }  // extern "C"

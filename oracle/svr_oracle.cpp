@@ -161,6 +161,10 @@ struct svro_grid {
     BlockMap map;
     std::vector<BlockCoord> coords;
     std::vector<float> sdf, weight, rgb, logits;
+    // fusion session: fixed-point running sums + counts, see svro_fuse_begin
+    int fuse_flags = -1;           // -1 = no session open
+    std::vector<int64_t> fsum;     // [voxel][4 + C]: sdf, r, g, b, logits
+    std::vector<uint32_t> fcount;  // [voxel]
     BlockCoord lo{0, 0, 0}, hi{0, 0, 0};
 
     double L() const { return h * B; }  // grid.hpp:112
@@ -925,6 +929,230 @@ int svro_load_sdgv(const char* path, svro_grid** out) {
             if (!is) throw Status(kData, "load_grid: truncated block data");
         }
         *out = hold.release();
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Fusion + de-noising (Eq. 9-11).  The reference ships
+// no code for this module; this is the restatement of the SPEC's contract with the
+// decisions the product shares:
+//   * association: voxel centre v*h (grid.hpp:124) -> Camera::project (camera.cpp:7-18,
+//     R^T (x - t) accumulated left to right, z <= 1e-6 = behind, pixel_in_frame margin 0)
+//     -> nearest pixel floor(p + 0.5); depth <= 0 or ScaleField value <= 0 -> no association
+//   * d = D(p) phi(p) - z_v  (positive in front of the surface, the grid's SDF sign; the
+//     SPEC examples fix the sign: d = -0.5 "behind surface" is rejected), reject d < -mu,
+//     integrate psi = min(d, mu)
+//   * running sums in 32.32 fixed point (int64): integer addition is associative, so any
+//     frame order gives bit-identical sums/counts (SPEC.md:227 order-independence)
+//   * finalize: mean = sum * 2^-32 / count; logits scaled to unit L2 norm (Eq. 11);
+//     weight = count (grid.hpp:57-58: weight doubles as the observation count)
+//   * denoise: num/den of a separable Gaussian over the (2r+1)^3 neighbourhood restricted
+//     to valid voxels, accumulated x, then y, then z in fp64; invalid voxels unchanged.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr double kFix = 4294967296.0;          // 2^32
+constexpr double kInvFix = 1.0 / 4294967296.0;  // 2^-32 (exact)
+
+inline int64_t to_fix(double v) { return static_cast<int64_t>(std::nearbyint(v * kFix)); }
+
+// Camera::project + pixel_in_frame (camera.cpp:7-18, camera.hpp:23-25,39-42).
+bool project_px(const svro_camera& c, const double x[3], double& px, double& py, double& z) {
+    const double d[3] = {x[0] - c.t[0], x[1] - c.t[1], x[2] - c.t[2]};
+    double xc[3];
+    for (int r = 0; r < 3; ++r) {  // (R^T)(r, k) = R(k, r)
+        double acc = c.R[r] * d[0];
+        acc = acc + c.R[3 + r] * d[1];
+        acc = acc + c.R[6 + r] * d[2];
+        xc[r] = acc;
+    }
+    if (xc[2] <= 1e-6) return false;
+    z = xc[2];
+    px = c.fx * xc[0] / xc[2] + c.cx;
+    py = c.fy * xc[1] / xc[2] + c.cy;
+    return px >= 0.0 && px <= c.width - 1 - 0.0 && py >= 0.0 && py <= c.height - 1 - 0.0;
+}
+}  // namespace
+
+extern "C" {
+
+int svro_fuse_begin(svro_grid* g, int flags) {
+    return guarded([&] {
+        if (flags & ~3) throw Status(kConfig, "fuse_begin: unknown flags");
+        g->fuse_flags = flags;
+        g->fsum.assign(g->coords.size() * g->V * (4 + g->C), 0);
+        g->fcount.assign(g->coords.size() * g->V, 0);
+    });
+}
+
+int svro_fuse_frames(svro_grid* g, const float* depth, const float* rgb, const float* sem,
+                     const svro_camera* cams, uint32_t n_frames, const double* scales, int sf_rows,
+                     int sf_cols, double mu, svro_fuse_report* rep) {
+    svro_fuse_report r{};
+    const int st = guarded([&] {
+        if (g->fuse_flags < 0) throw Status(kConfig, "fuse: no session (fuse_begin)");
+        if (!(mu > 0.0) || !(mu < 1048576.0)) throw Status(kConfig, "fuse: mu must be in (0, 2^20)");
+        if (((g->fuse_flags & 1) != 0) != (rgb != nullptr) || ((g->fuse_flags & 2) != 0) != (sem != nullptr))
+            throw Status(kConfig, "fuse: channels differ from the session's flags");
+        if (scales && (sf_rows < 2 || sf_cols < 2)) throw Status(kConfig, "scale field needs at least a 2x2 grid");
+        if (n_frames == 0) return;
+        const int W = cams[0].width, H = cams[0].height;
+        for (uint32_t f = 0; f < n_frames; ++f)
+            if (cams[f].width != W || cams[f].height != H)
+                throw Status(kConfig, "fuse: all frames must share one size");
+        if (scales && (W < 2 || H < 2)) throw Status(kConfig, "scale field image size too small");
+        const size_t V = g->V, K = 4 + g->C, nb = g->coords.size();
+        g->fsum.resize(nb * V * K, 0);  // blocks allocated since fuse_begin start empty
+        g->fcount.resize(nb * V, 0);
+        const int B = g->B, C = g->C;
+        std::atomic<uint64_t> a_in{0}, a_rej{0};
+        parallel_chunks(nb, [&](size_t b0, size_t b1) {
+            uint64_t in = 0, rej = 0;
+            for (size_t b = b0; b < b1; ++b)
+                for (size_t v = 0; v < V; ++v) {
+                    const int lx = static_cast<int>(v % B), ly = static_cast<int>((v / B) % B),
+                              lz = static_cast<int>(v / (B * B));
+                    const BlockCoord& bc = g->coords[b];
+                    const double x[3] = {static_cast<double>(bc.x * B + lx) * g->h,
+                                         static_cast<double>(bc.y * B + ly) * g->h,
+                                         static_cast<double>(bc.z * B + lz) * g->h};
+                    const size_t i = b * V + v;
+                    for (uint32_t f = 0; f < n_frames; ++f) {
+                        double px, py, z;
+                        if (!project_px(cams[f], x, px, py, z)) continue;
+                        const int ix = static_cast<int>(std::floor(px + 0.5));
+                        const int iy = static_cast<int>(std::floor(py + 0.5));
+                        const size_t pix = static_cast<size_t>(f) * W * H + static_cast<size_t>(iy) * W + ix;
+                        const float D = depth[pix];
+                        if (!(D > 0.0f)) continue;
+                        const double phi = scales ? scale_value(scales + static_cast<size_t>(f) * sf_rows * sf_cols,
+                                                                sf_rows, sf_cols, W, H, ix, iy)
+                                                  : 1.0;
+                        if (!(phi > 0.0)) continue;
+                        ++in;
+                        const double d = static_cast<double>(D) * phi - z;
+                        if (d < -mu) {
+                            ++rej;
+                            continue;
+                        }
+                        int64_t* s = &g->fsum[i * K];
+                        s[0] += to_fix(std::min(d, mu));
+                        if (rgb)
+                            for (int c = 0; c < 3; ++c) s[1 + c] += to_fix(static_cast<double>(rgb[3 * pix + c]));
+                        if (sem)
+                            for (int k = 0; k < C; ++k)
+                                s[4 + k] += to_fix(static_cast<double>(sem[static_cast<size_t>(C) * pix + k]));
+                        ++g->fcount[i];
+                    }
+                }
+            a_in += in;
+            a_rej += rej;
+        });
+        r.frames = n_frames;
+        r.in_view = a_in;
+        r.rejected = a_rej;
+        r.integrated = r.in_view - r.rejected;
+    });
+    if (rep) *rep = r;
+    return st;
+}
+
+int svro_fuse_finalize(svro_grid* g) {
+    return guarded([&] {
+        if (g->fuse_flags < 0) throw Status(kConfig, "fuse: no session (fuse_begin)");
+        const size_t V = g->V, K = 4 + g->C, C = g->C, nb = g->coords.size();
+        g->fsum.resize(nb * V * K, 0);
+        g->fcount.resize(nb * V, 0);
+        for (size_t i = 0; i < nb * V; ++i) {
+            const uint32_t n = g->fcount[i];
+            g->weight[i] = static_cast<float>(n);
+            if (!n) continue;
+            const double dn = static_cast<double>(n);
+            const int64_t* s = &g->fsum[i * K];
+            g->sdf[i] = static_cast<float>(static_cast<double>(s[0]) * kInvFix / dn);
+            if (g->fuse_flags & 1)
+                for (int c = 0; c < 3; ++c)
+                    g->rgb[3 * i + c] = static_cast<float>(static_cast<double>(s[1 + c]) * kInvFix / dn);
+            if (g->fuse_flags & 2) {
+                double m[64];
+                double nrm2 = 0.0;
+                for (size_t k = 0; k < C; ++k) {
+                    m[k] = static_cast<double>(s[4 + k]) * kInvFix / dn;
+                    nrm2 = nrm2 + m[k] * m[k];
+                }
+                const double nrm = std::sqrt(nrm2);
+                for (size_t k = 0; k < C; ++k)
+                    g->logits[C * i + k] = nrm > 0.0 ? static_cast<float>(m[k] / nrm) : 0.0f;
+            }
+        }
+        g->fuse_flags = -1;
+        std::vector<int64_t>().swap(g->fsum);
+        std::vector<uint32_t>().swap(g->fcount);
+    });
+}
+
+int svro_denoise(svro_grid* g, double sigma_vox, int radius) {
+    return guarded([&] {
+        if (!(sigma_vox > 0.0)) throw Status(kConfig, "denoise: sigma must be positive");
+        if (radius < 0 || radius > 4) throw Status(kConfig, "denoise: radius must be in [0, 4]");
+        if (g->C > 64) throw Status(kConfig, "denoise: at most 64 label channels");
+        double gw[9];
+        for (int d = -radius; d <= radius; ++d)
+            gw[d + radius] = std::exp(-static_cast<double>(d * d) / (2.0 * sigma_vox * sigma_vox));
+        const int B = g->B, C = g->C, K = 4 + C;
+        const size_t V = g->V, nb = g->coords.size();
+        const std::vector<float> sdf0 = g->sdf, rgb0 = g->rgb, lg0 = g->logits;
+        // valid neighbour voxel -> flat index, else -1
+        auto locate = [&](int vx, int vy, int vz) -> int64_t {
+            const BlockCoord bc = g->block_of_voxel(vx, vy, vz);
+            const uint32_t bi = g->map.find(bc);
+            if (bi == kInvalid) return -1;
+            const size_t i = static_cast<size_t>(bi) * V + g->local_index(vx, vy, vz, bc);
+            return g->weight[i] > 0.0f ? static_cast<int64_t>(i) : -1;
+        };
+        auto prop = [&](size_t i, int k) -> double {
+            if (k == 0) return sdf0[i];
+            if (k < 4) return rgb0[3 * i + k - 1];
+            return lg0[static_cast<size_t>(C) * i + k - 4];
+        };
+        parallel_chunks(nb, [&](size_t b0, size_t b1) {
+            std::vector<double> num(K);
+            for (size_t b = b0; b < b1; ++b)
+                for (size_t v = 0; v < V; ++v) {
+                    const size_t i = b * V + v;
+                    if (!(g->weight[i] > 0.0f)) continue;
+                    const BlockCoord& bc = g->coords[b];
+                    const int cx = bc.x * B + static_cast<int>(v % B);
+                    const int cy = bc.y * B + static_cast<int>((v / B) % B);
+                    const int cz = bc.z * B + static_cast<int>(v / (B * B));
+                    std::fill(num.begin(), num.end(), 0.0);
+                    double den = 0.0;
+                    for (int dz = -radius; dz <= radius; ++dz) {
+                        std::vector<double> ny(K, 0.0);
+                        double dy_den = 0.0;
+                        for (int dy = -radius; dy <= radius; ++dy) {
+                            std::vector<double> nx(K, 0.0);
+                            double dx_den = 0.0;
+                            for (int dx = -radius; dx <= radius; ++dx) {
+                                const int64_t j = locate(cx + dx, cy + dy, cz + dz);
+                                const double w = gw[dx + radius];
+                                for (int k = 0; k < K; ++k) nx[k] = nx[k] + w * (j >= 0 ? prop(j, k) : 0.0);
+                                dx_den = dx_den + w * (j >= 0 ? 1.0 : 0.0);
+                            }
+                            const double w = gw[dy + radius];
+                            for (int k = 0; k < K; ++k) ny[k] = ny[k] + w * nx[k];
+                            dy_den = dy_den + w * dx_den;
+                        }
+                        const double w = gw[dz + radius];
+                        for (int k = 0; k < K; ++k) num[k] = num[k] + w * ny[k];
+                        den = den + w * dy_den;
+                    }
+                    g->sdf[i] = static_cast<float>(num[0] / den);
+                    for (int c = 0; c < 3; ++c) g->rgb[3 * i + c] = static_cast<float>(num[1 + c] / den);
+                    for (int k = 0; k < C; ++k) g->logits[static_cast<size_t>(C) * i + k] = static_cast<float>(num[4 + k] / den);
+                }
+        });
     });
 }
 

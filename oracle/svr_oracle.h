@@ -86,6 +86,22 @@ int svro_eikonal(const svro_grid* g, const double* x, uint64_t n, double scale, 
 int svro_rmsprop(svro_grid* g, const double* grad_sdf, const double* grad_rgb, const uint8_t* active,
                  float lr, float alpha, float eps, float* rms_state);
 
+/* Fusion + denoise (decisions in svr_oracle.cpp / DESIGN.md "Fusion").
+ * flags: bit0 fuse color, bit1 fuse semantic logits.  depth [n][H][W], rgb [n][H][W][3],
+ * sem [n][H][W][C], scales [n][rows][cols] (NULL = 1). */
+typedef struct {
+    uint64_t frames;
+    uint64_t in_view;    /* voxel-frame pairs projecting on a pixel with depth > 0 and scale > 0 */
+    uint64_t integrated; /* in_view pairs with d >= -mu */
+    uint64_t rejected;   /* in_view pairs with d < -mu (behind the surface beyond the band) */
+} svro_fuse_report;
+int svro_fuse_begin(svro_grid* g, int flags);
+int svro_fuse_frames(svro_grid* g, const float* depth, const float* rgb, const float* sem,
+                     const svro_camera* cams, uint32_t n_frames, const double* scales, int sf_rows,
+                     int sf_cols, double mu, svro_fuse_report* rep);
+int svro_fuse_finalize(svro_grid* g);
+int svro_denoise(svro_grid* g, double sigma_vox, int radius);
+
 int svro_save_sdgv(const svro_grid* g, const char* path);
 int svro_load_sdgv(const char* path, svro_grid** out);
 

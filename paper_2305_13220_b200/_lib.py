@@ -79,6 +79,11 @@ class RenderStats(ctypes.Structure):
     _fields_ = [("rays", c_uint64), ("samples", c_uint64), ("valid_samples", c_uint64)]
 
 
+class FuseReport(ctypes.Structure):
+    _fields_ = [("frames", c_uint64), ("in_view", c_uint64), ("integrated", c_uint64),
+                ("rejected", c_uint64)]
+
+
 class SceneSpec(ctypes.Structure):
     _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
                 ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
@@ -127,12 +132,18 @@ _PROTOS = {
     "svr_sample_uniform": (_I, [c_void_p, c_uint64, c_uint64, P]),
     "svr_eikonal": (_I, [c_void_p, P, c_uint64, c_double, POINTER(c_double), POINTER(c_uint64)]),
     "svr_rmsprop_step": (_I, [c_void_p, c_float, c_float, c_float]),
+    "svr_fuse_begin": (_I, [c_void_p, c_int32]),
+    "svr_fuse_frames": (_I, [c_void_p, P, P, P, P, c_uint32, P, c_int32, c_int32, c_double,
+                             POINTER(FuseReport)]),
+    "svr_fuse_finalize": (_I, [c_void_p]),
+    "svr_denoise": (_I, [c_void_p, c_double, c_int32]),
     # svr_synth.h (host-only fixtures)
     "svr_scene_spec_default": (None, [POINTER(SceneSpec)]),
     "svr_scene_create": (_I, [POINTER(SceneSpec), POINTER(c_void_p)]),
     "svr_scene_destroy": (None, [c_void_p]),
     "svr_scene_camera": (_I, [c_void_p, c_int32, POINTER(Camera)]),
     "svr_scene_depth": (_I, [c_void_p, P, c_uint32, P, c_int32]),
+    "svr_scene_frames": (_I, [c_void_p, P, c_uint32, P, P, P, c_int32, c_int32]),
     "svr_scene_sdf": (_I, [c_void_p, P, c_uint64, P]),
     "svr_scene_fill_payload": (_I, [c_void_p, c_double, c_int32, c_int32, c_double, P, c_uint64,
                                     P, P, P, P, c_int32]),

@@ -107,27 +107,7 @@ __global__ void k_depth_to_keys(const float* __restrict__ depth, const svr_camer
         have = dv > 0.0f;
         double scale = 1.0;
         if (have && scales) {
-            const double* grid = scales + static_cast<size_t>(f) * rows * cols;
-            const double sx = __ddiv_rn(static_cast<double>(cols - 1), static_cast<double>(W - 1));
-            const double sy = __ddiv_rn(static_cast<double>(rows - 1), static_cast<double>(H - 1));
-            double gx = __dmul_rn(static_cast<double>(x), sx);
-            double gy = __dmul_rn(static_cast<double>(y), sy);
-            const double cmax = static_cast<double>(cols - 1), rmax = static_cast<double>(rows - 1);
-            gx = gx < 0.0 ? 0.0 : (cmax < gx ? cmax : gx);
-            gy = gy < 0.0 ? 0.0 : (rmax < gy ? rmax : gy);
-            const int c0 = min(static_cast<int>(gx), cols - 2);
-            const int r0 = min(static_cast<int>(gy), rows - 2);
-            const double fx = __dsub_rn(gx, static_cast<double>(c0));
-            const double fy = __dsub_rn(gy, static_cast<double>(r0));
-            const int b = r0 * cols + c0;
-            const double w[4] = {__dmul_rn(__dsub_rn(1.0, fx), __dsub_rn(1.0, fy)),
-                                 __dmul_rn(fx, __dsub_rn(1.0, fy)),
-                                 __dmul_rn(__dsub_rn(1.0, fx), fy), __dmul_rn(fx, fy)};
-            const int idx[4] = {b, b + 1, b + cols, b + cols + 1};
-            double v = 0.0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) v = __dadd_rn(v, __dmul_rn(w[k], grid[idx[k]]));
-            scale = v;
+            scale = scale_field_value(scales + static_cast<size_t>(f) * rows * cols, rows, cols, W, H, x, y);
             have = scale > 0.0;
         }
         if (have) {

@@ -5,6 +5,7 @@
 // numerical result comes from the sm_100a kernels in svr_render.cu / svr_activate.cu /
 // svr_grads.cu, and a missing or failing device surfaces as SVR_ERR_CUDA.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -217,6 +218,10 @@ struct svr_grid {
     DevBuf active_list, active_count;  // count: u64 + per-CTA scratch
     DevBuf rms;                        // RMSProp state float4 [rms_blocks][512]
     uint64_t rms_blocks = 0;
+    // fusion session: 32.32 fixed-point sums [fuse_blocks][4 + C][512] + counts [.][512]
+    int fuse_flags = -1;
+    uint64_t fuse_blocks = 0;
+    DevBuf fuse_sum, fuse_cnt;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
     void* sort_tmp_p = nullptr;
     size_t sort_tmp_bytes = 0;
@@ -1142,6 +1147,161 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps) {
         svr_internal::launch_rmsprop(g->pay, g->grad, g->rms.as<float4>(), g->active,
                                      g->active_list.as<uint32_t>(), dcount, nb, lr, alpha, eps, g->stream);
         SVR_LAUNCHED();
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Fusion + de-noising, kernels K12/K13 in svr_fusion.cu.
+// ---------------------------------------------------------------------------
+namespace {
+// Grow the session's sums to the current block count (new rows zero).
+void fuse_grow(svr_grid* g) {
+    const uint64_t nb = g->n();
+    if (g->fuse_blocks >= nb) return;
+    const size_t per_sum = static_cast<size_t>(4 + g->C) * kVox * sizeof(long long);
+    const size_t per_cnt = kVox * sizeof(uint32_t);
+    DevBuf s2, c2;
+    s2.ensure(std::max<size_t>(nb * per_sum, 1));
+    c2.ensure(std::max<size_t>(nb * per_cnt, 1));
+    SVR_CK(cudaMemsetAsync(s2.p, 0, nb * per_sum, g->stream));
+    SVR_CK(cudaMemsetAsync(c2.p, 0, nb * per_cnt, g->stream));
+    if (g->fuse_blocks) {
+        SVR_CK(cudaMemcpyAsync(s2.p, g->fuse_sum.p, g->fuse_blocks * per_sum, cudaMemcpyDeviceToDevice, g->stream));
+        SVR_CK(cudaMemcpyAsync(c2.p, g->fuse_cnt.p, g->fuse_blocks * per_cnt, cudaMemcpyDeviceToDevice, g->stream));
+    }
+    SVR_CK(cudaStreamSynchronize(g->stream));
+    std::swap(g->fuse_sum.p, s2.p);
+    std::swap(g->fuse_sum.bytes, s2.bytes);
+    std::swap(g->fuse_cnt.p, c2.p);
+    std::swap(g->fuse_cnt.bytes, c2.bytes);
+    g->fuse_blocks = nb;
+}
+}  // namespace
+
+int svr_fuse_begin(svr_grid* g, int32_t flags) {
+    return guarded([&] {
+        if (flags & ~(SVR_FUSE_COLOR | SVR_FUSE_SEMANTIC)) throw Fail{SVR_ERR_CONFIG, "fuse_begin: unknown flags"};
+        DeviceGuard dg(g->device);
+        g->fuse_flags = -1;
+        g->fuse_blocks = 0;
+        fuse_grow(g);
+        g->fuse_flags = flags;
+    });
+}
+
+int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const float* semantic,
+                    const svr_camera* cams, uint32_t n_frames, const double* scales, int32_t sf_rows,
+                    int32_t sf_cols, double mu, svr_fuse_report* report) {
+    svr_fuse_report rep{};
+    const int st = guarded([&] {
+        if (g->fuse_flags < 0) throw Fail{SVR_ERR_CONFIG, "fuse: no session (svr_fuse_begin)"};
+        if (!(mu > 0.0) || !(mu < 1048576.0)) throw Fail{SVR_ERR_CONFIG, "fuse: mu must be in (0, 2^20)"};
+        if (((g->fuse_flags & SVR_FUSE_COLOR) != 0) != (rgb != nullptr) ||
+            ((g->fuse_flags & SVR_FUSE_SEMANTIC) != 0) != (semantic != nullptr))
+            throw Fail{SVR_ERR_CONFIG, "fuse: channels differ from the session's flags"};
+        if (scales && (sf_rows < 2 || sf_cols < 2))
+            throw Fail{SVR_ERR_CONFIG, "scale field needs at least a 2x2 grid"};
+        if (n_frames == 0) return;
+        if (!depth || !cams) throw Fail{SVR_ERR_DATA, "fuse: depth and cameras are required"};
+        std::vector<svr_camera> hc(n_frames);
+        if (is_device_ptr(cams))
+            SVR_CK(cudaMemcpy(hc.data(), cams, n_frames * sizeof(svr_camera), cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(hc.data(), cams, n_frames * sizeof(svr_camera));
+        const int32_t W = hc[0].width, H = hc[0].height;
+        for (const svr_camera& c : hc)
+            if (c.width != W || c.height != H) throw Fail{SVR_ERR_CONFIG, "fuse: all frames must share one size"};
+        if (W < 1 || H < 1) throw Fail{SVR_ERR_CONFIG, "fuse: empty image"};
+        if (scales && (W < 2 || H < 2)) throw Fail{SVR_ERR_CONFIG, "scale field image size too small"};
+        DeviceGuard dg(g->device);
+        fuse_grow(g);
+        const uint32_t nb = static_cast<uint32_t>(g->n());
+        const size_t npx = static_cast<size_t>(W) * H;
+        const size_t sf = scales ? static_cast<size_t>(sf_rows) * sf_cols : 0;
+        // frames per launch: keep one launch's images L2-resident (~64 MB)
+        const size_t per_frame = npx * (4 + (rgb ? 12 : 0) + (semantic ? 4 * g->C : 0)) + sf * 8;
+        const uint32_t batch = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(n_frames, (64u << 20) / per_frame)));
+        Stage st(g->stream);
+        auto* counters = static_cast<unsigned long long*>(st.alloc(16));
+        SVR_CK(cudaMemsetAsync(counters, 0, 16, g->stream));
+        const svr_camera* dcams = st.in(cams, n_frames);
+        for (uint32_t f0 = 0; f0 < n_frames; f0 += batch) {
+            const uint32_t nf = std::min(batch, n_frames - f0);
+            Stage sb(g->stream);
+            const float* dd = sb.in(depth + f0 * npx, nf * npx);
+            const float* dr = sb.in(rgb ? rgb + 3 * f0 * npx : nullptr, 3 * nf * npx);
+            const float* ds = sb.in(semantic ? semantic + static_cast<size_t>(g->C) * f0 * npx : nullptr,
+                                    static_cast<size_t>(g->C) * nf * npx);
+            const double* dsc = sb.in(scales ? scales + f0 * sf : nullptr, nf * sf);
+            svr_internal::launch_fuse(g->coords4, nb, dcams + f0, nf, W, H, g->C, dd, dr, ds, dsc, sf_rows,
+                                      sf_cols, g->h, mu, g->fuse_sum.as<long long>(), g->fuse_cnt.as<uint32_t>(),
+                                      counters, g->stream);
+            sb.finish();
+        }
+        unsigned long long hcnt[2] = {0, 0};
+        SVR_CK(cudaMemcpyAsync(hcnt, counters, 16, cudaMemcpyDeviceToHost, g->stream));
+        st.finish();
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        rep.frames = n_frames;
+        rep.in_view = hcnt[0];
+        rep.rejected = hcnt[1];
+        rep.integrated = hcnt[0] - hcnt[1];
+    });
+    if (report) *report = rep;
+    return st;
+}
+
+int svr_fuse_finalize(svr_grid* g) {
+    return guarded([&] {
+        if (g->fuse_flags < 0) throw Fail{SVR_ERR_CONFIG, "fuse: no session (svr_fuse_begin)"};
+        DeviceGuard dg(g->device);
+        fuse_grow(g);
+        svr_internal::launch_fuse_finalize(g->fuse_sum.as<long long>(), g->fuse_cnt.as<uint32_t>(),
+                                           static_cast<uint32_t>(g->n()), g->C, g->fuse_flags, g->pay, g->weight,
+                                           g->logits, g->vmask, g->meta, g->stream);
+        SVR_LAUNCHED();
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        g->dense_dirty = true;
+        g->fuse_flags = -1;
+        g->fuse_blocks = 0;
+        DevBuf rel_s, rel_c;  // the sums are released with these
+        std::swap(rel_s.p, g->fuse_sum.p);
+        std::swap(rel_s.bytes, g->fuse_sum.bytes);
+        std::swap(rel_c.p, g->fuse_cnt.p);
+        std::swap(rel_c.bytes, g->fuse_cnt.bytes);
+    });
+}
+
+int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
+    return guarded([&] {
+        if (!(sigma_vox > 0.0)) throw Fail{SVR_ERR_CONFIG, "denoise: sigma must be positive"};
+        if (radius < 0 || radius > 4) throw Fail{SVR_ERR_CONFIG, "denoise: radius must be in [0, 4]"};
+        DeviceGuard dg(g->device);
+        const uint64_t nb = g->n();
+        if (!nb) return;
+        g->ensure_lookup();
+        double gw[9];
+        for (int d = -radius; d <= radius; ++d)
+            gw[d + radius] = std::exp(-static_cast<double>(d * d) / (2.0 * sigma_vox * sigma_vox));
+        float4* pay2 = nullptr;
+        float* lg2 = nullptr;
+        SVR_CK(cudaMalloc(&pay2, g->cap_blocks * kVox * sizeof(float4)));
+        if (cudaMalloc(&lg2, g->cap_blocks * kVox * g->C * sizeof(float)) != cudaSuccess) {
+            cudaFree(pay2);
+            throw Fail{SVR_ERR_CUDA, "denoise: out of device memory"};
+        }
+        svr_internal::launch_denoise(g->view(), g->coords4, pay2, lg2, radius, gw, g->stream);
+        const cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) SVR_CK(cudaStreamSynchronize(g->stream));
+        if (e != cudaSuccess) {
+            cudaFree(pay2);
+            cudaFree(lg2);
+            throw Fail{SVR_ERR_CUDA, std::string("denoise: ") + cudaGetErrorString(e)};
+        }
+        std::swap(g->pay, pay2);
+        std::swap(g->logits, lg2);
+        cudaFree(pay2);
+        cudaFree(lg2);
     });
 }
 

@@ -124,4 +124,16 @@ void launch_rmsprop(float4* pay, float4* grad, float4* rms, uint8_t* active, con
                     const unsigned long long* count, uint32_t n_max, float lr, float alpha, float eps,
                     cudaStream_t s);
 
+// Fusion + de-noising (svr_fusion.cu)
+void launch_fuse(const int32_t* coords4, uint32_t n_blocks, const svr_camera* cams, uint32_t n_frames,
+                 int32_t W, int32_t H, int32_t C, const float* depth, const float* rgb, const float* sem,
+                 const double* scales, int32_t rows, int32_t cols, double h, double mu, long long* fsum,
+                 uint32_t* fcount, unsigned long long* counters, cudaStream_t s);
+void launch_fuse_finalize(const long long* fsum, const uint32_t* fcount, uint32_t n_blocks, int32_t C,
+                          int flags, float4* pay, float* weight, float* logits, uint32_t* vmask,
+                          uint32_t* meta, cudaStream_t s);
+size_t denoise_smem(int radius);
+void launch_denoise(const svr_dev::GridView& g, const int32_t* coords4, float4* pay_out, float* logits_out,
+                    int32_t radius, const double* gw, cudaStream_t s);
+
 }  // namespace svr_internal

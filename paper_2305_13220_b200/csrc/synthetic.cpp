@@ -124,7 +124,8 @@ struct svr_scene {
         for (int c = 0; c < 3; ++c) rgb[c] = std::min(std::max(kBaseColor[label][c] * m, 0.0), 1.0);
     }
     // SyntheticScene::raycast (synthetic.cpp:89-162): returns z-depth (camera-z unit dir)
-    bool raycast(const svr_camera& cam, double u, double v, double& depth) const {
+    bool raycast(const svr_camera& cam, double u, double v, double& depth, int* label = nullptr,
+                 V3* point = nullptr) const {
         const double dc[3] = {(u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy, 1.0};
         V3 d;
         double dd[3];
@@ -134,6 +135,7 @@ struct svr_scene {
         const V3 o{cam.t[0], cam.t[1], cam.t[2]};
         double best_t = std::numeric_limits<double>::max();
         bool hit = false;
+        int best_label = -1;
         const double rh[3] = {room_half.x, room_half.y, room_half.z};
         for (int a = 0; a < 3; ++a) {
             if (d[a] == 0.0) continue;
@@ -142,6 +144,7 @@ struct svr_scene {
             if (t > 1e-9 && t < best_t) {
                 best_t = t;
                 hit = true;
+                best_label = (a == 2 && d[a] < 0.0) ? kLabelFloor : kLabelWall;
             }
         }
         for (const Object& obj : objects) {
@@ -156,6 +159,7 @@ struct svr_scene {
                 if (t > 1e-9 && t < best_t) {
                     best_t = t;
                     hit = true;
+                    best_label = obj.label;
                 }
             } else {
                 double t0 = -std::numeric_limits<double>::max();
@@ -181,10 +185,13 @@ struct svr_scene {
                 if (ok && t0 < t1 && t0 > 1e-9 && t0 < best_t && enter_axis >= 0) {
                     best_t = t0;
                     hit = true;
+                    best_label = obj.label;
                 }
             }
         }
         depth = best_t;
+        if (label) *label = best_label;
+        if (point) *point = {o.x + best_t * d.x, o.y + best_t * d.y, o.z + best_t * d.z};  // synthetic.cpp:158
         return hit;
     }
     // SyntheticScene::camera_for_frame (synthetic.cpp:164-192)
@@ -284,6 +291,47 @@ int svr_scene_depth(const svr_scene* s, const svr_camera* cams, uint32_t n, floa
                 double dep = 0.0;
                 if (!s->raycast(cams[f], x, y, dep)) escaped = true;
                 depth_out[r * W + x] = static_cast<float>(dep);
+            }
+        }
+    });
+    if (escaped) {
+        svr_internal::set_error("synthetic: ray escaped the room");
+        return SVR_ERR_DATA;
+    }
+    return SVR_OK;
+}
+
+int svr_scene_frames(const svr_scene* s, const svr_camera* cams, uint32_t n, float* depth_out,
+                     float* rgb_out, float* semantic_out, int32_t C, int32_t threads) {
+    if (n == 0) return SVR_OK;
+    if (semantic_out && C < 4) {
+        svr_internal::set_error("synthetic: semantic images need label_channels >= 4");
+        return SVR_ERR_CONFIG;
+    }
+    const int W = cams[0].width, H = cams[0].height;
+    const uint64_t rows = static_cast<uint64_t>(n) * H;
+    bool escaped = false;
+    parallel_range(rows, n_threads(threads), [&](uint64_t b, uint64_t e) {
+        for (uint64_t r = b; r < e; ++r) {
+            const uint32_t f = static_cast<uint32_t>(r / H);
+            const int y = static_cast<int>(r % H);
+            for (int x = 0; x < W; ++x) {
+                double dep = 0.0;
+                int lab = 0;
+                V3 p{0, 0, 0};
+                if (!s->raycast(cams[f], x, y, dep, &lab, &p) || lab < 0) {
+                    escaped = true;
+                    lab = 0;
+                }
+                const uint64_t px = r * W + x;
+                if (depth_out) depth_out[px] = static_cast<float>(dep);
+                if (rgb_out) {  // synthetic.cpp:337-339
+                    double c[3];
+                    s->color(p, lab, c);
+                    for (int k = 0; k < 3; ++k) rgb_out[3 * px + k] = static_cast<float>(c[k]);
+                }
+                if (semantic_out)  // synthetic.cpp:336: one-hot
+                    for (int k = 0; k < C; ++k) semantic_out[C * px + k] = (k == lab) ? 1.0f : 0.0f;
             }
         }
     });

@@ -15,7 +15,7 @@ from typing import Any
 import numpy as np
 
 from . import _lib
-from ._lib import AllocReport, Camera, GridInfo, RenderStats, check
+from ._lib import AllocReport, Camera, FuseReport, GridInfo, RenderStats, check
 
 try:  # torch is plumbing only (device buffers, streams); numpy works without it
     import torch
@@ -364,6 +364,40 @@ class SparseDenseGrid:
     def rmsprop_step(self, lr: float, alpha: float = 0.99, eps: float = 1e-8) -> None:
         """RMSProp on active blocks, then zero their gradients."""
         check(self._lib.svr_rmsprop_step(self._h, lr, alpha, eps))
+
+    # --- fusion + de-noising (SPEC.md:207-233) -----------------------------------------
+    def fuse_begin(self, color: bool = True, semantic: bool = True) -> None:
+        """Open a fusion session (zeroed fixed-point sums); see include/svr.h."""
+        check(self._lib.svr_fuse_begin(self._h, (1 if color else 0) | (2 if semantic else 0)))
+
+    def fuse_frames(self, depth, cameras, mu: float, rgb=None, semantic=None, scales=None) -> FuseReport:
+        """fuse_frame over depth[F][H][W] (+ rgb[F][H][W][3], semantic[F][H][W][C])."""
+        keep: list = []
+        cams = (Camera * len(cameras))(*cameras)
+        sc_ptr, rows, cols = None, 0, 0
+        if scales is not None:
+            sc = np.ascontiguousarray(scales, dtype=np.float64)
+            rows, cols = sc.shape[-2], sc.shape[-1]
+            sc_ptr = _in(sc, np.float64, keep)
+        rep = FuseReport()
+        check(self._lib.svr_fuse_frames(self._h, _in(depth, np.float32, keep), _in(rgb, np.float32, keep),
+                                        _in(semantic, np.float32, keep), ctypes.addressof(cams), len(cameras),
+                                        sc_ptr, rows, cols, mu, ctypes.byref(rep)))
+        return rep
+
+    def fuse_finalize(self) -> None:
+        check(self._lib.svr_fuse_finalize(self._h))
+
+    def fuse_all(self, depth, cameras, mu: float, rgb=None, semantic=None, scales=None) -> FuseReport:
+        """fuse_all: begin + every frame + finalize."""
+        self.fuse_begin(rgb is not None, semantic is not None)
+        rep = self.fuse_frames(depth, cameras, mu, rgb, semantic, scales)
+        self.fuse_finalize()
+        return rep
+
+    def denoise(self, sigma_vox: float = 1.0, radius: int = 1) -> None:
+        """denoise: separable Gaussian over the valid neighbourhood."""
+        check(self._lib.svr_denoise(self._h, sigma_vox, radius))
 
     # device-pointer plumbing for the multi-GPU reduction (paper_2305_13220_b200.distributed)
     def active_set_mask(self, mask) -> None:

@@ -51,6 +51,19 @@ class SyntheticScene:
                                         threads))
         return out
 
+    def frames(self, cams: list[Camera], threads: int = 0, label_channels: int | None = None):
+        """(depth[F][H][W], rgb[F][H][W][3], semantic[F][H][W][C]) as generate_dataset renders
+        them (synthetic.cpp:318-340): GT z-depth, scene colour at the hit, one-hot hit label."""
+        C = self.spec.label_channels if label_channels is None else label_channels
+        arr = (Camera * len(cams))(*cams)
+        F, H, W = len(cams), self.spec.height, self.spec.width
+        depth = np.empty((F, H, W), np.float32)
+        rgb = np.empty((F, H, W, 3), np.float32)
+        sem = np.empty((F, H, W, C), np.float32)
+        check(self._lib.svr_scene_frames(self._h, ctypes.addressof(arr), F, depth.ctypes.data,
+                                         rgb.ctypes.data, sem.ctypes.data, C, threads))
+        return depth, rgb, sem
+
     def sdf(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
         out = np.empty(len(x), np.float64)

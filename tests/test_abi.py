@@ -49,7 +49,8 @@ def test_kernels_are_sm100a_sass():
     out = subprocess.run([tool, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     names = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
-    for k in ("k_march", "k_forward", "k_backward", "k_query", "k_depth_to_keys", "k_hash_find"):
+    for k in ("k_march", "k_forward", "k_backward", "k_query", "k_depth_to_keys", "k_hash_find", "k_fuse",
+              "k_denoise"):
         assert k in names, k
     assert "REDG.E.ADD.F32x4" in names  # vector float atomics in the backward scatter
 
