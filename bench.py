@@ -451,7 +451,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world == 1 and not args.no_extra:
         try:
             line["extra_configs"] = {"cfg2_image_forward": bench_cfg2(dev, stream),
-                                     "cfg4_activation_and_query": bench_cfg4(dev, stream)}
+                                     "cfg4_activation_and_query": bench_cfg4(dev, stream),
+                                     "cfg3_fusion_and_denoise": bench_fusion(dev, stream,
+                                                                             cpu=not args.no_cpu_baseline)}
         except Exception as e:  # pragma: no cover
             line["extra_configs"] = {"error": str(e)}
     if world == 1 and not args.no_cpu_baseline:
@@ -547,6 +549,63 @@ def bench_cfg4(dev, stream, n_frames=300, k=256):
             "blocks_per_s": rep.blocks_added / act_s, "query_points": len(pts),
             "query_valid": int(valid.sum().item()), "query_ms": ms,
             "query_points_per_s": len(pts) / (ms * 1e-3)}
+
+
+def bench_fusion(dev, stream, cpu=True):
+    """SURVEY.md 8(f) rank 3 on the cfg3 grid: fuse_all of the 64 activation frames (640x480
+    GT depth + rgb + one-hot semantics, mu = L*R) from HBM-resident images, then denoise
+    (radius 1, sigma 1 voxel).  CPU: the oracle on all host cores over the first 2 frames."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    cfg = CFG3
+    scene = make_scene(cfg)
+    cams = scene.cameras(cfg["act_frames"])
+    depth, rgb, sem = scene.frames(cams)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
+    g.set_stream(stream)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    mu = 8 * cfg["h"] * cfg["dilation"]
+    dd, dr, ds = (torch.from_numpy(a).to(dev) for a in (depth, rgb, sem))
+    torch.cuda.synchronize()
+    rep = {}
+
+    def fuse():
+        rep["r"] = g.fuse_all(dd, cams, mu, rgb=dr, semantic=ds)
+
+    fuse_ms = _events_ms(stream, fuse, 3)
+    r = rep["r"]
+    den_ms = _events_ms(stream, lambda: g.denoise(1.0, 1), 3)
+    A, C = g.block_count(), cfg["C"]
+    vox = A * 512
+    # algorithmic bytes of one denoise: read + write payload float4 + logits, read validity
+    den_bytes = vox * (16 + 4 * C) * 2 + A * 64
+    out = {"blocks": A, "frames": len(cams), "voxel_frame_pairs": vox * len(cams),
+           "associations": int(r.in_view), "integrated": int(r.integrated), "rejected": int(r.rejected),
+           "fuse_all_ms": fuse_ms, "voxel_frames_per_s": vox * len(cams) / (fuse_ms * 1e-3),
+           "associations_per_s": r.in_view / (fuse_ms * 1e-3),
+           "denoise_ms": den_ms, "denoise_voxels_per_s": vox / (den_ms * 1e-3),
+           "denoise_GBps_algorithmic": den_bytes / (den_ms * 1e-3) / 1e9,
+           "launches": {"fuse_all": "memset x2 + k_fuse x ceil(64 / batch) + k_fuse_finalize",
+                        "denoise": "k_denoise x1"}}
+    if cpu:
+        from oracle import OracleGrid
+
+        og = OracleGrid(cfg["h"], 8, C, capacity=max(A, 1 << 21))
+        og.allocate_blocks(g.coords())
+        cores = os.cpu_count() or 1
+        OracleGrid.set_threads(cores)
+        og.fuse_begin(True, True)
+        t0 = time.perf_counter()
+        og.fuse_frames(depth[:2], cams[:2], mu, rgb=rgb[:2], sem=sem[:2])
+        dt = time.perf_counter() - t0
+        OracleGrid.set_threads(1)
+        out["cpu_baseline"] = {"value": vox * 2 / dt, "unit": "voxel_frames/s", "cores": cores, "kind": "port",
+                               "sample": f"fuse_frames over the first 2 frames ({dt:.2f} s)"}
+    del g
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

@@ -110,7 +110,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather),
  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
  * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
- * "pipe_min_blocks". */
+ * "pipe_min_blocks", "fuse_batch" (frames per fusion launch, 0 = auto). */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 
 /* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */
@@ -208,7 +208,8 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
  *   distance     d = D(p) * phi(p) - z_v (positive in front of the surface), rejected when
  *                d < -mu, integrated as psi = min(d, mu)
  *   running mean sums in 32.32 fixed point + counts: any frame order gives bit-identical
- *                results; |rgb|, |semantic| * frames must stay < 2^31
+ *                results; each |rgb|, |semantic| value < 2^19 and every
+ *                per-voxel sum < 2^31 in magnitude
  *   finalize     sdf/rgb/logits = sum / count, logits scaled to unit L2 norm (Eq. 11),
  *                weight = count (grid.hpp:57-58), voxels never associated keep their
  *                payload with weight 0 (unobserved)
@@ -228,7 +229,7 @@ typedef struct {
  * the sdf is always fused.  Re-opening discards an open session. */
 int svr_fuse_begin(svr_grid* g, int32_t flags);
 /* fuse_frame over n_frames frames (fuse_all = begin + frames + finalize).  rgb / semantic
- * must be given exactly when the session's flags select them.  mu in (0, 2^20). */
+ * must be given exactly when the session's flags select them.  mu in (0, 2^19). */
 int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const float* semantic,
                     const svr_camera* cams, uint32_t n_frames, const double* scales,
                     int32_t sf_rows, int32_t sf_cols, double mu, svr_fuse_report* report);

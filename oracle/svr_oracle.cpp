@@ -992,7 +992,7 @@ int svro_fuse_frames(svro_grid* g, const float* depth, const float* rgb, const f
     svro_fuse_report r{};
     const int st = guarded([&] {
         if (g->fuse_flags < 0) throw Status(kConfig, "fuse: no session (fuse_begin)");
-        if (!(mu > 0.0) || !(mu < 1048576.0)) throw Status(kConfig, "fuse: mu must be in (0, 2^20)");
+        if (!(mu > 0.0) || !(mu < 524288.0)) throw Status(kConfig, "fuse: mu must be in (0, 2^19)");
         if (((g->fuse_flags & 1) != 0) != (rgb != nullptr) || ((g->fuse_flags & 2) != 0) != (sem != nullptr))
             throw Status(kConfig, "fuse: channels differ from the session's flags");
         if (scales && (sf_rows < 2 || sf_cols < 2)) throw Status(kConfig, "scale field needs at least a 2x2 grid");

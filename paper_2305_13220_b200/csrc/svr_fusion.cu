@@ -15,9 +15,15 @@ namespace {
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr double kFix = 4294967296.0;          // 2^32
 constexpr double kInvFix = 1.0 / 4294967296.0;  // 2^-32
-constexpr int kFuseThreads = 256;               // 2 voxels per thread
+constexpr int kFuseThreads = 512;               // one voxel per thread
 
-__device__ __forceinline__ long long to_fix(double v) { return __double2ll_rn(__dmul_rn(v, kFix)); }
+// round-to-nearest-even of v * 2^32 through the 1.5 * 2^52 shifter: one DADD + one integer
+// subtract instead of an XU conversion; exact (== llrint) for |v| < 2^19, the input domain
+// svr_fuse_frames documents.
+__device__ __forceinline__ long long to_fix(double v) {
+    const double t = __dadd_rn(__dmul_rn(v, kFix), 6755399441055744.0);
+    return __double_as_longlong(t) - 0x4338000000000000LL;
+}
 
 // Conservative per-(block, frame) cull: the block's voxel centres span the box
 // [c*8, c*8+7] * h.  bit0: corner surely behind the camera (z < -1e-6); bit5: corner not
@@ -52,63 +58,69 @@ struct FuseArgs {
     unsigned long long* counters;  // in_view, rejected
 };
 
-// One CTA per block, 2 voxels per thread, the frame batch looped inside so the running sums
-// live in registers for the whole launch (KC >= 0: C logit sums in registers too; KC < 0:
-// logit sums read-modify-written in HBM, each voxel owned by one thread).
+// One CTA of 512 threads per block (one voxel per thread), the frame batch looped inside so
+// the running sums live in registers for the whole launch (KC > 0: the C logit sums too;
+// KC <= 0: logit sums read-modify-written in HBM, each voxel owned by one thread).  Frames
+// are taken 64 at a time: one pass evaluates the block-vs-frame cull for all 64 (thread =
+// frame * 8 + corner), then the CTA walks only the visible frames without further barriers.
 template <int KC>
 __global__ void __launch_bounds__(kFuseThreads) k_fuse(FuseArgs a) {
-    __shared__ unsigned s_cull;
+    __shared__ unsigned s_vis[kFuseThreads / 32];
     const uint32_t b = blockIdx.x;
     const int4 bc = a.coords[b];
     const int K = 4 + a.C;
     constexpr int KR = KC > 0 ? KC : 1;
-    long long acc[2][4];
-    long long lacc[2][KR];
-    uint32_t cnt[2];
-    double x[2][3];
+    const int v = threadIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     long long* base = a.fsum + static_cast<size_t>(b) * K * kVox;
+    long long acc[4];
+    long long lacc[KR];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int v = threadIdx.x + j * kFuseThreads;
+    for (int k = 0; k < 4; ++k) acc[k] = base[k * kVox + v];
+    if (KC > 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[j][k] = base[k * kVox + v];
-        if (KC > 0) {
-#pragma unroll
-            for (int k = 0; k < KR; ++k) lacc[j][k] = base[(4 + k) * kVox + v];
-        }
-        cnt[j] = a.fcount[static_cast<size_t>(b) * kVox + v];
-        // voxel_to_world (grid.hpp:124-126)
-        x[j][0] = __dmul_rn(static_cast<double>(bc.x * kRes + (v & 7)), a.h);
-        x[j][1] = __dmul_rn(static_cast<double>(bc.y * kRes + ((v >> 3) & 7)), a.h);
-        x[j][2] = __dmul_rn(static_cast<double>(bc.z * kRes + (v >> 6)), a.h);
+        for (int k = 0; k < KR; ++k) lacc[k] = base[(4 + k) * kVox + v];
     }
+    uint32_t cnt = a.fcount[static_cast<size_t>(b) * kVox + v];
+    // voxel_to_world (grid.hpp:124-126)
+    const double x0 = __dmul_rn(static_cast<double>(bc.x * kRes + (v & 7)), a.h);
+    const double x1 = __dmul_rn(static_cast<double>(bc.y * kRes + ((v >> 3) & 7)), a.h);
+    const double x2 = __dmul_rn(static_cast<double>(bc.z * kRes + (v >> 6)), a.h);
     unsigned long long in_view = 0, rejected = 0;
     const size_t npx = static_cast<size_t>(a.W) * a.H;
-    for (uint32_t f = 0; f < a.n_frames; ++f) {
-        const svr_camera& c = a.cams[f];
-        if (threadIdx.x < 32) {
-            unsigned fl = 0;
-            if (threadIdx.x < 8) {
-                const int cc = threadIdx.x;
+    for (uint32_t f0 = 0; f0 < a.n_frames; f0 += 64) {
+        const uint32_t nf = min(64u, a.n_frames - f0);
+        {
+            const uint32_t fr = threadIdx.x >> 3;
+            const int cc = threadIdx.x & 7;
+            unsigned fl = 63u;
+            if (fr < nf) {
                 const double cx[3] = {(bc.x * kRes + 7.0 * (cc & 1)) * a.h,
                                       (bc.y * kRes + 7.0 * ((cc >> 1) & 1)) * a.h,
                                       (bc.z * kRes + 7.0 * (cc >> 2)) * a.h};
-                fl = corner_flags(c, cx);
+                fl = corner_flags(a.cams[f0 + fr], cx);
             }
-            const unsigned all = __reduce_and_sync(kFull, threadIdx.x < 8 ? fl : 63u);
-            const unsigned any_near = __reduce_or_sync(kFull, threadIdx.x < 8 ? (fl & 32u) : 0u);
-            if (threadIdx.x == 0) s_cull = (all & 1u) || (!any_near && (all & 30u));
+            unsigned all = fl, any_near = fl & 32u;
+#pragma unroll
+            for (int off = 1; off < 8; off <<= 1) {
+                all &= __shfl_xor_sync(kFull, all, off);
+                any_near |= __shfl_xor_sync(kFull, any_near, off);
+            }
+            const bool vis = fr < nf && !((all & 1u) || (!any_near && (all & 30u)));
+            const unsigned bal = __ballot_sync(kFull, vis && cc == 0);  // bits 0, 8, 16, 24
+            if (lane == 0)
+                s_vis[warp] = (bal & 1u) | ((bal >> 7) & 2u) | ((bal >> 14) & 4u) | ((bal >> 21) & 8u);
         }
         __syncthreads();
-        const bool cull = s_cull;
-        __syncthreads();
-        if (cull) continue;
-        const float* dimg = a.depth + f * npx;
+        unsigned long long mask = 0;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int w = 0; w < 16; ++w) mask |= static_cast<unsigned long long>(s_vis[w]) << (4 * w);
+        __syncthreads();
+        while (mask) {
+            const uint32_t f = f0 + __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            const svr_camera& c = a.cams[f];
             // Camera::project (camera.cpp:7-18): x_c = R^T (x - t), accumulated left to right
-            const double d0 = __dsub_rn(x[j][0], c.t[0]), d1 = __dsub_rn(x[j][1], c.t[1]),
-                         d2 = __dsub_rn(x[j][2], c.t[2]);
+            const double d0 = __dsub_rn(x0, c.t[0]), d1 = __dsub_rn(x1, c.t[1]), d2 = __dsub_rn(x2, c.t[2]);
             double xc[3];
 #pragma unroll
             for (int r = 0; r < 3; ++r)
@@ -123,7 +135,8 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(FuseArgs a) {
             const int ix = static_cast<int>(floor(__dadd_rn(px, 0.5)));
             const int iy = static_cast<int>(floor(__dadd_rn(py, 0.5)));
             const size_t pix = static_cast<size_t>(iy) * a.W + ix;
-            const float D = __ldg(dimg + pix);
+            const size_t gp = f * npx + pix;
+            const float D = __ldg(a.depth + gp);
             if (!(D > 0.0f)) continue;
             double phi = 1.0;
             if (a.scales) {
@@ -137,42 +150,36 @@ __global__ void __launch_bounds__(kFuseThreads) k_fuse(FuseArgs a) {
                 ++rejected;
                 continue;
             }
-            acc[j][0] += to_fix(smin(sd, a.mu));
-            const size_t gp = f * npx + pix;
+            acc[0] += to_fix(smin(sd, a.mu));
             if (a.rgb) {
 #pragma unroll
-                for (int k = 0; k < 3; ++k) acc[j][1 + k] += to_fix(static_cast<double>(__ldg(a.rgb + 3 * gp + k)));
+                for (int k = 0; k < 3; ++k) acc[1 + k] += to_fix(static_cast<double>(__ldg(a.rgb + 3 * gp + k)));
             }
             if (a.sem) {
                 const float* sp = a.sem + static_cast<size_t>(a.C) * gp;
                 if (KC > 0) {
 #pragma unroll
-                    for (int k = 0; k < KR; ++k) lacc[j][k] += to_fix(static_cast<double>(__ldg(sp + k)));
+                    for (int k = 0; k < KR; ++k) lacc[k] += to_fix(static_cast<double>(__ldg(sp + k)));
                 } else {
-                    const int v = threadIdx.x + j * kFuseThreads;
                     for (int k = 0; k < a.C; ++k) base[(4 + k) * kVox + v] += to_fix(static_cast<double>(__ldg(sp + k)));
                 }
             }
-            ++cnt[j];
+            ++cnt;
         }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int v = threadIdx.x + j * kFuseThreads;
+    for (int k = 0; k < 4; ++k) base[k * kVox + v] = acc[k];
+    if (KC > 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) base[k * kVox + v] = acc[j][k];
-        if (KC > 0) {
-#pragma unroll
-            for (int k = 0; k < KR; ++k) base[(4 + k) * kVox + v] = lacc[j][k];
-        }
-        a.fcount[static_cast<size_t>(b) * kVox + v] = cnt[j];
+        for (int k = 0; k < KR; ++k) base[(4 + k) * kVox + v] = lacc[k];
     }
+    a.fcount[static_cast<size_t>(b) * kVox + v] = cnt;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         in_view += __shfl_xor_sync(kFull, in_view, off);
         rejected += __shfl_xor_sync(kFull, rejected, off);
     }
-    if ((threadIdx.x & 31) == 0 && in_view) {
+    if (lane == 0 && in_view) {
         atomicAdd(a.counters, in_view);
         if (rejected) atomicAdd(a.counters + 1, rejected);
     }

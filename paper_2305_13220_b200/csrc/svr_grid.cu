@@ -221,6 +221,9 @@ struct svr_grid {
     // fusion session: 32.32 fixed-point sums [fuse_blocks][4 + C][512] + counts [.][512]
     int fuse_flags = -1;
     uint64_t fuse_blocks = 0;
+    uint32_t fuse_batch = 0;  // frames per k_fuse launch, 0 = auto
+    DevBuf pay_spare, logits_spare;  // denoise output planes, swapped with pay / logits
+    uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
     void* sort_tmp_p = nullptr;
@@ -547,6 +550,9 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "fuse_batch") {
+            if (value < 0) throw Fail{SVR_ERR_CONFIG, "tuning: fuse_batch >= 0"};
+            g->fuse_batch = static_cast<uint32_t>(value);
         } else {
             throw Fail{SVR_ERR_CONFIG, "tuning: unknown key " + k};
         }
@@ -1154,26 +1160,31 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps) {
 // Fusion + de-noising, kernels K12/K13 in svr_fusion.cu.
 // ---------------------------------------------------------------------------
 namespace {
-// Grow the session's sums to the current block count (new rows zero).
+// Grow the session's sums to the current block count (new rows zero).  The buffers stay
+// cached in the handle between sessions (re-zeroed by svr_fuse_begin).
 void fuse_grow(svr_grid* g) {
     const uint64_t nb = g->n();
     if (g->fuse_blocks >= nb) return;
     const size_t per_sum = static_cast<size_t>(4 + g->C) * kVox * sizeof(long long);
     const size_t per_cnt = kVox * sizeof(uint32_t);
-    DevBuf s2, c2;
-    s2.ensure(std::max<size_t>(nb * per_sum, 1));
-    c2.ensure(std::max<size_t>(nb * per_cnt, 1));
-    SVR_CK(cudaMemsetAsync(s2.p, 0, nb * per_sum, g->stream));
-    SVR_CK(cudaMemsetAsync(c2.p, 0, nb * per_cnt, g->stream));
-    if (g->fuse_blocks) {
-        SVR_CK(cudaMemcpyAsync(s2.p, g->fuse_sum.p, g->fuse_blocks * per_sum, cudaMemcpyDeviceToDevice, g->stream));
-        SVR_CK(cudaMemcpyAsync(c2.p, g->fuse_cnt.p, g->fuse_blocks * per_cnt, cudaMemcpyDeviceToDevice, g->stream));
+    if (g->fuse_sum.bytes < nb * per_sum || g->fuse_cnt.bytes < nb * per_cnt) {
+        DevBuf s2, c2;
+        const uint64_t rows = std::max<uint64_t>(nb, g->cap_blocks);
+        s2.ensure(rows * per_sum);
+        c2.ensure(rows * per_cnt);
+        if (g->fuse_blocks) {
+            SVR_CK(cudaMemcpyAsync(s2.p, g->fuse_sum.p, g->fuse_blocks * per_sum, cudaMemcpyDeviceToDevice, g->stream));
+            SVR_CK(cudaMemcpyAsync(c2.p, g->fuse_cnt.p, g->fuse_blocks * per_cnt, cudaMemcpyDeviceToDevice, g->stream));
+        }
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        std::swap(g->fuse_sum.p, s2.p);
+        std::swap(g->fuse_sum.bytes, s2.bytes);
+        std::swap(g->fuse_cnt.p, c2.p);
+        std::swap(g->fuse_cnt.bytes, c2.bytes);
     }
-    SVR_CK(cudaStreamSynchronize(g->stream));
-    std::swap(g->fuse_sum.p, s2.p);
-    std::swap(g->fuse_sum.bytes, s2.bytes);
-    std::swap(g->fuse_cnt.p, c2.p);
-    std::swap(g->fuse_cnt.bytes, c2.bytes);
+    const uint64_t f = g->fuse_blocks;
+    SVR_CK(cudaMemsetAsync(static_cast<char*>(g->fuse_sum.p) + f * per_sum, 0, (nb - f) * per_sum, g->stream));
+    SVR_CK(cudaMemsetAsync(static_cast<char*>(g->fuse_cnt.p) + f * per_cnt, 0, (nb - f) * per_cnt, g->stream));
     g->fuse_blocks = nb;
 }
 }  // namespace
@@ -1195,7 +1206,7 @@ int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const flo
     svr_fuse_report rep{};
     const int st = guarded([&] {
         if (g->fuse_flags < 0) throw Fail{SVR_ERR_CONFIG, "fuse: no session (svr_fuse_begin)"};
-        if (!(mu > 0.0) || !(mu < 1048576.0)) throw Fail{SVR_ERR_CONFIG, "fuse: mu must be in (0, 2^20)"};
+        if (!(mu > 0.0) || !(mu < 524288.0)) throw Fail{SVR_ERR_CONFIG, "fuse: mu must be in (0, 2^19)"};
         if (((g->fuse_flags & SVR_FUSE_COLOR) != 0) != (rgb != nullptr) ||
             ((g->fuse_flags & SVR_FUSE_SEMANTIC) != 0) != (semantic != nullptr))
             throw Fail{SVR_ERR_CONFIG, "fuse: channels differ from the session's flags"};
@@ -1218,9 +1229,16 @@ int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const flo
         const uint32_t nb = static_cast<uint32_t>(g->n());
         const size_t npx = static_cast<size_t>(W) * H;
         const size_t sf = scales ? static_cast<size_t>(sf_rows) * sf_cols : 0;
-        // frames per launch: keep one launch's images L2-resident (~64 MB)
+        // frames per launch: every launch streams the running sums once (~(8 (4 + C) + 4) B per
+        // voxel each way), so a launch takes as many frames as possible -- all of them when the
+        // images are device-resident, else what 1 GB of staging holds.
         const size_t per_frame = npx * (4 + (rgb ? 12 : 0) + (semantic ? 4 * g->C : 0)) + sf * 8;
-        const uint32_t batch = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(n_frames, (64u << 20) / per_frame)));
+        const bool resident = is_device_ptr(depth) && (!rgb || is_device_ptr(rgb)) &&
+                              (!semantic || is_device_ptr(semantic)) && (!scales || is_device_ptr(scales));
+        const uint32_t batch = g->fuse_batch ? std::min(g->fuse_batch, n_frames)
+                               : resident ? n_frames
+                                        : static_cast<uint32_t>(std::max<size_t>(
+                                              1, std::min<size_t>(n_frames, (1ull << 30) / per_frame)));
         Stage st(g->stream);
         auto* counters = static_cast<unsigned long long*>(st.alloc(16));
         SVR_CK(cudaMemsetAsync(counters, 0, 16, g->stream));
@@ -1264,11 +1282,6 @@ int svr_fuse_finalize(svr_grid* g) {
         g->dense_dirty = true;
         g->fuse_flags = -1;
         g->fuse_blocks = 0;
-        DevBuf rel_s, rel_c;  // the sums are released with these
-        std::swap(rel_s.p, g->fuse_sum.p);
-        std::swap(rel_s.bytes, g->fuse_sum.bytes);
-        std::swap(rel_c.p, g->fuse_cnt.p);
-        std::swap(rel_c.bytes, g->fuse_cnt.bytes);
     });
 }
 
@@ -1283,25 +1296,24 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
         double gw[9];
         for (int d = -radius; d <= radius; ++d)
             gw[d + radius] = std::exp(-static_cast<double>(d * d) / (2.0 * sigma_vox * sigma_vox));
-        float4* pay2 = nullptr;
-        float* lg2 = nullptr;
-        SVR_CK(cudaMalloc(&pay2, g->cap_blocks * kVox * sizeof(float4)));
-        if (cudaMalloc(&lg2, g->cap_blocks * kVox * g->C * sizeof(float)) != cudaSuccess) {
-            cudaFree(pay2);
-            throw Fail{SVR_ERR_CUDA, "denoise: out of device memory"};
+        // output planes: the spare pair left by the previous denoise (same row capacity)
+        if (g->spare_cap != g->cap_blocks) {
+            g->pay_spare.bytes = 0;
+            g->logits_spare.bytes = 0;
         }
-        svr_internal::launch_denoise(g->view(), g->coords4, pay2, lg2, radius, gw, g->stream);
-        const cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess) SVR_CK(cudaStreamSynchronize(g->stream));
-        if (e != cudaSuccess) {
-            cudaFree(pay2);
-            cudaFree(lg2);
-            throw Fail{SVR_ERR_CUDA, std::string("denoise: ") + cudaGetErrorString(e)};
-        }
-        std::swap(g->pay, pay2);
-        std::swap(g->logits, lg2);
-        cudaFree(pay2);
-        cudaFree(lg2);
+        g->pay_spare.ensure(g->cap_blocks * kVox * sizeof(float4));
+        g->logits_spare.ensure(g->cap_blocks * kVox * g->C * sizeof(float));
+        g->spare_cap = g->cap_blocks;
+        svr_internal::launch_denoise(g->view(), g->coords4, g->pay_spare.as<float4>(), g->logits_spare.as<float>(),
+                                     radius, gw, g->stream);
+        SVR_LAUNCHED();
+        // the new planes become the payload; the old ones the next call's spare pair
+        float4* old_pay = g->pay;
+        float* old_lg = g->logits;
+        g->pay = g->pay_spare.as<float4>();
+        g->logits = g->logits_spare.as<float>();
+        g->pay_spare.p = old_pay;
+        g->logits_spare.p = old_lg;
     });
 }
 
