@@ -241,6 +241,23 @@ int svr_fuse_finalize(svr_grid* g);
  * the valid set; weights / validity unchanged.  radius in [0, 4], sigma_vox > 0. */
 int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius);
 
+/* ---- meshing (meshing.hpp:23-28, meshing.cpp:168-273; mesh_io.cpp:30-68) ----
+ * marching_cubes(grid, iso): iso surface over every cell whose 8 corners are allocated and
+ * observed (cells across block faces included), vertices on cell edges by linear
+ * interpolation, deduplicated per edge (first occurrence in (block, z, y, x, triangle)
+ * order numbers the vertex), degenerate / zero-area (<= 1e-12) triangles dropped, normal /
+ * colour / label from fp64 trilinear queries -- the reference's Mesh word for word.  The
+ * mesh stays on the device (handle-owned) until the next call.  Edge keys need the block
+ * AABB within 2^18 x 2^18 x 2^17 blocks (SVR_ERR_CONFIG otherwise). */
+int svr_marching_cubes(svr_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles);
+/* Copy the last mesh out: vertices / normals / colors [nv][3] f64, labels [nv] i32,
+ * triangles [nt][3] i32 (host or device pointers; NULL skips). */
+int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors, int32_t* labels,
+                 int32_t* triangles);
+/* export_ply (mesh_io.cpp:30-68) of the last mesh: binary little-endian PLY with float
+ * xyz + normals, uchar rgb = lround(clamp(c) * 255), int label, uchar-count int triangles. */
+int svr_mesh_save_ply(svr_grid* g, const char* path);
+
 #ifdef __cplusplus
 }
 #endif

@@ -171,6 +171,20 @@ class _Base:
         return keep, [_ptr(d), _ptr(keep[1]), _ptr(keep[2]), ctypes.addressof(arr), len(cams), _ptr(sc),
                       rows, cols]
 
+    def marching_cubes(self, iso=0.0) -> dict:
+        """marching_cubes -> {vertices, normals, colors [nv,3] f64, labels [nv] i32,
+        triangles [nt,3] i32}."""
+        nv, nt = c_uint64(), c_uint64()
+        self._check(getattr(self.lib(), self._prefix + "marching_cubes")(self._h, iso, ctypes.byref(nv),
+                                                                          ctypes.byref(nt)))
+        m = {"vertices": np.empty((nv.value, 3)), "normals": np.empty((nv.value, 3)),
+             "colors": np.empty((nv.value, 3)), "labels": np.empty(nv.value, np.int32),
+             "triangles": np.empty((nt.value, 3), np.int32)}
+        getattr(self.lib(), self._prefix + "mesh_get")(self._h, *[_ptr(m[k]) for k in
+                                                                  ("vertices", "normals", "colors", "labels",
+                                                                   "triangles")])
+        return m
+
     def fuse_finalize(self):
         self._check(getattr(self.lib(), self._prefix + "fuse_finalize")(self._h))
 
@@ -208,6 +222,8 @@ _COMMON = {
     "load_sdgv": (c_int, [c_char_p, POINTER(c_void_p)]),
     "get_payload": (c_int, [c_void_p, c_uint32, c_uint32, P, P, P, P]),
     "fuse_begin": (c_int, [c_void_p, c_int]),
+    "marching_cubes": (c_int, [c_void_p, c_double, POINTER(c_uint64), POINTER(c_uint64)]),
+    "mesh_get": (c_int, [c_void_p, P, P, P, P, P]),
     "fuse_finalize": (c_int, [c_void_p]),
 }
 
@@ -234,6 +250,7 @@ class OracleGrid(_Base):
         "rmsprop": (c_int, [c_void_p, P, P, P, c_float, c_float, c_float, P]),
         "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double, POINTER(FuseReport)]),
         "denoise": (c_int, [c_void_p, c_double, c_int]),
+        "mc_table": (c_int, [P, P]),
     })
 
     def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
@@ -357,7 +374,13 @@ class RefGrid(_Base):
         "render_backward": (c_int, [c_void_p, P, P, P]),
         "grad_get": (c_int, [c_void_p, P, P]),
         "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double]),
+        "mesh_export_ply": (c_int, [c_void_p, c_char_p]),
+        "mesh_area": (c_double, [c_void_p]),
     })
+
+    def export_ply(self, path):
+        """export_ply (mesh_io.cpp:30-68) of the last marching_cubes mesh."""
+        self._check(self.lib().svrr_mesh_export_ply(self._h, str(path).encode()))
 
     def fuse_frames(self, depth, cams, mu, rgb=None, sem=None, scales=None):
         keep, args = self._fuse_args(depth, cams, rgb, sem, scales)

@@ -22,6 +22,8 @@
 #include "core/errors.hpp"
 #include "core/grid.hpp"
 #include "core/grid_io.hpp"
+#include "core/mesh_io.hpp"
+#include "core/meshing.hpp"
 #include "core/parallel.hpp"
 #include "core/scale_field.hpp"
 
@@ -47,6 +49,7 @@ struct svrr_grid {
     int fuse_flags = -1;
     std::vector<int64_t> fsum;
     std::vector<uint32_t> fcount;
+    Mesh mesh;  // last svrr_marching_cubes result
 };
 
 typedef struct {
@@ -506,5 +509,41 @@ int svrr_get_payload(const svrr_grid* w, uint32_t first, uint32_t n, float* sdf,
     }
     return 0;
 }
+
+}  // extern "C"
+
+// marching_cubes (meshing.cpp:168-273) and export_ply (mesh_io.cpp:30-68), the reference's
+// own code.
+extern "C" {
+
+int svrr_marching_cubes(svrr_grid* w, double iso, uint64_t* nv, uint64_t* nt) {
+    return guarded([&] {
+        w->mesh = marching_cubes(*w->g, iso);
+        *nv = w->mesh.vertices.size();
+        *nt = w->mesh.triangles.size();
+    });
+}
+
+int svrr_mesh_get(const svrr_grid* w, double* v, double* n, double* c, int32_t* labels, int32_t* tris) {
+    const Mesh& m = w->mesh;
+    for (size_t i = 0; i < m.vertices.size(); ++i)
+        for (int a = 0; a < 3; ++a) {
+            if (v) v[3 * i + a] = m.vertices[i][a];
+            if (n) n[3 * i + a] = m.normals[i][a];
+            if (c) c[3 * i + a] = m.colors[i][a];
+        }
+    if (labels)
+        for (size_t i = 0; i < m.labels.size(); ++i) labels[i] = m.labels[i];
+    if (tris)
+        for (size_t i = 0; i < m.triangles.size(); ++i)
+            for (int k = 0; k < 3; ++k) tris[3 * i + k] = m.triangles[i][k];
+    return 0;
+}
+
+int svrr_mesh_export_ply(const svrr_grid* w, const char* path) {
+    return guarded([&] { export_ply(w->mesh, path); });
+}
+
+double svrr_mesh_area(const svrr_grid* w) { return w->mesh.area(); }
 
 }  // extern "C"

@@ -5,6 +5,7 @@
 #include "svr_oracle.h"
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -165,6 +166,9 @@ struct svro_grid {
     int fuse_flags = -1;           // -1 = no session open
     std::vector<int64_t> fsum;     // [voxel][4 + C]: sdf, r, g, b, logits
     std::vector<uint32_t> fcount;  // [voxel]
+    // last marching_cubes result (svro_mesh_get)
+    std::vector<double> mv, mn, mc;  // vertices / normals / colors, 3 per vertex
+    std::vector<int32_t> ml, mt;     // labels, triangles (3 per)
     BlockCoord lo{0, 0, 0}, hi{0, 0, 0};
 
     double L() const { return h * B; }  // grid.hpp:112
@@ -1154,6 +1158,253 @@ int svro_denoise(svro_grid* g, double sigma_vox, int radius) {
                 }
         });
     });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Marching cubes (meshing.cpp:168-273) + the 256-case table it builds (meshing.cpp:56-150),
+// restated.  Table rules: edges are the corner pairs differing in one bit, numbered
+// axis * 4 + rank of the lower corner among the corners with that bit clear; faces are
+// cyclic quads (base, base+u, base+u+v, base+v) with (u, v) the other two axes in
+// increasing order, x faces then y then z, side 0 before side 1.  On a face, 2 sign
+// changes pair up; 4 (alternating) pair so that each inside corner is cut off by the two
+// edges next to it.  Segments chain into loops, walked from the lowest edge; a loop whose
+// midpoint polygon normal points from the outside corners to the inside ones is reversed;
+// loops are fan-triangulated from their first edge.
+// ---------------------------------------------------------------------------
+namespace {
+struct McTable {
+    int edge_a[12], edge_b[12], edge_axis[12];
+    std::vector<std::array<int, 3>> tris[256];
+};
+
+const McTable& mc_table() {
+    static const McTable T = [] {
+        McTable t{};
+        for (int a = 0; a < 3; ++a) {
+            int slot = 0;
+            for (int c = 0; c < 8; ++c)
+                if (!((c >> a) & 1)) {
+                    t.edge_a[a * 4 + slot] = c;
+                    t.edge_b[a * 4 + slot] = c | (1 << a);
+                    t.edge_axis[a * 4 + slot] = a;
+                    ++slot;
+                }
+        }
+        auto edge_of = [&](int p, int q) {
+            for (int e = 0; e < 12; ++e)
+                if ((t.edge_a[e] == p && t.edge_b[e] == q) || (t.edge_a[e] == q && t.edge_b[e] == p)) return e;
+            return -1;
+        };
+        int faces[6][4];
+        for (int a = 0, f = 0; a < 3; ++a) {
+            const int u = a == 0 ? 1 : 0, v = a == 2 ? 1 : 2;
+            for (int side = 0; side < 2; ++side, ++f) {
+                const int b = side << a;
+                faces[f][0] = b;
+                faces[f][1] = b | (1 << u);
+                faces[f][2] = b | (1 << u) | (1 << v);
+                faces[f][3] = b | (1 << v);
+            }
+        }
+        for (int cfg = 0; cfg < 256; ++cfg) {
+            auto in = [&](int c) { return (cfg >> c) & 1; };
+            int nbr[12][2], deg[12] = {0};
+            auto join = [&](int e, int f) {
+                nbr[e][deg[e]++] = f;
+                nbr[f][deg[f]++] = e;
+            };
+            for (const auto& q : faces) {
+                int cut[4], n = 0;
+                for (int i = 0; i < 4; ++i)
+                    if (in(q[i]) != in(q[(i + 1) & 3])) cut[n++] = edge_of(q[i], q[(i + 1) & 3]);
+                if (n == 2) join(cut[0], cut[1]);
+                if (n == 4)
+                    for (int k = 0; k < 4; ++k)  // each inside corner: its two incident edges
+                        if (in(q[k])) join(edge_of(q[(k + 3) & 3], q[k]), edge_of(q[k], q[(k + 1) & 3]));
+            }
+            bool seen[12] = {false};
+            for (int e0 = 0; e0 < 12; ++e0) {
+                if (deg[e0] != 2 || seen[e0]) continue;
+                std::vector<int> loop;
+                int cur = e0, prev = -1;
+                do {
+                    loop.push_back(cur);
+                    seen[cur] = true;
+                    const int nx = nbr[cur][0] == prev ? nbr[cur][1] : nbr[cur][0];
+                    prev = cur;
+                    cur = nx;
+                } while (cur != e0);
+                if (loop.size() < 3) continue;
+                // orientation: sum of mid_i x mid_{i+1} vs (mean outside corner - mean inside corner)
+                auto mid = [&](int e, int a) {
+                    return 0.5 * (((t.edge_a[e] >> a) & 1) + ((t.edge_b[e] >> a) & 1));
+                };
+                double nrm[3] = {0, 0, 0};
+                for (size_t i = 0; i < loop.size(); ++i) {
+                    const int e = loop[i], f = loop[(i + 1) % loop.size()];
+                    nrm[0] += mid(e, 1) * mid(f, 2) - mid(e, 2) * mid(f, 1);
+                    nrm[1] += mid(e, 2) * mid(f, 0) - mid(e, 0) * mid(f, 2);
+                    nrm[2] += mid(e, 0) * mid(f, 1) - mid(e, 1) * mid(f, 0);
+                }
+                double mi[3] = {0, 0, 0}, mo[3] = {0, 0, 0};
+                int ni = 0, no = 0;
+                for (int c = 0; c < 8; ++c) {
+                    double* m = in(c) ? mi : mo;
+                    (in(c) ? ni : no) += 1;
+                    for (int a = 0; a < 3; ++a) m[a] += (c >> a) & 1;
+                }
+                double dot = 0.0;
+                for (int a = 0; a < 3; ++a)
+                    dot += nrm[a] * (mo[a] / std::max(no, 1) - mi[a] / std::max(ni, 1));
+                if (dot < 0.0) std::reverse(loop.begin(), loop.end());
+                for (size_t i = 1; i + 1 < loop.size(); ++i) t.tris[cfg].push_back({loop[0], loop[i], loop[i + 1]});
+            }
+        }
+        return t;
+    }();
+    return T;
+}
+}  // namespace
+
+extern "C" {
+
+int svro_mc_table(int32_t* counts, int32_t* tris) {  // counts[256], tris[256][16][3] (-1 pad)
+    const McTable& t = mc_table();
+    for (int c = 0; c < 256; ++c) {
+        counts[c] = static_cast<int32_t>(t.tris[c].size());
+        for (int i = 0; i < 16; ++i)
+            for (int k = 0; k < 3; ++k)
+                tris[(c * 16 + i) * 3 + k] = i < static_cast<int>(t.tris[c].size()) ? t.tris[c][i][k] : -1;
+    }
+    return 0;
+}
+
+int svro_marching_cubes(svro_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles) {
+    return guarded([&] {
+        const McTable& T = mc_table();
+        const int B = g->B;
+        const size_t V = g->V, nb = g->coords.size();
+        // corner value: allocated and observed (meshing.cpp:175-184)
+        auto corner = [&](int vx, int vy, int vz, double& sdf) {
+            const BlockCoord bc = g->block_of_voxel(vx, vy, vz);
+            const uint32_t bi = g->map.find(bc);
+            if (bi == kInvalid) return false;
+            const size_t i = static_cast<size_t>(bi) * V + g->local_index(vx, vy, vz, bc);
+            if (!(g->weight[i] > 0.0f)) return false;
+            sdf = g->sdf[i];
+            return true;
+        };
+        struct Raw {
+            int64_t key[3][4];
+            double p[3][3];
+        };
+        std::vector<std::vector<Raw>> per(nb);
+        parallel_chunks(nb, [&](size_t b0, size_t b1) {
+            for (size_t b = b0; b < b1; ++b) {
+                const BlockCoord& bc = g->coords[b];
+                for (int lz = 0; lz < B; ++lz)
+                    for (int ly = 0; ly < B; ++ly)
+                        for (int lx = 0; lx < B; ++lx) {
+                            const int ax = bc.x * B + lx, ay = bc.y * B + ly, az = bc.z * B + lz;
+                            double s[8];
+                            bool ok = true;
+                            for (int c = 0; c < 8 && ok; ++c)
+                                ok = corner(ax + (c & 1), ay + ((c >> 1) & 1), az + ((c >> 2) & 1), s[c]);
+                            if (!ok) continue;
+                            int cfg = 0;
+                            for (int c = 0; c < 8; ++c)
+                                if (s[c] < iso) cfg |= 1 << c;
+                            for (const auto& tri : T.tris[cfg]) {
+                                Raw r;
+                                for (int k = 0; k < 3; ++k) {
+                                    const int e = tri[k], ca = T.edge_a[e], cb = T.edge_b[e], axis = T.edge_axis[e];
+                                    const int va[3] = {ax + (ca & 1), ay + ((ca >> 1) & 1), az + ((ca >> 2) & 1)};
+                                    const double tt = (iso - s[ca]) / (s[cb] - s[ca]);
+                                    for (int a = 0; a < 3; ++a) r.p[k][a] = static_cast<double>(va[a]) * g->h;
+                                    r.p[k][axis] += tt * g->h;
+                                    r.key[k][0] = va[0], r.key[k][1] = va[1], r.key[k][2] = va[2], r.key[k][3] = axis;
+                                }
+                                per[b].push_back(r);
+                            }
+                        }
+            }
+        });
+        // first-occurrence vertex numbering + degenerate / zero-area filter (meshing.cpp:233-251)
+        struct KeyH {
+            size_t operator()(const std::array<int64_t, 4>& k) const {
+                uint64_t h = static_cast<uint64_t>(k[0]) * 0x9E3779B97F4A7C15ull;
+                h ^= static_cast<uint64_t>(k[1]) * 0xBF58476D1CE4E5B9ull + (h >> 31);
+                h ^= static_cast<uint64_t>(k[2]) * 0x94D049BB133111EBull + (h >> 29);
+                return static_cast<size_t>(h ^ static_cast<uint64_t>(k[3]));
+            }
+        };
+        std::unordered_map<std::array<int64_t, 4>, int32_t, KeyH> vid;
+        g->mv.clear(), g->mt.clear();
+        for (const auto& list : per)
+            for (const Raw& r : list) {
+                int32_t idx[3];
+                for (int k = 0; k < 3; ++k) {
+                    const std::array<int64_t, 4> key{r.key[k][0], r.key[k][1], r.key[k][2], r.key[k][3]};
+                    auto it = vid.find(key);
+                    if (it == vid.end()) {
+                        it = vid.emplace(key, static_cast<int32_t>(g->mv.size() / 3)).first;
+                        g->mv.insert(g->mv.end(), r.p[k], r.p[k] + 3);
+                    }
+                    idx[k] = it->second;
+                }
+                if (idx[0] == idx[1] || idx[1] == idx[2] || idx[0] == idx[2]) continue;
+                const double* v0 = &g->mv[3 * idx[0]];
+                const double* v1 = &g->mv[3 * idx[1]];
+                const double* v2 = &g->mv[3 * idx[2]];
+                const double e1[3] = {v1[0] - v0[0], v1[1] - v0[1], v1[2] - v0[2]};
+                const double e2[3] = {v2[0] - v0[0], v2[1] - v0[1], v2[2] - v0[2]};
+                const double c[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                                     e1[0] * e2[1] - e1[1] * e2[0]};
+                if (0.5 * std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]) <= 1e-12) continue;
+                g->mt.insert(g->mt.end(), idx, idx + 3);
+            }
+        // vertex attributes from fp64 trilinear queries (meshing.cpp:254-270)
+        const size_t nv = g->mv.size() / 3;
+        g->mn.assign(3 * nv, 0.0);
+        g->mc.assign(3 * nv, 0.0);
+        g->ml.assign(nv, 0);
+        parallel_chunks(nv, [&](size_t i0, size_t i1) {
+            std::vector<double> lg(g->C);
+            for (size_t i = i0; i < i1; ++i) {
+                g->mn[3 * i + 2] = 1.0;  // UnitZ default
+                Corners cc;
+                if (!gather(*g, &g->mv[3 * i], cc)) continue;
+                Interp it{};
+                interpolate(*g, cc, it);
+                const double n2 = it.grad[0] * it.grad[0] + it.grad[1] * it.grad[1] + it.grad[2] * it.grad[2];
+                if (std::sqrt(n2) > 1e-12) {
+                    const double n = std::sqrt(n2);  // normalized(): v / sqrt(squaredNorm)
+                    for (int a = 0; a < 3; ++a) g->mn[3 * i + a] = it.grad[a] / n;
+                }
+                for (int a = 0; a < 3; ++a) g->mc[3 * i + a] = std::min(std::max(it.rgb[a], 0.0), 1.0);
+                std::fill(lg.begin(), lg.end(), 0.0);
+                for (int j = 0; j < 8; ++j) {
+                    const float* l = &g->logits[static_cast<size_t>(g->C) *
+                                                (static_cast<size_t>(cc.block[j]) * g->V + cc.voxel[j])];
+                    for (int k = 0; k < g->C; ++k) lg[k] += cc.w[j] * l[k];
+                }
+                g->ml[i] = static_cast<int32_t>(std::max_element(lg.begin(), lg.end()) - lg.begin());
+            }
+        });
+        *n_vertices = nv;
+        *n_triangles = g->mt.size() / 3;
+    });
+}
+
+int svro_mesh_get(const svro_grid* g, double* v, double* n, double* c, int32_t* labels, int32_t* tris) {
+    if (v) std::memcpy(v, g->mv.data(), g->mv.size() * 8);
+    if (n) std::memcpy(n, g->mn.data(), g->mn.size() * 8);
+    if (c) std::memcpy(c, g->mc.data(), g->mc.size() * 8);
+    if (labels) std::memcpy(labels, g->ml.data(), g->ml.size() * 4);
+    if (tris) std::memcpy(tris, g->mt.data(), g->mt.size() * 4);
+    return 0;
 }
 
 }  // extern "C"

@@ -102,6 +102,12 @@ int svro_fuse_frames(svro_grid* g, const float* depth, const float* rgb, const f
 int svro_fuse_finalize(svro_grid* g);
 int svro_denoise(svro_grid* g, double sigma_vox, int radius);
 
+/* marching_cubes (meshing.cpp:168-273); the mesh is kept in the handle for svro_mesh_get:
+ * vertices/normals/colors [nv][3] f64, labels [nv] i32, triangles [nt][3] i32. */
+int svro_mc_table(int32_t* counts, int32_t* tris);
+int svro_marching_cubes(svro_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles);
+int svro_mesh_get(const svro_grid* g, double* v, double* n, double* c, int32_t* labels, int32_t* tris);
+
 int svro_save_sdgv(const svro_grid* g, const char* path);
 int svro_load_sdgv(const char* path, svro_grid** out);
 

@@ -223,6 +223,7 @@ struct svr_grid {
     uint64_t fuse_blocks = 0;
     uint32_t fuse_batch = 0;  // frames per k_fuse launch, 0 = auto
     DevBuf pay_spare, logits_spare;  // denoise output planes, swapped with pay / logits
+    svr_internal::MeshBufs mesh;     // last svr_marching_cubes result
     uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
@@ -1314,6 +1315,110 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
         g->logits = g->logits_spare.as<float>();
         g->pay_spare.p = old_pay;
         g->logits_spare.p = old_lg;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Marching cubes (meshing.cpp:168-273) and the PLY writer (mesh_io.cpp:30-68).
+// ---------------------------------------------------------------------------
+int svr_marching_cubes(svr_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        g->mesh.nv = g->mesh.nt = 0;
+        if (g->n()) {
+            // edge keys: voxel coordinates relative to the AABB in 21 / 21 / 20 bits
+            const int64_t ex = (static_cast<int64_t>(g->hi[0]) - g->lo[0] + 1) * kRes;
+            const int64_t ey = (static_cast<int64_t>(g->hi[1]) - g->lo[1] + 1) * kRes;
+            const int64_t ez = (static_cast<int64_t>(g->hi[2]) - g->lo[2] + 1) * kRes;
+            if (ex >= (1 << 21) || ey >= (1 << 21) || ez >= (1 << 20))
+                throw Fail{SVR_ERR_CONFIG, "marching_cubes: block AABB wider than 2^18 x 2^18 x 2^17 blocks"};
+            g->ensure_lookup();
+            try {
+                svr_internal::run_marching_cubes(g->view(), g->coords4, g->nbr.as<uint32_t>(), g->lo, iso, g->mesh,
+                                                 g->stream);
+            } catch (const svr_internal::Status& e) {
+                throw Fail{e.code, e.msg};
+            }
+        }
+        if (n_vertices) *n_vertices = g->mesh.nv;
+        if (n_triangles) *n_triangles = g->mesh.nt;
+    });
+}
+
+int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors, int32_t* labels,
+                 int32_t* triangles) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
+        auto copy = [&](void* dst, const void* src, size_t bytes) {
+            if (!dst || !bytes) return;
+            SVR_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, g->stream));
+        };
+        copy(vertices, g->mesh.v, nv * 24);
+        copy(normals, g->mesh.n, nv * 24);
+        copy(colors, g->mesh.c, nv * 24);
+        copy(labels, g->mesh.l, nv * 4);
+        copy(triangles, g->mesh.t, nt * 12);
+        SVR_CK(cudaStreamSynchronize(g->stream));
+    });
+}
+
+int svr_mesh_save_ply(svr_grid* g, const char* path) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
+        std::vector<double> v(3 * nv), n(3 * nv), c(3 * nv);
+        std::vector<int32_t> l(nv), t(3 * nt);
+        if (nv) {
+            SVR_CK(cudaMemcpyAsync(v.data(), g->mesh.v, nv * 24, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaMemcpyAsync(n.data(), g->mesh.n, nv * 24, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaMemcpyAsync(c.data(), g->mesh.c, nv * 24, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaMemcpyAsync(l.data(), g->mesh.l, nv * 4, cudaMemcpyDeviceToHost, g->stream));
+        }
+        if (nt) SVR_CK(cudaMemcpyAsync(t.data(), g->mesh.t, nt * 12, cudaMemcpyDeviceToHost, g->stream));
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("export_ply: cannot open ") + path};
+        // header of export_ply: positions, normals, uchar colours, int label, triangle lists
+        os << "ply\nformat binary_little_endian 1.0\n"
+           << "element vertex " << nv << "\n"
+           << "property float x\nproperty float y\nproperty float z\n"
+           << "property float nx\nproperty float ny\nproperty float nz\n"
+           << "property uchar red\nproperty uchar green\nproperty uchar blue\n"
+           << "property int label\n"
+           << "element face " << nt << "\n"
+           << "property list uchar int vertex_indices\n"
+           << "end_header\n";
+        const size_t rec = 12 + 12 + 3 + 4;
+        std::vector<char> body(nv * rec + nt * 13);
+        char* o = body.data();
+        auto put = [&](const void* p, size_t k) {
+            std::memcpy(o, p, k);
+            o += k;
+        };
+        for (uint64_t i = 0; i < nv; ++i) {
+            for (int a = 0; a < 3; ++a) {
+                const float f = static_cast<float>(v[3 * i + a]);
+                put(&f, 4);
+            }
+            for (int a = 0; a < 3; ++a) {
+                const float f = static_cast<float>(n[3 * i + a]);
+                put(&f, 4);
+            }
+            for (int a = 0; a < 3; ++a) {  // lround(clamp(c, 0, 1) * 255)
+                const double cl = std::min(std::max(c[3 * i + a], 0.0), 1.0);
+                const uint8_t u = static_cast<uint8_t>(std::lround(cl * 255.0));
+                put(&u, 1);
+            }
+            put(&l[i], 4);
+        }
+        for (uint64_t i = 0; i < nt; ++i) {
+            const uint8_t three = 3;
+            put(&three, 1);
+            put(&t[3 * i], 12);
+        }
+        os.write(body.data(), static_cast<std::streamsize>(body.size()));
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("export_ply: write failed for ") + path};
     });
 }
 

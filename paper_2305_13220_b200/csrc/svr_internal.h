@@ -136,4 +136,20 @@ size_t denoise_smem(int radius);
 void launch_denoise(const svr_dev::GridView& g, const int32_t* coords4, float4* pay_out, float* logits_out,
                     int32_t radius, const double* gw, cudaStream_t s);
 
+// Marching cubes (svr_mesh.cu): the last mesh of a handle, device resident.
+struct MeshBufs {
+    double* v = nullptr;   // [nv][3] vertices
+    double* n = nullptr;   // [nv][3] unit normals
+    double* c = nullptr;   // [nv][3] colours in [0, 1]
+    int32_t* l = nullptr;  // [nv] argmax labels
+    int32_t* t = nullptr;  // [nt][3] triangles
+    uint64_t nv = 0, nt = 0, cap_v = 0, cap_t = 0;
+    void reserve(uint64_t nv, uint64_t nt);
+    void release();
+    ~MeshBufs() { release(); }
+};
+// Needs the lookup structures (dense / hash + neighbour table) of the current grid.
+void run_marching_cubes(const svr_dev::GridView& g, const int32_t* coords4, const uint32_t* nbr,
+                        const int32_t* lo_block, double iso, MeshBufs& out, cudaStream_t s);
+
 }  // namespace svr_internal

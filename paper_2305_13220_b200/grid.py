@@ -399,6 +399,23 @@ class SparseDenseGrid:
         """denoise: separable Gaussian over the valid neighbourhood."""
         check(self._lib.svr_denoise(self._h, sigma_vox, radius))
 
+    # --- meshing (meshing.cpp:168-273, mesh_io.cpp:30-68) ----------------------------------
+    def marching_cubes(self, iso: float = 0.0) -> dict:
+        """marching_cubes -> {vertices, normals, colors [nv,3] f64, labels [nv] i32,
+        triangles [nt,3] i32} (the reference's Mesh)."""
+        nv, nt = ctypes.c_uint64(), ctypes.c_uint64()
+        check(self._lib.svr_marching_cubes(self._h, iso, ctypes.byref(nv), ctypes.byref(nt)))
+        m = {"vertices": np.empty((nv.value, 3)), "normals": np.empty((nv.value, 3)),
+             "colors": np.empty((nv.value, 3)), "labels": np.empty(nv.value, np.int32),
+             "triangles": np.empty((nt.value, 3), np.int32)}
+        check(self._lib.svr_mesh_get(self._h, *[m[k].ctypes.data if m[k].size else None for k in
+                                               ("vertices", "normals", "colors", "labels", "triangles")]))
+        return m
+
+    def save_ply(self, path: str) -> None:
+        """export_ply of the last marching_cubes mesh."""
+        check(self._lib.svr_mesh_save_ply(self._h, str(path).encode()))
+
     # device-pointer plumbing for the multi-GPU reduction (paper_2305_13220_b200.distributed)
     def active_set_mask(self, mask) -> None:
         keep: list = []

@@ -50,7 +50,7 @@ def test_kernels_are_sm100a_sass():
     assert "sm_100a" in out
     names = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
     for k in ("k_march", "k_forward", "k_backward", "k_query", "k_depth_to_keys", "k_hash_find", "k_fuse",
-              "k_denoise"):
+              "k_denoise", "k_mc_count", "k_mc_emit", "k_mc_attrs"):
         assert k in names, k
     assert "REDG.E.ADD.F32x4" in names  # vector float atomics in the backward scatter
 

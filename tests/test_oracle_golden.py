@@ -38,10 +38,11 @@ class _Cam:
 
 @pytest.mark.skipif(not os.path.exists(oracle.REF_TESTS), reason="compiled reference not built")
 def test_reference_suite_verbatim():
-    """proj/tests/test_grid.cpp (20 cases) + test_camera.cpp (6) against the shims."""
+    """proj/tests/test_grid.cpp (20 cases) + test_camera.cpp (6) + test_meshing.cpp (9)
+    against the shims."""
     r = subprocess.run([oracle.REF_TESTS], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert "26 passed" in r.stdout
+    assert "35 passed" in r.stdout
 
 
 def test_hash_golden():
