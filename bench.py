@@ -14,6 +14,7 @@ Under torchrun (N > 1) every rank drives one GPU; rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -577,6 +578,13 @@ def bench_fusion(dev, stream, cpu=True):
     fuse_ms = _events_ms(stream, fuse, 3)
     r = rep["r"]
     den_ms = _events_ms(stream, lambda: g.denoise(1.0, 1), 3)
+    mc = {}
+
+    def mesh():
+        mc["n"] = g._lib.svr_marching_cubes(g._h, 0.0, ctypes.byref(mc.setdefault("nv", ctypes.c_uint64())),
+                                            ctypes.byref(mc.setdefault("nt", ctypes.c_uint64())))
+
+    mc_ms = _events_ms(stream, mesh, 3)
     A, C = g.block_count(), cfg["C"]
     vox = A * 512
     # algorithmic bytes of one denoise: read + write payload float4 + logits, read validity
@@ -587,8 +595,12 @@ def bench_fusion(dev, stream, cpu=True):
            "associations_per_s": r.in_view / (fuse_ms * 1e-3),
            "denoise_ms": den_ms, "denoise_voxels_per_s": vox / (den_ms * 1e-3),
            "denoise_GBps_algorithmic": den_bytes / (den_ms * 1e-3) / 1e9,
+           "marching_cubes_ms": mc_ms, "mesh_vertices": int(mc["nv"].value), "mesh_triangles": int(mc["nt"].value),
+           "marching_cubes_cells_per_s": vox / (mc_ms * 1e-3),
            "launches": {"fuse_all": "memset x2 + k_fuse x ceil(64 / batch) + k_fuse_finalize",
-                        "denoise": "k_denoise x1"}}
+                        "denoise": "k_denoise x1",
+                        "marching_cubes": "k_mc_count, k_mc_emit, k_mc_heads, k_mc_resolve, k_mc_keep, "
+                                          "k_mc_compact, k_mc_attrs + CUB scans / radix sort"}}
     if cpu:
         from oracle import OracleGrid
 
@@ -603,6 +615,23 @@ def bench_fusion(dev, stream, cpu=True):
         OracleGrid.set_threads(1)
         out["cpu_baseline"] = {"value": vox * 2 / dt, "unit": "voxel_frames/s", "cores": cores, "kind": "port",
                                "sample": f"fuse_frames over the first 2 frames ({dt:.2f} s)"}
+        # marching cubes: the oracle on a contiguous middle slab of 40000 blocks (index order is
+        # ascending (z, y, x), so the slab is spatially coherent and crosses the surfaces)
+        nb = min(A, 40000)
+        b0 = (A - nb) // 2
+        p = g.get_payload(b0, nb)
+        om = OracleGrid(cfg["h"], 8, C, capacity=max(A, 1 << 21))
+        om.allocate_blocks(g.coords()[b0:b0 + nb])
+        om.set_payload(0, nb, **p)
+        OracleGrid.set_threads(cores)
+        t0 = time.perf_counter()
+        sm = om.marching_cubes(0.0)
+        dt = time.perf_counter() - t0
+        OracleGrid.set_threads(1)
+        out["cpu_baseline_marching_cubes"] = {"value": nb * 512 / dt, "unit": "cells/s", "cores": cores,
+                                              "kind": "port",
+                                              "sample": f"blocks [{b0}, {b0 + nb}) -> {len(sm['triangles'])} "
+                                                        f"triangles ({dt:.2f} s)"}
     del g
     torch.cuda.empty_cache()
     return out
