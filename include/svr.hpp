@@ -1,7 +1,8 @@
 // svr.hpp -- header-only C++ host mirror of the reference grid / renderer interface over
 // the C-ABI in svr.h.  Names, argument meaning and error behaviour follow the reference
 // (/root/reference/proj/src/core/grid.hpp:100-223, allocation.hpp:13-29, grid_io.hpp:14-15,
-// errors.hpp:8-31; renderer ops per SPEC.md:268-319), so code written against
+// meshing.hpp:10-28, mesh_io.hpp:12, errors.hpp:8-31; renderer ops per SPEC.md:268-319,
+// fusion per SPEC.md:207-233), so code written against
 // svr::SparseDenseGrid switches to the B200 build by changing the include and namespace:
 //
 //     #include "svr.hpp"                       // instead of "core/grid.hpp" + friends
@@ -203,6 +204,45 @@ inline SparseDenseGrid load_grid(const std::string& path, int device = 0) {
     svr_grid* g = nullptr;
     check(svr_grid_load_sdgv(path.c_str(), device, &g));
     return SparseDenseGrid(g);
+}
+
+// fusion module: fuse_all = begin + frames + finalize; images as in svr.h
+using FuseReport = svr_fuse_report;
+inline FuseReport fuse_all(SparseDenseGrid& grid, const float* depth, const float* rgb, const float* semantic,
+                           const Camera* cams, std::uint32_t n_frames, const double* scales, int sf_rows,
+                           int sf_cols, double mu) {
+    FuseReport r{};
+    check(svr_fuse_begin(grid.handle(), (rgb ? SVR_FUSE_COLOR : 0) | (semantic ? SVR_FUSE_SEMANTIC : 0)));
+    check(svr_fuse_frames(grid.handle(), depth, rgb, semantic, cams, n_frames, scales, sf_rows, sf_cols, mu, &r));
+    check(svr_fuse_finalize(grid.handle()));
+    return r;
+}
+inline void denoise(SparseDenseGrid& grid, double sigma_vox = 1.0, int radius = 1) {
+    check(svr_denoise(grid.handle(), sigma_vox, radius));
+}
+
+// Mesh + marching_cubes + export_ply (meshing.hpp:10-28, mesh_io.hpp:12): flat arrays in the
+// reference's element order (vertices / normals / colors xyz per vertex, triangles ijk).
+struct Mesh {
+    std::vector<double> vertices, normals, colors;
+    std::vector<std::int32_t> labels, triangles;
+    std::size_t vertex_count() const { return labels.size(); }
+    std::size_t triangle_count() const { return triangles.size() / 3; }
+};
+inline Mesh marching_cubes(SparseDenseGrid& grid, double iso = 0.0) {
+    std::uint64_t nv = 0, nt = 0;
+    check(svr_marching_cubes(grid.handle(), iso, &nv, &nt));
+    Mesh m;
+    m.vertices.resize(3 * nv), m.normals.resize(3 * nv), m.colors.resize(3 * nv);
+    m.labels.resize(nv), m.triangles.resize(3 * nt);
+    check(svr_mesh_get(grid.handle(), nv ? m.vertices.data() : nullptr, nv ? m.normals.data() : nullptr,
+                       nv ? m.colors.data() : nullptr, nv ? m.labels.data() : nullptr,
+                       nt ? m.triangles.data() : nullptr));
+    return m;
+}
+// export_ply of the grid's last marching_cubes mesh (written from the device copy)
+inline void export_ply(SparseDenseGrid& grid, const std::string& path) {
+    check(svr_mesh_save_ply(grid.handle(), path.c_str()));
 }
 
 }  // namespace svr::b200

@@ -154,6 +154,30 @@ int main() {
         CHECK(l.voxel_size() == g.voxel_size());
         CHECK(l.label_channels() == 3);
     }
+    {  // marching cubes on an analytic sphere (test_meshing.cpp:44-55) + export_ply
+        SparseDenseGrid g(0.015, 8, 2);
+        std::vector<double> shell;
+        const int n = 6000;
+        for (int i = 0; i < n; ++i) {  // fibonacci_sphere (test_meshing.cpp:18-30), r = 0.5
+            const double z = 1.0 - 2.0 * (i + 0.5) / n, rad = std::sqrt(1.0 - z * z);
+            const double th = M_PI * (3.0 - std::sqrt(5.0)) * i;
+            shell.insert(shell.end(), {0.5 * rad * std::cos(th), 0.5 * rad * std::sin(th), 0.5 * z});
+        }
+        allocate_for_points(g, shell.data(), n, 1);
+        fill_all(g, [](double x, double y, double z) { return float(std::sqrt(x * x + y * y + z * z) - 0.5); });
+        const Mesh m = marching_cubes(g, 0.0);
+        CHECK(m.vertex_count() > 1000 && m.triangle_count() > 2000);
+        bool near = true;
+        for (std::size_t i = 0; i < m.vertex_count(); ++i) {
+            const double* v = &m.vertices[3 * i];
+            near &= std::abs(std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]) - 0.5) < 0.0075;
+        }
+        CHECK(near);
+        export_ply(g, "/tmp/svr_hpp_test.ply");
+        std::FILE* f = std::fopen("/tmp/svr_hpp_test.ply", "rb");
+        CHECK(f != nullptr);
+        if (f) std::fclose(f);
+    }
     {  // ConfigError mirrors grid.cpp:83-85
         bool thrown = false;
         try {
