@@ -384,17 +384,24 @@ def run_ours(args, cfg, rank, world, local_rank):
             reduce_active_grads(grid, dev)
         grid.grad_zero_active()
 
+    # host_async: pinned host arrays move on the library's copy streams through double-buffered
+    # device slots, so step i+1's H2D overlaps step i's kernels (every step still copies its
+    # own inputs in and its outputs out inside the timed region)
+    grid.set_tuning("host_async", 1)
     for _ in range(2):
         step_host()
+    grid.synchronize()
     torch.cuda.synchronize(dev)
     if dist is not None:
         dist.barrier()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 10))
     w0 = time.perf_counter()
     for _ in range(e2e_steps):
         step_host()
+    grid.synchronize()
     torch.cuda.synchronize(dev)
     e2e_s = (time.perf_counter() - w0) / e2e_steps
+    grid.set_tuning("host_async", 0)
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -442,7 +449,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
         "e2e": {"value": valid_total / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
-                "path": "SparseDenseGrid.render_forward/backward via C-ABI with pinned host buffers"},
+                "path": "SparseDenseGrid.render_forward/backward via C-ABI with pinned host buffers, "
+                        "host_async (copies of step i+1 overlap kernels of step i)"},
         "gpu_launches": launches_per_step * args.steps,
         "library_launches": {"cub_radix_sort": library_launches_per_step * args.steps},
         "clocks": clk,

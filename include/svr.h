@@ -110,7 +110,11 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather),
  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
  * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
- * "pipe_min_blocks", "fuse_batch" (frames per fusion launch, 0 = auto). */
+ * "pipe_min_blocks", "fuse_batch" (frames per fusion launch, 0 = auto), "host_async" (0/1:
+ * render_forward / render_backward given PINNED host arrays return without waiting; the
+ * transfers run on two internal copy streams through double-buffered device slots so one
+ * step's copies overlap the previous step's kernels; host outputs are valid, and host inputs
+ * may be reused, only after svr_grid_synchronize). */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 
 /* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */

@@ -224,6 +224,26 @@ struct svr_grid {
     uint32_t fuse_batch = 0;  // frames per k_fuse launch, 0 = auto
     DevBuf pay_spare, logits_spare;  // denoise output planes, swapped with pay / logits
     svr_internal::MeshBufs mesh;     // last svr_marching_cubes result
+    // "host_async" pipelined host I/O for render_forward / render_backward: pinned host arrays
+    // move on two copy streams through double-buffered device slots, so the transfers of one
+    // step overlap the kernels of the previous one; results are valid after synchronize.
+    struct AsyncSlot {
+        DevBuf o, d, up, out;
+        cudaEvent_t in_ev = nullptr, up_ev = nullptr, fwd_ev = nullptr, out_ev = nullptr, free_ev = nullptr;
+        bool used = false;
+    };
+    bool host_async = false;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    AsyncSlot aslot[2];
+    int aslot_next = 0, ctx_aslot = -1;
+    void ensure_async() {
+        if (h2d) return;
+        SVR_CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        SVR_CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (AsyncSlot& a : aslot)
+            for (cudaEvent_t* e : {&a.in_ev, &a.up_ev, &a.fwd_ev, &a.out_ev, &a.free_ev})
+                SVR_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
     uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
@@ -237,6 +257,14 @@ struct svr_grid {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
+        if (h2d) {
+            cudaStreamSynchronize(h2d);
+            cudaStreamSynchronize(d2h);
+            for (AsyncSlot& a : aslot)
+                for (cudaEvent_t e : {a.in_ev, a.up_ev, a.fwd_ev, a.out_ev, a.free_ev}) cudaEventDestroy(e);
+            cudaStreamDestroy(h2d);
+            cudaStreamDestroy(d2h);
+        }
         for (void* p : {static_cast<void*>(slots), static_cast<void*>(coords4), static_cast<void*>(pay),
                         static_cast<void*>(weight), static_cast<void*>(logits), static_cast<void*>(vmask),
                         static_cast<void*>(meta), static_cast<void*>(grad), static_cast<void*>(active),
@@ -505,6 +533,10 @@ int svr_grid_synchronize(svr_grid* g) {
     return guarded([&] {
         DeviceGuard dg(g->device);
         SVR_CK(cudaStreamSynchronize(g->stream));
+        if (g->h2d) {
+            SVR_CK(cudaStreamSynchronize(g->h2d));
+            SVR_CK(cudaStreamSynchronize(g->d2h));
+        }
     });
 }
 
@@ -551,6 +583,13 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "host_async") {
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            if (g->h2d) {
+                SVR_CK(cudaStreamSynchronize(g->h2d));
+                SVR_CK(cudaStreamSynchronize(g->d2h));
+            }
+            g->host_async = value != 0;
         } else if (k == "fuse_batch") {
             if (value < 0) throw Fail{SVR_ERR_CONFIG, "tuning: fuse_batch >= 0"};
             g->fuse_batch = static_cast<uint32_t>(value);
@@ -841,6 +880,81 @@ int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double 
     });
 }
 
+namespace {
+bool is_pinned_host(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// The forward kernels on g->stream: optional pre-march ray order, K4 march, optional
+// post-march order, K5 forward (+ records).  dO / dD / outputs are device pointers.
+void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n, double step,
+                     uint32_t max_samples, double beta, float* a, float* b, float* c, float* e) {
+    g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
+    const GridView v = g->view();
+    g->ctx_order = nullptr;
+    const bool sort = g->ray_sort != 0 && n > 1;
+    const bool cub_sort = sort && g->sort_impl == 1;
+    if (cub_sort) {
+        g->ord_keys.ensure(8 * n);
+        g->ord_ids.ensure(8 * n);
+        g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
+    } else if (sort) {
+        g->ord_ids.ensure(4 * svr_internal::ray_order_scratch_words(n));
+    }
+    uint32_t* k = g->ord_keys.as<uint32_t>();
+    uint32_t* id = g->ord_ids.as<uint32_t>();
+    auto order_rays = [&](bool post_march) {
+        const uint32_t* cnt = post_march ? g->counts.as<uint32_t>() : nullptr;
+        const double* tt = post_march ? g->tbuf.as<double>() : nullptr;
+        if (cub_sort) {
+            svr_internal::launch_ray_order(v, dO, dD, n, cnt, tt, max_samples, k, id, k + n, id + n,
+                                           g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream);
+        } else {
+            svr_internal::launch_ray_bucket_order(v, dO, dD, n, cnt, tt, max_samples, id, g->stream);
+            g->ctx_order = id;
+        }
+    };
+    if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
+    svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples, g->counts.as<uint32_t>(),
+                               g->tbuf.as<double>(), nullptr, g->stream);
+    if (sort && (g->ray_sort & 1)) order_rays(true);   // post-march: first-sample block
+    g->ctx_rec = g->use_records;
+    if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
+    float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;
+    const bool piped =
+        g->fwd_pipe && svr_internal::launch_render_forward_pipe(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
+                                                                g->tbuf.as<double>(), max_samples, step, beta, a, b,
+                                                                c, e, recp, g->stream, g->fwd_pipe_min_blocks,
+                                                                g->num_sms);
+    if (!piped)
+        svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
+                                            g->tbuf.as<double>(), max_samples, step, beta, a, b, c, e, nullptr,
+                                            recp, g->stream, g->fwd_min_blocks);
+}
+
+void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {
+    const uint64_t n = g->ctx_n;
+    const bool piped =
+        g->bwd_pipe && g->ctx_rec &&
+        svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
+                                                  g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
+                                                  g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
+                                                  g->stream, g->pipe_min_blocks, g->num_sms);
+    if (!piped)
+        svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
+                                             g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
+                                             g->ctx_step, g->ctx_beta, a, b, c,
+                                             g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream,
+                                             g->bwd_min_blocks);
+}
+}  // namespace
+
 int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n, double step,
                        uint32_t max_samples, double beta, float* rgb, float* depth, float* normal,
                        float* wsum, uint32_t* n_samples) {
@@ -852,77 +966,100 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
         DeviceGuard dg(g->device);
         g->ensure_lookup();
         g->ctx_valid = false;
-        Stage st(g->stream);
-        // retain rays for the backward pass: device arrays by pointer, host arrays copied
-        const double* dO = o;
-        const double* dD = d;
-        if (n && !is_device_ptr(o)) {
-            g->ray_o.ensure(24 * n);
-            SVR_CK(cudaMemcpyAsync(g->ray_o.p, o, 24 * n, cudaMemcpyHostToDevice, g->stream));
-            dO = g->ray_o.as<double>();
-            st.host_involved = true;
+        g->ctx_aslot = -1;
+        // host_async: every host array pinned -> transfers on the copy streams, no host sync
+        const void* arrs[7] = {o, d, rgb, depth, normal, wsum, n_samples};
+        bool async = g->host_async && n > 0, any_host = false;
+        for (const void* p : arrs) {
+            if (!p || is_device_ptr(p)) continue;
+            any_host = true;
+            async = async && is_pinned_host(p);
         }
-        if (n && !is_device_ptr(d)) {
-            g->ray_d.ensure(24 * n);
-            SVR_CK(cudaMemcpyAsync(g->ray_d.p, d, 24 * n, cudaMemcpyHostToDevice, g->stream));
-            dD = g->ray_d.as<double>();
-            st.host_involved = true;
-        }
-        g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
-        float* a = st.out(rgb, 3 * n);
-        float* b = st.out(depth, n);
-        float* c = st.out(normal, 3 * n);
-        float* e = st.out(wsum, n);
-        if (n) {
-            const GridView v = g->view();
-            g->ctx_order = nullptr;
-            const bool sort = g->ray_sort != 0 && n > 1;
-            const bool cub_sort = sort && g->sort_impl == 1;
-            if (cub_sort) {
-                g->ord_keys.ensure(8 * n);
-                g->ord_ids.ensure(8 * n);
-                g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
-            } else if (sort) {
-                g->ord_ids.ensure(4 * svr_internal::ray_order_scratch_words(n));
+        if (async && any_host) {
+            g->ensure_async();
+            const int si = g->aslot_next;
+            g->aslot_next ^= 1;
+            svr_grid::AsyncSlot& sl = g->aslot[si];
+            sl.o.ensure(24 * n);
+            sl.d.ensure(24 * n);
+            sl.out.ensure(36 * n);
+            if (sl.used) SVR_CK(cudaStreamWaitEvent(g->h2d, sl.free_ev, 0));  // slot's last backward done
+            const double* dO = o;
+            const double* dD = d;
+            if (!is_device_ptr(o)) {
+                SVR_CK(cudaMemcpyAsync(sl.o.p, o, 24 * n, cudaMemcpyHostToDevice, g->h2d));
+                dO = sl.o.as<double>();
             }
-            uint32_t* k = g->ord_keys.as<uint32_t>();
-            uint32_t* id = g->ord_ids.as<uint32_t>();
-            auto order_rays = [&](bool post_march) {
-                const uint32_t* cnt = post_march ? g->counts.as<uint32_t>() : nullptr;
-                const double* tt = post_march ? g->tbuf.as<double>() : nullptr;
-                if (cub_sort) {
-                    svr_internal::launch_ray_order(v, dO, dD, n, cnt, tt, max_samples, k, id, k + n, id + n,
-                                                   g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream);
-                } else {
-                    svr_internal::launch_ray_bucket_order(v, dO, dD, n, cnt, tt, max_samples, id, g->stream);
-                    g->ctx_order = id;
+            if (!is_device_ptr(d)) {
+                SVR_CK(cudaMemcpyAsync(sl.d.p, d, 24 * n, cudaMemcpyHostToDevice, g->h2d));
+                dD = sl.d.as<double>();
+            }
+            SVR_CK(cudaEventRecord(sl.in_ev, g->h2d));
+            SVR_CK(cudaStreamWaitEvent(g->stream, sl.in_ev, 0));
+            if (sl.used) SVR_CK(cudaStreamWaitEvent(g->stream, sl.out_ev, 0));  // slot outputs drained
+            float* so = sl.out.as<float>();
+            struct O {
+                float* host;
+                float* dev;
+                size_t bytes;
+            } outs[4] = {{rgb, so, 12 * n}, {depth, so + 3 * n, 4 * n}, {normal, so + 4 * n, 12 * n},
+                         {wsum, so + 7 * n, 4 * n}};
+            float* dev_out[4];
+            for (int i = 0; i < 4; ++i)
+                dev_out[i] = (!outs[i].host || is_device_ptr(outs[i].host)) ? outs[i].host : outs[i].dev;
+            forward_kernels(g, dO, dD, n, step, max_samples, beta, dev_out[0], dev_out[1], dev_out[2], dev_out[3]);
+            uint32_t* ns_dev = reinterpret_cast<uint32_t*>(so + 8 * n);
+            if (n_samples)
+                SVR_CK(cudaMemcpyAsync(is_device_ptr(n_samples) ? n_samples : ns_dev, g->counts.p, 4 * n,
+                                       cudaMemcpyDeviceToDevice, g->stream));
+            SVR_LAUNCHED();
+            SVR_CK(cudaEventRecord(sl.fwd_ev, g->stream));
+            SVR_CK(cudaStreamWaitEvent(g->d2h, sl.fwd_ev, 0));
+            for (int i = 0; i < 4; ++i)
+                if (dev_out[i] == outs[i].dev)
+                    SVR_CK(cudaMemcpyAsync(outs[i].host, outs[i].dev, outs[i].bytes, cudaMemcpyDeviceToHost, g->d2h));
+            if (n_samples && !is_device_ptr(n_samples))
+                SVR_CK(cudaMemcpyAsync(n_samples, ns_dev, 4 * n, cudaMemcpyDeviceToHost, g->d2h));
+            SVR_CK(cudaEventRecord(sl.out_ev, g->d2h));
+            // until this slot's backward runs, free_ev must not report it free
+            SVR_CK(cudaEventRecord(sl.free_ev, g->stream));
+            sl.used = true;
+            g->ctx_aslot = si;
+            g->ctx_o = dO;
+            g->ctx_d = dD;
+        } else {
+            Stage st(g->stream);
+            // retain rays for the backward pass: device arrays by pointer, host arrays copied
+            const double* dO = o;
+            const double* dD = d;
+            if (n && !is_device_ptr(o)) {
+                g->ray_o.ensure(24 * n);
+                SVR_CK(cudaMemcpyAsync(g->ray_o.p, o, 24 * n, cudaMemcpyHostToDevice, g->stream));
+                dO = g->ray_o.as<double>();
+                st.host_involved = true;
+            }
+            if (n && !is_device_ptr(d)) {
+                g->ray_d.ensure(24 * n);
+                SVR_CK(cudaMemcpyAsync(g->ray_d.p, d, 24 * n, cudaMemcpyHostToDevice, g->stream));
+                dD = g->ray_d.as<double>();
+                st.host_involved = true;
+            }
+            g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
+            float* a = st.out(rgb, 3 * n);
+            float* b = st.out(depth, n);
+            float* c = st.out(normal, 3 * n);
+            float* e = st.out(wsum, n);
+            if (n) {
+                forward_kernels(g, dO, dD, n, step, max_samples, beta, a, b, c, e);
+                if (n_samples) {
+                    uint32_t* ns = st.out(n_samples, n);
+                    SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));
                 }
-            };
-            if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
-            svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples,
-                                       g->counts.as<uint32_t>(), g->tbuf.as<double>(), nullptr, g->stream);
-            if (sort && (g->ray_sort & 1)) order_rays(true);   // post-march: first-sample block
-            g->ctx_rec = g->use_records;
-            if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
-            float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;
-            const bool piped =
-                g->fwd_pipe &&
-                svr_internal::launch_render_forward_pipe(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
-                                                         g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                         c, e, recp, g->stream, g->fwd_pipe_min_blocks,
-                                                         g->num_sms);
-            if (!piped)
-                svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
-                                                    g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                    c, e, nullptr, recp, g->stream, g->fwd_min_blocks);
-            if (n_samples) {
-                uint32_t* ns = st.out(n_samples, n);
-                SVR_CK(cudaMemcpyAsync(ns, g->counts.p, 4 * n, cudaMemcpyDeviceToDevice, g->stream));
             }
+            st.finish();
+            g->ctx_o = dO;
+            g->ctx_d = dD;
         }
-        st.finish();
-        g->ctx_o = dO;
-        g->ctx_d = dD;
         g->ctx_n = n;
         g->ctx_S = max_samples;
         g->ctx_step = step;
@@ -939,24 +1076,41 @@ int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, c
         DeviceGuard dg(g->device);
         const uint64_t n = g->ctx_n;
         if (!n) return;
+        if (g->ctx_aslot >= 0) {  // pipelined host I/O (the forward ran through a slot)
+            svr_grid::AsyncSlot& sl = g->aslot[g->ctx_aslot];
+            const float* up[3] = {d_rgb, d_depth, d_normal};
+            const size_t cnt[3] = {3 * n, n, 3 * n};
+            bool ok = true;
+            for (const float* p : up) ok = ok && (is_device_ptr(p) || is_pinned_host(p));
+            if (ok) {
+                sl.up.ensure(28 * n);
+                const float* dev[3];
+                size_t off = 0;
+                for (int i = 0; i < 3; ++i) {
+                    if (is_device_ptr(up[i])) {
+                        dev[i] = up[i];
+                    } else {
+                        float* dst = sl.up.as<float>() + off;
+                        SVR_CK(cudaMemcpyAsync(dst, up[i], 4 * cnt[i], cudaMemcpyHostToDevice, g->h2d));
+                        dev[i] = dst;
+                    }
+                    off += cnt[i];
+                }
+                SVR_CK(cudaEventRecord(sl.up_ev, g->h2d));
+                SVR_CK(cudaStreamWaitEvent(g->stream, sl.up_ev, 0));
+                backward_kernels(g, dev[0], dev[1], dev[2]);
+                SVR_LAUNCHED();
+                SVR_CK(cudaEventRecord(sl.free_ev, g->stream));
+                return;
+            }
+        }
         Stage st(g->stream);
         const float* a = st.in(d_rgb, 3 * n);
         const float* b = st.in(d_depth, n);
         const float* c = st.in(d_normal, 3 * n);
-        const bool piped =
-            g->bwd_pipe && g->ctx_rec &&
-            svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
-                                                      g->counts.as<uint32_t>(), g->tbuf.as<double>(),
-                                                      g->ctx_S, g->ctx_step, g->ctx_beta, a, b, c,
-                                                      g->rec.as<float4>(), g->stream,
-                                                      g->pipe_min_blocks, g->num_sms);
-        if (!piped)
-        svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
-                                             g->counts.as<uint32_t>(),
-                                             g->tbuf.as<double>(), g->ctx_S, g->ctx_step, g->ctx_beta,
-                                             a, b, c, g->ctx_rec ? g->rec.as<float4>() : nullptr,
-                                             g->stream, g->bwd_min_blocks);
+        backward_kernels(g, a, b, c);
         st.finish();
+        if (g->ctx_aslot >= 0) SVR_CK(cudaEventRecord(g->aslot[g->ctx_aslot].free_ev, g->stream));
     });
 }
 

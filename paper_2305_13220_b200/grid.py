@@ -308,6 +308,7 @@ class SparseDenseGrid:
         check(self._lib.svr_render_backward(self._h, _in(d_rgb, np.float32, keep),
                                             _in(d_depth, np.float32, keep),
                                             _in(d_normal, np.float32, keep)))
+        self._keep_up = keep  # host_async: pinned inputs are read after the call returns
 
     def render_stats(self) -> RenderStats:
         s = RenderStats()

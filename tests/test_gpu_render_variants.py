@@ -85,3 +85,41 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
     g.set_tuning("records", records)
     g.set_tuning("bwd_pipe", pipe)
     _check_fwd_bwd(g, case, 64)
+
+
+def test_host_async_pipeline_matches_synchronous():
+    """host_async: three forward/backward steps with different pinned ray batches issued
+    back to back (slots reused), outputs and accumulated gradients equal the synchronous
+    path's."""
+    import torch
+
+    case = scene_case()
+    n = len(case["o"])
+    rng = np.random.default_rng(4)
+    perms = [rng.permutation(n) for _ in range(3)]
+    batches = [{k: np.ascontiguousarray(case[k][p]) for k in ("o", "d", "dC", "dD", "dN")} for p in perms]
+    S = 64
+
+    def run(async_mode):
+        g = gpu_grid_from(case)
+        g.grad_zero()
+        g.set_tuning("host_async", int(async_mode))
+        outs = []
+        for b in batches:
+            pin = {k: torch.from_numpy(v).pin_memory() for k, v in b.items()}
+            out = {k: torch.empty(s, dtype=torch.float32).pin_memory()
+                   for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
+            out["n_samples"] = torch.empty(n, dtype=torch.int32).pin_memory()
+            g.render_forward(pin["o"], pin["d"], case["step"], S, case["beta"], out=out)
+            g.render_backward(pin["dC"], pin["dD"], pin["dN"])
+            outs.append((out, pin))  # keep the pinned inputs alive until synchronize
+        g.synchronize()
+        return [{k: v.numpy().copy() for k, v in o.items()} for o, _ in outs], g.grads()
+
+    ref_out, (ref_gs, ref_gr) = run(False)
+    out, (gs, gr) = run(True)
+    for a, b in zip(out, ref_out):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
+    assert_close(gs, ref_gs, what="grad_sdf")
+    assert_close(gr, ref_gr, what="grad_rgb")
