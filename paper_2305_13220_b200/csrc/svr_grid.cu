@@ -208,6 +208,7 @@ struct svr_grid {
     int pipe_min_blocks = 3;
     int num_sms = 148;
     int bwd_min_blocks = 3;
+    bool warp_agg = true;  // backward scatter: hand a lane's first cell run to the previous lane
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
     uint64_t ctx_n = 0;
@@ -583,6 +584,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "warp_agg") {
+            g->warp_agg = value != 0;
         } else if (k == "host_async") {
             SVR_CK(cudaStreamSynchronize(g->stream));
             if (g->h2d) {
@@ -945,13 +948,13 @@ void backward_kernels(svr_grid* g, const float* a, const float* b, const float* 
         svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                                   g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                                   g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
-                                                  g->stream, g->pipe_min_blocks, g->num_sms);
+                                                  g->stream, g->pipe_min_blocks, g->num_sms, g->warp_agg);
     if (!piped)
         svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                              g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                              g->ctx_step, g->ctx_beta, a, b, c,
                                              g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream,
-                                             g->bwd_min_blocks);
+                                             g->bwd_min_blocks, g->warp_agg);
 }
 }  // namespace
 

@@ -35,7 +35,7 @@ void launch_render_backward(const svr_dev::GridView& g, const double* o, const d
                             uint64_t n, const uint32_t* order, const uint32_t* counts,
                             const double* t, uint32_t S, double step, double beta,
                             const float* d_rgb, const float* d_depth, const float* d_normal,
-                            const float4* rec, cudaStream_t s, int min_blocks);
+                            const float4* rec, cudaStream_t s, int min_blocks, bool agg);
 // Sort rays for locality; *sorted_ids points into ids or ids_alt.  counts != NULL: key =
 // Morton code of the first sample's block (after the march); counts == NULL: key = origin
 // hash + octahedral-direction Morton code (before the march).
@@ -61,7 +61,8 @@ bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, co
                                  uint64_t n, const uint32_t* order, const uint32_t* counts,
                                  const double* t, uint32_t S, double step, double beta,
                                  const float* d_rgb, const float* d_depth, const float* d_normal,
-                                 const float4* rec, cudaStream_t s, int min_blocks, int num_sms);
+                                 const float4* rec, cudaStream_t s, int min_blocks, int num_sms,
+                                 bool agg);
 
 // Launchers (svr_activate.cu)
 struct KeySet {

@@ -617,6 +617,58 @@ __device__ __forceinline__ void scatter_corner(float4* grad, const SampleVal& v0
     }
 }
 
+// Warp-aggregated scatter of one lane's sample pair.  Along a ray consecutive samples share a
+// cell ~40 % of the time, so beyond merging a lane's own two samples, the first cell run of
+// lane l is handed to lane l-1 when it continues lane l-1's last run (one shuffle-down per
+// component); lane l-1 folds it into its last run's atomics.  Every contribution is still
+// issued exactly once: a lane that handed its only run away issues just what it received.
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 shfl_down4(float4 v) {
+    return make_float4(__shfl_down_sync(kFull, v.x, 1), __shfl_down_sync(kFull, v.y, 1),
+                       __shfl_down_sync(kFull, v.z, 1), __shfl_down_sync(kFull, v.w, 1));
+}
+template <int c>
+__device__ __forceinline__ void scatter_corner_agg(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                                   const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
+                                                   bool two, bool give, bool recv) {
+    const float4 a0 = ok0 ? corner_grad<c>(k0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 a1 = ok1 ? corner_grad<c>(k1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // first run F (address fa) and last run L (address v1.gidx[c]); one run when !two
+    const float4 F = two ? a0 : f4add(a0, a1);
+    const float4 in = shfl_down4(F);  // lane l+1's first run (used only when recv)
+    const uint32_t fa = ok0 ? v0.gidx[c] : v1.gidx[c];
+    if (two) {
+        if (!give) atomicAdd(grad + fa, a0);
+        atomicAdd(grad + v1.gidx[c], recv ? f4add(a1, in) : a1);
+    } else if (ok0 || ok1) {
+        if (give) {
+            if (recv) atomicAdd(grad + fa, in);
+        } else {
+            atomicAdd(grad + fa, recv ? f4add(F, in) : F);
+        }
+    }
+}
+__device__ __forceinline__ void scatter_pair_agg(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                                 const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
+                                                 int lane) {
+    const uint32_t first = ok0 ? v0.gidx[0] : (ok1 ? v1.gidx[0] : kInvalid);
+    const uint32_t last = ok1 ? v1.gidx[0] : first;
+    const bool two = ok0 && ok1 && v0.gidx[0] != v1.gidx[0];
+    const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
+    const bool give = lane > 0 && first != kInvalid && first == prev_last;
+    const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
+    scatter_corner_agg<0>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<1>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<2>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<3>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<4>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<5>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<6>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+    scatter_corner_agg<7>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
+}
+
 // ---------------------------------------------------------------------------
 // K6: backward.  Chunks of 64 samples are visited back to front; within a chunk the
 // suffix S_k = sum_{m>k} w_m v_m comes from a warp suffix scan (no cancellation-prone
@@ -704,15 +756,19 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
                                         w1, dC, dN, ih);
         if (ok0) mark_blocks(g, v0);
         if (ok1) mark_blocks(g, v1);
-        const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-        scatter_corner<0, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<1, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<2, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<3, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<4, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<5, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<6, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        scatter_corner<7, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        if (kMode == 3) {
+            scatter_pair_agg(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
+        } else {
+            const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
+            scatter_corner<0, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<1, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<2, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<3, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<4, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<5, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<6, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+            scatter_corner<7, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
+        }
         S_after += __shfl_sync(kFull, sinc, 0);
     }
 }
@@ -851,15 +907,19 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
                                             w1, dC, dN, ih);
             if (ok0) mark_blocks(g, v0);
             if (ok1) mark_blocks(g, v1);
-            const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-            scatter_corner<0, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<1, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<2, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<3, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<4, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<5, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<6, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            scatter_corner<7, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            if (kMode == 3) {
+                scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
+            } else {
+                const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
+                scatter_corner<0, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<1, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<2, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<3, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<4, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<5, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<6, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+                scatter_corner<7, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
+            }
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
         st = (st + 1) % kPipeStages;
@@ -1090,7 +1150,7 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
                             const uint32_t* order, const uint32_t* counts, const double* t,
                             uint32_t S, double step, double beta, const float* d_rgb,
                             const float* d_depth, const float* d_normal, const float4* rec,
-                            cudaStream_t s, int min_blocks) {
+                            cudaStream_t s, int min_blocks, bool agg) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
     const unsigned grid = grid_for(n * 32, 256);
@@ -1107,7 +1167,12 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
         case 203:
             r ? SVR_BWD(3, 2, true) : SVR_BWD(3, 2, false);
             break;
-        default: r ? SVR_BWD(3, 0, true) : SVR_BWD(3, 0, false); break;
+        default:
+            if (agg)
+                r ? SVR_BWD(3, 3, true) : SVR_BWD(3, 3, false);
+            else
+                r ? SVR_BWD(3, 0, true) : SVR_BWD(3, 0, false);
+            break;
     }
 #undef SVR_BWD
 #undef SVR_COMMA
@@ -1132,7 +1197,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
                                  const uint32_t* order, const uint32_t* counts, const double* t,
                                  uint32_t S, double step, double beta, const float* d_rgb,
                                  const float* d_depth, const float* d_normal, const float4* rec,
-                                 cudaStream_t s, int min_blocks, int num_sms) {
+                                 cudaStream_t s, int min_blocks, int num_sms, bool agg) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
     const size_t smem = sizeof(PipeSlot) * kPipeStages * kPipeWarps + 8 * kPipeStages * kPipeWarps;
@@ -1150,10 +1215,19 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
             g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
     } while (0)
     switch (min_blocks) {
-        case 1: SVR_PIPE(1); break;
-        case 2: SVR_PIPE(2); break;
+        case 1:
+            if (agg) SVR_PIPE(SVR_COMMA2(1, 3));
+            else SVR_PIPE(1);
+            break;
+        case 2:
+            if (agg) SVR_PIPE(SVR_COMMA2(2, 3));
+            else SVR_PIPE(2);
+            break;
         case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
-        default: SVR_PIPE(3); break;
+        default:
+            if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
+            else SVR_PIPE(3);
+            break;
     }
 #undef SVR_PIPE
 #undef SVR_COMMA2

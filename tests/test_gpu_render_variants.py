@@ -87,6 +87,18 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
     _check_fwd_bwd(g, case, 64)
 
 
+@pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe",
+                         [(2, 1, 1), (3, 1, 1), (3, 0, 1), (3, 1, 0), (3, 0, 0)])
+def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe):
+    """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward."""
+    for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):  # + invalid samples inside runs
+        g = gpu_grid_from(c)
+        g.set_tuning("pipe_min_blocks", pipe_min_blocks)
+        g.set_tuning("warp_agg", warp_agg)
+        g.set_tuning("bwd_pipe", bwd_pipe)
+        _check_fwd_bwd(g, c, 64)
+
+
 def test_host_async_pipeline_matches_synchronous():
     """host_async: three forward/backward steps with different pinned ray batches issued
     back to back (slots reused), outputs and accumulated gradients equal the synchronous
