@@ -61,8 +61,18 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.lines = []  # (perf_counter, line)
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line))
 
     def start(self):
+        """Start nvidia-smi -lms 50 and wait for its first sample, so the timed region that
+        follows is covered (nvidia-smi needs ~100+ ms to come up)."""
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -70,19 +80,35 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        threading.Thread(target=self._reader, daemon=True).start()
+        deadline = time.perf_counter() + 5.0
+        while not self.lines and time.perf_counter() < deadline:
+            time.sleep(0.01)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.t1 is None:
+            self.t1 = time.perf_counter()
+        time.sleep(0.06)  # one more sample period
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-            out = ""
+        t0 = self.t0 if self.t0 is not None else 0.0
+        # samples inside the timed region, plus the one straddling its end
+        inside = [ln for t, ln in self.lines if t0 <= t <= self.t1 + 0.06]
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in inside:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -96,7 +122,7 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "region_s": self.t1 - t0}
 
 
 # ----------------------------------------------------------------------------------
@@ -347,11 +373,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     t0.record(stream)
     for _ in range(args.steps):
         step(True)
     t1.record(stream)
     torch.cuda.synchronize(dev)
+    clocks.mark_stop()
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
@@ -648,7 +676,7 @@ def bench_fusion(dev, stream, cpu=True):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
