@@ -126,6 +126,7 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
     b0 = start_block(0), b1 = start_block(1), b2 = start_block(2);
     c0 = crossing(0, b0), c1 = crossing(1, b1), c2 = crossing(2, b2);
     const int32_t s0 = d[0] > 0.0 ? 1 : -1, s1 = d[1] > 0.0 ? 1 : -1, s2 = d[2] > 0.0 ? 1 : -1;
+
     const int32_t p0 = d[0] > 0.0 ? 1 : 0, p1 = d[1] > 0.0 ? 1 : 0, p2 = d[2] > 0.0 ? 1 : 0;
     // dense mode: occupancy bit index of (b0,b1,b2), updated incrementally per step
     // (the dense index is only built when the AABB has <= 2^28 cells)
@@ -135,6 +136,30 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
     double t = t0, cursor = -kInf;
     bool open = false;
     uint32_t cnt = 0;
+    // The walk only records the allocated runs [a, b) (contiguous allocated blocks merge,
+    // as march_intervals merges them); the samples are generated afterwards by the exact
+    // repeated-addition cursor, so the emission loop is not nested in -- and divergent
+    // with -- the DDA steps.  The walk stops once a conservative estimate of the samples
+    // covered exceeds S by more than one per run (the exact count per run differs from
+    // the estimate by at most one).
+    constexpr int kRuns = 4;
+    double ra[kRuns], rb[kRuns];
+    int nr = 0;
+    double est_cursor = -kInf;
+    double est = 0.0;
+    const double inv_step = 1.0 / step;
+    auto flush = [&]() {  // exact samples of the recorded runs (grid.cpp:337-353)
+        for (int i = 0; i < nr; ++i) {
+            const double a = ra[i], b = rb[i];
+            if (cursor < a) cursor = __dadd_rn(a, half_step);  // grid.cpp:345
+            while (cursor < b && cnt < S) {                    // grid.cpp:346-349
+                emit(cnt, cursor);
+                ++cnt;
+                cursor = __dadd_rn(cursor, step);
+            }
+        }
+        nr = 0;
+    };
     while (t < t1) {  // grid.cpp:306-333
         double t_exit = t1;
         int axis = -1;
@@ -144,19 +169,23 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         const bool alloc = g.use_dense
                                ? ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0
                                : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
-        if (alloc && !open) {
-            open = true;
-            if (cursor < t) cursor = __dadd_rn(t, half_step);  // grid.cpp:345
-        } else if (!alloc && open) {
-            open = false;
-        }
         if (alloc) {
-            while (cursor < t_exit && cnt < S) {  // grid.cpp:346-349
-                emit(cnt, cursor);
-                ++cnt;
-                cursor = __dadd_rn(cursor, step);
+            if (!open) {
+                open = true;
+                if (nr == kRuns) flush();
+                ra[nr] = t;
+                ++nr;
+                if (est_cursor < t) est_cursor = t + half_step;
             }
-            if (cnt >= S) break;
+            rb[nr - 1] = t_exit;
+            if (est_cursor < t_exit) {  // estimate of the samples in [est_cursor, t_exit)
+                const double k = ceil((t_exit - est_cursor) * inv_step);
+                est += k;
+                est_cursor += k * step;
+            }
+            if (est >= static_cast<double>(S) + nr + 1) break;
+        } else {
+            open = false;
         }
         if (axis < 0) break;
         t = t_exit;
@@ -175,6 +204,7 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         else if (a1) b1 = nb, c1 = c;
         else b2 = nb, c2 = c;
     }
+    flush();
     return cnt;
 }
 
