@@ -70,6 +70,8 @@ struct GridView {
     const uint32_t* meta;
     const float* logits;
     const uint32_t* nbr;    // [A][8]: entry of block + (k&1, k>>1&1, k>>2), k = 0..7
+    const uint8_t* bdist;   // dense mode: Chebyshev distance (blocks, capped) to the nearest
+                            // allocated block per AABB cell; 0 = allocated
     float4* grad;
     uint8_t* active;
     int32_t lo[3], hi[3];   // block AABB (grid.hpp:222)

@@ -71,6 +71,33 @@ __global__ void k_dense_build(const int4* __restrict__ coords, const uint32_t* _
     atomicOr(occ + (cell >> 5), 1u << (cell & 31));
 }
 
+// Chebyshev block-distance field over the dense AABB (for empty-space jumps in the march):
+// three separable windowed passes, out = min_k max(|k|, in[cell + k e_axis]), |k| <= cap;
+// pass 0 reads the occupancy bits (allocated = 0, empty = cap + 1).
+constexpr int kDistCap = 15;
+__global__ void k_bdist_pass(const uint32_t* __restrict__ occ, const uint8_t* __restrict__ in, uint8_t* out,
+                             int32_t dx, int32_t dy, int32_t dz, int axis) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t n = static_cast<uint64_t>(dx) * dy * dz;
+    if (i >= n) return;
+    const int32_t x = static_cast<int32_t>(i % dx), y = static_cast<int32_t>((i / dx) % dy),
+                  z = static_cast<int32_t>(i / (static_cast<uint64_t>(dx) * dy));
+    const int32_t pos = axis == 0 ? x : (axis == 1 ? y : z);
+    const int32_t len = axis == 0 ? dx : (axis == 1 ? dy : dz);
+    const int64_t stride = axis == 0 ? 1 : (axis == 1 ? dx : static_cast<int64_t>(dx) * dy);
+    int best = kDistCap + 1;
+    for (int k = -kDistCap; k <= kDistCap; ++k) {
+        const int32_t q = pos + k;
+        if (q < 0 || q >= len) continue;
+        const uint64_t j = static_cast<uint64_t>(static_cast<int64_t>(i) + k * stride);
+        const int v = axis == 0 ? (((occ[j >> 5] >> (j & 31)) & 1u) ? 0 : kDistCap + 1) : in[j];
+        const int ak = k < 0 ? -k : k;
+        const int m = v > ak ? v : ak;
+        if (m < best) best = m;
+    }
+    out[i] = static_cast<uint8_t>(best);
+}
+
 // Per-block table of the 8 blocks a trilinear cell can touch: entry k = lookup of
 // coord + (k & 1, (k >> 1) & 1, k >> 2) (k = 0 is the block itself), with the all-valid bit.
 __global__ void k_nbr_build(GridView g, const int4* __restrict__ coords, uint32_t n, uint32_t* nbr) {
@@ -221,6 +248,16 @@ void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n
     if (!n) return;
     k_dense_build<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), meta, n,
                                                   lo[0], lo[1], lo[2], dim[0], dim[1], dense, occ);
+}
+
+void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t* tmp, cudaStream_t s) {
+    const uint64_t n = static_cast<uint64_t>(dim[0]) * dim[1] * dim[2];
+    if (!n) return;
+    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    k_bdist_pass<<<grid, 256, 0, s>>>(occ, nullptr, tmp, dim[0], dim[1], dim[2], 0);
+    k_bdist_pass<<<grid, 256, 0, s>>>(occ, tmp, out, dim[0], dim[1], dim[2], 1);
+    k_bdist_pass<<<grid, 256, 0, s>>>(occ, out, tmp, dim[0], dim[1], dim[2], 2);
+    cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToDevice, s);
 }
 
 void launch_nbr_build(const GridView& g, const int32_t* coords4, uint32_t n, uint32_t* nbr,

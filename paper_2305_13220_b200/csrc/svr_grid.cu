@@ -187,7 +187,8 @@ struct svr_grid {
     bool dense_dirty = true;
     int use_dense = 0;
     int32_t dim[3] = {0, 0, 0};
-    DevBuf dense, occ, nbr;
+    DevBuf dense, occ, nbr, bdist, bdist_tmp;
+    bool use_jump = true;  // march: exact empty-space jumps over the block-distance field
 
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
@@ -286,6 +287,7 @@ struct svr_grid {
         v.meta = meta;
         v.logits = logits;
         v.nbr = nbr.as<uint32_t>();
+        v.bdist = (use_dense && use_jump) ? bdist.as<uint8_t>() : nullptr;
         v.grad = grad;
         v.active = active;
         for (int a = 0; a < 3; ++a) {
@@ -383,6 +385,10 @@ struct svr_grid {
             SVR_CK(cudaMemsetAsync(occ.p, 0, ((cells + 31) / 32) * 4, stream));
             svr_internal::launch_dense_build(coords4, meta, static_cast<uint32_t>(n()), lo, dim,
                                              dense.as<uint32_t>(), occ.as<uint32_t>(), stream);
+            SVR_LAUNCHED();
+            bdist.ensure(cells);
+            bdist_tmp.ensure(cells);
+            svr_internal::launch_bdist(occ.as<uint32_t>(), dim, bdist.as<uint8_t>(), bdist_tmp.as<uint8_t>(), stream);
             SVR_LAUNCHED();
             use_dense = 1;
         }
@@ -584,6 +590,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "march_jump") {
+            g->use_jump = value != 0;
         } else if (k == "warp_agg") {
             g->warp_agg = value != 0;
         } else if (k == "host_async") {

@@ -160,15 +160,62 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
         }
         nr = 0;
     };
+    // Empty-space jump (dense mode): every block within Chebyshev distance dist - 1 of an
+    // empty block is empty, so the walk may resume at the DDA state of a time t* that stays
+    // inside that cube (one block of margin).  The state at t* is exact: per axis the
+    // crossings before t* are counted with the same exactly-rounded crossing formula the
+    // walk uses (crossings of one axis are monotone), so the blocks / crossings after the
+    // jump are those the step-by-step walk reaches, and no sample is skipped (the cube is
+    // empty).
+    const double inv_md = 1.0 / fmax(fabs(d[0]), fmax(fabs(d[1]), fabs(d[2])));
     while (t < t1) {  // grid.cpp:306-333
         double t_exit = t1;
         int axis = -1;
         if (c0 < t_exit) t_exit = c0, axis = 0;
         if (c1 < t_exit) t_exit = c1, axis = 1;
         if (c2 < t_exit) t_exit = c2, axis = 2;
-        const bool alloc = g.use_dense
-                               ? ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0
-                               : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+        int dist = 0;
+        bool alloc;
+        if (g.bdist) {
+            dist = __ldg(g.bdist + static_cast<uint32_t>(cell));
+            alloc = dist == 0;
+        } else {
+            alloc = g.use_dense
+                        ? ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0
+                        : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+        }
+        if (dist >= 3) {
+            open = false;
+            const double ts = t + (dist - 2) * L * inv_md;
+            if (ts >= t1) break;  // the ray leaves the AABB inside empty space
+            int32_t nbv[3] = {b0, b1, b2};
+            double nc[3] = {c0, c1, c2};
+            const int32_t sv[3] = {s0, s1, s2};
+            bool out = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (d[a] == 0.0) continue;
+                const int32_t b = nbv[a];
+                const int32_t bx = static_cast<int32_t>(floor((o[a] + ts * d[a]) / L));
+                int32_t m = (bx - b) * sv[a];
+                m = m < 0 ? 0 : m;
+                while (m > 0 && !(crossing(a, b + (m - 1) * sv[a]) < ts)) --m;
+                double cm = crossing(a, b + m * sv[a]);
+                while (cm < ts) {
+                    ++m;
+                    cm = crossing(a, b + m * sv[a]);
+                }
+                nbv[a] = b + m * sv[a];
+                nc[a] = cm;
+                if (nbv[a] < g.lo[a] || nbv[a] > g.hi[a]) out = true;
+            }
+            if (out) break;
+            b0 = nbv[0], b1 = nbv[1], b2 = nbv[2];
+            c0 = nc[0], c1 = nc[1], c2 = nc[2];
+            cell = ((b2 - g.lo[2]) * g.dim[1] + (b1 - g.lo[1])) * g.dim[0] + (b0 - g.lo[0]);
+            t = ts;
+            continue;
+        }
         if (alloc) {
             if (!open) {
                 open = true;

@@ -213,3 +213,55 @@ def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup):
     assert np.array_equal(m["t"][mask], mo["t"][mask])
     assert np.array_equal(m["delta"][mask], mo["delta"][mask])
     assert mask.sum() > 500_000
+
+
+@pytest.mark.parametrize("jump", [1, 0])
+def test_march_empty_space_jumps_bit_exact(jump):
+    """Sparse block clusters inside a 96^3-block AABB, so most of each ray's walk crosses
+    wide empty space where the dense-mode march jumps over the block-distance field: counts,
+    t and delta must equal the oracle's step-by-step walk bit for bit (random rays, rays
+    through exact block corners / along block edges, axis-parallel and diagonal rays)."""
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    h = 0.01
+    L = 8 * h
+    rng = np.random.default_rng(21)
+    centres = rng.integers(0, 96, size=(40, 3))
+    cl = np.concatenate([c + rng.integers(-2, 3, size=(30, 3)) for c in centres])
+    cl = np.concatenate([cl, [[0, 0, 0], [95, 95, 95]]])  # pin the AABB
+    coords = np.unique(cl, axis=0).astype(np.int32)
+    og = OracleGrid(h, 8, 1)
+    og.allocate_blocks(coords)
+    A = len(coords)
+    og.set_payload(0, A, weight=np.ones((A, 512), np.float32))
+    g = SparseDenseGrid(h, 8, 1)
+    g.allocate_blocks(coords)
+    g.set_payload(0, A, weight=np.ones((A, 512), np.float32))
+    g.set_lookup(2)  # dense AABB index (the jump needs the distance field)
+    g.set_tuning("march_jump", jump)
+    n = 60_000
+    o = rng.uniform(-0.5, 96 * L + 0.5, size=(n, 3))
+    d = rng.normal(size=(n, 3))
+    k = n // 10
+    o[:k] = rng.integers(0, 97, size=(k, 3)) * L  # exact block corners
+    d[k:2 * k] = [1.0, 1.0, 1.0]                   # diagonals through corners
+    o[k:2 * k] = rng.integers(0, 97, size=(k, 3)) * L
+    d[2 * k:3 * k] = [1.0, 1.0, 0.0]
+    d[3 * k:4 * k, 1:] = 0.0                       # axis-parallel
+    d[3 * k:4 * k, 0] = np.sign(d[3 * k:4 * k, 0]) + (d[3 * k:4 * k, 0] == 0)
+    o[4 * k:5 * k, 2] = rng.integers(0, 97, size=k) * L  # rays in block face planes
+    d[4 * k:5 * k, 2] = 0.0
+    tgt = (coords[rng.integers(0, A, size=n - 5 * k)] + rng.uniform(0, 1, size=(n - 5 * k, 3))) * L
+    d[5 * k:] = tgt - o[5 * k:]  # the rest aim at allocated blocks across empty space
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    m = g.march(o, d, h / 2, 64)
+    OracleGrid.set_threads(8)
+    try:
+        mo = og.march(o, d, h / 2, 64)
+    finally:
+        OracleGrid.set_threads(1)
+    assert np.array_equal(m["counts"], mo["counts"])
+    mask = np.arange(64)[None, :] < m["counts"][:, None]
+    assert np.array_equal(m["t"][mask], mo["t"][mask])
+    assert np.array_equal(m["delta"][mask], mo["delta"][mask])
+    assert (m["counts"] > 0).sum() > n // 3
