@@ -446,11 +446,6 @@ __device__ __forceinline__ float warp_incl_suffix(float v, int lane) {
     }
     return v;
 }
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
-    return v;
-}
 
 // Reduce 8 per-lane values over the warp with 9 shuffles (reduce-scatter then butterfly):
 // afterwards lane 4 v (v = 0..7) holds the warp total of value v; returns this lane's.
