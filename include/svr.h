@@ -247,6 +247,31 @@ int svr_fuse_finalize(svr_grid* g);
  * the valid set; weights / validity unchanged.  radius in [0, 4], sigma_vox > 0. */
 int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius);
 
+/* ---- refinement losses (SPEC.md:286-319 backward_step, PAPER Eq. 12-14 / 23) ----
+ * Per-ray upstream gradients for svr_render_backward from the rendered rgb[n][3], depth[n]
+ * (distance along the ray), normal[n][3] (world, un-normalised), wsum[n] and the frame
+ * targets: tgt_rgb[n][3], prior_depth[n] (<= 0 invalid, may be NULL), prior_normal[n][3]
+ * (camera frame, all-zero invalid, may be NULL; needs cam_idx[n] into cams[n_cams]).
+ *   participating ray: wsum > 0 (at least one valid sample)
+ *   L_c = mean sum_ch |C - C*|                                   (colour L1)
+ *   L_d = mean (t - (a D + b))^2, (a, b) = least squares of t on D over the batch (fp64 2x2
+ *         normal equations; singular or fewer than 2 rays: a = 1, b = mean(t - D))
+ *   L_n = mean |normalize(R^T N) - n*|_1 over rays with |R^T N| > 1e-12
+ *   total = L_c + lambda_d L_d + lambda_n L_n (the Eikonal term: svr_eikonal with scale
+ *   lambda_eik); d_rgb / d_depth / d_normal = d total / d output (d/d(a,b) = 0 at the LS
+ *   optimum).  stats may be NULL (then no host synchronisation is needed). */
+typedef struct {
+    double L_c, L_d, L_n, total;
+    double a, b;          /* depth prior fit */
+    uint64_t n_c, n_d, n_n; /* rays in each term */
+    int32_t singular;     /* depth fit fell back to a = 1 */
+} svr_loss_stats;
+int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* depth, const float* normal,
+                      const float* wsum, const float* tgt_rgb, const float* prior_depth,
+                      const float* prior_normal, const uint32_t* cam_idx, const svr_camera* cams,
+                      uint32_t n_cams, double lambda_d, double lambda_n, float* d_rgb, float* d_depth,
+                      float* d_normal, svr_loss_stats* stats);
+
 /* ---- meshing (meshing.hpp:23-28, meshing.cpp:168-273; mesh_io.cpp:30-68) ----
  * marching_cubes(grid, iso): iso surface over every cell whose 8 corners are allocated and
  * observed (cells across block faces included), vertices on cell edges by linear

@@ -251,6 +251,8 @@ class OracleGrid(_Base):
         "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double, POINTER(FuseReport)]),
         "denoise": (c_int, [c_void_p, c_double, c_int]),
         "mc_table": (c_int, [P, P]),
+        "fit_depth_affine": (c_int, [P, P, c_uint64, POINTER(c_double), POINTER(c_double)]),
+        "render_losses": (c_int, [c_uint64, P, P, P, P, P, P, P, P, P, c_double, c_double, P, P, P, P]),
     })
 
     def __init__(self, voxel_size=0.015, block_res=8, label_channels=1, capacity=0, _handle=None):
@@ -352,6 +354,32 @@ def _o_fuse_frames(self, depth, cams, mu, rgb=None, sem=None, scales=None) -> Fu
 
 def _o_denoise(self, sigma_vox=1.0, radius=1):
     self._check(self.lib().svro_denoise(self._h, sigma_vox, radius))
+
+
+def fit_depth_affine(t, D):
+    """(a, b, singular) of the minibatch depth prior fit."""
+    t, D = _f64(t), _f64(D)
+    a, b = c_double(), c_double()
+    sing = OracleGrid.lib().svro_fit_depth_affine(_ptr(t), _ptr(D), len(t), ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value, bool(sing)
+
+
+def render_losses(out, tgt_rgb, prior_depth, prior_normal, cam_idx, cams, lambda_d=0.1, lambda_n=0.05):
+    """Refinement losses + per-ray upstream gradients, fp64."""
+    n = len(out["depth"])
+    f = lambda a, dt=np.float32: None if a is None else np.ascontiguousarray(a, dt)  # noqa: E731
+    arrs = [_f64(out["rgb"]), _f64(out["depth"]), _f64(out["normal"]), _f64(out["wsum"]),
+            f(tgt_rgb), f(prior_depth), f(prior_normal), f(cam_idx, np.uint32)]
+    camarr = (_Cam * len(cams))(*[_Cam.from_any(c) for c in cams])
+    g = {"d_rgb": np.empty((n, 3)), "d_depth": np.empty(n), "d_normal": np.empty((n, 3))}
+    stats = np.empty(10)
+    st = OracleGrid.lib().svro_render_losses(n, *[_ptr(a) for a in arrs], ctypes.addressof(camarr), lambda_d,
+                                             lambda_n, _ptr(g["d_rgb"]), _ptr(g["d_depth"]), _ptr(g["d_normal"]),
+                                             _ptr(stats))
+    if st:
+        raise OracleError(st, OracleGrid.lib().svro_last_error().decode())
+    keys = ("L_c", "L_d", "L_n", "total", "a", "b", "n_c", "n_d", "n_n", "singular")
+    return g, dict(zip(keys, stats.tolist()))
 
 
 OracleGrid.fuse_frames = _o_fuse_frames

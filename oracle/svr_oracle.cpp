@@ -1408,3 +1408,130 @@ int svro_mesh_get(const svro_grid* g, double* v, double* n, double* c, int32_t* 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Refinement losses (SPEC.md:286-319 backward_step, PAPER Eq. 12-14, 23): the per-ray
+// upstream gradients render_backward consumes.  Restatement with the SPEC's decisions:
+//   participating ray: rendered wsum > 0 (>= 1 valid sample; degenerate rays excluded)
+//   L_c = mean_rays sum_ch |C - C*|                      (colour L1)
+//   L_d = mean_rays (t - (a D + b))^2, D > 0; (a, b) = least squares of t on D over the batch
+//         (2x2 normal equations in fp64; singular or < 2 rays: a = 1, b = mean(t - D))
+//   L_n = mean_rays |normalize(R^T N) - n*|_1, |n*| > 0, |R^T N| > 1e-12
+//   total = L_c + lambda_d L_d + lambda_n L_n;  d/d(a, b) = 0 at the optimum (envelope)
+// ---------------------------------------------------------------------------
+namespace {
+inline double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+// (a, b) of the depth prior; *singular set when the fallback was used
+void depth_fit(const double* S, double& a, double& b, bool& singular) {
+    // S = {n, sum D, sum D^2, sum t, sum D t}
+    const double det = S[0] * S[2] - S[1] * S[1];
+    singular = !(S[0] >= 2.0) || !(det > 1e-12 * S[0] * S[2]);
+    if (singular) {
+        a = 1.0;
+        b = S[0] > 0.0 ? (S[3] - S[1]) / S[0] : 0.0;
+    } else {
+        a = (S[0] * S[4] - S[1] * S[3]) / det;
+        b = (S[3] - a * S[1]) / S[0];
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int svro_fit_depth_affine(const double* t, const double* D, uint64_t n, double* a, double* b) {
+    double S[5] = {0, 0, 0, 0, 0};
+    for (uint64_t i = 0; i < n; ++i) {
+        S[0] += 1.0;
+        S[1] += D[i];
+        S[2] += D[i] * D[i];
+        S[3] += t[i];
+        S[4] += D[i] * t[i];
+    }
+    bool singular = false;
+    depth_fit(S, *a, *b, singular);
+    return singular ? 1 : 0;
+}
+
+int svro_render_losses(uint64_t n, const double* rgb, const double* depth, const double* normal,
+                       const double* wsum, const float* tgt_rgb, const float* prior_depth,
+                       const float* prior_normal, const uint32_t* cam_idx, const svro_camera* cams,
+                       double lambda_d, double lambda_n, double* d_rgb, double* d_depth, double* d_normal,
+                       double* stats) {
+    return guarded([&] {
+        double S[5] = {0, 0, 0, 0, 0};
+        uint64_t nc = 0, nn = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            if (!(wsum[i] > 0.0)) continue;
+            ++nc;
+            if (prior_depth && prior_depth[i] > 0.0f) {
+                const double D = prior_depth[i], t = depth[i];
+                S[0] += 1.0, S[1] += D, S[2] += D * D, S[3] += t, S[4] += D * t;
+            }
+        }
+        double a = 1.0, b = 0.0;
+        bool singular = false;
+        depth_fit(S, a, b, singular);
+        const double nd = S[0];
+        // normal term participation needs the camera-frame normal
+        std::vector<double> ncam(3 * n, 0.0), len(n, 0.0);
+        if (prior_normal)
+            for (uint64_t i = 0; i < n; ++i) {
+                if (!(wsum[i] > 0.0)) continue;
+                const float* ps = prior_normal + 3 * i;
+                if (!(ps[0] != 0.0f || ps[1] != 0.0f || ps[2] != 0.0f)) continue;
+                const double* R = cams[cam_idx[i]].R;
+                double* c = &ncam[3 * i];
+                for (int r = 0; r < 3; ++r)  // R^T N
+                    c[r] = R[r] * normal[3 * i] + R[3 + r] * normal[3 * i + 1] + R[6 + r] * normal[3 * i + 2];
+                len[i] = std::sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+                if (len[i] > 1e-12) ++nn;
+            }
+        double Lc = 0.0, Ld = 0.0, Ln = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            double* gc = d_rgb + 3 * i;
+            double* gn = d_normal + 3 * i;
+            gc[0] = gc[1] = gc[2] = 0.0;
+            gn[0] = gn[1] = gn[2] = 0.0;
+            d_depth[i] = 0.0;
+            if (!(wsum[i] > 0.0)) continue;
+            for (int k = 0; k < 3; ++k) {
+                const double e = rgb[3 * i + k] - tgt_rgb[3 * i + k];
+                Lc += std::fabs(e);
+                gc[k] = sgn(e) / nc;
+            }
+            if (prior_depth && prior_depth[i] > 0.0f) {
+                const double r = depth[i] - (a * prior_depth[i] + b);
+                Ld += r * r;
+                d_depth[i] = lambda_d * 2.0 * r / nd;
+            }
+            if (len[i] > 1e-12) {
+                const double* c = &ncam[3 * i];
+                const double nh[3] = {c[0] / len[i], c[1] / len[i], c[2] / len[i]};
+                const float* ps = prior_normal + 3 * i;
+                double sg[3];
+                for (int k = 0; k < 3; ++k) {
+                    const double e = nh[k] - ps[k];
+                    Ln += std::fabs(e);
+                    sg[k] = sgn(e);
+                }
+                const double dot = nh[0] * sg[0] + nh[1] * sg[1] + nh[2] * sg[2];
+                double gcam[3];
+                for (int k = 0; k < 3; ++k) gcam[k] = (sg[k] - nh[k] * dot) / len[i] * (lambda_n / nn);
+                const double* R = cams[cam_idx[i]].R;
+                for (int r = 0; r < 3; ++r)  // R gcam
+                    gn[r] = R[3 * r] * gcam[0] + R[3 * r + 1] * gcam[1] + R[3 * r + 2] * gcam[2];
+            }
+        }
+        Lc = nc ? Lc / nc : 0.0;
+        Ld = nd > 0.0 ? Ld / nd : 0.0;
+        Ln = nn ? Ln / nn : 0.0;
+        stats[0] = Lc, stats[1] = Ld, stats[2] = Ln;
+        stats[3] = Lc + lambda_d * Ld + lambda_n * Ln;
+        stats[4] = a, stats[5] = b;
+        stats[6] = static_cast<double>(nc), stats[7] = nd, stats[8] = static_cast<double>(nn);
+        stats[9] = singular ? 1.0 : 0.0;
+    });
+}
+
+}  // extern "C"

@@ -108,6 +108,15 @@ int svro_mc_table(int32_t* counts, int32_t* tris);
 int svro_marching_cubes(svro_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles);
 int svro_mesh_get(const svro_grid* g, double* v, double* n, double* c, int32_t* labels, int32_t* tris);
 
+/* Refinement losses: per-ray upstream gradients of
+ * L_c + lambda_d L_d + lambda_n L_n; stats = {L_c, L_d, L_n, total, a, b, n_c, n_d, n_n, singular}. */
+int svro_fit_depth_affine(const double* t, const double* D, uint64_t n, double* a, double* b);
+int svro_render_losses(uint64_t n, const double* rgb, const double* depth, const double* normal,
+                       const double* wsum, const float* tgt_rgb, const float* prior_depth,
+                       const float* prior_normal, const uint32_t* cam_idx, const svro_camera* cams,
+                       double lambda_d, double lambda_n, double* d_rgb, double* d_depth, double* d_normal,
+                       double* stats);
+
 int svro_save_sdgv(const svro_grid* g, const char* path);
 int svro_load_sdgv(const char* path, svro_grid** out);
 

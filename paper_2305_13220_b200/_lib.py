@@ -84,6 +84,12 @@ class FuseReport(ctypes.Structure):
                 ("rejected", c_uint64)]
 
 
+class LossStats(ctypes.Structure):
+    _fields_ = [("L_c", c_double), ("L_d", c_double), ("L_n", c_double), ("total", c_double),
+                ("a", c_double), ("b", c_double), ("n_c", c_uint64), ("n_d", c_uint64), ("n_n", c_uint64),
+                ("singular", c_int32)]
+
+
 class SceneSpec(ctypes.Structure):
     _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
                 ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
@@ -137,6 +143,8 @@ _PROTOS = {
                              POINTER(FuseReport)]),
     "svr_fuse_finalize": (_I, [c_void_p]),
     "svr_denoise": (_I, [c_void_p, c_double, c_int32]),
+    "svr_render_losses": (_I, [c_void_p, c_uint64, P, P, P, P, P, P, P, P, P, c_uint32, c_double, c_double,
+                               P, P, P, POINTER(LossStats)]),
     "svr_marching_cubes": (_I, [c_void_p, c_double, POINTER(c_uint64), POINTER(c_uint64)]),
     "svr_mesh_get": (_I, [c_void_p, P, P, P, P, P]),
     "svr_mesh_save_ply": (_I, [c_void_p, c_char_p]),

@@ -226,6 +226,7 @@ struct svr_grid {
     uint32_t fuse_batch = 0;  // frames per k_fuse launch, 0 = auto
     DevBuf pay_spare, logits_spare;  // denoise output planes, swapped with pay / logits
     svr_internal::MeshBufs mesh;     // last svr_marching_cubes result
+    DevBuf loss_acc;                 // svr_render_losses reduction scratch
     // "host_async" pipelined host I/O for render_forward / render_backward: pinned host arrays
     // move on two copy streams through double-buffered device slots, so the transfers of one
     // step overlap the kernels of the previous one; results are valid after synchronize.
@@ -1480,6 +1481,59 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
         g->logits = g->logits_spare.as<float>();
         g->pay_spare.p = old_pay;
         g->logits_spare.p = old_lg;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Refinement losses, K15 in svr_losses.cu.
+// ---------------------------------------------------------------------------
+int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* depth, const float* normal,
+                      const float* wsum, const float* tgt_rgb, const float* prior_depth,
+                      const float* prior_normal, const uint32_t* cam_idx, const svr_camera* cams,
+                      uint32_t n_cams, double lambda_d, double lambda_n, float* d_rgb, float* d_depth,
+                      float* d_normal, svr_loss_stats* stats) {
+    return guarded([&] {
+        if (!rgb || !depth || !normal || !wsum || !tgt_rgb || !d_rgb || !d_depth || !d_normal)
+            throw Fail{SVR_ERR_DATA, "render_losses: rendered outputs, colour targets and gradients required"};
+        if (prior_normal && (!cam_idx || !cams || !n_cams))
+            throw Fail{SVR_ERR_DATA, "render_losses: the normal term needs cameras and per-ray camera indices"};
+        if (!(lambda_d >= 0.0) || !(lambda_n >= 0.0)) throw Fail{SVR_ERR_CONFIG, "render_losses: negative weight"};
+        DeviceGuard dg(g->device);
+        g->loss_acc.ensure(16 * sizeof(double));
+        Stage st(g->stream);
+        const float* a = st.in(rgb, 3 * n);
+        const float* b = st.in(depth, n);
+        const float* c = st.in(normal, 3 * n);
+        const float* w = st.in(wsum, n);
+        const float* t = st.in(tgt_rgb, 3 * n);
+        const float* pd = st.in(prior_depth, n);
+        const float* pn = st.in(prior_normal, 3 * n);
+        const uint32_t* ci = st.in(cam_idx, prior_normal ? n : 0);
+        const svr_camera* cm = st.in(cams, prior_normal ? n_cams : 0);
+        float* gc = st.out(d_rgb, 3 * n);
+        float* gd = st.out(d_depth, n);
+        float* gn = st.out(d_normal, 3 * n);
+        double* acc = g->loss_acc.as<double>();
+        svr_internal::launch_render_losses(n, a, b, c, w, t, pd, pn, ci, cm, lambda_d, lambda_n, gc, gd, gn, acc,
+                                           g->stream);
+        double h[16] = {0};
+        if (stats) SVR_CK(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+        st.finish();
+        if (stats) {
+            SVR_CK(cudaStreamSynchronize(g->stream));
+            svr_loss_stats o{};
+            o.n_c = static_cast<uint64_t>(h[5]);
+            o.n_d = static_cast<uint64_t>(h[0]);
+            o.n_n = static_cast<uint64_t>(h[6]);
+            o.L_c = o.n_c ? h[10] / h[5] : 0.0;
+            o.L_d = o.n_d ? h[11] / h[0] : 0.0;
+            o.L_n = o.n_n ? h[12] / h[6] : 0.0;
+            o.total = o.L_c + lambda_d * o.L_d + lambda_n * o.L_n;
+            o.a = h[7];
+            o.b = h[8];
+            o.singular = h[9] != 0.0 ? 1 : 0;
+            *stats = o;
+        }
     });
 }
 

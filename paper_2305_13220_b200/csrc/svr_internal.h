@@ -138,6 +138,12 @@ size_t denoise_smem(int radius);
 void launch_denoise(const svr_dev::GridView& g, const int32_t* coords4, float4* pay_out, float* logits_out,
                     int32_t radius, const double* gw, cudaStream_t s);
 
+// Refinement losses (svr_losses.cu); acc = 16 doubles of device scratch (see LossArgs)
+void launch_render_losses(uint64_t n, const float* rgb, const float* depth, const float* normal,
+                          const float* wsum, const float* tgt, const float* pdepth, const float* pnormal,
+                          const uint32_t* cam_idx, const svr_camera* cams, double lambda_d, double lambda_n,
+                          float* d_rgb, float* d_depth, float* d_normal, double* acc, cudaStream_t s);
+
 // Marching cubes (svr_mesh.cu): the last mesh of a handle, device resident.
 struct MeshBufs {
     double* v = nullptr;   // [nv][3] vertices

@@ -15,7 +15,7 @@ from typing import Any
 import numpy as np
 
 from . import _lib
-from ._lib import AllocReport, Camera, FuseReport, GridInfo, RenderStats, check
+from ._lib import AllocReport, Camera, FuseReport, GridInfo, LossStats, RenderStats, check
 
 try:  # torch is plumbing only (device buffers, streams); numpy works without it
     import torch
@@ -365,6 +365,32 @@ class SparseDenseGrid:
     def rmsprop_step(self, lr: float, alpha: float = 0.99, eps: float = 1e-8) -> None:
         """RMSProp on active blocks, then zero their gradients."""
         check(self._lib.svr_rmsprop_step(self._h, lr, alpha, eps))
+
+    # --- refinement losses (SPEC.md:286-319) ------------------------------------------
+    def render_losses(self, out: dict, tgt_rgb, prior_depth=None, prior_normal=None, cam_idx=None,
+                      cameras=None, lambda_d: float = 0.1, lambda_n: float = 0.05, grads: dict | None = None,
+                      stats: bool = True):
+        """Upstream gradients (d_rgb, d_depth, d_normal) of L_c + lambda_d L_d + lambda_n L_n for
+        render_backward, from a render_forward output dict; see include/svr.h."""
+        keep: list = []
+        n = out["depth"].shape[0]
+        like = out["depth"]
+        if grads is None:
+            grads = {}
+            for k, shape in (("d_rgb", (n, 3)), ("d_depth", (n,)), ("d_normal", (n, 3))):
+                grads[k], _ = _out(shape, np.float32, like)
+        ptr = {k: (v.data_ptr() if _is_tensor(v) else v.ctypes.data) for k, v in grads.items()}
+        cams = (Camera * max(len(cameras), 1))(*cameras) if cameras else None
+        st = LossStats()
+        check(self._lib.svr_render_losses(
+            self._h, n, _in(out["rgb"], np.float32, keep), _in(out["depth"], np.float32, keep),
+            _in(out["normal"], np.float32, keep), _in(out["wsum"], np.float32, keep),
+            _in(tgt_rgb, np.float32, keep), _in(prior_depth, np.float32, keep),
+            _in(prior_normal, np.float32, keep), _in(cam_idx, np.uint32, keep),
+            ctypes.addressof(cams) if cams is not None else None, len(cameras) if cameras else 0,
+            lambda_d, lambda_n, ptr["d_rgb"], ptr["d_depth"], ptr["d_normal"],
+            ctypes.byref(st) if stats else None))
+        return grads, ({f: getattr(st, f) for f, _ in LossStats._fields_} if stats else None)
 
     # --- fusion + de-noising (SPEC.md:207-233) -----------------------------------------
     def fuse_begin(self, color: bool = True, semantic: bool = True) -> None:
