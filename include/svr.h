@@ -272,6 +272,22 @@ int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* de
                       uint32_t n_cams, double lambda_d, double lambda_n, float* d_rgb, float* d_depth,
                       float* d_normal, svr_loss_stats* stats);
 
+/* A refinement batch (SPEC.md RenderConfig: images_per_batch x rays_per_image rays) from the
+ * frames rgb[F][H][W][3] / prior depth[F][H][W] / prior normal[F][H][W][3] (camera frame;
+ * depth / normal may be NULL -> 0 targets; pass device arrays, host ones are staged per
+ * call): image slot j takes frame splitmix(seed, j) mod F, ray i pixel splitmix(seed, i)
+ * mod W*H; o = camera centre, d = Camera::ray_direction (camera.cpp:27-30, fp64 reference
+ * order); targets are the pixel's values; cam_idx = frame, pixel = frame * W * H + y * W + x.
+ * Outputs other than o / d may be NULL. */
+int svr_sample_frame_rays(svr_grid* g, const svr_camera* cams, uint32_t n_frames, const float* rgb,
+                          const float* depth, const float* normal, uint32_t images_per_batch,
+                          uint32_t rays_per_image, uint64_t seed, double* o, double* d, float* tgt_rgb,
+                          float* prior_depth, float* prior_normal, uint32_t* cam_idx, uint32_t* pixel);
+/* sample_eikonal_points part (a): the samples of the last forward with
+ * |sdf| < band (the forward's fp32 interpolated sdf; needs records = 1), as points
+ * out[cap][3] in (ray, sample) order; *n_out = how many qualify (may exceed cap). */
+int svr_band_points(svr_grid* g, double band, uint64_t cap, double* out, uint64_t* n_out);
+
 /* ---- meshing (meshing.hpp:23-28, meshing.cpp:168-273; mesh_io.cpp:30-68) ----
  * marching_cubes(grid, iso): iso surface over every cell whose 8 corners are allocated and
  * observed (cells across block faces included), vertices on cell edges by linear

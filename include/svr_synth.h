@@ -43,9 +43,10 @@ int svr_scene_depth(const svr_scene* s, const svr_camera* cams, uint32_t n, floa
                     int32_t threads);
 /* The frame images of generate_dataset (synthetic.cpp:318-340) per integer pixel: GT
  * z-depth [n][H][W], rgb = scene.color(hit point, hit label) [n][H][W][3], semantic =
- * one-hot(hit label) [n][H][W][C] (C >= 4).  Any output may be NULL. */
+ * one-hot(hit label) [n][H][W][C] (C >= 4), camera-frame surface normal R^T n [n][H][W][3].
+ * Any output may be NULL. */
 int svr_scene_frames(const svr_scene* s, const svr_camera* cams, uint32_t n, float* depth_out,
-                     float* rgb_out, float* semantic_out, int32_t C, int32_t threads);
+                     float* rgb_out, float* semantic_out, int32_t C, float* normal_out, int32_t threads);
 /* SyntheticScene::sdf (synthetic.cpp:71-80) */
 int svr_scene_sdf(const svr_scene* s, const double* x, uint64_t n, double* out);
 /* Fills block payloads in the reference per-block layout (grid.hpp:62-66):

@@ -145,6 +145,9 @@ _PROTOS = {
     "svr_denoise": (_I, [c_void_p, c_double, c_int32]),
     "svr_render_losses": (_I, [c_void_p, c_uint64, P, P, P, P, P, P, P, P, P, c_uint32, c_double, c_double,
                                P, P, P, POINTER(LossStats)]),
+    "svr_sample_frame_rays": (_I, [c_void_p, P, c_uint32, P, P, P, c_uint32, c_uint32, c_uint64, P, P, P, P, P, P,
+                                   P]),
+    "svr_band_points": (_I, [c_void_p, c_double, c_uint64, P, POINTER(c_uint64)]),
     "svr_marching_cubes": (_I, [c_void_p, c_double, POINTER(c_uint64), POINTER(c_uint64)]),
     "svr_mesh_get": (_I, [c_void_p, P, P, P, P, P]),
     "svr_mesh_save_ply": (_I, [c_void_p, c_char_p]),
@@ -154,7 +157,7 @@ _PROTOS = {
     "svr_scene_destroy": (None, [c_void_p]),
     "svr_scene_camera": (_I, [c_void_p, c_int32, POINTER(Camera)]),
     "svr_scene_depth": (_I, [c_void_p, P, c_uint32, P, c_int32]),
-    "svr_scene_frames": (_I, [c_void_p, P, c_uint32, P, P, P, c_int32, c_int32]),
+    "svr_scene_frames": (_I, [c_void_p, P, c_uint32, P, P, P, c_int32, P, c_int32]),
     "svr_scene_sdf": (_I, [c_void_p, P, c_uint64, P]),
     "svr_scene_fill_payload": (_I, [c_void_p, c_double, c_int32, c_int32, c_double, P, c_uint64,
                                     P, P, P, P, c_int32]),

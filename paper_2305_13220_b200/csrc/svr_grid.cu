@@ -1537,6 +1537,68 @@ int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* de
     });
 }
 
+int svr_sample_frame_rays(svr_grid* g, const svr_camera* cams, uint32_t n_frames, const float* rgb,
+                          const float* depth, const float* normal, uint32_t images_per_batch,
+                          uint32_t rays_per_image, uint64_t seed, double* o, double* d, float* tgt_rgb,
+                          float* prior_depth, float* prior_normal, uint32_t* cam_idx, uint32_t* pixel) {
+    return guarded([&] {
+        if (!n_frames || !cams) throw Fail{SVR_ERR_DATA, "sample_frame_rays: no frames"};
+        if (!o || !d) throw Fail{SVR_ERR_DATA, "sample_frame_rays: ray outputs required"};
+        if (tgt_rgb && !rgb) throw Fail{SVR_ERR_DATA, "sample_frame_rays: colour targets need the rgb frames"};
+        std::vector<svr_camera> hc(n_frames);
+        if (is_device_ptr(cams))
+            SVR_CK(cudaMemcpy(hc.data(), cams, n_frames * sizeof(svr_camera), cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(hc.data(), cams, n_frames * sizeof(svr_camera));
+        const int32_t W = hc[0].width, H = hc[0].height;
+        for (const svr_camera& c : hc)
+            if (c.width != W || c.height != H) throw Fail{SVR_ERR_CONFIG, "sample_frame_rays: frames differ in size"};
+        const uint64_t n = static_cast<uint64_t>(images_per_batch) * rays_per_image;
+        if (!n) return;
+        if (static_cast<uint64_t>(n_frames) * W * H >= (1ull << 32))
+            throw Fail{SVR_ERR_CONFIG, "sample_frame_rays: more than 2^32 frame pixels"};
+        DeviceGuard dg(g->device);
+        Stage st(g->stream);
+        const size_t npx = static_cast<size_t>(n_frames) * W * H;
+        const svr_camera* dc = st.in(cams, n_frames);
+        const float* ri = st.in(rgb, 3 * npx);
+        const float* di = st.in(depth, npx);
+        const float* ni = st.in(normal, 3 * npx);
+        double* a = st.out(o, 3 * n);
+        double* b = st.out(d, 3 * n);
+        float* t = st.out(tgt_rgb, 3 * n);
+        float* pd = st.out(prior_depth, n);
+        float* pn = st.out(prior_normal, 3 * n);
+        uint32_t* ci = st.out(cam_idx, n);
+        uint32_t* px = st.out(pixel, n);
+        svr_internal::launch_sample_frame_rays(dc, n_frames, W, H, rays_per_image, n, seed, ri, di, ni, a, b, t, pd, pn,
+                                               ci, px, g->stream);
+        st.finish();
+    });
+}
+
+int svr_band_points(svr_grid* g, double band, uint64_t cap, double* out, uint64_t* n_out) {
+    return guarded([&] {
+        if (!g->ctx_valid) throw Fail{SVR_ERR_DATA, "band_points: no retained forward context"};
+        if (!g->ctx_rec) throw Fail{SVR_ERR_CONFIG, "band_points: needs the forward records (tuning records = 1)"};
+        DeviceGuard dg(g->device);
+        const uint64_t n = g->ctx_n;
+        uint64_t total = 0;
+        if (n) {
+            g->scratch_a.ensure(8 * n + 16);
+            const size_t tb = std::max<size_t>(svr_internal::band_points_tmp_bytes(n), 16);
+            g->scratch_c.ensure(tb);
+            Stage st(g->stream);
+            double* pts = out ? st.out(out, 3 * cap) : nullptr;
+            total = svr_internal::band_points(g->ctx_o, g->ctx_d, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
+                                              g->rec.as<float4>(), n, g->ctx_S, static_cast<float>(band),
+                                              g->scratch_a.as<uint32_t>(), g->scratch_c.p, tb, cap, pts, g->stream);
+            st.finish();
+        }
+        if (n_out) *n_out = total;
+    });
+}
+
 // ---------------------------------------------------------------------------
 // Marching cubes (meshing.cpp:168-273) and the PLY writer (mesh_io.cpp:30-68).
 // ---------------------------------------------------------------------------

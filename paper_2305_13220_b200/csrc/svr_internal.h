@@ -144,6 +144,16 @@ void launch_render_losses(uint64_t n, const float* rgb, const float* depth, cons
                           const uint32_t* cam_idx, const svr_camera* cams, double lambda_d, double lambda_n,
                           float* d_rgb, float* d_depth, float* d_normal, double* acc, cudaStream_t s);
 
+// Refinement batch + Eikonal band points (svr_refine.cu)
+void launch_sample_frame_rays(const svr_camera* cams, uint32_t n_frames, int32_t W, int32_t H,
+                              uint32_t rays_per_image, uint64_t n, uint64_t seed, const float* rgb_img,
+                              const float* depth_img, const float* normal_img, double* o, double* d, float* tgt,
+                              float* pdepth, float* pnormal, uint32_t* cam_idx, uint32_t* pixel, cudaStream_t s);
+uint64_t band_points(const double* o, const double* d, const uint32_t* counts, const double* t,
+                     const float4* rec, uint64_t n, uint32_t S, float band, uint32_t* scratch, void* tmp,
+                     size_t tmp_bytes, uint64_t cap, double* pts, cudaStream_t s);
+size_t band_points_tmp_bytes(uint64_t n);
+
 // Marching cubes (svr_mesh.cu): the last mesh of a handle, device resident.
 struct MeshBufs {
     double* v = nullptr;   // [nv][3] vertices

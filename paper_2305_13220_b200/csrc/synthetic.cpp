@@ -125,7 +125,7 @@ struct svr_scene {
     }
     // SyntheticScene::raycast (synthetic.cpp:89-162): returns z-depth (camera-z unit dir)
     bool raycast(const svr_camera& cam, double u, double v, double& depth, int* label = nullptr,
-                 V3* point = nullptr) const {
+                 V3* point = nullptr, V3* normal = nullptr) const {
         const double dc[3] = {(u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy, 1.0};
         V3 d;
         double dd[3];
@@ -136,6 +136,7 @@ struct svr_scene {
         double best_t = std::numeric_limits<double>::max();
         bool hit = false;
         int best_label = -1;
+        V3 best_n{0.0, 0.0, 1.0};
         const double rh[3] = {room_half.x, room_half.y, room_half.z};
         for (int a = 0; a < 3; ++a) {
             if (d[a] == 0.0) continue;
@@ -145,6 +146,8 @@ struct svr_scene {
                 best_t = t;
                 hit = true;
                 best_label = (a == 2 && d[a] < 0.0) ? kLabelFloor : kLabelWall;
+                const double nv = d[a] > 0.0 ? -1.0 : 1.0;  // synthetic.cpp:104-106
+                best_n = {a == 0 ? nv : 0.0, a == 1 ? nv : 0.0, a == 2 ? nv : 0.0};
             }
         }
         for (const Object& obj : objects) {
@@ -160,6 +163,11 @@ struct svr_scene {
                     best_t = t;
                     hit = true;
                     best_label = obj.label;
+                    // (o + t d - c).normalized() (synthetic.cpp:120)
+                    const V3 q{o.x + t * d.x - obj.center.x, o.y + t * d.y - obj.center.y,
+                               o.z + t * d.z - obj.center.z};
+                    const double qn = std::sqrt(sqnorm(q));
+                    best_n = {q.x / qn, q.y / qn, q.z / qn};
                 }
             } else {
                 double t0 = -std::numeric_limits<double>::max();
@@ -186,12 +194,15 @@ struct svr_scene {
                     best_t = t0;
                     hit = true;
                     best_label = obj.label;
+                    const double nv = d[enter_axis] > 0.0 ? -1.0 : 1.0;  // synthetic.cpp:147-149
+                    best_n = {enter_axis == 0 ? nv : 0.0, enter_axis == 1 ? nv : 0.0, enter_axis == 2 ? nv : 0.0};
                 }
             }
         }
         depth = best_t;
         if (label) *label = best_label;
         if (point) *point = {o.x + best_t * d.x, o.y + best_t * d.y, o.z + best_t * d.z};  // synthetic.cpp:158
+        if (normal) *normal = best_n;
         return hit;
     }
     // SyntheticScene::camera_for_frame (synthetic.cpp:164-192)
@@ -302,7 +313,7 @@ int svr_scene_depth(const svr_scene* s, const svr_camera* cams, uint32_t n, floa
 }
 
 int svr_scene_frames(const svr_scene* s, const svr_camera* cams, uint32_t n, float* depth_out,
-                     float* rgb_out, float* semantic_out, int32_t C, int32_t threads) {
+                     float* rgb_out, float* semantic_out, int32_t C, float* normal_out, int32_t threads) {
     if (n == 0) return SVR_OK;
     if (semantic_out && C < 4) {
         svr_internal::set_error("synthetic: semantic images need label_channels >= 4");
@@ -318,8 +329,8 @@ int svr_scene_frames(const svr_scene* s, const svr_camera* cams, uint32_t n, flo
             for (int x = 0; x < W; ++x) {
                 double dep = 0.0;
                 int lab = 0;
-                V3 p{0, 0, 0};
-                if (!s->raycast(cams[f], x, y, dep, &lab, &p) || lab < 0) {
+                V3 p{0, 0, 0}, nw{0, 0, 1};
+                if (!s->raycast(cams[f], x, y, dep, &lab, &p, &nw) || lab < 0) {
                     escaped = true;
                     lab = 0;
                 }
@@ -329,6 +340,12 @@ int svr_scene_frames(const svr_scene* s, const svr_camera* cams, uint32_t n, flo
                     double c[3];
                     s->color(p, lab, c);
                     for (int k = 0; k < 3; ++k) rgb_out[3 * px + k] = static_cast<float>(c[k]);
+                }
+                if (normal_out) {  // synthetic.cpp:333-335: camera-frame normal R^T n
+                    const svr_camera& c = cams[f];
+                    for (int k = 0; k < 3; ++k)
+                        normal_out[3 * px + k] =
+                            static_cast<float>((c.R[k] * nw.x + c.R[3 + k] * nw.y) + c.R[6 + k] * nw.z);
                 }
                 if (semantic_out)  // synthetic.cpp:336: one-hot
                     for (int k = 0; k < C; ++k) semantic_out[C * px + k] = (k == lab) ? 1.0f : 0.0f;

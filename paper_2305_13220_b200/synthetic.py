@@ -51,18 +51,22 @@ class SyntheticScene:
                                         threads))
         return out
 
-    def frames(self, cams: list[Camera], threads: int = 0, label_channels: int | None = None):
+    def frames(self, cams: list[Camera], threads: int = 0, label_channels: int | None = None,
+               normals: bool = False):
         """(depth[F][H][W], rgb[F][H][W][3], semantic[F][H][W][C]) as generate_dataset renders
-        them (synthetic.cpp:318-340): GT z-depth, scene colour at the hit, one-hot hit label."""
+        them (synthetic.cpp:318-340): GT z-depth, scene colour at the hit, one-hot hit label;
+        with normals=True also the camera-frame normal map [F][H][W][3]."""
         C = self.spec.label_channels if label_channels is None else label_channels
         arr = (Camera * len(cams))(*cams)
         F, H, W = len(cams), self.spec.height, self.spec.width
         depth = np.empty((F, H, W), np.float32)
         rgb = np.empty((F, H, W, 3), np.float32)
         sem = np.empty((F, H, W, C), np.float32)
+        nrm = np.empty((F, H, W, 3), np.float32) if normals else None
         check(self._lib.svr_scene_frames(self._h, ctypes.addressof(arr), F, depth.ctypes.data,
-                                         rgb.ctypes.data, sem.ctypes.data, C, threads))
-        return depth, rgb, sem
+                                         rgb.ctypes.data, sem.ctypes.data, C,
+                                         nrm.ctypes.data if normals else None, threads))
+        return (depth, rgb, sem, nrm) if normals else (depth, rgb, sem)
 
     def sdf(self, x) -> np.ndarray:
         x = np.ascontiguousarray(x, np.float64).reshape(-1, 3)
