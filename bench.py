@@ -490,7 +490,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             line["extra_configs"] = {"cfg2_image_forward": bench_cfg2(dev, stream),
                                      "cfg4_activation_and_query": bench_cfg4(dev, stream),
                                      "cfg3_fusion_and_denoise": bench_fusion(dev, stream,
-                                                                             cpu=not args.no_cpu_baseline)}
+                                                                             cpu=not args.no_cpu_baseline),
+                                     "cfg3_refine_step": bench_refine(dev, stream)}
         except Exception as e:  # pragma: no cover
             line["extra_configs"] = {"error": str(e)}
     if world == 1 and not args.no_cpu_baseline:
@@ -669,6 +670,48 @@ def bench_fusion(dev, stream, cpu=True):
                                               "sample": f"blocks [{b0}, {b0 + nb}) -> {len(sm['triangles'])} "
                                                         f"triangles ({dt:.2f} s)"}
     del g
+    torch.cuda.empty_cache()
+    return out
+
+
+def bench_refine(dev, stream, steps=20):
+    """SURVEY.md 8(f) / SPEC.md:320-327: the full refinement step at the paper's batch (64 images
+    x 1024 rays) on the cfg3 grid with device-resident 640x480 frames (rgb, depth prior,
+    normal prior): sample batch -> forward -> losses -> backward -> Eikonal -> RMSProp."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+    from paper_2305_13220_b200.refine import RefineConfig, Refiner, frames_to_device
+
+    cfg = CFG3
+    scene = make_scene(cfg)
+    cams = scene.cameras(cfg["act_frames"])
+    depth, rgb, _, nrm = scene.frames(cams, normals=True)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
+    g.set_stream(stream)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    r, dp, nm = frames_to_device(rgb, depth, nrm, device=dev)
+    mu = 8 * cfg["h"] * cfg["dilation"]
+    # 256 samples: with R = 2 the allocated shell in front of a surface alone is 2 L = 16 cm =
+    # 32 samples at h/2 and rays cross other shells first; 64 would stop most rays short
+    ref = Refiner(g, cams, r, dp, nm, step_m=cfg["h"] / 2, beta=2 * cfg["h"], mu=mu,
+                  config=RefineConfig(max_samples=256))
+    ref.run(3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ref.run(steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    st = ref.step(0, 1, stats=True)
+    out = {"rays_per_step": ref.n, "max_samples": 256, "ms_per_step": ms, "rays_per_s": ref.n / (ms * 1e-3),
+           "loss": {k: st[k] for k in ("L_c", "L_d", "L_n", "L_eik", "total")},
+           "launches_per_step": "k_sample_frame_rays, ray order x2 (+CUB), k_march, k_forward, k_loss_sums, "
+                                "k_loss_fit, k_loss_grad, k_backward (S > 64: non-pipelined), k_band_count (+CUB scan), k_band_write, "
+                                "k_sample_uniform, k_eik_stats, k_eik_scatter, k_active_*, k_rmsprop"}
+    del ref, g
     torch.cuda.empty_cache()
     return out
 
