@@ -48,8 +48,16 @@ class Refiner:
     """
 
     def __init__(self, grid, cameras, rgb, depth=None, normal=None, *, step_m, beta, mu,
-                 config: RefineConfig | None = None):
+                 config: RefineConfig | None = None, group=None):
         import torch
+        import torch.distributed as dist
+
+        # data parallel over a process group: each rank draws its own batch, the per-rank
+        # means are scaled by 1/world and the voxel gradients summed (distributed.py) before
+        # the update, so every replica applies the same step
+        self.group = group
+        self.world = dist.get_world_size(group) if (group is not None or dist.is_initialized()) else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
 
         self.g = grid
         self.cfg = config or RefineConfig()
@@ -84,23 +92,31 @@ class Refiner:
         ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
         check(lib.svr_sample_frame_rays(
             g._h, self.cams_dev.data_ptr(), len(self.cams), ptr(self.rgb), ptr(self.depth), ptr(self.normal),
-            c.images_per_batch, c.rays_per_image, c.seed * 1000003 + i, ptr(self.o), ptr(self.d), ptr(self.tgt),
+            c.images_per_batch, c.rays_per_image, (c.seed * 1000003 + i) * 65599 + self.rank, ptr(self.o),
+            ptr(self.d), ptr(self.tgt),
             ptr(self.pd), ptr(self.pn), ptr(self.ci), None))
         g.render_forward(self.o, self.d, self.step_m, c.max_samples, self.beta, out=self.out)
         _, st = g.render_losses(self.out, self.tgt, self.pd if self.depth is not None else None,
                                 self.pn if self.normal is not None else None, self.ci, self.cams,
                                 c.lambda_d, c.lambda_n, grads=self.grads, stats=stats)
+        if self.world > 1:
+            for t in self.grads.values():
+                t.mul_(1.0 / self.world)
         g.render_backward(self.grads["d_rgb"], self.grads["d_depth"], self.grads["d_normal"])
         nb = ctypes.c_uint64()
         check(lib.svr_band_points(g._h, 0.5 * self.mu, c.band_cap, self.pts.data_ptr(), ctypes.byref(nb)))
         m = min(nb.value, c.band_cap)
         if c.uniform_points:
-            check(lib.svr_sample_uniform(g._h, c.uniform_points, c.seed * 7919 + i,
+            check(lib.svr_sample_uniform(g._h, c.uniform_points, (c.seed * 7919 + i) * 65599 + self.rank,
                                          self.pts[m:].data_ptr()))
             m += c.uniform_points
         eik = (0.0, 0)
         if m and c.lambda_eik > 0:
-            eik = g.eikonal(self.pts[:m], c.lambda_eik)
+            eik = g.eikonal(self.pts[:m], c.lambda_eik / self.world)
+        if self.world > 1:
+            from .distributed import reduce_active_grads
+
+            reduce_active_grads(g, self.dev, self.group)
         g.rmsprop_step(self.lr_at(i, steps), c.alpha, c.eps)
         if stats:
             st = dict(st)
