@@ -221,6 +221,30 @@ inline void denoise(SparseDenseGrid& grid, double sigma_vox = 1.0, int radius = 
     check(svr_denoise(grid.handle(), sigma_vox, radius));
 }
 
+// refinement: loss layer of backward_step, batch sampling, band points
+using LossStats = svr_loss_stats;
+inline LossStats render_losses(SparseDenseGrid& grid, std::uint64_t n, const RenderOutputs& out,
+                               const float* tgt_rgb, const float* prior_depth, const float* prior_normal,
+                               const std::uint32_t* cam_idx, const Camera* cams, std::uint32_t n_cams,
+                               double lambda_d, double lambda_n, float* d_rgb, float* d_depth, float* d_normal) {
+    LossStats st{};
+    check(svr_render_losses(grid.handle(), n, out.rgb, out.depth, out.normal, out.wsum, tgt_rgb, prior_depth,
+                            prior_normal, cam_idx, cams, n_cams, lambda_d, lambda_n, d_rgb, d_depth, d_normal, &st));
+    return st;
+}
+inline void sample_frame_rays(SparseDenseGrid& grid, const Camera* cams, std::uint32_t n_frames, const float* rgb,
+                              const float* depth, const float* normal, std::uint32_t images_per_batch,
+                              std::uint32_t rays_per_image, std::uint64_t seed, double* o, double* d,
+                              float* tgt_rgb, float* prior_depth, float* prior_normal, std::uint32_t* cam_idx) {
+    check(svr_sample_frame_rays(grid.handle(), cams, n_frames, rgb, depth, normal, images_per_batch, rays_per_image,
+                                seed, o, d, tgt_rgb, prior_depth, prior_normal, cam_idx, nullptr));
+}
+inline std::uint64_t band_points(SparseDenseGrid& grid, double band, std::uint64_t cap, double* out) {
+    std::uint64_t n = 0;
+    check(svr_band_points(grid.handle(), band, cap, out, &n));
+    return n;
+}
+
 // Mesh + marching_cubes + export_ply (meshing.hpp:10-28, mesh_io.hpp:12): flat arrays in the
 // reference's element order (vertices / normals / colors xyz per vertex, triangles ijk).
 struct Mesh {
