@@ -612,9 +612,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, co
         const float incl = warp_incl_scan(tau0 + tau1, lane);
         float excl = __shfl_up_sync(kFull, incl, 1);
         if (lane == 0) excl = 0.f;
-        const float P0 = tau_base + excl, P1 = P0 + tau0;
-        const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
-        const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
+        // T0 = exp(-P0); w0 = T0 (1 - e^-tau0); T1 = T0 e^-tau0 = T0 - w0 (one exp per pair)
+        const float T0 = expf(-(tau_base + excl));
+        const float w0 = -T0 * expm1f(-tau0);
+        const float T1 = T0 - w0;
+        const float w1 = ok1 ? -T1 * expm1f(-tau1) : 0.f;
         acc[0] += w0 * v0.r + w1 * v1.r;
         acc[1] += w0 * v0.gc + w1 * v1.gc;
         acc[2] += w0 * v0.b + w1 * v1.b;
@@ -623,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, co
         acc[5] += w0 * v0.gy + w1 * v1.gy;
         acc[6] += w0 * v0.gz + w1 * v1.gz;
         acc[7] += w0 + w1;
-        nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
+        if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
         tau_base += __shfl_sync(kFull, incl, 31);
     }
     write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
