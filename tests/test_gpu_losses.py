@@ -62,3 +62,23 @@ def test_losses_device_resident_no_sync():
                              cam_idx, cams)
     for k in ("d_rgb", "d_depth", "d_normal"):
         assert_close(grads[k].cpu().numpy(), ref[k], rtol=1e-6, atol_frac=1e-7, what=k)
+
+
+@pytest.mark.parametrize("which", ["colour_only", "no_normal", "no_depth"])
+def test_losses_optional_terms_match_oracle(which):
+    case, cams, cam_idx, _, tgt, pd, pn = _toy(8)
+    pd = None if which in ("colour_only", "no_depth") else pd
+    pn = None if which in ("colour_only", "no_normal") else pn
+    g = gpu_grid_from(case)
+    out = g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    grads, st = g.render_losses(out, tgt, pd, pn, cam_idx, cams, 0.1, 0.05)
+    og, ost = oracle_losses(out, tgt, pd, pn, cam_idx, cams, 0.1, 0.05)
+    for k in ("n_c", "n_d", "n_n"):
+        assert st[k] == ost[k], k
+    assert st["total"] == pytest.approx(ost["total"], rel=1e-9)
+    for k in ("d_rgb", "d_depth", "d_normal"):
+        assert_close(grads[k], og[k], rtol=1e-5, atol_frac=1e-6, what=k)
+    if pd is None:
+        assert not np.any(grads["d_depth"])
+    if pn is None:
+        assert not np.any(grads["d_normal"])
