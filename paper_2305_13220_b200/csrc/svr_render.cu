@@ -344,11 +344,14 @@ __device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3
 }
 
 // Full gather + trilinear interpolation of sdf, grad(sdf) and rgb (fp32 payload math).
+// kDiag (diagnostic builds of k_forward only; results are wrong): 1 = no payload loads,
+// 2 = no block lookup (base block assumed to be block 0 and fully valid)
+template <int kDiag = 0>
 __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
                                             double t, SampleVal& v) {
     int base[3];
     cell_geom(g, o, d, t, base, v);
-    const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
+    const uint32_t e0 = kDiag == 2 ? kFullBit : lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
     const bool ok = corner_addrs<true>(g, base, e0, v);
     if (!ok) {
         v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
@@ -358,7 +361,14 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
     v.e0 = e0;
     float4 p[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + v.gidx[c]);
+    for (int c = 0; c < 8; ++c) {
+        if (kDiag == 1) {
+            const float q = static_cast<float>(v.gidx[c] & 1023) * 1e-4f;
+            p[c] = make_float4(q, q, q, q);
+        } else {
+            p[c] = __ldg(g.pay + v.gidx[c]);
+        }
+    }
     const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
     const float w[8] = {x0 * y0 * z0, x1 * y0 * z0, x0 * y1 * z0, x1 * y1 * z0,
                         x0 * y0 * z1, x1 * y0 * z1, x0 * y1 * z1, x1 * y1 * z1};
@@ -382,9 +392,10 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
 }
 
 // A lane slot past the ray's sample count: well-defined zeros (accumulated with w = 0).
+template <int kDiag = 0>
 __device__ __forceinline__ bool eval_slot(const GridView& g, const double o[3], const double d[3],
                                           bool in, double t, SampleVal& v) {
-    if (in) return eval_sample(g, o, d, t, v);
+    if (in) return eval_sample<kDiag>(g, o, d, t, v);
     zero_sample(v);
     return false;
 }
@@ -577,7 +588,7 @@ __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__
 // K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
 // chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
 // ---------------------------------------------------------------------------
-template <int kThreads, int kMinBlocks>
+template <int kThreads, int kMinBlocks, int kDiag = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, const double* __restrict__ O,
                                                     const double* __restrict__ D, uint64_t n,
                                                     const uint32_t* __restrict__ order,
@@ -600,9 +611,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, co
     for (uint32_t base = 0; base < cnt; base += 64) {
         const PairT p = load_pair(tr, cnt, base, lane, step);
         SampleVal v0, v1;
-        const bool ok0 = eval_slot(g, o, d, p.in0, p.t0, v0);
-        const bool ok1 = eval_slot(g, o, d, p.in1, p.t1, v1);
-        if (rec) {  // per-sample record for the backward (coalesced: 64 B per lane)
+        const bool ok0 = eval_slot<kDiag == 3 ? 0 : kDiag>(g, o, d, p.in0, p.t0, v0);
+        const bool ok1 = eval_slot<kDiag == 3 ? 0 : kDiag>(g, o, d, p.in1, p.t1, v1);
+        if (rec && kDiag != 3) {  // per-sample record for the backward (coalesced: 64 B per lane)
             float4* rr = rec + (r * S + base + 2 * lane) * 2;
             if (p.in0) store_record(rr, v0);
             if (p.in1) store_record(rr + 2, v1);
@@ -1215,6 +1226,16 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
         case 11: SVR_FWD(768, 1); break;  // one 24-warp CTA per SM: concurrent warps = adjacent rays
         case 12: SVR_FWD(512, 1); break;
         case 13: SVR_FWD(1024, 1); break;
+        // diagnostics (wrong results): 101 no payload loads, 102 no block lookup, 103 no records
+        case 101: k_forward<256, 3, 1><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
+                                                                           rgb, depth, normal, wsum, valid_counter, rec);
+            break;
+        case 102: k_forward<256, 3, 2><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
+                                                                           rgb, depth, normal, wsum, valid_counter, rec);
+            break;
+        case 103: k_forward<256, 3, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
+                                                                           rgb, depth, normal, wsum, valid_counter, rec);
+            break;
         default: SVR_FWD(256, 3); break;
     }
 #undef SVR_FWD
