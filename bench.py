@@ -350,8 +350,44 @@ def run_ours(args, cfg, rank, world, local_rank):
             e[2].record(stream)
             ev.append(e)
         if dist is not None:
-            reduce_active_grads(grid, dev)  # K7 mask union + K8 NCCL all-reduce
+            reducer["fn"]()  # K7 mask union + K8p peer-memory all-reduce (or K8 pack + NCCL)
         grid.grad_zero_active()
+
+    # N > 1: the gradient reduction runs either as the fused peer-memory kernel over CUDA IPC
+    # mappings (K8p, distributed.PeerGradReducer) or as pack + NCCL all-reduce + unpack; both
+    # are timed over a few steps before the measurement and the faster one is used
+    reducer = {"fn": None, "used": None, "calib_ms": {}}
+    if dist is not None:
+        from paper_2305_13220_b200.distributed import PeerGradReducer
+
+        variants = {"nccl": lambda: reduce_active_grads(grid, dev)}
+        if args.reduce in ("auto", "peer"):
+            try:
+                peer = PeerGradReducer(grid, dev)
+                variants["peer"] = peer.reduce
+            except Exception as e:  # pragma: no cover - no IPC / P2P on this system
+                log(f"[rank {rank}] peer reduction unavailable: {e}")
+        if args.reduce == "nccl":
+            variants.pop("peer", None)
+        for name, fn in variants.items():
+            reducer["fn"] = fn
+            for _ in range(2):
+                step(False)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            for _ in range(3):
+                step(False)
+            c1.record(stream)
+            torch.cuda.synchronize(dev)
+            tt = torch.tensor([c0.elapsed_time(c1) / 3], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            reducer["calib_ms"][name] = float(tt.item())
+        best = min(reducer["calib_ms"], key=reducer["calib_ms"].get)
+        if args.reduce == "peer" and "peer" in variants:
+            best = "peer"
+        reducer["fn"], reducer["used"] = variants[best], best
 
     # ours per step: k_ray_keys_dir, k_march, k_ray_keys, k_forward, k_backward,
     # k_active_count/scan/write, k_grad_zero_active (+ k_active_* / pack / unpack for N > 1);
@@ -409,7 +445,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         grid.render_forward(o_h, d_h, step_len, S, beta, out=outs_h)
         grid.render_backward(dC_h, dD_h, dN_h)
         if dist is not None:
-            reduce_active_grads(grid, dev)
+            reducer["fn"]()
         grid.grad_zero_active()
 
     # host_async: pinned host arrays move on the library's copy streams through double-buffered
@@ -465,6 +501,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "valid_samples_per_gpu": valid_per_step, "max_samples": S,
                    "step_m": step_len, "beta_m": beta, "lookup": "dense" if info.lookup_mode == 2 else "hash",
                    "parallelism": f"rays sharded over {world} GPU(s), grid replicated",
+                   "grad_reduction": ({"used": reducer["used"], "calibration_ms_per_step": reducer["calib_ms"]}
+                                      if world > 1 else None),
                    "l2": f"no flush: inputs exceed L2 (payload+grad planes "
                          f"{info.block_count * 512 * 32 / 1e9:.1f} GB vs 126 MB L2)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -724,6 +762,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 side measurements")
+    ap.add_argument("--reduce", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N > 1 gradient reduction: fused peer-memory kernel, NCCL, or the faster of both")
     ap.add_argument("--rays-per-pose", type=int, default=CFG3["rays_per_pose"])
     ap.add_argument("--act-frames", type=int, default=CFG3["act_frames"])
     args = ap.parse_args()

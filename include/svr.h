@@ -206,6 +206,24 @@ int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* 
  * handle (allocated on first use). */
 int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
 
+/* ---- multi-GPU gradient reduction over peer memory ----
+ * The NCCL path (svr_active_blocks -> svr_grad_pack -> all-reduce -> svr_grad_unpack) has a
+ * fused alternative that reads and writes the ranks' gradient planes directly over NVLink:
+ * every rank exports its plane (svr_grad_ipc_handle), opens the others' (svr_ipc_open, a
+ * CUDA IPC mapping), and after a cross-rank barrier each rank reduces its 1/world slice of
+ * the common ascending active-row list, summing in rank order and storing the sum into every
+ * plane (svr_grad_peer_allreduce); a second barrier completes the step.  peer_planes[q] is
+ * rank q's plane in this process (NULL at q == rank = own); world <= 8.  Handles stay valid
+ * while the grid does not grow (re-export after allocating blocks). */
+#define SVR_IPC_HANDLE_BYTES 64
+int svr_grad_ipc_handle(svr_grid* g, void* handle_out, uint64_t* plane_bytes);
+/* The gradient plane itself (float4 [capacity][512], device memory of the handle's GPU). */
+int svr_grad_plane(svr_grid* g, void** ptr_out, uint64_t* plane_bytes);
+int svr_ipc_open(const void* handle, int32_t device, void** ptr_out);
+int svr_ipc_close(void* ptr);
+int svr_grad_peer_allreduce(svr_grid* g, void* const* peer_planes, uint32_t world, uint32_t rank,
+                            const uint32_t* rows, uint64_t n_rows);
+
 /* ---- fusion + de-noising (SPEC.md:207-233 module "fusion", PAPER Eq. 9-11, sec. 3.4.3) ----
  * The reference declares the state (VoxelBlock::sum_*, grid.hpp:59-68) but ships no code;
  * the contract is the SPEC's:

@@ -143,6 +143,11 @@ _PROTOS = {
                              POINTER(FuseReport)]),
     "svr_fuse_finalize": (_I, [c_void_p]),
     "svr_denoise": (_I, [c_void_p, c_double, c_int32]),
+    "svr_grad_ipc_handle": (_I, [c_void_p, P, POINTER(c_uint64)]),
+    "svr_grad_plane": (_I, [c_void_p, POINTER(c_void_p), POINTER(c_uint64)]),
+    "svr_ipc_open": (_I, [P, c_int32, POINTER(c_void_p)]),
+    "svr_ipc_close": (_I, [c_void_p]),
+    "svr_grad_peer_allreduce": (_I, [c_void_p, P, c_uint32, c_uint32, P, c_uint64]),
     "svr_render_losses": (_I, [c_void_p, c_uint64, P, P, P, P, P, P, P, P, P, c_uint32, c_double, c_double,
                                P, P, P, POINTER(LossStats)]),
     "svr_sample_frame_rays": (_I, [c_void_p, P, c_uint32, P, P, P, c_uint32, c_uint32, c_uint64, P, P, P, P, P, P,

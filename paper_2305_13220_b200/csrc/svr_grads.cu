@@ -98,6 +98,28 @@ __global__ void k_bdist_pass(const uint32_t* __restrict__ occ, const uint8_t* __
     out[i] = static_cast<uint8_t>(best);
 }
 
+// K8p: active-block gradient all-reduce directly over the ranks' gradient planes (peer memory:
+// NVLink P2P through CUDA IPC mappings).  Rank r owns the slice [r n / W, (r + 1) n / W) of
+// the ascending active list; for each of its rows every thread sums one float4 over the W
+// planes in rank order (bitwise identical on every rank) and stores the sum into all W
+// planes -- reduce-scatter and all-gather in one pass, no pack / unpack buffers.
+constexpr int kMaxPeers = 8;
+struct PeerPlanes {
+    float4* p[kMaxPeers];
+};
+__global__ void __launch_bounds__(512) k_peer_allreduce(PeerPlanes pl, uint32_t world, const uint32_t* __restrict__ rows,
+                                                        uint64_t first, uint64_t count) {
+    for (uint64_t j = blockIdx.x; j < count; j += gridDim.x) {
+        const size_t v = static_cast<size_t>(rows[first + j]) * kVox + threadIdx.x;
+        float4 acc = pl.p[0][v];
+        for (uint32_t q = 1; q < world; ++q) {
+            const float4 x = pl.p[q][v];
+            acc.x += x.x, acc.y += x.y, acc.z += x.z, acc.w += x.w;
+        }
+        for (uint32_t q = 0; q < world; ++q) pl.p[q][v] = acc;
+    }
+}
+
 // Per-block table of the 8 blocks a trilinear cell can touch: entry k = lookup of
 // coord + (k & 1, (k >> 1) & 1, k >> 2) (k = 0 is the block itself), with the all-valid bit.
 __global__ void k_nbr_build(GridView g, const int4* __restrict__ coords, uint32_t n, uint32_t* nbr) {
@@ -258,6 +280,18 @@ void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, tmp, out, dim[0], dim[1], dim[2], 1);
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, out, tmp, dim[0], dim[1], dim[2], 2);
     cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToDevice, s);
+}
+
+void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank, const uint32_t* rows,
+                           uint64_t n_rows, cudaStream_t s) {
+    if (!n_rows || !world) return;
+    PeerPlanes pl{};
+    for (uint32_t q = 0; q < world; ++q) pl.p[q] = planes[q];
+    const uint64_t first = n_rows * rank / world, last = n_rows * (rank + 1) / world;
+    if (last <= first) return;
+    const uint64_t count = last - first;
+    const unsigned grid = static_cast<unsigned>(count < 148u * 8u ? count : 148u * 8u);
+    k_peer_allreduce<<<grid, 512, 0, s>>>(pl, world, rows, first, count);
 }
 
 void launch_nbr_build(const GridView& g, const int32_t* coords4, uint32_t n, uint32_t* nbr,

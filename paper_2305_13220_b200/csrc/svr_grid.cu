@@ -1485,6 +1485,60 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
 }
 
 // ---------------------------------------------------------------------------
+// Peer-memory gradient all-reduce (K8p in svr_grads.cu).
+// ---------------------------------------------------------------------------
+int svr_grad_ipc_handle(svr_grid* g, void* handle_out, uint64_t* plane_bytes) {
+    return guarded([&] {
+        if (!handle_out) throw Fail{SVR_ERR_DATA, "grad_ipc_handle: output required"};
+        DeviceGuard dg(g->device);
+        if (!g->grad) throw Fail{SVR_ERR_DATA, "grad_ipc_handle: the grid has no blocks yet"};
+        cudaIpcMemHandle_t h;
+        SVR_CK(cudaIpcGetMemHandle(&h, g->grad));
+        static_assert(sizeof(h) == SVR_IPC_HANDLE_BYTES, "IPC handle size");
+        std::memcpy(handle_out, &h, sizeof(h));
+        if (plane_bytes) *plane_bytes = g->cap_blocks * kVox * sizeof(float4);
+    });
+}
+
+int svr_grad_plane(svr_grid* g, void** ptr_out, uint64_t* plane_bytes) {
+    return guarded([&] {
+        if (ptr_out) *ptr_out = g->grad;
+        if (plane_bytes) *plane_bytes = g->cap_blocks * kVox * sizeof(float4);
+    });
+}
+
+int svr_ipc_open(const void* handle, int32_t device, void** ptr_out) {
+    return guarded([&] {
+        DeviceGuard dg(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        SVR_CK(cudaIpcOpenMemHandle(ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int svr_ipc_close(void* ptr) {
+    return guarded([&] { SVR_CK(cudaIpcCloseMemHandle(ptr)); });
+}
+
+int svr_grad_peer_allreduce(svr_grid* g, void* const* peer_planes, uint32_t world, uint32_t rank,
+                            const uint32_t* rows, uint64_t n_rows) {
+    return guarded([&] {
+        if (world < 1 || world > 8 || rank >= world) throw Fail{SVR_ERR_CONFIG, "peer_allreduce: 1 <= world <= 8"};
+        DeviceGuard dg(g->device);
+        float4* planes[8];
+        for (uint32_t q = 0; q < world; ++q) {
+            planes[q] = static_cast<float4*>(peer_planes ? peer_planes[q] : nullptr);
+            if (q == rank && !planes[q]) planes[q] = g->grad;
+            if (!planes[q]) throw Fail{SVR_ERR_DATA, "peer_allreduce: missing peer plane"};
+        }
+        Stage st(g->stream);
+        const uint32_t* r = st.in(rows, n_rows);
+        svr_internal::launch_peer_allreduce(planes, world, rank, r, n_rows, g->stream);
+        st.finish();
+    });
+}
+
+// ---------------------------------------------------------------------------
 // Refinement losses, K15 in svr_losses.cu.
 // ---------------------------------------------------------------------------
 int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* depth, const float* normal,

@@ -83,6 +83,73 @@ class _GridStore:
         self.grid.grad_unpack(blocks, packed)
 
 
+class PeerGradReducer:
+    """The fused alternative to steps 2-4 (K8p): every rank maps the other ranks' gradient
+    planes (CUDA IPC over NVLink), and after a barrier each rank reduces its 1/world slice of
+    the common active list straight in peer memory -- sum in rank order, store to every
+    plane -- so there is no pack buffer, no unpack and no NCCL ring for the 2.4 GB payload.
+    Only the u8 mask union still goes through the process group.  Construct after the grid
+    has all its blocks (the planes must not be reallocated while mapped)."""
+
+    def __init__(self, grid, device, group=None):
+        import ctypes
+
+        from ._lib import check
+
+        self.grid, self.device, self.group = grid, torch.device(device), group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 8:
+            raise ValueError("PeerGradReducer: at most 8 ranks")
+        lib = grid._lib
+        h = (ctypes.c_uint8 * 64)()
+        nbytes = ctypes.c_uint64()
+        check(lib.svr_grad_ipc_handle(grid._h, ctypes.addressof(h), ctypes.byref(nbytes)))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, (bytes(h), nbytes.value), group=group)
+        self.ptrs = (ctypes.c_void_p * self.world)()
+        self.opened = []
+        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        for q, (hb, _) in enumerate(allh):
+            if q == self.rank:
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+            check(lib.svr_ipc_open(ctypes.addressof(buf), dev, ctypes.byref(p)))
+            self.ptrs[q] = p.value
+            self.opened.append(p)
+        self._gloo = dist.get_backend(group) == "gloo"
+
+    def reduce(self) -> torch.Tensor:
+        import ctypes
+
+        from ._lib import check
+
+        store = _GridStore(self.grid, self.device)
+        mask = store.mask_tensor()
+        if self._gloo:
+            m = mask.cpu()
+            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
+            mask = m.to(self.device)
+        else:
+            dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=self.group)
+        store.set_mask(mask)
+        blocks = store.active_list()
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)  # every rank's backward is in its plane
+        if blocks.numel():
+            check(self.grid._lib.svr_grad_peer_allreduce(self.grid._h, ctypes.addressof(self.ptrs), self.world, self.rank,
+                                                         blocks.data_ptr(), blocks.numel()))
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)  # every slice is summed into every plane
+        return blocks
+
+    def close(self):
+        for p in self.opened:
+            self.grid._lib.svr_ipc_close(p)
+        self.opened = []
+
+
 def reduce_active_grads(grid, device, group=None) -> torch.Tensor:
     """Sum the active-block gradients of `grid` across the process group."""
     return allreduce_active(_GridStore(grid, device), group)

@@ -1,0 +1,114 @@
+"""GPU: the peer-memory active-block all-reduce (K8p).  (1) Emulated ranks: W gradient
+planes on one GPU, one kernel launch per rank slice -- every plane ends with the rank-order
+sum.  (2) Real CUDA IPC plumbing: 2 processes on the one GPU (gloo for the host barriers),
+each mapping the other's plane; the kernels never wait on each other (host barriers between
+launches), so this is safe on a single device."""
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+COORDS = np.array([[x, y, z] for z in range(3) for y in range(3) for x in range(4)], np.int32)
+
+
+def _rank_grads(rank, A):
+    rng = np.random.default_rng(100 + rank)
+    rows = np.sort(rng.choice(A, size=A // 2, replace=False)).astype(np.uint32)
+    vals = rng.normal(size=(len(rows), 512, 4)).astype(np.float32)
+    return rows, vals
+
+
+def _load(g, rows, vals):
+    import torch
+
+    g.grad_zero()
+    A = g.block_count()
+    g.grad_unpack(torch.from_numpy(rows.astype(np.int32)).cuda(), torch.from_numpy(vals).cuda())
+    m = np.zeros(A, np.uint8)
+    m[rows] = 1
+    g.active_set_mask(torch.from_numpy(m).cuda())
+
+
+def _expected(world, A):
+    tot = np.zeros((A, 512, 4), np.float32)
+    union = np.zeros(A, bool)
+    for r in range(world):
+        rows, vals = _rank_grads(r, A)
+        tot[rows] += vals  # rank order, float32: the kernel's summation order
+        union[rows] = True
+    return tot, union
+
+
+def _plane(g):
+    gs, gr = g.grads()
+    return np.concatenate([gs[..., None], gr], axis=-1)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_peer_allreduce_emulated_ranks(world):
+    from paper_2305_13220_b200 import SparseDenseGrid
+    from paper_2305_13220_b200._lib import check
+
+    grids = []
+    for r in range(world):
+        g = SparseDenseGrid(0.02, 8, 1)
+        g.allocate_blocks(COORDS)
+        _load(g, *_rank_grads(r, len(COORDS)))
+        grids.append(g)
+    planes = (ctypes.c_void_p * world)()
+    for r, g in enumerate(grids):
+        p = ctypes.c_void_p()
+        check(g._lib.svr_grad_plane(g._h, ctypes.byref(p), None))
+        planes[r] = p.value
+    tot, union = _expected(world, len(COORDS))
+    rows = np.flatnonzero(union).astype(np.uint32)
+    for r, g in enumerate(grids):  # one launch per rank slice, in sequence
+        check(g._lib.svr_grad_peer_allreduce(g._h, ctypes.addressof(planes), world, r, rows.ctypes.data, len(rows)))
+        g.synchronize()
+    for g in grids:
+        got = _plane(g)
+        assert np.array_equal(got[union], tot[union])
+        assert not got[~union].any()
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+    from paper_2305_13220_b200.distributed import PeerGradReducer
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    g = SparseDenseGrid(0.02, 8, 1)
+    g.allocate_blocks(COORDS)
+    _load(g, *_rank_grads(rank, len(COORDS)))
+    red = PeerGradReducer(g, "cuda:0")
+    blocks = red.reduce()
+    np.save(os.path.join(out_dir, f"r{rank}.npy"), _plane(g))
+    np.save(os.path.join(out_dir, f"b{rank}.npy"), blocks.cpu().numpy())
+    red.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_allreduce_ipc_two_processes_one_gpu(tmp_path):
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world = 2
+    mp.spawn(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    tot, union = _expected(world, len(COORDS))
+    for r in range(world):
+        got = np.load(tmp_path / f"r{r}.npy")
+        assert np.array_equal(got[union], tot[union]), r
+        assert not got[~union].any()
+        assert np.array_equal(np.load(tmp_path / f"b{r}.npy"), np.flatnonzero(union))
