@@ -288,6 +288,17 @@ def traffic_from_profiles():
         return {}
 
 
+def _all_reduce(dist, t, op=None):
+    """all_reduce that also works on a gloo group (CPU round trip)."""
+    op = dist.ReduceOp.SUM if op is None else op
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def run_ours(args, cfg, rank, world, local_rank):
     import torch
 
@@ -360,7 +371,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     if dist is not None:
         from paper_2305_13220_b200.distributed import PeerGradReducer
 
-        variants = {"nccl": lambda: reduce_active_grads(grid, dev)}
+        variants = {}
+        if dist.get_backend() == "nccl":
+            variants["nccl"] = lambda: reduce_active_grads(grid, dev)
         if args.reduce in ("auto", "peer"):
             try:
                 peer = PeerGradReducer(grid, dev)
@@ -382,7 +395,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             c1.record(stream)
             torch.cuda.synchronize(dev)
             tt = torch.tensor([c0.elapsed_time(c1) / 3], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            _all_reduce(dist, tt, dist.ReduceOp.MAX)
             reducer["calib_ms"][name] = float(tt.item())
         best = min(reducer["calib_ms"], key=reducer["calib_ms"].get)
         if args.reduce == "peer" and "peer" in variants:
@@ -424,10 +437,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     bwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
     if dist is not None:
         t = torch.tensor([ms, fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _all_reduce(dist, t, dist.ReduceOp.MAX)
         ms, fwd_ms, bwd_ms = (float(v) for v in t.tolist())
         vt = torch.tensor([valid_per_step, marched_per_step], dtype=torch.float64, device=dev)
-        dist.all_reduce(vt)
+        _all_reduce(dist, vt)
         valid_total, marched_total = (int(v) for v in vt.tolist())
     else:
         valid_total, marched_total = valid_per_step, marched_per_step
@@ -468,7 +481,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     grid.set_tuning("host_async", 0)
     if dist is not None:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _all_reduce(dist, t, dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = n_rays * (48 + 28)
     d2h = n_rays * 32
@@ -774,12 +787,21 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
+    # test hook (CI on a 1-GPU box): SVR_BENCH_PG=gloo + SVR_BENCH_SAME_GPU=1 run every rank
+    # on cuda:0 with host-side collectives, which is safe on one device only because no kernel
+    # then waits for another rank's kernel (NCCL kernels would)
+    if os.environ.get("SVR_BENCH_SAME_GPU") == "1":
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("SVR_BENCH_PG", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:
