@@ -143,6 +143,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "fwd_split") {
+            g->fwd_split = value != 0;
         } else if (k == "march_jump") {
             g->use_jump = value != 0;
         } else if (k == "warp_agg") {

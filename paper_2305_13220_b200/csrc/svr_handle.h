@@ -201,6 +201,7 @@ struct svr_grid {
     int ray_sort = 3;
     int sort_impl = 1;  // 1: CUB radix sort (default, best order), 0: in-house bucketed counting sort
     int fwd_min_blocks = 3;
+    bool fwd_split = true;  // forward lane layout: samples l and 32 + l (false: 2l and 2l + 1)
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
     bool fwd_pipe = false;    // persistent forward streaming t rows (measured slower: off)

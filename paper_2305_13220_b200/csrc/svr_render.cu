@@ -644,6 +644,72 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, co
         atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
 }
 
+// K5 with the split lane layout: lane l owns samples base + l and base + 32 + l, so the
+// 32 lanes of one gather instruction walk 32 consecutive samples (neighbouring lanes share
+// cells and cache lines).
+template <int kThreads, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_split(GridView g, const double* __restrict__ O,
+                                                    const double* __restrict__ D, uint64_t n,
+                                                    const uint32_t* __restrict__ order,
+                                                    const uint32_t* __restrict__ counts,
+                                                    const double* __restrict__ T, uint32_t S,
+                                                    double step, float ib, float* rgb, float* depth,
+                                                    float* normal, float* wsum,
+                                                    unsigned long long* valid_counter, float4* rec) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const uint64_t r = order ? order[w] : w;
+    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    const uint32_t cnt = counts[r];
+    const double* tr = T + r * S;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
+    float tau_base = 0.f;
+    uint32_t nvalid = 0;
+    for (uint32_t base = 0; base < cnt; base += 64) {
+        const uint32_t k0 = base + lane, k1 = base + 32 + lane;
+        const bool in0 = k0 < cnt, in1 = k1 < cnt;
+        const double t0 = in0 ? tr[k0] : 0.0, t1 = in1 ? tr[k1] : 0.0;
+        double tn0 = __shfl_down_sync(kFull, t0, 1);
+        const double t1_l0 = __shfl_sync(kFull, t1, 0);
+        double tn1 = __shfl_down_sync(kFull, t1, 1);
+        if (lane == 31) {
+            tn0 = t1_l0;
+            if (k1 + 1 < cnt) tn1 = tr[k1 + 1];
+        }
+        const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
+        const float d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn1, t1)) : static_cast<float>(step);
+        SampleVal v0, v1;
+        const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
+        const bool ok1 = eval_slot(g, o, d, in1, t1, v1);
+        if (rec) {
+            if (in0) store_record(rec + (r * S + k0) * 2, v0);
+            if (in1) store_record(rec + (r * S + k1) * 2, v1);
+        }
+        const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
+        const float tau1 = ok1 ? density(v1.s, ib) * d1 : 0.f;
+        const float inc0 = warp_incl_scan(tau0, lane);
+        const float inc1 = warp_incl_scan(tau1, lane);
+        const float tot0 = __shfl_sync(kFull, inc0, 31);
+        const float w0 = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
+        const float w1 = -expf(-(tau_base + tot0 + inc1 - tau1)) * expm1f(-tau1);
+        acc[0] += w0 * v0.r + w1 * v1.r;
+        acc[1] += w0 * v0.gc + w1 * v1.gc;
+        acc[2] += w0 * v0.b + w1 * v1.b;
+        acc[3] += w0 * static_cast<float>(t0) + w1 * static_cast<float>(t1);
+        acc[4] += w0 * v0.gx + w1 * v1.gx;
+        acc[5] += w0 * v0.gy + w1 * v1.gy;
+        acc[6] += w0 * v0.gz + w1 * v1.gz;
+        acc[7] += w0 + w1;
+        if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
+        tau_base += tot0 + __shfl_sync(kFull, inc1, 31);
+    }
+    write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
+    if (lane == 0 && valid_counter && nvalid)
+        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+}
+
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
 //   g_sdf = w_c dL/ds + dw_c . (w_k dN),  g_rgb = w_c w_k dC.
 struct CornerCoef {
@@ -1226,6 +1292,10 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
         case 11: SVR_FWD(768, 1); break;  // one 24-warp CTA per SM: concurrent warps = adjacent rays
         case 12: SVR_FWD(512, 1); break;
         case 13: SVR_FWD(1024, 1); break;
+        case 104: k_forward_split<256, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
+                                                                                ib, rgb, depth, normal, wsum,
+                                                                                valid_counter, rec);
+            break;
         // diagnostics (wrong results): 101 no payload loads, 102 no block lookup, 103 no records
         case 101: k_forward<256, 3, 1><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
                                                                            rgb, depth, normal, wsum, valid_counter, rec);
