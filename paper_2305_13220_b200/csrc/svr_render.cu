@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(256) k_ray_keys(GridView g, const double* __re
     ids[r] = static_cast<uint32_t>(r);
 }
 
-// Pre-march ordering: 10-bit hash of the origin (1 mm cells) above a 22-bit Morton code of
+// Pre-march ordering: 8-bit hash of the origin (1 mm cells) above a 16-bit Morton code of
 // the octahedral direction, so rays from one camera with nearby pixels march together.
 __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__ O,
                                                       const double* __restrict__ D, uint64_t n,
@@ -571,16 +571,18 @@ __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__
         const double vv = (1.0 - fabs(u)) * (v >= 0.0 ? 1.0 : -1.0);
         u = uu, v = vv;
     }
-    const uint32_t qu = min(2047u, static_cast<uint32_t>((u * 0.5 + 0.5) * 2048.0));
-    const uint32_t qv = min(2047u, static_cast<uint32_t>((v * 0.5 + 0.5) * 2048.0));
+    // 8-bit origin hash above a 16-bit Morton code of the direction (256 x 256 octahedral
+    // bins): 24-bit keys, three radix passes
+    const uint32_t qu = min(255u, static_cast<uint32_t>((u * 0.5 + 0.5) * 256.0));
+    const uint32_t qv = min(255u, static_cast<uint32_t>((v * 0.5 + 0.5) * 256.0));
     uint32_t m = 0;
 #pragma unroll
-    for (int b = 0; b < 11; ++b) m |= (((qu >> b) & 1u) << (2 * b)) | (((qv >> b) & 1u) << (2 * b + 1));
+    for (int b = 0; b < 8; ++b) m |= (((qu >> b) & 1u) << (2 * b)) | (((qv >> b) & 1u) << (2 * b + 1));
     unsigned long long h = 0x9E3779B97F4A7C15ull;
 #pragma unroll
     for (int a = 0; a < 3; ++a)
         h = mix64(h ^ static_cast<unsigned long long>(llrint(O[3 * r + a] * 1000.0)));
-    keys[r] = (static_cast<uint32_t>(h >> 54) << 22) | m;
+    keys[r] = (static_cast<uint32_t>(h >> 56) << 16) | m;
     ids[r] = static_cast<uint32_t>(r);
 }
 
@@ -1352,9 +1354,17 @@ void launch_ray_order(const GridView& g, const double* o, const double* d, uint6
         k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids);
     else         // pre-march: origin + direction
         k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
+    // sort only the key bits in use: 24 for the pre-march key; 3 x (bits per axis of the
+    // block AABB) for the post-march Morton key (empty rays carry all ones and sort last)
+    int end_bit = 24;
+    if (counts) {
+        int bits = 1;
+        while (bits < 10 && ((1 << bits) < g.dim[0] || (1 << bits) < g.dim[1] || (1 << bits) < g.dim[2])) ++bits;
+        end_bit = 3 * bits;
+    }
     cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
     size_t bytes = tmp_bytes;
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, 32, s);
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, end_bit, s);
     *sorted_ids = vb.Current();
 }
 
