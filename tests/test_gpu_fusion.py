@@ -119,3 +119,17 @@ def test_denoise_matches_oracle_bit_exact(radius, sigma):
     OracleGrid.set_threads(1)
     g.denoise(sigma, radius)
     _same(g.get_payload(), og.get_payload())
+
+
+def test_fuse_denoise_hash_lookup_mode():
+    """the same fusion + denoise through the hash lookup (no dense AABB index)."""
+    sc, cams, depth, rgb, sem, og = _case(C=4, n_frames=6)
+    g = _gpu_grid(og, 0.05, 4)
+    g.set_lookup(1)
+    og.fuse_begin(True, True)
+    og.fuse_frames(depth, cams, 0.4, rgb=rgb, sem=sem)
+    og.fuse_finalize()
+    og.denoise(1.0, 2)
+    g.fuse_all(depth, cams, 0.4, rgb=rgb, semantic=sem)
+    g.denoise(1.0, 2)
+    _same(g.get_payload(), og.get_payload())
