@@ -25,6 +25,7 @@ def _rank_grads(rank, A):
 def _load(g, rows, vals):
     import torch
 
+    g.set_stream(torch.cuda.current_stream())  # the torch-made device inputs are ordered on it
     g.grad_zero()
     A = g.block_count()
     g.grad_unpack(torch.from_numpy(rows.astype(np.int32)).cuda(), torch.from_numpy(vals).cuda())
