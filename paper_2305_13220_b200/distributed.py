@@ -127,6 +127,7 @@ class PeerGradReducer:
 
         store = _GridStore(self.grid, self.device)
         mask = store.mask_tensor()
+        self.grid.synchronize()  # the mask (and the backward) are complete whatever stream reads them
         if self._gloo:
             m = mask.cpu()
             dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)

@@ -82,6 +82,8 @@ class Refiner:
         self.pts = torch.empty((self.cfg.band_cap + self.cfg.uniform_points, 3), dtype=torch.float64, device=dev)
         self._camarr = (Camera * len(self.cams))(*self.cams)
         self.cams_dev = torch.frombuffer(bytearray(bytes(self._camarr)), dtype=torch.uint8).to(dev)
+        # the frames / cameras were uploaded on torch's stream; the grid may run on its own
+        torch.cuda.synchronize(dev)
 
     def lr_at(self, i: int, steps: int) -> float:
         """exponential decay to lr * gamma at the final step."""

@@ -51,6 +51,7 @@ def test_losses_device_resident_no_sync():
 
     case, cams, cam_idx, _, tgt, pd, pn = _toy(7)
     g = gpu_grid_from(case)
+    g.set_stream(torch.cuda.current_stream())  # inputs below are made on torch's stream
     dev = torch.device("cuda:0")
     o, d = (torch.from_numpy(case[k]).to(dev) for k in ("o", "d"))
     out = g.render_forward(o, d, case["step"], 64, case["beta"])
