@@ -64,7 +64,10 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
         svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
                                             g->tbuf.as<double>(), max_samples, step, beta, a, b, c, e, nullptr,
                                             recp, g->stream,
-                                            (g->fwd_split && g->fwd_min_blocks == 3) ? 104 : g->fwd_min_blocks);
+                                            g->fwd_min_blocks != 3 ? g->fwd_min_blocks
+                                            : g->fwd_split == 2  ? 109
+                                            : g->fwd_split == 1  ? 104
+                                                                 : 3);
 }
 
 void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {

@@ -144,7 +144,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
         } else if (k == "fwd_split") {
-            g->fwd_split = value != 0;
+            if (value < 0 || value > 2) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..2"};
+            g->fwd_split = static_cast<int>(value);
         } else if (k == "march_jump") {
             g->use_jump = value != 0;
         } else if (k == "warp_agg") {

@@ -712,6 +712,71 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_split(GridView
         atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
 }
 
+// K5, sequential halves: one sample per lane per pass (samples base + 32 h + l), so only
+// one sample's state is live -- fewer registers, more resident warps.
+template <int kThreads, int kMinBlocks, bool kOdSmem = false>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_seq(GridView g, const double* __restrict__ O,
+                                                    const double* __restrict__ D, uint64_t n,
+                                                    const uint32_t* __restrict__ order,
+                                                    const uint32_t* __restrict__ counts,
+                                                    const double* __restrict__ T, uint32_t S,
+                                                    double step, float ib, float* rgb, float* depth,
+                                                    float* normal, float* wsum,
+                                                    unsigned long long* valid_counter, float4* rec) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (w >= n) return;
+    const uint64_t r = order ? order[w] : w;
+    // the ray's origin / direction: registers, or (kOdSmem) a per-warp shared slot read at
+    // each use, which frees 12 registers
+    __shared__ double s_od[kThreads / 32][6];
+    double o_r[3], d_r[3];
+    const double* o = o_r;
+    const double* d = d_r;
+    if (kOdSmem) {
+        const int wib = threadIdx.x >> 5;
+        if (lane < 6) s_od[wib][lane] = lane < 3 ? O[3 * r + lane] : D[3 * r + lane - 3];
+        __syncwarp();
+        o = s_od[wib];
+        d = s_od[wib] + 3;
+    } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) o_r[a] = O[3 * r + a], d_r[a] = D[3 * r + a];
+    }
+    const uint32_t cnt = counts[r];
+    const double* tr = T + r * S;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
+    float tau_base = 0.f;
+    uint32_t nvalid = 0;
+    for (uint32_t base = 0; base < cnt; base += 32) {
+        const uint32_t k0 = base + lane;
+        const bool in0 = k0 < cnt;
+        const double t0 = in0 ? tr[k0] : 0.0;
+        double tn0 = __shfl_down_sync(kFull, t0, 1);
+        if (lane == 31 && k0 + 1 < cnt) tn0 = tr[k0 + 1];
+        const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
+        SampleVal v0;
+        const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
+        if (rec && in0) store_record(rec + (r * S + k0) * 2, v0);
+        const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
+        const float inc0 = warp_incl_scan(tau0, lane);
+        const float w0 = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
+        acc[0] += w0 * v0.r;
+        acc[1] += w0 * v0.gc;
+        acc[2] += w0 * v0.b;
+        acc[3] += w0 * static_cast<float>(t0);
+        acc[4] += w0 * v0.gx;
+        acc[5] += w0 * v0.gy;
+        acc[6] += w0 * v0.gz;
+        acc[7] += w0;
+        if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0));
+        tau_base += __shfl_sync(kFull, inc0, 31);
+    }
+    write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
+    if (lane == 0 && valid_counter && nvalid)
+        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+}
+
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
 //   g_sdf = w_c dL/ds + dw_c . (w_k dN),  g_rgb = w_c w_k dC.
 struct CornerCoef {
@@ -1294,6 +1359,30 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
         case 11: SVR_FWD(768, 1); break;  // one 24-warp CTA per SM: concurrent warps = adjacent rays
         case 12: SVR_FWD(512, 1); break;
         case 13: SVR_FWD(1024, 1); break;
+        case 105: k_forward_seq<256, 4><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
+                                                                              ib, rgb, depth, normal, wsum,
+                                                                              valid_counter, rec);
+            break;
+        case 109: k_forward_seq<256, 4, true><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S,
+                                                                                    step, ib, rgb, depth, normal,
+                                                                                    wsum, valid_counter, rec);
+            break;
+        case 110: k_forward_seq<256, 5, true><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S,
+                                                                                    step, ib, rgb, depth, normal,
+                                                                                    wsum, valid_counter, rec);
+            break;
+        case 107: k_forward_seq<256, 5><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
+                                                                              ib, rgb, depth, normal, wsum,
+                                                                              valid_counter, rec);
+            break;
+        case 108: k_forward_seq<256, 6><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
+                                                                              ib, rgb, depth, normal, wsum,
+                                                                              valid_counter, rec);
+            break;
+        case 106: k_forward_seq<256, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
+                                                                              ib, rgb, depth, normal, wsum,
+                                                                              valid_counter, rec);
+            break;
         case 104: k_forward_split<256, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
                                                                                 ib, rgb, depth, normal, wsum,
                                                                                 valid_counter, rec);

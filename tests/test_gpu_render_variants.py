@@ -137,9 +137,10 @@ def test_host_async_pipeline_matches_synchronous():
     assert_close(gr, ref_gr, what="grad_rgb")
 
 
-@pytest.mark.parametrize("split", [0, 1])
+@pytest.mark.parametrize("split", [0, 1, 2])
 def test_forward_lane_layouts_match_oracle(split):
-    """fwd_split: lane l owns samples (l, 32 + l) [default] or (2l, 2l + 1)."""
+    """fwd_split: one sample per lane per pass [default], lane l owns samples (l, 32 + l), or
+    (2l, 2l + 1)."""
     for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
         g = gpu_grid_from(c)
         g.set_tuning("fwd_split", split)
