@@ -1034,7 +1034,7 @@ struct PipeSlot {
     float4 rec[128];
 };
 
-template <int kMinBlocks, int kMode = 0>
+template <int kMinBlocks, int kMode = 0, int kStages = kPipeStages>
 __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
@@ -1044,13 +1044,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
                     uint64_t warps_total) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    PipeSlot* slots = reinterpret_cast<PipeSlot*>(smem_raw) + wib * kPipeStages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(PipeSlot) * kPipeStages * kPipeWarps) +
-                     wib * kPipeStages;
+    PipeSlot* slots = reinterpret_cast<PipeSlot*>(smem_raw) + wib * kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(PipeSlot) * kStages * kPipeWarps) +
+                     wib * kStages;
     const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
     const uint32_t tbytes = S * 8, rbytes = S * 32;
     if (lane == 0) {
-        for (int st = 0; st < kPipeStages; ++st) mbar_init(bars + st, 1);
+        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     };
     // prologue
     if (lane == 0)
-        for (int st = 0; st < kPipeStages - 1; ++st) {
+        for (int st = 0; st < kStages - 1; ++st) {
             const uint64_t i = w0 + st * warps_total;
             if (i < n) issue(i, st);
         }
@@ -1073,8 +1073,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     int st = 0;
     for (uint64_t i = w0; i < n; i += warps_total) {
         {  // keep kStages-1 rays in flight: refill the stage released last iteration
-            const uint64_t nxt = i + (kPipeStages - 1) * warps_total;
-            const int nst = (st + kPipeStages - 1) % kPipeStages;
+            const uint64_t nxt = i + (kStages - 1) * warps_total;
+            const int nst = (st + kStages - 1) % kStages;
             if (lane == 0 && nxt < n) issue(nxt, nst);
         }
         const uint64_t r = ray_of(i);
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
             }
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
-        st = (st + 1) % kPipeStages;
+        st = (st + 1) % kStages;
     }
 }
 
@@ -1464,13 +1464,15 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
                                  cudaStream_t s, int min_blocks, int num_sms, bool agg) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
-    const size_t smem = sizeof(PipeSlot) * kPipeStages * kPipeWarps + 8 * kPipeStages * kPipeWarps;
+    const int stages = (min_blocks == 4 || min_blocks == 5) ? 2 : kPipeStages;
+    const size_t smem = sizeof(PipeSlot) * stages * kPipeWarps + 8 * stages * kPipeWarps;
     const float ib = static_cast<float>(1.0 / beta);
     uint64_t ctas = static_cast<uint64_t>(num_sms) * (min_blocks % 100);
     const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
     if (ctas > need) ctas = need;
     const uint64_t warps_total = ctas * kPipeWarps;
 #define SVR_COMMA2(a, b) a, b
+#define SVR_COMMA3(a, b, c) a, b, c
 #define SVR_PIPE(...)                                                                             \
     do {                                                                                          \
         cudaFuncSetAttribute(k_backward_pipe<__VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1487,6 +1489,8 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
             if (agg) SVR_PIPE(SVR_COMMA2(2, 3));
             else SVR_PIPE(2);
             break;
+        case 4: SVR_PIPE(SVR_COMMA3(4, 3, 2)); break;  // 2-stage ring, 64 registers
+        case 5: SVR_PIPE(SVR_COMMA3(5, 3, 2)); break;
         case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
         default:
             if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
@@ -1495,6 +1499,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     }
 #undef SVR_PIPE
 #undef SVR_COMMA2
+#undef SVR_COMMA3
     return true;
 }
 
