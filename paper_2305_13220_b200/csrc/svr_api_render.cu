@@ -50,7 +50,7 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
     };
     if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
     svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples, g->counts.as<uint32_t>(),
-                               g->tbuf.as<double>(), nullptr, g->stream);
+                               g->tbuf.as<double>(), nullptr, g->stream, g->march_variant);
     if (sort && (g->ray_sort & 1)) order_rays(true);   // post-march: first-sample block
     g->ctx_rec = g->use_records;
     if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);

@@ -146,6 +146,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
         } else if (k == "fwd_split") {
             if (value < 0 || value > 2) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..2"};
             g->fwd_split = static_cast<int>(value);
+        } else if (k == "march_variant") {
+            g->march_variant = static_cast<int>(value);
         } else if (k == "march_jump") {
             g->use_jump = value != 0;
         } else if (k == "warp_agg") {

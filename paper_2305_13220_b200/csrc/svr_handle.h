@@ -187,7 +187,8 @@ struct svr_grid {
     int use_dense = 0;
     int32_t dim[3] = {0, 0, 0};
     DevBuf dense, occ, nbr, bdist, bdist_tmp;
-    bool use_jump = true;  // march: exact empty-space jumps over the block-distance field
+    bool use_jump = true;   // march: exact empty-space jumps over the block-distance field
+    int march_variant = 2;  // k_march build: 0 o / d in registers; 1/2/3 in shared memory, 8/6/7 CTAs
 
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;

@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(256) k_query(GridView g, const double* __restr
 // Crossing times are recomputed from plane equations exactly as the reference does;
 // only the stepped axis' crossing changes per step, so the other two are cached.
 // ---------------------------------------------------------------------------
-template <typename Emit>
-__device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[3],
-                                              const double d[3], double step, uint32_t S,
+// o / d: anything indexable as o[a] (registers, or a strided shared-memory view)
+template <typename V, typename Emit>
+__device__ __forceinline__ uint32_t march_dev(const GridView& g, const V& o, const V& d, double step, uint32_t S,
                                               Emit&& emit) {
     if (g.n_blocks == 0 || S == 0) return 0;
     const double L = g.L;
@@ -255,17 +255,37 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const double o[
     return cnt;
 }
 
-__global__ void __launch_bounds__(128) k_march(GridView g, const double* __restrict__ O,
+// per-thread o / d kept in shared memory (SoA, stride = CTA size) instead of 12 registers
+struct StridedVec {
+    const double* base;
+    int stride;
+    __device__ __forceinline__ double operator[](int a) const { return base[a * stride]; }
+};
+
+template <int kMinBlocks, bool kSmem>
+__global__ void __launch_bounds__(128, kMinBlocks) k_march(GridView g, const double* __restrict__ O,
                                                const double* __restrict__ D, uint64_t n,
                                                const uint32_t* __restrict__ order, double step,
                                                uint32_t S, uint32_t* counts, double* T, double* delta) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t r = order ? order[i] : i;
-    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
     double* tr = T + r * S;
-    const uint32_t cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+    uint32_t cnt;
+    if (kSmem) {
+        __shared__ double s_od[6][128];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            s_od[a][threadIdx.x] = O[3 * r + a];
+            s_od[3 + a][threadIdx.x] = D[3 * r + a];
+        }
+        const StridedVec o{&s_od[0][threadIdx.x], 128}, d{&s_od[3][threadIdx.x], 128};
+        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+    } else {
+        const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+        const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+    }
     counts[r] = cnt;
     if (delta) {
         double* dr = delta + r * S;
@@ -1337,9 +1357,15 @@ void launch_query(const GridView& g, const double* x, uint64_t n, double* sdf, d
 
 void launch_march(const GridView& g, const double* o, const double* d, uint64_t n,
                   const uint32_t* order, double step, uint32_t S, uint32_t* counts, double* t,
-                  double* delta, cudaStream_t s) {
+                  double* delta, cudaStream_t s, int variant) {
     if (!n) return;
-    k_march<<<grid_for(n, 128), 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta);
+    const unsigned grid = grid_for(n, 128);
+    switch (variant) {
+        case 1: k_march<8, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+        case 2: k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+        case 3: k_march<7, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+        default: k_march<1, false><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+    }
 }
 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
