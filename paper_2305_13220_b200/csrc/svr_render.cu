@@ -1165,6 +1165,131 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
 }
 
 // ---------------------------------------------------------------------------
+// K6s: the pipelined backward with one sample per lane per 32-sample pass (samples 32 h + l),
+// like k_forward_seq: pass A turns the staged records into tau and the exclusive prefix of
+// both halves; pass B walks the halves back to front (suffix S_k carried across), evaluates
+// one sample per lane and scatters with the one-step warp hand-off (lane l's cell run joins
+// lane l-1's when it is the same cell).  Fewer live registers per lane than K6p.
+// ---------------------------------------------------------------------------
+template <int kMinBlocks, int kStages>
+__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
+    k_backward_seq(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
+                   const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
+                   const double* __restrict__ T, uint32_t S, double step, float ib,
+                   const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
+                   const float* __restrict__ d_normal, const float4* __restrict__ rec,
+                   uint64_t warps_total) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    PipeSlot* slots = reinterpret_cast<PipeSlot*>(smem_raw) + wib * kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(PipeSlot) * kStages * kPipeWarps) +
+                     wib * kStages;
+    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
+    const uint32_t tbytes = S * 8, rbytes = S * 32;
+    if (lane == 0) {
+        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
+    auto issue = [&](uint64_t i, int st) {
+        const uint64_t r = ray_of(i);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bars + st, tbytes + rbytes);
+        bulk_g2s(slots[st].t, T + r * S, tbytes, bars + st);
+        bulk_g2s(slots[st].rec, rec + r * S * 2, rbytes, bars + st);
+    };
+    if (lane == 0)
+        for (int st = 0; st < kStages - 1; ++st) {
+            const uint64_t i = w0 + st * warps_total;
+            if (i < n) issue(i, st);
+        }
+    const float ih = static_cast<float>(g.inv_h);
+    uint32_t phase = 0;
+    int st = 0;
+    for (uint64_t i = w0; i < n; i += warps_total) {
+        {
+            const uint64_t nxt = i + (kStages - 1) * warps_total;
+            const int nst = (st + kStages - 1) % kStages;
+            if (lane == 0 && nxt < n) issue(nxt, nst);
+        }
+        const uint64_t r = ray_of(i);
+        const uint32_t cnt = counts[r];
+        mbar_wait(bars + st, (phase >> st) & 1u);
+        phase ^= 1u << st;
+        const PipeSlot& sl = slots[st];
+        if (cnt) {
+            const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
+            const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+            const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
+            const float dD = d_depth[r];
+            const float dN[3] = {d_normal[3 * r], d_normal[3 * r + 1], d_normal[3 * r + 2]};
+            // pass A: tau_k from the records (s, validity) and delta_k from the t row
+            float tau[2], dl[2], P[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = 32 * h + lane;
+                const bool in = k < cnt;
+                dl[h] = (k + 1 < cnt) ? static_cast<float>(__dsub_rn(sl.t[k + 1], sl.t[k])) : static_cast<float>(step);
+                const bool ok = in && __float_as_uint(sl.rec[2 * k + 1].w) != kInvalid;
+                tau[h] = ok ? density(sl.rec[2 * k].x, ib) * dl[h] : 0.f;
+            }
+            const float inc0 = warp_incl_scan(tau[0], lane);
+            const float inc1 = warp_incl_scan(tau[1], lane);
+            P[0] = inc0 - tau[0];
+            P[1] = __shfl_sync(kFull, inc0, 31) + inc1 - tau[1];
+            // pass B: back to front
+            float S_after = 0.f;
+#pragma unroll
+            for (int h = 1; h >= 0; --h) {
+                const uint32_t k = 32 * h + lane;
+                const bool in = k < cnt;
+                const double t = in ? sl.t[k] : 0.0;
+                SampleVal v;
+                const bool ok = eval_from_record(g, o, d, in, t, sl.rec + 2 * k, v);
+                const float sg = ok ? density(v.s, ib) : 0.f;
+                const float w = ok ? -expf(-P[h]) * expm1f(-tau[h]) : 0.f;
+                const float Tn = expf(-(P[h] + tau[h]));
+                const float vv = ok ? dC[0] * v.r + dC[1] * v.gc + dC[2] * v.b + dD * static_cast<float>(t) +
+                                          dN[0] * v.gx + dN[1] * v.gy + dN[2] * v.gz
+                                    : 0.f;
+                const float u = w * vv;
+                const float sinc = warp_incl_suffix(u, lane);
+                float sexc = __shfl_down_sync(kFull, sinc, 1);
+                if (lane == 31) sexc = 0.f;
+                const float Sk = S_after + sexc;
+                const CornerCoef c = make_coef(v, ok ? dl[h] * density_ds(v.s, sg, ib) * (Tn * vv - Sk) : 0.f, w,
+                                               dC, dN, ih);
+                if (ok) mark_blocks(g, v);
+                // one-step hand-off: lane l's run joins lane l-1's when it is the same cell
+                const uint32_t cell = ok ? v.gidx[0] : kInvalid;
+                const uint32_t prev = __shfl_up_sync(kFull, cell, 1);
+                const bool give = lane > 0 && ok && cell == prev;
+                const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
+#define SVR_SEQ_CORNER(cc)                                                                        \
+    {                                                                                             \
+        const float4 a = ok ? corner_grad<cc>(c) : make_float4(0.f, 0.f, 0.f, 0.f);               \
+        const float4 inb = shfl_down4(a);                                                         \
+        if (ok) {                                                                                 \
+            if (give) {                                                                           \
+                if (recv) atomicAdd(g.grad + v.gidx[cc], inb);                                    \
+            } else {                                                                              \
+                atomicAdd(g.grad + v.gidx[cc], recv ? f4add(a, inb) : a);                         \
+            }                                                                                     \
+        }                                                                                         \
+    }
+                SVR_SEQ_CORNER(0) SVR_SEQ_CORNER(1) SVR_SEQ_CORNER(2) SVR_SEQ_CORNER(3)
+                SVR_SEQ_CORNER(4) SVR_SEQ_CORNER(5) SVR_SEQ_CORNER(6) SVR_SEQ_CORNER(7)
+#undef SVR_SEQ_CORNER
+                S_after += __shfl_sync(kFull, sinc, 0);
+            }
+        }
+        __syncwarp();
+        st = (st + 1) % kStages;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K5p: pipelined forward (max_samples <= 64, even).  Persistent warps, 3-stage ring of
 // t rows streamed with cp.async.bulk; while ray i is gathered and composited, ray i+1's
 // t row is already resident and its base-voxel block lookups are in flight, and ray i+2's
@@ -1493,12 +1618,21 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     const int stages = (min_blocks == 4 || min_blocks == 5) ? 2 : kPipeStages;
     const size_t smem = sizeof(PipeSlot) * stages * kPipeWarps + 8 * stages * kPipeWarps;
     const float ib = static_cast<float>(1.0 / beta);
-    uint64_t ctas = static_cast<uint64_t>(num_sms) * (min_blocks % 100);
+    const int mb_eff = min_blocks >= 600 ? (min_blocks == 601 ? 3 : (min_blocks == 602 ? 4 : 5)) : min_blocks % 100;
+    uint64_t ctas = static_cast<uint64_t>(num_sms) * mb_eff;
     const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
     if (ctas > need) ctas = need;
     const uint64_t warps_total = ctas * kPipeWarps;
 #define SVR_COMMA2(a, b) a, b
 #define SVR_COMMA3(a, b, c) a, b, c
+#define SVR_SEQ(MB, ST)                                                                           \
+    do {                                                                                          \
+        const size_t sm = sizeof(PipeSlot) * (ST) * kPipeWarps + 8 * (ST) * kPipeWarps;           \
+        cudaFuncSetAttribute(k_backward_seq<MB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             static_cast<int>(sm));                                               \
+        k_backward_seq<MB, ST><<<static_cast<unsigned>(ctas), kPipeWarps * 32, sm, s>>>(          \
+            g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
+    } while (0)
 #define SVR_PIPE(...)                                                                             \
     do {                                                                                          \
         cudaFuncSetAttribute(k_backward_pipe<__VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -1518,12 +1652,16 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
         case 4: SVR_PIPE(SVR_COMMA3(4, 3, 2)); break;  // 2-stage ring, 64 registers
         case 5: SVR_PIPE(SVR_COMMA3(5, 3, 2)); break;
         case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
+        case 601: SVR_SEQ(3, 3); break;  // one sample per lane per pass
+        case 602: SVR_SEQ(4, 2); break;
+        case 603: SVR_SEQ(5, 2); break;
         default:
             if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
             else SVR_PIPE(3);
             break;
     }
 #undef SVR_PIPE
+#undef SVR_SEQ
 #undef SVR_COMMA2
 #undef SVR_COMMA3
     return true;

@@ -88,7 +88,8 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
 
 
 @pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe",
-                         [(2, 1, 1), (3, 1, 1), (3, 0, 1), (3, 1, 0), (3, 0, 0)])
+                         [(2, 1, 1), (3, 1, 1), (3, 0, 1), (3, 1, 0), (3, 0, 0), (4, 1, 1),
+                          (601, 1, 1), (602, 1, 1)])
 def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe):
     """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward."""
     for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):  # + invalid samples inside runs
