@@ -325,6 +325,9 @@ int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors,
 /* export_ply (mesh_io.cpp:30-68) of the last mesh: binary little-endian PLY with float
  * xyz + normals, uchar rgb = lround(clamp(c) * 255), int label, uchar-count int triangles. */
 int svr_mesh_save_ply(svr_grid* g, const char* path);
+/* export_obj (mesh_io.cpp:155-164) of the last mesh: "v x y z" (9 significant digits) and
+ * 1-based "f i j k" lines. */
+int svr_mesh_save_obj(svr_grid* g, const char* path);
 
 #ifdef __cplusplus
 }

@@ -404,7 +404,12 @@ class RefGrid(_Base):
         "fuse_frames": (c_int, [c_void_p, P, P, P, P, c_uint32, P, c_int, c_int, c_double]),
         "mesh_export_ply": (c_int, [c_void_p, c_char_p]),
         "mesh_area": (c_double, [c_void_p]),
+        "mesh_export_obj": (c_int, [c_void_p, c_char_p]),
     })
+
+    def export_obj(self, path):
+        """export_obj (mesh_io.cpp:155-164) of the last marching_cubes mesh."""
+        self._check(self.lib().svrr_mesh_export_obj(self._h, str(path).encode()))
 
     def export_ply(self, path):
         """export_ply (mesh_io.cpp:30-68) of the last marching_cubes mesh."""

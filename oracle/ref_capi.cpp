@@ -546,4 +546,8 @@ int svrr_mesh_export_ply(const svrr_grid* w, const char* path) {
 
 double svrr_mesh_area(const svrr_grid* w) { return w->mesh.area(); }
 
+int svrr_mesh_export_obj(const svrr_grid* w, const char* path) {
+    return guarded([&] { export_obj(w->mesh, path); });
+}
+
 }  // extern "C"

@@ -156,6 +156,7 @@ _PROTOS = {
     "svr_marching_cubes": (_I, [c_void_p, c_double, POINTER(c_uint64), POINTER(c_uint64)]),
     "svr_mesh_get": (_I, [c_void_p, P, P, P, P, P]),
     "svr_mesh_save_ply": (_I, [c_void_p, c_char_p]),
+    "svr_mesh_save_obj": (_I, [c_void_p, c_char_p]),
     # svr_synth.h (host-only fixtures)
     "svr_scene_spec_default": (None, [POINTER(SceneSpec)]),
     "svr_scene_create": (_I, [POINTER(SceneSpec), POINTER(c_void_p)]),

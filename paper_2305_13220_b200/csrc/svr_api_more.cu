@@ -383,6 +383,25 @@ int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors,
     });
 }
 
+int svr_mesh_save_obj(svr_grid* g, const char* path) {
+    return guarded([&] {
+        DeviceGuard dg(g->device);
+        const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
+        std::vector<double> v(3 * nv);
+        std::vector<int32_t> t(3 * nt);
+        if (nv) SVR_CK(cudaMemcpyAsync(v.data(), g->mesh.v, nv * 24, cudaMemcpyDeviceToHost, g->stream));
+        if (nt) SVR_CK(cudaMemcpyAsync(t.data(), g->mesh.t, nt * 12, cudaMemcpyDeviceToHost, g->stream));
+        SVR_CK(cudaStreamSynchronize(g->stream));
+        std::ofstream os(path);
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("export_obj: cannot open ") + path};
+        os.precision(9);  // export_obj (mesh_io.cpp:155-164): "v x y z", 1-based "f i j k"
+        for (uint64_t i = 0; i < nv; ++i) os << "v " << v[3 * i] << " " << v[3 * i + 1] << " " << v[3 * i + 2] << "\n";
+        for (uint64_t i = 0; i < nt; ++i)
+            os << "f " << t[3 * i] + 1 << " " << t[3 * i + 1] + 1 << " " << t[3 * i + 2] + 1 << "\n";
+        if (!os) throw Fail{SVR_ERR_DATA, std::string("export_obj: write failed for ") + path};
+    });
+}
+
 int svr_mesh_save_ply(svr_grid* g, const char* path) {
     return guarded([&] {
         DeviceGuard dg(g->device);

@@ -443,6 +443,10 @@ class SparseDenseGrid:
         """export_ply of the last marching_cubes mesh."""
         check(self._lib.svr_mesh_save_ply(self._h, str(path).encode()))
 
+    def save_obj(self, path: str) -> None:
+        """export_obj of the last marching_cubes mesh."""
+        check(self._lib.svr_mesh_save_obj(self._h, str(path).encode()))
+
     # device-pointer plumbing for the multi-GPU reduction (paper_2305_13220_b200.distributed)
     def active_set_mask(self, mask) -> None:
         keep: list = []

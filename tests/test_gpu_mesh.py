@@ -70,7 +70,7 @@ def test_fused_scene_mesh_matches_oracle():
 
 
 @pytest.mark.skipif(not ref_available(), reason="reference not compiled (oracle/_ref)")
-def test_ply_bytes_match_reference_export(tmp_path):
+def test_ply_and_obj_bytes_match_reference_export(tmp_path):
     og = OracleGrid(0.02, 8, 2)
     cs, pay = sphere_payload(og, 0.15, 0.02, holes=0.02)
     g = _gpu_from(og, pay, 0.02)
@@ -82,6 +82,10 @@ def test_ply_bytes_match_reference_export(tmp_path):
     g.save_ply(tmp_path / "gpu.ply")
     rg.export_ply(tmp_path / "ref.ply")
     a, b = (tmp_path / "gpu.ply").read_bytes(), (tmp_path / "ref.ply").read_bytes()
+    assert len(a) > 10000 and a == b
+    g.save_obj(tmp_path / "gpu.obj")
+    rg.export_obj(tmp_path / "ref.obj")
+    a, b = (tmp_path / "gpu.obj").read_bytes(), (tmp_path / "ref.obj").read_bytes()
     assert len(a) > 10000 and a == b
 
 
