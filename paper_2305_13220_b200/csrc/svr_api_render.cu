@@ -42,7 +42,7 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
         const double* tt = post_march ? g->tbuf.as<double>() : nullptr;
         if (cub_sort) {
             svr_internal::launch_ray_order(v, dO, dD, n, cnt, tt, max_samples, k, id, k + n, id + n,
-                                           g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream);
+                                           g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream, g->ray_key);
         } else {
             svr_internal::launch_ray_bucket_order(v, dO, dD, n, cnt, tt, max_samples, id, g->stream);
             g->ctx_order = id;
@@ -72,9 +72,11 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
 
 void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {
     const uint64_t n = g->ctx_n;
+    // bwd_order (experiment): 0 = the forward's sorted order, 1 = caller order
+    const uint32_t* border = g->bwd_order == 1 ? nullptr : g->ctx_order;
     const bool piped =
         g->bwd_pipe && g->ctx_rec &&
-        svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
+        svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, border,
                                                   g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                                   g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
                                                   g->stream, g->pipe_min_blocks, g->num_sms, g->warp_agg);

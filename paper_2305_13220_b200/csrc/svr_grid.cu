@@ -146,6 +146,10 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
         } else if (k == "fwd_split") {
             if (value < 0 || value > 2) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..2"};
             g->fwd_split = static_cast<int>(value);
+        } else if (k == "ray_key") {
+            g->ray_key = static_cast<int>(value);
+        } else if (k == "bwd_order") {
+            g->bwd_order = static_cast<int>(value);
         } else if (k == "march_variant") {
             g->march_variant = static_cast<int>(value);
         } else if (k == "march_jump") {

@@ -212,6 +212,8 @@ struct svr_grid {
     int pipe_min_blocks = 3;
     int num_sms = 148;
     int bwd_min_blocks = 3;
+    int bwd_order = 0;
+    int ray_key = 0;  // post-march sort key: 0 first-sample block, 1 middle-sample block, 2 half blocks
     bool warp_agg = true;  // backward scatter: hand a lane's first cell run to the previous lane
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;

@@ -42,7 +42,7 @@ void launch_render_backward(const svr_dev::GridView& g, const double* o, const d
 void launch_ray_order(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
                       const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
-                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s);
+                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s, int key_mode = 0);
 size_t ray_order_tmp_bytes(uint64_t n);
 // In-house bucketed counting sort (svr_sort.cu): order = scratch[0, n).  counts == NULL:
 // origin + direction buckets (pre-march); else first-sample block buckets (post-march).

@@ -556,17 +556,21 @@ __global__ void __launch_bounds__(256) k_ray_keys(GridView g, const double* __re
                                                   const double* __restrict__ D, uint64_t n,
                                                   const uint32_t* __restrict__ counts,
                                                   const double* __restrict__ T, uint32_t S,
-                                                  uint32_t* keys, uint32_t* ids) {
+                                                  uint32_t* keys, uint32_t* ids, int mode) {
     const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= n) return;
     uint32_t key = 0xFFFFFFFFu;
     if (counts[r]) {
-        const double t = T[r * S];
+        // mode 0: block of the first sample; 1: block of the middle sample; 2: first sample at
+        // half-block resolution
+        const double t = T[r * S + (mode == 1 ? counts[r] / 2 : 0)];
+        const double cell = mode == 2 ? 0.5 * g.L : g.L;
+        const int scale = mode == 2 ? 2 : 1;
         uint32_t b[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const double x = O[3 * r + a] + t * D[3 * r + a];
-            int32_t v = static_cast<int32_t>(floor(x / g.L)) - g.lo[a];
+            int32_t v = static_cast<int32_t>(floor(x / cell)) - scale * g.lo[a];
             v = v < 0 ? 0 : (v > 1023 ? 1023 : v);
             b[a] = static_cast<uint32_t>(v);
         }
@@ -1588,18 +1592,20 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
 void launch_ray_order(const GridView& g, const double* o, const double* d, uint64_t n,
                       const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
-                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s) {
+                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s, int key_mode) {
     if (!n) return;
     if (counts)  // post-march: first-sample block
-        k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids);
+        k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids, key_mode);
     else         // pre-march: origin + direction
         k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
     // sort only the key bits in use: 24 for the pre-march key; 3 x (bits per axis of the
     // block AABB) for the post-march Morton key (empty rays carry all ones and sort last)
     int end_bit = 24;
     if (counts) {
+        const int sc = key_mode == 2 ? 2 : 1;
         int bits = 1;
-        while (bits < 10 && ((1 << bits) < g.dim[0] || (1 << bits) < g.dim[1] || (1 << bits) < g.dim[2])) ++bits;
+        while (bits < 10 && ((1 << bits) < sc * g.dim[0] || (1 << bits) < sc * g.dim[1] || (1 << bits) < sc * g.dim[2]))
+            ++bits;
         end_bit = 3 * bits;
     }
     cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
