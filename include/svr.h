@@ -111,7 +111,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
  * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
  * "pipe_min_blocks", "fwd_split" (forward lane layout, default 2: one sample per lane per 32-sample
- * pass with the ray's o / d in shared memory, 4 CTAs of 256 threads per SM; 1: lane l owns
+ * pass with the ray's o / d in shared memory, 64-thread CTAs, 32 warps per SM; 1: lane l owns
  * samples l and 32 + l; 0: samples 2l and 2l + 1), "march_jump" (0/1, default 1: exact
  * empty-space jumps over the block-distance field), "warp_agg" (0/1, default 1: the backward scatter hands a lane's first
  * cell run to the previous lane when it continues that lane's last run, one atomic per run),

@@ -202,8 +202,8 @@ struct svr_grid {
     int ray_sort = 3;
     int sort_impl = 1;  // 1: CUB radix sort (default, best order), 0: in-house bucketed counting sort
     int fwd_min_blocks = 3;
-    // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 4 CTAs of
-    // 256 per SM (default); 1 = samples l and 32 + l; 0 = samples 2l and 2l + 1
+    // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 16 CTAs of
+    // 64 per SM (default); 1 = samples l and 32 + l; 0 = samples 2l and 2l + 1
     int fwd_split = 2;
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk

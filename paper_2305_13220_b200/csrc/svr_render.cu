@@ -1522,6 +1522,18 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
                                                                                     step, ib, rgb, depth, normal,
                                                                                     wsum, valid_counter, rec);
             break;
+        case 111: k_forward_seq<128, 8, true><<<grid_for(n * 32, 128), 128, 0, s>>>(g, o, d, n, order, counts, t, S,
+                                                                                    step, ib, rgb, depth, normal,
+                                                                                    wsum, valid_counter, rec);
+            break;
+        case 113: k_forward_seq<64, 16, true><<<grid_for(n * 32, 64), 64, 0, s>>>(g, o, d, n, order, counts, t, S,
+                                                                                  step, ib, rgb, depth, normal,
+                                                                                  wsum, valid_counter, rec);
+            break;
+        case 112: k_forward_seq<512, 2, true><<<grid_for(n * 32, 512), 512, 0, s>>>(g, o, d, n, order, counts, t, S,
+                                                                                    step, ib, rgb, depth, normal,
+                                                                                    wsum, valid_counter, rec);
+            break;
         case 110: k_forward_seq<256, 5, true><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S,
                                                                                     step, ib, rgb, depth, normal,
                                                                                     wsum, valid_counter, rec);
