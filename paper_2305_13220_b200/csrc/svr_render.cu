@@ -262,8 +262,8 @@ struct StridedVec {
     __device__ __forceinline__ double operator[](int a) const { return base[a * stride]; }
 };
 
-template <int kMinBlocks, bool kSmem>
-__global__ void __launch_bounds__(128, kMinBlocks) k_march(GridView g, const double* __restrict__ O,
+template <int kMinBlocks, bool kSmem, int kThreads = 128>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_march(GridView g, const double* __restrict__ O,
                                                const double* __restrict__ D, uint64_t n,
                                                const uint32_t* __restrict__ order, double step,
                                                uint32_t S, uint32_t* counts, double* T, double* delta) {
@@ -273,13 +273,13 @@ __global__ void __launch_bounds__(128, kMinBlocks) k_march(GridView g, const dou
     double* tr = T + r * S;
     uint32_t cnt;
     if (kSmem) {
-        __shared__ double s_od[6][128];
+        __shared__ double s_od[6][kThreads];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             s_od[a][threadIdx.x] = O[3 * r + a];
             s_od[3 + a][threadIdx.x] = D[3 * r + a];
         }
-        const StridedVec o{&s_od[0][threadIdx.x], 128}, d{&s_od[3][threadIdx.x], 128};
+        const StridedVec o{&s_od[0][threadIdx.x], kThreads}, d{&s_od[3][threadIdx.x], kThreads};
         cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
     } else {
         const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
@@ -1493,6 +1493,8 @@ void launch_march(const GridView& g, const double* o, const double* d, uint64_t 
         case 1: k_march<8, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
         case 2: k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
         case 3: k_march<7, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+        case 4: k_march<12, true, 64><<<grid_for(n, 64), 64, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
+        case 5: k_march<3, true, 256><<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
         default: k_march<1, false><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
     }
 }
