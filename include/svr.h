@@ -309,6 +309,30 @@ int svr_sample_frame_rays(svr_grid* g, const svr_camera* cams, uint32_t n_frames
  * out[cap][3] in (ray, sample) order; *n_out = how many qualify (may exceed cap). */
 int svr_band_points(svr_grid* g, double band, uint64_t cap, double* out, uint64_t* n_out);
 
+/* ---- native refine loop (SPEC.md:320-327 refine; paper_2305_13220_b200/refine.py is the same
+ * composition in Python, with data parallelism over a process group) ----
+ * An svr_refiner owns device copies of the frames (rgb [F][H][W][3], optional depth prior
+ * [F][H][W] and camera-frame normal prior [F][H][W][3]) and the per-step buffers; each
+ * svr_refiner_step runs: batch sampling -> render_forward -> render_losses -> render_backward
+ * -> band + uniform Eikonal points -> svr_eikonal(lambda_eik) -> svr_rmsprop_step(lr_i) with
+ * lr_i = lr * gamma^(i / (steps - 1)).  stats (optional) gets the loss breakdown (its total
+ * includes lambda_eik * L_eik), eik_loss (optional) the Eikonal mean. */
+typedef struct {
+    uint32_t rays_per_image, images_per_batch; /* RenderConfig: 1024 x 64 */
+    double lambda_d, lambda_n, lambda_eik;     /* 0.1, 0.05, 0.1 */
+    double lr, gamma, alpha, eps;              /* 1e-3, 0.1, RMSProp 0.99, 1e-8 */
+    uint32_t max_samples, uniform_points, band_cap;
+    uint64_t seed;
+    double step, beta, mu; /* sample spacing (h/2), Laplace beta (2h), truncation (band mu/2) */
+} svr_refine_config;
+typedef struct svr_refiner svr_refiner;
+void svr_refine_config_default(svr_refine_config* cfg); /* step / beta / mu left 0: set them */
+int svr_refiner_create(svr_grid* g, const svr_camera* cams, uint32_t n_frames, const float* rgb,
+                       const float* depth, const float* normal, const svr_refine_config* cfg,
+                       svr_refiner** out);
+int svr_refiner_step(svr_refiner* r, uint32_t i, uint32_t steps, svr_loss_stats* stats, double* eik_loss);
+int svr_refiner_destroy(svr_refiner* r);
+
 /* ---- meshing (meshing.hpp:23-28, meshing.cpp:168-273; mesh_io.cpp:30-68) ----
  * marching_cubes(grid, iso): iso surface over every cell whose 8 corners are allocated and
  * observed (cells across block faces included), vertices on cell edges by linear

@@ -90,6 +90,14 @@ class LossStats(ctypes.Structure):
                 ("singular", c_int32)]
 
 
+class RefineConfig(ctypes.Structure):
+    _fields_ = [("rays_per_image", c_uint32), ("images_per_batch", c_uint32), ("lambda_d", c_double),
+                ("lambda_n", c_double), ("lambda_eik", c_double), ("lr", c_double), ("gamma", c_double),
+                ("alpha", c_double), ("eps", c_double), ("max_samples", c_uint32), ("uniform_points", c_uint32),
+                ("band_cap", c_uint32), ("seed", c_uint64), ("step", c_double), ("beta", c_double),
+                ("mu", c_double)]
+
+
 class SceneSpec(ctypes.Structure):
     _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
                 ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
@@ -153,6 +161,10 @@ _PROTOS = {
     "svr_sample_frame_rays": (_I, [c_void_p, P, c_uint32, P, P, P, c_uint32, c_uint32, c_uint64, P, P, P, P, P, P,
                                    P]),
     "svr_band_points": (_I, [c_void_p, c_double, c_uint64, P, POINTER(c_uint64)]),
+    "svr_refine_config_default": (None, [POINTER(RefineConfig)]),
+    "svr_refiner_create": (_I, [c_void_p, P, c_uint32, P, P, P, POINTER(RefineConfig), POINTER(c_void_p)]),
+    "svr_refiner_step": (_I, [c_void_p, c_uint32, c_uint32, POINTER(LossStats), POINTER(c_double)]),
+    "svr_refiner_destroy": (_I, [c_void_p]),
     "svr_marching_cubes": (_I, [c_void_p, c_double, POINTER(c_uint64), POINTER(c_uint64)]),
     "svr_mesh_get": (_I, [c_void_p, P, P, P, P, P]),
     "svr_mesh_save_ply": (_I, [c_void_p, c_char_p]),

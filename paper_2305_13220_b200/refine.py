@@ -146,3 +146,65 @@ def frames_to_device(rgb, depth=None, normal=None, device="cuda"):
 
     f = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)  # noqa: E731
     return f(rgb), f(depth), f(normal)
+
+
+class NativeRefiner:
+    """The same loop run by the library's own C++ host code (svr_refiner_* in include/svr.h):
+    frames copied to the device once, every per-step buffer owned by the handle.  Single
+    GPU; use Refiner(group=...) for data parallelism."""
+
+    def __init__(self, grid, cameras, rgb, depth=None, normal=None, *, step_m, beta, mu,
+                 config: RefineConfig | None = None):
+        from ._lib import RefineConfig as CCfg
+
+        c = config or RefineConfig()
+        lib = grid._lib
+        cc = CCfg()
+        lib.svr_refine_config_default(ctypes.byref(cc))
+        for f, _ in CCfg._fields_:
+            if hasattr(c, f):
+                setattr(cc, f, getattr(c, f))
+        cc.step, cc.beta, cc.mu = step_m, beta, mu
+        self.g, self.lib, self.cfg = grid, lib, c
+        arr = (Camera * len(cameras))(*cameras)
+        keep = []
+        ptr = lambda a: None if a is None else (a.data_ptr() if hasattr(a, "data_ptr") else  # noqa: E731
+                                                 (keep.append(np.ascontiguousarray(a, np.float32)) or keep[-1].ctypes.data))
+        h = ctypes.c_void_p()
+        check(lib.svr_refiner_create(grid._h, ctypes.addressof(arr), len(cameras), ptr(rgb), ptr(depth), ptr(normal),
+                                     ctypes.byref(cc), ctypes.byref(h)))
+        self._h = h
+
+    def step(self, i: int, steps: int, stats: bool = False) -> dict | None:
+        from ._lib import LossStats
+
+        st = LossStats()
+        el = ctypes.c_double()
+        check(self.lib.svr_refiner_step(self._h, i, steps, ctypes.byref(st) if stats else None, ctypes.byref(el)))
+        if not stats:
+            return None
+        out = {f: getattr(st, f) for f, _ in LossStats._fields_}
+        out["L_eik"] = el.value
+        out["lr"] = self.cfg.lr * self.cfg.gamma ** (i / max(steps - 1, 1))
+        return out
+
+    def run(self, steps: int, log_every: int = 0) -> list[dict]:
+        trace = []
+        for i in range(steps):
+            want = bool(log_every) and (i % log_every == 0 or i == steps - 1)
+            st = self.step(i, steps, stats=want)
+            if want:
+                st["step"] = i
+                trace.append(st)
+        return trace
+
+    def close(self):
+        if self._h:
+            self.lib.svr_refiner_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
