@@ -13,6 +13,8 @@
 // (restated in build_table below) and lives in constant memory.
 #include <algorithm>
 #include <array>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -350,7 +352,8 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw Status{SVR_ERR_CUDA, std::string("marching_cubes: ") + what + ": " + cudaGetErrorString(e)};
 }
 
-bool g_table_ready[64] = {};
+std::mutex g_table_mu;
+std::set<int> g_table_ready;  // devices whose constant-memory case table is loaded
 }  // namespace
 
 void MeshBufs::release() {
@@ -388,14 +391,17 @@ void run_marching_cubes(const GridView& g, const int32_t* coords4, const uint32_
                         double iso, MeshBufs& out, cudaStream_t s) {
     int dev = 0;
     ck(cudaGetDevice(&dev), "device");
-    if (dev < 64 && !g_table_ready[dev]) {
+    {
+        std::lock_guard<std::mutex> lock(g_table_mu);
+        if (!g_table_ready.count(dev)) {
         const Table t = build_table();
         ck(cudaMemcpyToSymbol(c_mc_count, t.count, sizeof(t.count)), "table");
         ck(cudaMemcpyToSymbol(c_mc_tri, t.tri, sizeof(t.tri)), "table");
         ck(cudaMemcpyToSymbol(c_edge_a, t.ea, 12), "table");
         ck(cudaMemcpyToSymbol(c_edge_b, t.eb, 12), "table");
         ck(cudaMemcpyToSymbol(c_edge_axis, t.eaxis, 12), "table");
-        g_table_ready[dev] = true;
+        g_table_ready.insert(dev);
+        }
     }
     out.nv = out.nt = 0;
     const uint32_t A = g.n_blocks;
