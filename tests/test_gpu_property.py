@@ -61,3 +61,32 @@ def test_render_path_random_grids(seed, h, nb, holes, S):
     assert_close(gs, ogs, what="grad_sdf")
     assert_close(gr, ogr, what="grad_rgb")
     assert np.array_equal(g.active_mask(), act)
+
+
+@settings(max_examples=15, deadline=None, suppress_health_check=list(HealthCheck))
+@given(seed=st.integers(0, 2 ** 31 - 1), nb=st.integers(1, 40), holes=st.sampled_from([0.0, 0.05, 0.3]),
+       iso=st.sampled_from([0.0, 0.01, -0.02]))
+def test_marching_cubes_random_grids(seed, nb, holes, iso):
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    rng = np.random.default_rng(seed)
+    h = 0.02
+    coords = np.unique(rng.integers(-2, 3, size=(nb, 3)), axis=0).astype(np.int32)
+    A = len(coords)
+    v = np.arange(512)
+    X = (coords[:, None, :] * 8 + np.stack([v % 8, (v // 8) % 8, v // 64], 1)[None]) * h
+    c = rng.uniform(-0.1, 0.1, 3)
+    pay = {"sdf": (np.linalg.norm(X - c, axis=2) - rng.uniform(0.05, 0.2)
+                   + rng.normal(0, 0.002, (A, 512))).astype(np.float32),
+           "weight": (rng.uniform(size=(A, 512)) >= holes).astype(np.float32),
+           "rgb": rng.uniform(-0.1, 1.1, (A, 512, 3)).astype(np.float32),
+           "logits": rng.normal(size=(A, 512, 3)).astype(np.float32)}
+    og = OracleGrid(h, 8, 3)
+    og.allocate_blocks(coords)
+    og.set_payload(0, A, **pay)
+    g = SparseDenseGrid(h, 8, 3)
+    g.allocate_blocks(coords)
+    g.set_payload(0, A, **pay)
+    a, b = g.marching_cubes(iso), og.marching_cubes(iso)
+    for k in b:
+        assert np.array_equal(a[k], b[k]), k
