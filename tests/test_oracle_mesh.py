@@ -60,3 +60,28 @@ def test_empty_grid_and_positive_field():
     og.set_payload(0, A, sdf=np.full((A, 512), 0.5, np.float32), weight=np.ones((A, 512), np.float32))
     m = og.marching_cubes(0.0)
     assert len(m["vertices"]) == 0 and len(m["triangles"]) == 0
+
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=20, deadline=None, suppress_health_check=list(HealthCheck))
+@given(seed=st.integers(0, 2 ** 31 - 1), nb=st.integers(1, 30), holes=st.sampled_from([0.0, 0.1]),
+       iso=st.sampled_from([0.0, 0.015]))
+def test_random_grids_match_reference(seed, nb, holes, iso):
+    rng = np.random.default_rng(seed)
+    h = 0.02
+    coords = np.unique(rng.integers(-2, 3, size=(nb, 3)), axis=0).astype(np.int32)
+    A = len(coords)
+    v = np.arange(512)
+    X = (coords[:, None, :] * 8 + np.stack([v % 8, (v // 8) % 8, v // 64], 1)[None]) * h
+    pay = {"sdf": (np.sin(9 * X[..., 0]) * 0.05 + X[..., 2] - 0.01 + rng.normal(0, 0.003, (A, 512))).astype(np.float32),
+           "weight": (rng.uniform(size=(A, 512)) >= holes).astype(np.float32),
+           "rgb": rng.uniform(0, 1, (A, 512, 3)).astype(np.float32),
+           "logits": rng.normal(size=(A, 512, 2)).astype(np.float32)}
+    og, rg = _pair(h)
+    for g in (og, rg):
+        g.allocate_blocks(coords)
+        g.set_payload(0, A, **pay)
+    _same(og.marching_cubes(iso), rg.marching_cubes(iso))
