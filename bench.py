@@ -92,6 +92,10 @@ class ClockSampler:
     def mark_stop(self):
         self.t1 = time.perf_counter()
 
+    def have_samples(self) -> bool:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        return any(t >= t0 for t, _ in self.lines)
+
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -429,9 +433,21 @@ def run_ours(args, cfg, rank, world, local_rank):
     t1.record(stream)
     torch.cuda.synchronize(dev)
     clocks.mark_stop()
+    # a timed region shorter than nvidia-smi's sampling period may hold no sample: keep the
+    # GPU under the same load with untimed steps until one arrives (at most 1 s)
+    extended = 0
+    t_ext = time.perf_counter()
+    while not clocks.have_samples() and time.perf_counter() - t_ext < 1.0:
+        step(False)
+        torch.cuda.synchronize(dev)
+        extended += 1
+    if extended:
+        clocks.mark_stop()
     if dist is not None:
         dist.barrier()
     clk = clocks.stop()
+    if extended:
+        clk["extended_untimed_steps"] = extended
     ms = t0.elapsed_time(t1) / args.steps
     fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
     bwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
