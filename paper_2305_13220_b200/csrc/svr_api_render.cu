@@ -65,6 +65,7 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
                                             g->tbuf.as<double>(), max_samples, step, beta, a, b, c, e, nullptr,
                                             recp, g->stream,
                                             g->fwd_min_blocks != 3 ? g->fwd_min_blocks
+                                            : g->fwd_split == 3  ? 119
                                             : g->fwd_split == 2  ? 113
                                             : g->fwd_split == 1  ? 104
                                                                  : 3);

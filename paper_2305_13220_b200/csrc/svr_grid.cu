@@ -144,7 +144,7 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
         } else if (k == "fwd_split") {
-            if (value < 0 || value > 2) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..2"};
+            if (value < 0 || value > 3) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..3"};
             g->fwd_split = static_cast<int>(value);
         } else if (k == "ray_key") {
             g->ray_key = static_cast<int>(value);

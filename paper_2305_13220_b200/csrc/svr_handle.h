@@ -204,7 +204,7 @@ struct svr_grid {
     int fwd_min_blocks = 3;
     // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 16 CTAs of
     // 64 per SM (default); 1 = samples l and 32 + l; 0 = samples 2l and 2l + 1
-    int fwd_split = 2;
+    int fwd_split = 3;
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
     bool fwd_pipe = false;    // persistent forward streaming t rows (measured slower: off)

@@ -801,6 +801,86 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_seq(GridView g
         atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
 }
 
+// K5, sequential halves over K consecutive (sorted) rays per warp with the per-ray set-up
+// taken off the critical path: one load of the K ray ids, then the K origins / directions
+// (to shared memory) and sample counts in one parallel round trip, and every t value one
+// pass ahead (the next pass of this ray, or the first pass of the next ray) -- the chain
+// order -> o/d -> count -> t -> lookup -> payload of k_forward_seq shrinks to
+// lookup -> payload per pass.  Same arithmetic per sample as k_forward_seq.
+template <int kThreads, int kMinBlocks, int K>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_multi(GridView g, const double* __restrict__ O,
+                                                    const double* __restrict__ D, uint64_t n,
+                                                    const uint32_t* __restrict__ order,
+                                                    const uint32_t* __restrict__ counts,
+                                                    const double* __restrict__ T, uint32_t S,
+                                                    double step, float ib, float* rgb, float* depth,
+                                                    float* normal, float* wsum,
+                                                    unsigned long long* valid_counter, float4* rec) {
+    static_assert(6 * K <= 32, "one lane per origin / direction component");
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t w0 = ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * K;
+    if (w0 >= n) return;
+    const int nr = n - w0 < static_cast<uint64_t>(K) ? static_cast<int>(n - w0) : K;
+    __shared__ double s_od[kThreads / 32][K][6];
+    uint32_t my_r = 0, my_cnt = 0;  // lane j < nr: ray j's id and sample count
+    if (lane < nr) my_r = order ? order[w0 + lane] : static_cast<uint32_t>(w0 + lane);
+    {
+        const int j = lane / 6, a = lane - 6 * (lane / 6);
+        const uint32_t rj = __shfl_sync(kFull, my_r, j < K ? j : 0);
+        if (j < nr) s_od[wib][j][a] = a < 3 ? O[3ull * rj + a] : D[3ull * rj + a - 3];
+        if (lane < nr) my_cnt = counts[my_r];
+    }
+    __syncwarp();
+    uint32_t nvalid = 0;
+    // t of the lane's sample in the upcoming pass
+    uint32_t r = __shfl_sync(kFull, my_r, 0), cnt = __shfl_sync(kFull, my_cnt, 0);
+    double t_cur = static_cast<uint32_t>(lane) < cnt ? T[static_cast<uint64_t>(r) * S + lane] : 0.0;
+    for (int j = 0; j < nr; ++j) {
+        const double* o = s_od[wib][j];
+        const double* d = o + 3;
+        const double* tr = T + static_cast<uint64_t>(r) * S;
+        const uint32_t r1 = __shfl_sync(kFull, my_r, j + 1 < K ? j + 1 : 0);
+        const uint32_t cnt1 = j + 1 < nr ? __shfl_sync(kFull, my_cnt, j + 1 < K ? j + 1 : 0) : 0u;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
+        float tau_base = 0.f;
+        for (uint32_t base = 0; base < cnt; base += 32) {
+            const uint32_t k0 = base + lane;
+            const bool in0 = k0 < cnt;
+            const double t0 = in0 ? t_cur : 0.0;
+            // one pass ahead: this ray's next pass, else the next ray's first pass
+            t_cur = base + 32 < cnt ? (k0 + 32 < cnt ? tr[k0 + 32] : 0.0)
+                                    : (static_cast<uint32_t>(lane) < cnt1 ? T[static_cast<uint64_t>(r1) * S + lane] : 0.0);
+            double tn0 = __shfl_down_sync(kFull, t0, 1);
+            const double tl0 = __shfl_sync(kFull, t_cur, 0);
+            if (lane == 31) tn0 = tl0;
+            const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
+            SampleVal v0;
+            const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
+            if (rec && in0) store_record(rec + (static_cast<uint64_t>(r) * S + k0) * 2, v0);
+            const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
+            const float inc0 = warp_incl_scan(tau0, lane);
+            const float w = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
+            acc[0] += w * v0.r;
+            acc[1] += w * v0.gc;
+            acc[2] += w * v0.b;
+            acc[3] += w * static_cast<float>(t0);
+            acc[4] += w * v0.gx;
+            acc[5] += w * v0.gy;
+            acc[6] += w * v0.gz;
+            acc[7] += w;
+            if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0));
+            tau_base += __shfl_sync(kFull, inc0, 31);
+        }
+        if (cnt == 0)  // no pass ran: the next ray's first pass is still to be fetched
+            t_cur = static_cast<uint32_t>(lane) < cnt1 ? T[static_cast<uint64_t>(r1) * S + lane] : 0.0;
+        write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
+        r = r1;
+        cnt = cnt1;
+    }
+    if (lane == 0 && valid_counter && nvalid)
+        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+}
+
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
 //   g_sdf = w_c dL/ds + dw_c . (w_k dN),  g_rgb = w_c w_k dC.
 struct CornerCoef {
@@ -1532,6 +1612,19 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
                                                                                   step, ib, rgb, depth, normal,
                                                                                   wsum, valid_counter, rec);
             break;
+#define SVR_FWD_MULTI(TH, MB, K)                                                                  \
+    k_forward_multi<TH, MB, K><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(                   \
+        g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec)
+        case 114: SVR_FWD_MULTI(64, 16, 2); break;
+        case 115: SVR_FWD_MULTI(64, 16, 4); break;
+        case 116: SVR_FWD_MULTI(128, 8, 4); break;
+        case 117: SVR_FWD_MULTI(64, 16, 3); break;
+        case 118: SVR_FWD_MULTI(64, 16, 5); break;
+        case 119: SVR_FWD_MULTI(64, 16, 1); break;
+        case 120: SVR_FWD_MULTI(128, 8, 1); break;
+        case 121: SVR_FWD_MULTI(256, 4, 1); break;
+        case 122: SVR_FWD_MULTI(32, 32, 1); break;
+#undef SVR_FWD_MULTI
         case 112: k_forward_seq<512, 2, true><<<grid_for(n * 32, 512), 512, 0, s>>>(g, o, d, n, order, counts, t, S,
                                                                                     step, ib, rgb, depth, normal,
                                                                                     wsum, valid_counter, rec);

@@ -42,11 +42,12 @@ def main():
     outs["n_samples"] = None
     S, step, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
     print(f"blocks={g.block_count()} rays={n}", flush=True)
+    first = None
     for combo in itertools.product(*[v for _, v in knobs]):
         for (k, _), v in zip(knobs, combo):
             g.set_tuning(k, v)
         f_ms, b_ms = [], []
-        for it in range(6):
+        for it in range(2 + int(os.environ.get("ITERS", "4"))):
             e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             e[0].record(stream)
             g.render_forward(o, d, step, S, beta, out=outs)
@@ -59,8 +60,13 @@ def main():
                 f_ms.append(e[0].elapsed_time(e[1]))
                 b_ms.append(e[1].elapsed_time(e[2]))
         tag = " ".join(f"{k}={v}" for (k, _), v in zip(knobs, combo))
+        got = torch.cat([outs[k].reshape(n, -1) for k in ("rgb", "depth", "normal", "wsum")], 1).cpu()
+        if first is None:
+            first = got
+        same = "same" if torch.equal(got, first) else f"DIFF max {float((got - first).abs().max()):.3g}"
         print(f"{tag}: fwd {statistics.mean(f_ms):7.3f} ms  bwd {statistics.mean(b_ms):7.3f} ms  "
-              f"total {statistics.mean(f_ms) + statistics.mean(b_ms):7.3f}", flush=True)
+              f"total {statistics.mean(f_ms) + statistics.mean(b_ms):7.3f}  outputs vs first config: {same}",
+              flush=True)
 
 
 if __name__ == "__main__":

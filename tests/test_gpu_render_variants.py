@@ -138,11 +138,22 @@ def test_host_async_pipeline_matches_synchronous():
     assert_close(gr, ref_gr, what="grad_rgb")
 
 
-@pytest.mark.parametrize("split", [0, 1, 2])
+@pytest.mark.parametrize("split", [0, 1, 2, 3])
 def test_forward_lane_layouts_match_oracle(split):
-    """fwd_split: one sample per lane per pass [default], lane l owns samples (l, 32 + l), or
-    (2l, 2l + 1)."""
+    """fwd_split: one sample per lane per pass with t one pass ahead [default], the same without
+    the prefetch, lane l owns samples (l, 32 + l), or (2l, 2l + 1)."""
     for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
         g = gpu_grid_from(c)
         g.set_tuning("fwd_split", split)
         _check_fwd_bwd(g, c, 64)
+
+
+@pytest.mark.parametrize("case_id", [119, 114, 115, 117, 122])
+@pytest.mark.parametrize("S", [8, 33, 100])
+def test_forward_prefetch_variants_match_oracle(case_id, S):
+    """k_forward_multi: K = 1..4 consecutive rays per warp with the per-ray set-up and every t
+    value fetched one pass ahead, at sample budgets below, just above and beyond one pass."""
+    c = scene_case()
+    g = gpu_grid_from(c)
+    g.set_tuning("fwd_min_blocks", case_id)
+    _check_fwd_bwd(g, c, S)
