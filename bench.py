@@ -8,7 +8,10 @@ ray at step h/2, Laplace beta = 2h.  One step = render_forward (march + fused fo
 + render_backward (fused adjoint + vector-atomic scatter) + active-block gradient
 reduction (NCCL all-reduce over NVLink for N > 1) + zeroing of the active gradients.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+`--workload cfg5` (BASELINE.json configs[4]): the same grid, 8M rays per step in total split
+over the GPUs (strong scaling).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3|cfg5]
 Under torchrun (N > 1) every rank drives one GPU; rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -35,7 +38,16 @@ STEP_B_SAMPLE, STEP_B_RAY = FWD_B_SAMPLE + BWD_B_SAMPLE, FWD_B_RAY + BWD_B_RAY
 
 CFG3 = dict(room=(11.0, 11.0, 3.0), h=0.01, dilation=2, C=4, width=640, height=480,
             n_objects=4, seed=1, fov=70.0, act_frames=64, ray_poses=64, rays_per_pose=16384,
-            max_samples=64)
+            max_samples=64, name="cfg3")
+# BASELINE.json configs[4]: the cfg3 grid, 8M rays per iteration (64 poses x 131072 px) split
+# over the ranks (strong scaling); `--workload cfg5`
+CFG5 = dict(CFG3, rays_per_pose=131072, strong=True, name="cfg5")
+WORKLOADS = {
+    "cfg3": ("cfg3: ScanNet-scale synthetic room 11x11x3 m, 1 cm voxels, 8^3 blocks, R=2 activation from 64 "
+             "ring-camera GT depth frames, 1M rays/GPU/step (64 poses x 16384 px), <=64 samples/ray, fwd+bwd"),
+    "cfg5": ("cfg5: the cfg3 grid (11x11x3 m, 1 cm voxels, R=2 from 64 GT depth frames), 8M rays/step in total "
+             "(64 poses x 131072 px) split contiguously over the GPUs, <=64 samples/ray, fwd+bwd"),
+}
 
 
 def log(*a):
@@ -147,10 +159,20 @@ def activation_frames(scene, cfg):
 
 
 def rays_for_rank(scene, cfg, rank, world):
-    """Global ray set = world x (poses x rays_per_pose); rank r owns a contiguous shard."""
+    """Global ray set = world x (poses x rays_per_pose) (weak scaling), or poses x rays_per_pose
+    whatever the world size (cfg5, strong scaling); rank r owns a contiguous shard."""
     from paper_2305_13220_b200.synthetic import uniform_floats
 
     poses, rpp = cfg["ray_poses"], cfg["rays_per_pose"]
+    if cfg.get("strong"):
+        if (poses * rpp) % world:
+            raise SystemExit(f"{poses * rpp} rays do not split evenly over {world} ranks")
+        o, d = scene.rays(poses, rpp, seed=0)
+        n = poses * rpp // world
+        u = uniform_floats(7 * n * world, 1).reshape(n * world, 7)[rank * n:(rank + 1) * n]
+        o, d = o[rank * n:(rank + 1) * n], d[rank * n:(rank + 1) * n]
+        return (np.ascontiguousarray(o), np.ascontiguousarray(d), np.ascontiguousarray(u[:, :3]),
+                np.ascontiguousarray(u[:, 3]), np.ascontiguousarray(u[:, 4:]))
     o, d = scene.rays(poses * world, rpp, seed=0)
     n = poses * rpp
     o, d = o[rank * n:(rank + 1) * n], d[rank * n:(rank + 1) * n]
@@ -209,7 +231,7 @@ def cpu_baseline_port(coords, payload_chunks, o, d, dC, dD, dN, cfg):
     sps, rps, info = time_cpu_render(og, o, d, cfg, dC, dD, dN, "port")
     return {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
             "rays_per_s": rps,
-            "sample": f"{info['rays']} cfg3 rays (first rays of the step), fwd+bwd, "
+            "sample": f"{info['rays']} {cfg.get('name', 'cfg3')} rays (first rays of the step), fwd+bwd, "
                       f"{info['valid_samples']} valid samples in {info['seconds']:.2f} s"}
 
 
@@ -268,14 +290,14 @@ def run_reference(args, cfg, rank, world):
     value = nvalid / t
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "impl": "reference", "rays_per_s": n / t,
-            "config": {"workload": "cfg3 ScanNet-scale synthetic room 11x11x3 m, 1 cm voxels, "
-                                   "R=2, fwd+bwd; bounded CPU ray sample per step",
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "impl": "reference", "rays_per_s": n / t,
+            "config": {"workload": WORKLOADS[cfg["name"]] + "; bounded CPU ray sample per step",
                        "blocks": int(len(coords)), "rays_per_step": n,
                        "max_samples": cfg["max_samples"]},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
-                             "sample": f"{n} cfg3 rays per step (of 1M), fwd+bwd, {nvalid} valid samples"},
+                             "sample": f"{n} {cfg['name']} rays per step (of {len(o)}), fwd+bwd, "
+                                       f"{nvalid} valid samples"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -283,13 +305,19 @@ def run_reference(args, cfg, rank, world):
 # ----------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------
-def traffic_from_profiles():
+def traffic_from_profiles(workload, rays_per_gpu):
+    """Per-launch DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) captured for
+    this workload at this per-GPU ray count, else {} (reported as null)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)
+            entries = json.load(f)["captures"]
     except Exception:
         return {}
+    for e in entries:
+        if e.get("workload") == workload and e.get("rays_per_gpu") == rays_per_gpu:
+            return e["bytes"]
+    return {}
 
 
 def _all_reduce(dist, t, op=None):
@@ -509,7 +537,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     bwd_bytes = valid_per_step * BWD_B_SAMPLE + n_rays * BWD_B_RAY
     fwd_bytes = valid_per_step * FWD_B_SAMPLE + n_rays * FWD_B_RAY
     step_bytes = valid_per_step * STEP_B_SAMPLE + n_rays * STEP_B_RAY
-    traffic = traffic_from_profiles()
+    traffic = traffic_from_profiles(cfg["name"], n_rays)
     # the dominant single kernel is the backward (one launch: k_backward_pipe); the forward
     # call is several launches (ordering, k_march, k_forward) and is reported beside it
     dom, dom_ms, dom_bytes = "k_backward_pipe", bwd_ms, bwd_bytes
@@ -519,13 +547,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "value": valid_total / (ms * 1e-3),
         "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
         "rays_per_s": rays_total / (ms * 1e-3),
         "samples_marched_per_s": marched_total / (ms * 1e-3),
-        "config": {"workload": "cfg3: ScanNet-scale synthetic room 11x11x3 m, 1 cm voxels, 8^3 blocks, "
-                               "R=2 activation from 64 ring-camera GT depth frames, 1M rays/GPU/step "
-                               "(64 poses x 16384 px), <=64 samples/ray, fwd+bwd",
+        "config": {"workload": WORKLOADS[cfg["name"]],
                    "blocks": int(info.block_count), "rays_per_gpu": n_rays,
                    "valid_samples_per_gpu": valid_per_step, "max_samples": S,
                    "step_m": step_len, "beta_m": beta, "lookup": "dense" if info.lookup_mode == 2 else "hash",
@@ -552,7 +578,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     }
     del grid
     torch.cuda.empty_cache()
-    if world == 1 and not args.no_extra:
+    if world == 1 and not args.no_extra and cfg["name"] == "cfg3":
         try:
             line["extra_configs"] = {"cfg2_image_forward": bench_cfg2(dev, stream),
                                      "cfg4_activation_and_query": bench_cfg4(dev, stream),
@@ -793,10 +819,14 @@ def main():
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 side measurements")
     ap.add_argument("--reduce", default="auto", choices=["auto", "peer", "nccl"],
                     help="N > 1 gradient reduction: fused peer-memory kernel, NCCL, or the faster of both")
-    ap.add_argument("--rays-per-pose", type=int, default=CFG3["rays_per_pose"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS),
+                    help="cfg3: 1M rays per GPU (weak scaling, default); cfg5: 8M rays split over the GPUs")
+    ap.add_argument("--rays-per-pose", type=int, default=None)
     ap.add_argument("--act-frames", type=int, default=CFG3["act_frames"])
     args = ap.parse_args()
-    cfg = dict(CFG3, rays_per_pose=args.rays_per_pose, act_frames=args.act_frames)
+    base = CFG5 if args.workload == "cfg5" else CFG3
+    cfg = dict(base, name=args.workload, act_frames=args.act_frames,
+               rays_per_pose=args.rays_per_pose or base["rays_per_pose"])
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -60,15 +60,24 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
                                                                 g->tbuf.as<double>(), max_samples, step, beta, a, b,
                                                                 c, e, recp, g->stream, g->fwd_pipe_min_blocks,
                                                                 g->num_sms);
-    if (!piped)
+    if (!piped) {
+        const int fcase = g->fwd_min_blocks != 3 ? g->fwd_min_blocks
+                          : g->fwd_split == 3    ? 119
+                          : g->fwd_split == 2    ? 113
+                          : g->fwd_split == 1    ? 104
+                                                 : 3;
+        // k_forward_multi starts from {id, count} in sorted order when the rays were sorted
+        const uint2* hdr = nullptr;
+        if (g->ray_hdr && g->ctx_order && fcase >= 114 && fcase <= 122) {
+            g->ord_hdr.ensure(8 * n);
+            svr_internal::launch_ray_headers(g->ctx_order, g->counts.as<uint32_t>(), n, g->ord_hdr.as<uint2>(),
+                                             g->stream);
+            hdr = g->ord_hdr.as<uint2>();
+        }
         svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
                                             g->tbuf.as<double>(), max_samples, step, beta, a, b, c, e, nullptr,
-                                            recp, g->stream,
-                                            g->fwd_min_blocks != 3 ? g->fwd_min_blocks
-                                            : g->fwd_split == 3  ? 119
-                                            : g->fwd_split == 2  ? 113
-                                            : g->fwd_split == 1  ? 104
-                                                                 : 3);
+                                            recp, g->stream, fcase, hdr);
+    }
 }
 
 void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {

@@ -143,6 +143,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "ray_hdr") {
+            g->ray_hdr = value != 0;
         } else if (k == "fwd_split") {
             if (value < 0 || value > 3) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..3"};
             g->fwd_split = static_cast<int>(value);

@@ -30,7 +30,9 @@ void launch_render_forward(const svr_dev::GridView& g, const double* o, const do
                            const double* t, uint32_t S, double step, double beta, float* rgb,
                            float* depth, float* normal, float* wsum,
                            unsigned long long* valid_counter, float4* rec, cudaStream_t s,
-                           int min_blocks);
+                           int min_blocks, const uint2* hdr = nullptr);
+void launch_ray_headers(const uint32_t* order, const uint32_t* counts, uint64_t n, uint2* hdr,
+                        cudaStream_t s);
 void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
                             uint64_t n, const uint32_t* order, const uint32_t* counts,
                             const double* t, uint32_t S, double step, double beta,

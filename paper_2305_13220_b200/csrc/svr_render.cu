@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_seq(GridView g
 // pass ahead (the next pass of this ray, or the first pass of the next ray) -- the chain
 // order -> o/d -> count -> t -> lookup -> payload of k_forward_seq shrinks to
 // lookup -> payload per pass.  Same arithmetic per sample as k_forward_seq.
-template <int kThreads, int kMinBlocks, int K>
+template <int kThreads, int kMinBlocks, int K, bool kHdr>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_multi(GridView g, const double* __restrict__ O,
                                                     const double* __restrict__ D, uint64_t n,
                                                     const uint32_t* __restrict__ order,
@@ -815,7 +815,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_multi(GridView
                                                     const double* __restrict__ T, uint32_t S,
                                                     double step, float ib, float* rgb, float* depth,
                                                     float* normal, float* wsum,
-                                                    unsigned long long* valid_counter, float4* rec) {
+                                                    unsigned long long* valid_counter, float4* rec,
+                                                    const uint2* __restrict__ hdr) {
     static_assert(6 * K <= 32, "one lane per origin / direction component");
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t w0 = ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * K;
@@ -823,12 +824,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_multi(GridView
     const int nr = n - w0 < static_cast<uint64_t>(K) ? static_cast<int>(n - w0) : K;
     __shared__ double s_od[kThreads / 32][K][6];
     uint32_t my_r = 0, my_cnt = 0;  // lane j < nr: ray j's id and sample count
-    if (lane < nr) my_r = order ? order[w0 + lane] : static_cast<uint32_t>(w0 + lane);
+    if (lane < nr) {
+        if (kHdr) {  // {id, count} in sorted order: one load level less
+            const uint2 h = hdr[w0 + lane];
+            my_r = h.x, my_cnt = h.y;
+        } else {
+            my_r = order ? order[w0 + lane] : static_cast<uint32_t>(w0 + lane);
+        }
+    }
     {
         const int j = lane / 6, a = lane - 6 * (lane / 6);
         const uint32_t rj = __shfl_sync(kFull, my_r, j < K ? j : 0);
         if (j < nr) s_od[wib][j][a] = a < 3 ? O[3ull * rj + a] : D[3ull * rj + a - 3];
-        if (lane < nr) my_cnt = counts[my_r];
+        if (lane < nr && !kHdr) my_cnt = counts[my_r];
     }
     __syncwarp();
     uint32_t nvalid = 0;
@@ -1583,7 +1591,7 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
                            const uint32_t* order, const uint32_t* counts, const double* t, uint32_t S,
                            double step, double beta, float* rgb, float* depth, float* normal,
                            float* wsum, unsigned long long* valid_counter, float4* rec,
-                           cudaStream_t s, int min_blocks) {
+                           cudaStream_t s, int min_blocks, const uint2* hdr) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
 #define SVR_FWD(TH, MB)                                                                         \
@@ -1613,8 +1621,12 @@ void launch_render_forward(const GridView& g, const double* o, const double* d, 
                                                                                   wsum, valid_counter, rec);
             break;
 #define SVR_FWD_MULTI(TH, MB, K)                                                                  \
-    k_forward_multi<TH, MB, K><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(                   \
-        g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec)
+    if (hdr)                                                                                      \
+        k_forward_multi<TH, MB, K, true><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(         \
+            g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec, hdr); \
+    else                                                                                          \
+        k_forward_multi<TH, MB, K, false><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(        \
+            g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec, nullptr)
         case 114: SVR_FWD_MULTI(64, 16, 2); break;
         case 115: SVR_FWD_MULTI(64, 16, 4); break;
         case 116: SVR_FWD_MULTI(128, 8, 4); break;
@@ -1694,6 +1706,19 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
     }
 #undef SVR_BWD
 #undef SVR_COMMA
+}
+
+// {id, sample count} of every ray in sorted order, for the forward's first load level
+__global__ void k_ray_headers(const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
+                              uint64_t n, uint2* __restrict__ hdr) {
+    const uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w >= n) return;
+    const uint32_t r = order[w];
+    hdr[w] = make_uint2(r, counts[r]);
+}
+
+void launch_ray_headers(const uint32_t* order, const uint32_t* counts, uint64_t n, uint2* hdr, cudaStream_t s) {
+    if (n) k_ray_headers<<<grid_for(n, 256), 256, 0, s>>>(order, counts, n, hdr);
 }
 
 void launch_ray_order(const GridView& g, const double* o, const double* d, uint64_t n,

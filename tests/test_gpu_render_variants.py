@@ -150,10 +150,13 @@ def test_forward_lane_layouts_match_oracle(split):
 
 @pytest.mark.parametrize("case_id", [119, 114, 115, 117, 122])
 @pytest.mark.parametrize("S", [8, 33, 100])
-def test_forward_prefetch_variants_match_oracle(case_id, S):
+@pytest.mark.parametrize("hdr", [0, 1])
+def test_forward_prefetch_variants_match_oracle(case_id, S, hdr):
     """k_forward_multi: K = 1..4 consecutive rays per warp with the per-ray set-up and every t
-    value fetched one pass ahead, at sample budgets below, just above and beyond one pass."""
+    value fetched one pass ahead, at sample budgets below, just above and beyond one pass; with
+    and without the {id, count} header pass (ray_hdr)."""
     c = scene_case()
     g = gpu_grid_from(c)
     g.set_tuning("fwd_min_blocks", case_id)
+    g.set_tuning("ray_hdr", hdr)
     _check_fwd_bwd(g, c, S)
