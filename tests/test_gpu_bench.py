@@ -40,3 +40,12 @@ def test_reference_arm_contract():
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_cfg5_strong_scaling_line():
+    """--workload cfg5 (BASELINE configs[4]): total rays fixed, scaling "strong"; traffic is
+    only reported for a captured (workload, rays per GPU) pair, so null at this reduced size."""
+    d = _run("--workload", "cfg5", "--rays-per-pose", "4096", "--steps", "3", "--warmup", "3", "--no-cpu-baseline")
+    assert d["scaling"] == "strong" and d["config"]["workload"].startswith("cfg5")
+    assert d["config"]["rays_per_gpu"] == 64 * 4096 and d["roofline"]["traffic"] is None
+    assert "extra_configs" not in d
