@@ -352,6 +352,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     cams, depth = activation_frames(scene, cfg)
     grid = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22, device=local_rank)
     grid.set_stream(stream)
+    # A/B hook for the performance knobs (results unaffected): SVR_TUNING="key=v,key=v"
+    for kv in filter(None, os.environ.get("SVR_TUNING", "").split(",")):
+        k, v = kv.split("=")
+        grid.set_tuning(k.strip(), int(v))
     rep = grid.allocate_for_frames(depth, cams, cfg["dilation"])
     coords = grid.coords()
     chunks = []
@@ -458,6 +462,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     t0.record(stream)
     for _ in range(args.steps):
         step(True)
+    grid.join()  # the last step's zeroing (side stream, zero_async) inside the timed region
     t1.record(stream)
     torch.cuda.synchronize(dev)
     clocks.mark_stop()

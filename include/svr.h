@@ -101,6 +101,9 @@ int svr_grid_destroy(svr_grid* g);
  * be complete in the order of this stream when a call is issued. */
 int svr_grid_set_stream(svr_grid* g, void* cuda_stream);
 int svr_grid_synchronize(svr_grid* g);
+/* Orders the handle's stream after the handle's internal side-stream work (a pending
+ * zero_async zeroing) without blocking the host; every call but render_forward does this. */
+int svr_grid_join(svr_grid* g);
 int svr_grid_get_info(svr_grid* g, svr_grid_info* out);
 int svr_grid_set_lookup(svr_grid* g, int32_t mode);
 /* Performance knobs (results are unaffected): "ray_sort" (bit 1: order the march by origin +
@@ -121,7 +124,10 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * render_forward / render_backward given PINNED host arrays return without waiting; the
  * transfers run on two internal copy streams through double-buffered device slots so one
  * step's copies overlap the previous step's kernels; host outputs are valid, and host inputs
- * may be reused, only after svr_grid_synchronize). */
+ * may be reused, only after svr_grid_synchronize), "zero_async" (0-16, default 8:
+ * svr_grad_zero_active zeroes on an internal side stream so the zeroing overlaps the next
+ * svr_render_forward; every other call on the handle -- render_backward first -- orders its
+ * work after it, so results are unchanged; n > 0 = n CTAs per SM on a lowest-priority stream). */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 
 /* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */
@@ -222,7 +228,9 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
  * while the grid does not grow (re-export after allocating blocks). */
 #define SVR_IPC_HANDLE_BYTES 64
 int svr_grad_ipc_handle(svr_grid* g, void* handle_out, uint64_t* plane_bytes);
-/* The gradient plane itself (float4 [capacity][512], device memory of the handle's GPU). */
+/* The gradient plane itself (float4 [capacity][512], device memory of the handle's GPU).
+ * Work that reads it outside this API must follow svr_grid_synchronize (a pending
+ * zero_async zeroing runs on the handle's side stream). */
 int svr_grad_plane(svr_grid* g, void** ptr_out, uint64_t* plane_bytes);
 int svr_ipc_open(const void* handle, int32_t device, void** ptr_out);
 int svr_ipc_close(void* ptr);

@@ -173,6 +173,7 @@ public:
 
     void set_stream(void* cuda_stream) { check(svr_grid_set_stream(g_, cuda_stream)); }
     void synchronize() const { check(svr_grid_synchronize(g_)); }
+    void join() const { check(svr_grid_join(g_)); }
 
 private:
     svr_grid* g_ = nullptr;

@@ -117,6 +117,7 @@ _PROTOS = {
     "svr_grid_destroy": (_I, [c_void_p]),
     "svr_grid_set_stream": (_I, [c_void_p, c_void_p]),
     "svr_grid_synchronize": (_I, [c_void_p]),
+    "svr_grid_join": (_I, [c_void_p]),
     "svr_grid_get_info": (_I, [c_void_p, POINTER(GridInfo)]),
     "svr_grid_set_lookup": (_I, [c_void_p, c_int32]),
     "svr_grid_set_tuning": (_I, [c_void_p, c_char_p, ctypes.c_int64]),

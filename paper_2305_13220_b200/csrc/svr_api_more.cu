@@ -44,7 +44,7 @@ void fuse_grow(svr_grid* g) {
 int svr_fuse_begin(svr_grid* g, int32_t flags) {
     return guarded([&] {
         if (flags & ~(SVR_FUSE_COLOR | SVR_FUSE_SEMANTIC)) throw Fail{SVR_ERR_CONFIG, "fuse_begin: unknown flags"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->fuse_flags = -1;
         g->fuse_blocks = 0;
         fuse_grow(g);
@@ -76,7 +76,7 @@ int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const flo
             if (c.width != W || c.height != H) throw Fail{SVR_ERR_CONFIG, "fuse: all frames must share one size"};
         if (W < 1 || H < 1) throw Fail{SVR_ERR_CONFIG, "fuse: empty image"};
         if (scales && (W < 2 || H < 2)) throw Fail{SVR_ERR_CONFIG, "scale field image size too small"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         fuse_grow(g);
         const uint32_t nb = static_cast<uint32_t>(g->n());
         const size_t npx = static_cast<size_t>(W) * H;
@@ -124,7 +124,7 @@ int svr_fuse_frames(svr_grid* g, const float* depth, const float* rgb, const flo
 int svr_fuse_finalize(svr_grid* g) {
     return guarded([&] {
         if (g->fuse_flags < 0) throw Fail{SVR_ERR_CONFIG, "fuse: no session (svr_fuse_begin)"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         fuse_grow(g);
         svr_internal::launch_fuse_finalize(g->fuse_sum.as<long long>(), g->fuse_cnt.as<uint32_t>(),
                                            static_cast<uint32_t>(g->n()), g->C, g->fuse_flags, g->pay, g->weight,
@@ -141,7 +141,7 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
     return guarded([&] {
         if (!(sigma_vox > 0.0)) throw Fail{SVR_ERR_CONFIG, "denoise: sigma must be positive"};
         if (radius < 0 || radius > 4) throw Fail{SVR_ERR_CONFIG, "denoise: radius must be in [0, 4]"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t nb = g->n();
         if (!nb) return;
         g->ensure_lookup();
@@ -175,7 +175,7 @@ int svr_denoise(svr_grid* g, double sigma_vox, int32_t radius) {
 int svr_grad_ipc_handle(svr_grid* g, void* handle_out, uint64_t* plane_bytes) {
     return guarded([&] {
         if (!handle_out) throw Fail{SVR_ERR_DATA, "grad_ipc_handle: output required"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (!g->grad) throw Fail{SVR_ERR_DATA, "grad_ipc_handle: the grid has no blocks yet"};
         cudaIpcMemHandle_t h;
         SVR_CK(cudaIpcGetMemHandle(&h, g->grad));
@@ -209,7 +209,7 @@ int svr_grad_peer_allreduce(svr_grid* g, void* const* peer_planes, uint32_t worl
                             const uint32_t* rows, uint64_t n_rows) {
     return guarded([&] {
         if (world < 1 || world > 8 || rank >= world) throw Fail{SVR_ERR_CONFIG, "peer_allreduce: 1 <= world <= 8"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         float4* planes[8];
         for (uint32_t q = 0; q < world; ++q) {
             planes[q] = static_cast<float4*>(peer_planes ? peer_planes[q] : nullptr);
@@ -237,7 +237,7 @@ int svr_render_losses(svr_grid* g, uint64_t n, const float* rgb, const float* de
         if (prior_normal && (!cam_idx || !cams || !n_cams))
             throw Fail{SVR_ERR_DATA, "render_losses: the normal term needs cameras and per-ray camera indices"};
         if (!(lambda_d >= 0.0) || !(lambda_n >= 0.0)) throw Fail{SVR_ERR_CONFIG, "render_losses: negative weight"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->loss_acc.ensure(16 * sizeof(double));
         Stage st(g->stream);
         const float* a = st.in(rgb, 3 * n);
@@ -296,7 +296,7 @@ int svr_sample_frame_rays(svr_grid* g, const svr_camera* cams, uint32_t n_frames
         if (!n) return;
         if (static_cast<uint64_t>(n_frames) * W * H >= (1ull << 32))
             throw Fail{SVR_ERR_CONFIG, "sample_frame_rays: more than 2^32 frame pixels"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         const size_t npx = static_cast<size_t>(n_frames) * W * H;
         const svr_camera* dc = st.in(cams, n_frames);
@@ -320,7 +320,7 @@ int svr_band_points(svr_grid* g, double band, uint64_t cap, double* out, uint64_
     return guarded([&] {
         if (!g->ctx_valid) throw Fail{SVR_ERR_DATA, "band_points: no retained forward context"};
         if (!g->ctx_rec) throw Fail{SVR_ERR_CONFIG, "band_points: needs the forward records (tuning records = 1)"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t n = g->ctx_n;
         uint64_t total = 0;
         if (n) {
@@ -343,7 +343,7 @@ int svr_band_points(svr_grid* g, double band, uint64_t cap, double* out, uint64_
 // ---------------------------------------------------------------------------
 int svr_marching_cubes(svr_grid* g, double iso, uint64_t* n_vertices, uint64_t* n_triangles) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->mesh.nv = g->mesh.nt = 0;
         if (g->n()) {
             // edge keys: voxel coordinates relative to the AABB in 21 / 21 / 20 bits
@@ -368,7 +368,7 @@ int svr_marching_cubes(svr_grid* g, double iso, uint64_t* n_vertices, uint64_t* 
 int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors, int32_t* labels,
                  int32_t* triangles) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
         auto copy = [&](void* dst, const void* src, size_t bytes) {
             if (!dst || !bytes) return;
@@ -385,7 +385,7 @@ int svr_mesh_get(svr_grid* g, double* vertices, double* normals, double* colors,
 
 int svr_mesh_save_obj(svr_grid* g, const char* path) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
         std::vector<double> v(3 * nv);
         std::vector<int32_t> t(3 * nt);
@@ -404,7 +404,7 @@ int svr_mesh_save_obj(svr_grid* g, const char* path) {
 
 int svr_mesh_save_ply(svr_grid* g, const char* path) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t nv = g->mesh.nv, nt = g->mesh.nt;
         std::vector<double> v(3 * nv), n(3 * nv), c(3 * nv);
         std::vector<int32_t> l(nv), t(3 * nt);

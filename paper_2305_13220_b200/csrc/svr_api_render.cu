@@ -107,7 +107,7 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
         if (!(step > 0.0)) throw Fail{SVR_ERR_CONFIG, "render: step must be positive"};
         if (max_samples < 1 || max_samples > 2048)
             throw Fail{SVR_ERR_CONFIG, "render: max_samples must be in [1, 2048]"};
-        DeviceGuard dg(g->device);
+        DeviceGuard dg(g->device);  // no join: march + forward overlap a pending zero_async
         g->ensure_lookup();
         g->ctx_valid = false;
         g->ctx_aslot = -1;
@@ -217,7 +217,7 @@ int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, c
         if (!g->ctx_valid) throw Fail{SVR_ERR_DATA, "render_backward: no retained forward context"};
         if (!d_rgb || !d_depth || !d_normal)
             throw Fail{SVR_ERR_DATA, "render_backward: upstream gradients required"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint64_t n = g->ctx_n;
         if (!n) return;
         if (g->ctx_aslot >= 0) {  // pipelined host I/O (the forward ran through a slot)
@@ -260,7 +260,7 @@ int svr_render_backward(svr_grid* g, const float* d_rgb, const float* d_depth, c
 
 int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         svr_render_stats s{};
         s.rays = g->ctx_valid ? g->ctx_n : 0;
         if (g->ctx_valid && g->ctx_n) {
@@ -289,7 +289,7 @@ int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
 
 int svr_grad_zero(svr_grid* g) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (!g->n()) return;
         SVR_CK(cudaMemsetAsync(g->grad, 0, g->n() * kVox * sizeof(float4), g->stream));
         SVR_CK(cudaMemsetAsync(g->active, 0, g->n(), g->stream));
@@ -298,7 +298,7 @@ int svr_grad_zero(svr_grid* g) {
 
 int svr_grad_get(svr_grid* g, float* g_sdf, float* g_rgb) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (!g->n()) return;
         Stage st(g->stream);
         const uint64_t V = g->n() * kVox;
@@ -311,7 +311,7 @@ int svr_grad_get(svr_grid* g, float* g_sdf, float* g_rgb) {
 
 int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* count) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint32_t nb = static_cast<uint32_t>(g->n());
         Stage st(g->stream);
         if (mask && nb) {
@@ -345,7 +345,7 @@ int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* coun
 
 int svr_active_set_mask(svr_grid* g, const uint8_t* mask) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint32_t nb = static_cast<uint32_t>(g->n());
         Stage st(g->stream);
         const uint8_t* m = st.in(mask, nb);
@@ -356,7 +356,7 @@ int svr_active_set_mask(svr_grid* g, const uint8_t* mask) {
 
 int svr_grad_pack(svr_grid* g, const uint32_t* blocks, uint64_t n, float* out) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         const uint32_t* b = st.in(blocks, n);
         float* o = st.out(out, n * kVox * 4);
@@ -367,7 +367,7 @@ int svr_grad_pack(svr_grid* g, const uint32_t* blocks, uint64_t n, float* out) {
 
 int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float* in) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         const uint32_t* b = st.in(blocks, n);
         const float* i = st.in(in, n * kVox * 4);
@@ -378,16 +378,29 @@ int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float
 
 int svr_grad_zero_active(svr_grid* g) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint32_t nb = static_cast<uint32_t>(g->n());
         if (!nb) return;
         g->active_list.ensure(nb * 4);
         g->active_count.ensure(8 + 4 * ((nb + 1023) / 1024 + 2));
         auto* dcount = g->active_count.as<unsigned long long>();
         svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
+        cudaStream_t zs = g->stream;
+        if (g->zero_async) {  // overlaps the next render_forward; joined by the next other call
+            g->ensure_side();
+            SVR_CK(cudaEventRecord(g->side_fork, g->stream));
+            SVR_CK(cudaStreamWaitEvent(g->side, g->side_fork, 0));
+            zs = g->side;
+        }
+        // side stream: a few CTAs per SM at the lowest priority, so the next forward's CTAs
+        // keep the SMs and the zeroing fills their idle store bandwidth
         svr_internal::launch_grad_zero_active(g->grad, g->active, g->active_list.as<uint32_t>(), dcount,
-                                              nb, g->stream);
+                                              nb, zs, g->zero_async ? static_cast<unsigned>(g->zero_async) : 16u);
         SVR_LAUNCHED();
+        if (g->zero_async) {
+            SVR_CK(cudaEventRecord(g->side_join, g->side));
+            g->side_pending = true;
+        }
     });
 }
 
@@ -395,7 +408,7 @@ int svr_sample_uniform(svr_grid* g, uint64_t n, uint64_t seed, double* out) {
     return guarded([&] {
         if (g->n() == 0) throw Fail{SVR_ERR_DATA, "sample_uniform: empty grid"};  // grid.cpp:358
         if (!n) return;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         double* o = st.out(out, 3 * n);
         svr_internal::launch_sample_uniform(g->coords4, static_cast<uint32_t>(g->n()), g->L, n, seed, o,
@@ -406,7 +419,7 @@ int svr_sample_uniform(svr_grid* g, uint64_t n, uint64_t seed, double* out) {
 
 int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* loss, uint64_t* n_valid) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         double sums[2] = {0.0, 0.0};
         if (n && g->n()) {
             g->ensure_lookup();
@@ -430,7 +443,7 @@ int svr_eikonal(svr_grid* g, const double* x, uint64_t n, double scale, double* 
 
 int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const uint32_t nb = static_cast<uint32_t>(g->n());
         if (!nb) return;
         if (g->rms_blocks < nb) {  // grow the state, new rows start at zero

@@ -338,9 +338,11 @@ void launch_grad_unpack(float4* grad, const uint32_t* blocks, uint64_t n, const 
 }
 
 void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list,
-                             const unsigned long long* count, uint32_t n_max, cudaStream_t s) {
+                             const unsigned long long* count, uint32_t n_max, cudaStream_t s,
+                             unsigned ctas_per_sm) {
     if (!n_max) return;
-    const unsigned grid = n_max < 148u * 16u ? n_max : 148u * 16u;
+    const unsigned cap = 148u * ctas_per_sm;
+    const unsigned grid = n_max < cap ? n_max : cap;
     k_grad_zero_active<<<grid, 128, 0, s>>>(grad, active, list, count);
 }
 

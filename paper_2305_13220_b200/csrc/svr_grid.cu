@@ -71,13 +71,13 @@ int svr_grid_create(double voxel_size, int32_t block_res, int32_t label_channels
 }
 
 int svr_grid_destroy(svr_grid* g) {
-    delete g;
+    delete g;  // ~svr_grid synchronises the handle's stream, the side stream and the copy streams
     return SVR_OK;
 }
 
 int svr_grid_set_stream(svr_grid* g, void* s) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         SVR_CK(cudaStreamSynchronize(g->stream));
         if (g->own_stream) cudaStreamDestroy(g->stream);
         g->stream = static_cast<cudaStream_t>(s);
@@ -91,8 +91,8 @@ int svr_grid_set_stream(svr_grid* g, void* s) {
 
 int svr_grid_synchronize(svr_grid* g) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
-        SVR_CK(cudaStreamSynchronize(g->stream));
+        GridGuard dg(g);
+        SVR_CK(cudaStreamSynchronize(g->stream));  // joined with the side stream (GridGuard)
         if (g->h2d) {
             SVR_CK(cudaStreamSynchronize(g->h2d));
             SVR_CK(cudaStreamSynchronize(g->d2h));
@@ -100,9 +100,13 @@ int svr_grid_synchronize(svr_grid* g) {
     });
 }
 
+int svr_grid_join(svr_grid* g) {
+    return guarded([&] { GridGuard dg(g); });
+}
+
 int svr_grid_get_info(svr_grid* g, svr_grid_info* out) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->ensure_lookup();
         svr_grid_info i{};
         i.voxel_size = g->h;
@@ -143,6 +147,10 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "zero_async") {
+            g->join_side();
+            if (value < 0 || value > 16) throw Fail{SVR_ERR_CONFIG, "tuning: zero_async is 0..16"};
+            g->zero_async = static_cast<int>(value);
         } else if (k == "ray_hdr") {
             g->ray_hdr = value != 0;
         } else if (k == "fwd_split") {
@@ -178,7 +186,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode) {
     return guarded([&] {
         if (mode < SVR_LOOKUP_AUTO || mode > SVR_LOOKUP_DENSE)
             throw Fail{SVR_ERR_CONFIG, "lookup: unknown mode"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->lookup_pref = mode;
         g->dense_dirty = true;
         g->ensure_lookup();
@@ -187,7 +195,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode) {
 
 int svr_grid_allocate_blocks(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (n == 0) return;
         std::vector<int32_t> hc(3 * n);
         if (is_device_ptr(coords)) {
@@ -257,7 +265,7 @@ int svr_grid_activate_points(svr_grid* g, const double* xyz, uint64_t n, int32_t
     svr_alloc_report rep{};
     const int st = guarded([&] {
         if (dilation < 0) throw Fail{SVR_ERR_CONFIG, "allocate: dilation must be >= 0"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage stg(g->stream);
         const double* dx = stg.in(xyz, 3 * n);
         svr_internal::KeySet ks;
@@ -291,7 +299,7 @@ int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* c
     svr_alloc_report rep{};
     const int st = guarded([&] {
         if (dilation < 0) throw Fail{SVR_ERR_CONFIG, "allocate: dilation must be >= 0"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (n_frames == 0) {
             g->commit(nullptr, 0, dilation, rep);
             return;
@@ -355,7 +363,7 @@ int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* c
 
 int svr_grid_find(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_out) {
     return guarded([&] {
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         if (!n) return;
         Stage st(g->stream);
         const int32_t* dc = st.in(coords, 3 * n);
@@ -369,7 +377,7 @@ int svr_grid_coords(svr_grid* g, int32_t* out) {
     return guarded([&] {
         if (g->coords.empty()) return;
         if (is_device_ptr(out)) {
-            DeviceGuard dg(g->device);
+            GridGuard dg(g);
             SVR_CK(cudaMemcpy(out, g->coords.data(), g->coords.size() * 4, cudaMemcpyHostToDevice));
         } else {
             std::memcpy(out, g->coords.data(), g->coords.size() * 4);
@@ -383,7 +391,7 @@ int svr_grid_set_payload(svr_grid* g, uint32_t first, uint32_t n, const float* s
         if (static_cast<uint64_t>(first) + n > g->n())
             throw Fail{SVR_ERR_DATA, "payload: block range out of bounds"};
         if (!n) return;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         const uint64_t V = static_cast<uint64_t>(n) * kVox;
         const float* a = st.in(sdf, V);
@@ -403,7 +411,7 @@ int svr_grid_get_payload(svr_grid* g, uint32_t first, uint32_t n, float* sdf, fl
         if (static_cast<uint64_t>(first) + n > g->n())
             throw Fail{SVR_ERR_DATA, "payload: block range out of bounds"};
         if (!n) return;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         Stage st(g->stream);
         const uint64_t V = static_cast<uint64_t>(n) * kVox;
         float* a = st.out(sdf, V);
@@ -420,7 +428,7 @@ int svr_query(svr_grid* g, const double* x, uint64_t n, double* sdf, double* gra
               double* logits, uint8_t* valid) {
     return guarded([&] {
         if (!n) return;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->ensure_lookup();
         Stage st(g->stream);
         const double* dx = st.in(x, 3 * n);
@@ -439,7 +447,7 @@ int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double 
     return guarded([&] {
         if (!(step > 0.0)) throw Fail{SVR_ERR_CONFIG, "march: step must be positive"};
         if (!n) return;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         g->ensure_lookup();
         Stage st(g->stream);
         const double* dO = st.in(o, 3 * n);

@@ -254,6 +254,26 @@ struct svr_grid {
             for (cudaEvent_t* e : {&a.in_ev, &a.up_ev, &a.fwd_ev, &a.out_ev, &a.free_ev})
                 SVR_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    // "zero_async": svr_grad_zero_active runs its zeroing kernel on a side stream, so it
+    // overlaps the next render_forward (march + forward never touch the gradient planes or
+    // the active flags); every other entry point joins the side stream first (GridGuard).
+    int zero_async = 8;  // 0: in order on the handle's stream; n > 0: side stream, n CTAs per SM
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_fork = nullptr, side_join = nullptr;
+    bool side_pending = false;
+    void ensure_side() {
+        if (side) return;
+        int lo = 0, hi = 0;
+        SVR_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // lo = numerically largest = lowest
+        SVR_CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+        SVR_CK(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
+        SVR_CK(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
+    }
+    void join_side() {
+        if (!side_pending) return;
+        SVR_CK(cudaStreamWaitEvent(stream, side_join, 0));
+        side_pending = false;
+    }
     uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
     DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
@@ -267,6 +287,12 @@ struct svr_grid {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
+        if (side) {
+            cudaStreamSynchronize(side);
+            cudaEventDestroy(side_fork);
+            cudaEventDestroy(side_join);
+            cudaStreamDestroy(side);
+        }
         if (h2d) {
             cudaStreamSynchronize(h2d);
             cudaStreamSynchronize(d2h);
@@ -468,3 +494,11 @@ struct svr_grid {
         tbuf.ensure(nr * S * 8);
     }
 };
+
+namespace svr_host {
+// Entry-point guard: the handle's device, and the handle's stream joined with any pending
+// side-stream work (zero_async) -- every entry point except render_forward uses it.
+struct GridGuard : DeviceGuard {
+    explicit GridGuard(svr_grid* g) : DeviceGuard(g->device) { g->join_side(); }
+};
+}  // namespace svr_host

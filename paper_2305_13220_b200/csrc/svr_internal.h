@@ -117,7 +117,8 @@ void launch_grad_pack(const float4* grad, const uint32_t* blocks, uint64_t n, fl
 void launch_grad_unpack(float4* grad, const uint32_t* blocks, uint64_t n, const float4* in,
                         cudaStream_t s);
 void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list,
-                             const unsigned long long* count, uint32_t n_max, cudaStream_t s);
+                             const unsigned long long* count, uint32_t n_max, cudaStream_t s,
+                             unsigned ctas_per_sm = 16);
 
 // Launchers (svr_regularize.cu)
 void launch_sample_uniform(const int32_t* coords4, uint32_t A, double L, uint64_t n, uint64_t seed,

@@ -57,7 +57,7 @@ int svr_refiner_create(svr_grid* g, const svr_camera* cams, uint32_t n_frames, c
         if (!cfg || !out || !cams || !rgb || !n_frames) throw Fail{SVR_ERR_DATA, "refiner: frames and config required"};
         if (!(cfg->step > 0.0) || !(cfg->beta > 0.0) || !(cfg->mu > 0.0))
             throw Fail{SVR_ERR_CONFIG, "refiner: step, beta and mu must be positive"};
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         auto r = std::make_unique<svr_refiner>();
         r->g = g;
         r->cfg = *cfg;
@@ -88,7 +88,7 @@ int svr_refiner_step(svr_refiner* r, uint32_t i, uint32_t steps, svr_loss_stats*
     return guarded([&] {
         svr_grid* g = r->g;
         const svr_refine_config& c = r->cfg;
-        DeviceGuard dg(g->device);
+        GridGuard dg(g);
         const bool has_d = r->depth.p != nullptr, has_n = r->normal.p != nullptr;
         // seeds as paper_2305_13220_b200/refine.py (rank 0)
         ck(svr_sample_frame_rays(g, r->cams.as<svr_camera>(), r->n_frames, r->rgb.as<float>(),
@@ -125,7 +125,7 @@ int svr_refiner_step(svr_refiner* r, uint32_t i, uint32_t steps, svr_loss_stats*
 int svr_refiner_destroy(svr_refiner* r) {
     return guarded([&] {
         if (!r) return;
-        DeviceGuard dg(r->g->device);
+        GridGuard dg(r->g);
         cudaStreamSynchronize(r->g->stream);
         delete r;
     });

@@ -127,6 +127,10 @@ class SparseDenseGrid:
     def synchronize(self) -> None:
         check(self._lib.svr_grid_synchronize(self._h))
 
+    def join(self) -> None:
+        """Order the handle's stream after its side-stream work (no host wait)."""
+        check(self._lib.svr_grid_join(self._h))
+
     def set_lookup(self, mode: int) -> None:
         check(self._lib.svr_grid_set_lookup(self._h, mode))
 

@@ -160,3 +160,27 @@ def test_forward_prefetch_variants_match_oracle(case_id, S, hdr):
     g.set_tuning("fwd_min_blocks", case_id)
     g.set_tuning("ray_hdr", hdr)
     _check_fwd_bwd(g, c, S)
+
+
+def test_zero_async_overlap_keeps_results():
+    """zero_async: svr_grad_zero_active zeroes on the side stream while the next forward runs;
+    the backward (and every read) is ordered after it -- same gradients as the in-order zeroing,
+    step after step, and the planes read back zero right after the call."""
+    c = scene_case()
+    got = {}
+    for za in (0, 1):
+        g = gpu_grid_from(c)
+        g.set_tuning("zero_async", za)
+        g.grad_zero()
+        seq = []
+        for it in range(3):
+            g.render_forward(c["o"], c["d"], c["step"], 64, c["beta"])
+            g.render_backward(c["dC"], c["dD"], c["dN"])
+            seq.append(tuple(a.copy() for a in g.grads()))
+            g.grad_zero_active()
+            gs, gr = g.grads()
+            assert not gs.any() and not gr.any()
+        got[za] = seq
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a[0], b[0]) or np.allclose(a[0], b[0], rtol=1e-5, atol=1e-7)
+        assert np.array_equal(a[1], b[1]) or np.allclose(a[1], b[1], rtol=1e-5, atol=1e-7)
