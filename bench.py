@@ -585,7 +585,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.empty_cache()
     if world == 1 and not args.no_extra and cfg["name"] == "cfg3":
         try:
-            line["extra_configs"] = {"cfg2_image_forward": bench_cfg2(dev, stream),
+            line["extra_configs"] = {"cfg1_reference_case": bench_cfg1(dev, stream, cpu=not args.no_cpu_baseline),
+                                     "cfg2_image_forward": bench_cfg2(dev, stream),
                                      "cfg4_activation_and_query": bench_cfg4(dev, stream),
                                      "cfg3_fusion_and_denoise": bench_fusion(dev, stream,
                                                                              cpu=not args.no_cpu_baseline),
@@ -615,6 +616,91 @@ def _events_ms(stream, fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def bench_cfg1(dev, stream, cpu=True):
+    """configs[0] (the reference's CPU-runnable case): 5x5x3 m room, 2 cm voxels (R=2 from 24
+    ring frames), 4096 rays from the 24 ring poses, fwd+bwd.  GPU: device time per step
+    (forward + backward + zeroing, launch-bound at this size); cpu_baseline leg: the reference
+    grid code compiled verbatim + the spec renderer (oracle/_ref), all host cores and 1 core."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+    from paper_2305_13220_b200.synthetic import uniform_floats
+
+    cfg = dict(CFG3, room=(5.0, 5.0, 3.0), h=0.02, act_frames=24, ray_poses=24)
+    scene = make_scene(cfg)
+    cams, depth = activation_frames(scene, cfg)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
+    g.set_stream(stream)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    coords = g.coords()
+    chunks = []
+    fill_in_chunks(scene, cfg, coords, lambda f, n, p: (g.set_payload(f, n, **p), chunks.append((f, n, p))))
+    o, d = scene.rays(24, 171, seed=0)
+    o, d = np.ascontiguousarray(o[:4096]), np.ascontiguousarray(d[:4096])
+    u = uniform_floats(7 * 4096, 1).reshape(4096, 7)
+    dC, dD, dN = (np.ascontiguousarray(a) for a in (u[:, :3], u[:, 3], u[:, 4:]))
+    dev_in = [torch.from_numpy(a).to(dev) for a in (o, d, dC, dD, dN)]
+    n = 4096
+    outs = {k: torch.empty(s, dtype=torch.float32, device=dev)
+            for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
+    outs["n_samples"] = None
+    step, S, beta = cfg["h"] / 2, 64, 2 * cfg["h"]
+
+    def one():
+        g.render_forward(dev_in[0], dev_in[1], step, S, beta, out=outs)
+        g.render_backward(dev_in[2], dev_in[3], dev_in[4])
+        g.grad_zero_active()
+        g.join()
+
+    ms = _events_ms(stream, one, 50)
+    st = g.render_stats()
+    out = {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),
+           "ms_per_step": ms, "samples_per_s": st.valid_samples / (ms * 1e-3)}
+    # launch-bound at this size: the same step captured once into a CUDA graph and replayed
+    try:
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            one()
+        gms = _events_ms(stream, graph.replay, 50)
+        out["cuda_graph"] = {"ms_per_step": gms, "samples_per_s": st.valid_samples / (gms * 1e-3)}
+    except Exception as e:  # pragma: no cover
+        out["cuda_graph"] = {"error": str(e)[:200]}
+    if cpu:
+        import oracle
+
+        Grid = oracle.RefGrid if oracle.ref_available() else oracle.OracleGrid
+        rg = Grid(cfg["h"], 8, cfg["C"], capacity=1 << 21)
+        rg.allocate_blocks(coords)
+        for f, nb, p in chunks:
+            rg.set_payload(f, nb, **p)
+        res = {}
+        for cores in (os.cpu_count() or 1, 1):
+            Grid.set_threads(cores)
+            best = None
+            for _ in range(3):
+                t0 = time.perf_counter()
+                if Grid is oracle.RefGrid:
+                    f = rg.render_forward(o, d, step, S, beta)
+                    rg.render_backward(dC, dD, dN)
+                else:
+                    f = rg.render_forward(o, d, step, S, beta)
+                    rg.render_backward(o, d, step, S, beta, dC, dD, dN)
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+            res[cores] = (int(f["n_valid"].sum()) / best, best)
+        Grid.set_threads(1)
+        allc = os.cpu_count() or 1
+        out["cpu_baseline"] = {"value": res[allc][0], "unit": "samples/s", "cores": allc,
+                               "kind": "reference" if Grid is oracle.RefGrid else "port",
+                               "ms_per_step": res[allc][1] * 1e3,
+                               "single_core": {"value": res[1][0], "ms_per_step": res[1][1] * 1e3},
+                               "sample": "the whole cfg1 step (4096 rays fwd+bwd), best of 3"}
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
 def bench_cfg2(dev, stream):
     """configs[1]: 5x5x3 m room, 2 cm voxels (R=2 from 24 ring frames), one full 640x480
     image from camera_for_frame(0), forward only (color/depth/normal)."""
@@ -636,6 +722,7 @@ def bench_cfg2(dev, stream):
             for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
     outs["n_samples"] = None
     g.set_tuning("records", 0)  # inference: no backward context needed
+    g.set_tuning("ray_sort", 0)  # a full image in raster order is coherent already: 0.56 vs 0.71 ms sorted
     ms = _events_ms(stream, lambda: g.render_forward(od, dd, cfg["h"] / 2, 64, 2 * cfg["h"], out=outs), 20)
     st = g.render_stats()
     return {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),

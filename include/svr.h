@@ -108,7 +108,9 @@ int svr_grid_get_info(svr_grid* g, svr_grid_info* out);
 int svr_grid_set_lookup(svr_grid* g, int32_t mode);
 /* Performance knobs (results are unaffected): "ray_sort" (bit 1: order the march by origin +
  * octahedral direction; bit 0: order forward/backward by the Morton code of each ray's
- * first-sample block; default 3 = both),
+ * first-sample block; default 3 = both -- for random ray batches; a full image in raster
+ * order is coherent already and renders faster with 0), "sort_min_rays" (default 32768:
+ * smaller batches skip both orderings),
  * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for),
  * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather),
  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /

@@ -26,7 +26,8 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
     g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
     const GridView v = g->view();
     g->ctx_order = nullptr;
-    const bool sort = g->ray_sort != 0 && n > 1;
+    // below sort_min_rays the two ordering sorts cost more than the coherence they buy
+    const bool sort = g->ray_sort != 0 && n > 1 && n >= g->sort_min_rays;
     const bool cub_sort = sort && g->sort_impl == 1;
     if (cub_sort) {
         g->ord_keys.ensure(8 * n);

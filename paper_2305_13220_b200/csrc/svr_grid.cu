@@ -147,6 +147,9 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_min_blocks") {
             g->bwd_min_blocks = static_cast<int>(value);
+        } else if (k == "sort_min_rays") {
+            if (value < 0) throw Fail{SVR_ERR_CONFIG, "tuning: sort_min_rays must be >= 0"};
+            g->sort_min_rays = static_cast<uint64_t>(value);
         } else if (k == "zero_async") {
             g->join_side();
             if (value < 0 || value > 16) throw Fail{SVR_ERR_CONFIG, "tuning: zero_async is 0..16"};

@@ -201,6 +201,7 @@ struct svr_grid {
     // bit 1: order the march by origin + direction; bit 0: order forward/backward by the
     // block of each ray's first sample (3 = both)
     int ray_sort = 3;
+    uint64_t sort_min_rays = 32768;  // smaller batches are rendered in caller order
     int sort_impl = 1;  // 1: CUB radix sort (default, best order), 0: in-house bucketed counting sort
     int fwd_min_blocks = 3;
     // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 16 CTAs of

@@ -64,4 +64,6 @@ def gpu_grid_from(case, lookup=None):
     g.set_payload(0, len(case["coords"]), **case["pay"])
     if lookup is not None:
         g.set_lookup(lookup)
+    # the test batches are small: keep the production (sorted) ordering path under test
+    g.set_tuning("sort_min_rays", 0)
     return g

@@ -184,3 +184,23 @@ def test_zero_async_overlap_keeps_results():
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a[0], b[0]) or np.allclose(a[0], b[0], rtol=1e-5, atol=1e-7)
         assert np.array_equal(a[1], b[1]) or np.allclose(a[1], b[1], rtol=1e-5, atol=1e-7)
+
+
+def test_small_batches_skip_the_ordering():
+    """sort_min_rays: a batch below the threshold renders in caller order -- same outputs
+    (bit for bit: the per-ray arithmetic does not depend on the order) and gradients within
+    the atomic-order tolerance."""
+    c = scene_case()
+    res = []
+    for smr in (0, 1 << 20):
+        g = gpu_grid_from(c)
+        g.set_tuning("sort_min_rays", smr)
+        g.grad_zero()
+        out = g.render_forward(c["o"], c["d"], c["step"], 64, c["beta"])
+        g.render_backward(c["dC"], c["dD"], c["dN"])
+        res.append((out, g.grads(), g.active_mask()))
+    for k in ("rgb", "depth", "normal", "wsum", "n_samples"):
+        assert np.array_equal(res[0][0][k], res[1][0][k]), k
+    assert_close(res[1][1][0], res[0][1][0], what="grad_sdf")
+    assert_close(res[1][1][1], res[0][1][1], what="grad_rgb")
+    assert np.array_equal(res[0][2], res[1][2])
