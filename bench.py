@@ -467,10 +467,20 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize(dev)
     clocks.mark_stop()
     # a timed region shorter than nvidia-smi's sampling period may hold no sample: keep the
-    # GPU under the same load with untimed steps until one arrives (at most 1 s)
+    # GPU under the same load with untimed steps until one arrives (at most 1 s).  Rank 0
+    # decides for all ranks, so every rank runs the same number of steps (collectives).
     extended = 0
     t_ext = time.perf_counter()
-    while not clocks.have_samples() and time.perf_counter() - t_ext < 1.0:
+
+    def more():
+        want = rank == 0 and not clocks.have_samples() and time.perf_counter() - t_ext < 1.0
+        if dist is None:
+            return want
+        f = torch.tensor([1.0 if want else 0.0], dtype=torch.float64, device=dev)
+        _all_reduce(dist, f, dist.ReduceOp.MAX)
+        return f.item() > 0
+
+    while more():
         step(False)
         torch.cuda.synchronize(dev)
         extended += 1

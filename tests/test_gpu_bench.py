@@ -49,3 +49,27 @@ def test_cfg5_strong_scaling_line():
     assert d["scaling"] == "strong" and d["config"]["workload"].startswith("cfg5")
     assert d["config"]["rays_per_gpu"] == 64 * 4096 and d["roofline"]["traffic"] is None
     assert "extra_configs" not in d
+
+
+@pytest.mark.parametrize("workload,rpp", [("cfg3", 2048), ("cfg5", 4096)])
+def test_two_rank_line_on_one_gpu(workload, rpp):
+    """The N > 1 path of bench.py under torchrun: two ranks with host-side (gloo) collectives on
+    cuda:0 -- safe on one device because no kernel waits for another rank's kernel.  Every rank
+    must run the same number of steps (a divergent count would hang a collective)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, SVR_BENCH_PG="gloo", SVR_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--workload", workload, "--rays-per-pose", str(rpp), "--steps", "3",
+                        "--warmup", "3", "--no-extra", "--no-cpu-baseline"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["grad_reduction"]["used"] in ("peer", "nccl")
+    assert d["scaling"] == ("strong" if workload == "cfg5" else "weak")
