@@ -31,6 +31,15 @@ def test_binding_covers_the_abi():
     assert declared_symbols() == set(_lib.EXPORTED)
 
 
+def test_integration_maps_every_entry_point():
+    """INTEGRATION.md names every svr.h entry point next to the reference interface it
+    replaces (or marks it as runtime plumbing)."""
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "svr.h")).read(), flags=re.S)
+    missing = [n for n in sorted(set(re.findall(r"\b(svr_\w+)\s*\(", hdr))) if n not in text]
+    assert not missing, missing
+
+
 def test_abi_version_and_struct_sizes():
     lib = _lib.load()
     assert lib.svr_abi_version() == 1
