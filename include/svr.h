@@ -119,7 +119,10 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * pass with the ray's o / d in shared memory, 64-thread CTAs, 32 warps per SM, each lane's t
  * loaded one pass ahead; 2: the same without the t prefetch; 1: lane l owns samples l and
  * 32 + l; 0: samples 2l and 2l + 1), "ray_hdr" (0/1, default 0: with fwd_split 3 and sorted rays, a
- * k_ray_headers pass hands the forward {id, count} in sorted order -- measured neutral), "march_jump" (0/1, default 1: exact
+ * k_ray_headers pass hands the forward {id, count} in sorted order -- measured neutral),
+ * "bwd_hdr" (0/1, default 1: the pipelined backward streams each ray's origin, direction,
+ * upstream gradients and sample count into its ring slot with cp.async, completed on the
+ * slot's mbarrier, instead of loading them when the ray starts), "march_jump" (0/1, default 1: exact
  * empty-space jumps over the block-distance field), "warp_agg" (0/1, default 1: the backward scatter hands a lane's first
  * cell run to the previous lane when it continues that lane's last run, one atomic per run),
  * "fuse_batch" (frames per fusion launch, 0 = auto), "host_async" (0/1:

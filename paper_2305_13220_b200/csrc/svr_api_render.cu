@@ -90,7 +90,8 @@ void backward_kernels(svr_grid* g, const float* a, const float* b, const float* 
         svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, border,
                                                   g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                                   g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
-                                                  g->stream, g->pipe_min_blocks, g->num_sms, g->warp_agg);
+                                                  g->stream, g->pipe_min_blocks, g->num_sms, g->warp_agg,
+                                                  g->bwd_hdr);
     if (!piped)
         svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                              g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,

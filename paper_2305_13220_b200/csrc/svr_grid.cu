@@ -154,6 +154,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->join_side();
             if (value < 0 || value > 16) throw Fail{SVR_ERR_CONFIG, "tuning: zero_async is 0..16"};
             g->zero_async = static_cast<int>(value);
+        } else if (k == "bwd_hdr") {
+            g->bwd_hdr = value != 0;
         } else if (k == "ray_hdr") {
             g->ray_hdr = value != 0;
         } else if (k == "fwd_split") {

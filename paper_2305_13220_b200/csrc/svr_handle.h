@@ -207,7 +207,8 @@ struct svr_grid {
     // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 16 CTAs of
     // 64 per SM (default); 1 = samples l and 32 + l; 0 = samples 2l and 2l + 1
     int fwd_split = 3;
-    int ray_hdr = 0;  // fwd_split 3: a k_ray_headers pass gives the forward {id, count} in sorted order
+    int ray_hdr = 0;
+    bool bwd_hdr = true;  // k_backward_pipe streams each ray's scalars with its t / record rows  // fwd_split 3: a k_ray_headers pass gives the forward {id, count} in sorted order
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
     bool fwd_pipe = false;    // persistent forward streaming t rows (measured slower: off)

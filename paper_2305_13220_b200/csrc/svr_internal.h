@@ -64,7 +64,7 @@ bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, co
                                  const double* t, uint32_t S, double step, double beta,
                                  const float* d_rgb, const float* d_depth, const float* d_normal,
                                  const float4* rec, cudaStream_t s, int min_blocks, int num_sms,
-                                 bool agg);
+                                 bool agg, bool hdr = false);
 
 // Launchers (svr_activate.cu)
 struct KeySet {

@@ -1141,12 +1141,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
+// The ray's scalars (kHdr): origin / direction, upstream gradients and sample count, copied
+// into the slot by 14 lanes with cp.async and completed on the slot's mbarrier.
+struct PipeHdr {
+    double o[3], d[3];
+    float dC[3], dD, dN[3];
+    uint32_t cnt;
+};
 struct PipeSlot {
     double t[64];
     float4 rec[128];
+    PipeHdr hdr;
 };
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// arrive on `bar` once this thread's earlier cp.async copies have landed (no pending-count
+// increment: the barrier's expected count includes these arrivals)
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 
-template <int kMinBlocks, int kMode = 0, int kStages = kPipeStages>
+template <int kMinBlocks, int kMode = 0, int kStages = kPipeStages, bool kHdr = false>
 __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
@@ -1162,24 +1181,43 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
     const uint32_t tbytes = S * 8, rbytes = S * 32;
     if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, 1);
+        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, kHdr ? 33 : 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
     auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
-    auto issue = [&](uint64_t i, int st) {  // lane 0: stream ray i's t + record rows
-        const uint64_t r = ray_of(i);
+    auto issue = [&](uint64_t r, int st) {  // lane 0: stream ray r's t + record rows
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(bars + st, tbytes + rbytes);
         bulk_g2s(slots[st].t, T + r * S, tbytes, bars + st);
         bulk_g2s(slots[st].rec, rec + r * S * 2, rbytes, bars + st);
     };
+    auto issue_hdr = [&](uint64_t r, int st) {  // every lane (kHdr): ray r's scalars + arrive
+        PipeHdr& h = slots[st].hdr;
+        if (lane < 3) cp_async_8(&h.o[lane], O + 3 * r + lane);
+        else if (lane < 6) cp_async_8(&h.d[lane - 3], D + 3 * r + lane - 3);
+        else if (lane < 9) cp_async_4(&h.dC[lane - 6], d_rgb + 3 * r + lane - 6);
+        else if (lane == 9) cp_async_4(&h.dD, d_depth + r);
+        else if (lane < 13) cp_async_4(&h.dN[lane - 10], d_normal + 3 * r + lane - 10);
+        else if (lane == 13) cp_async_4(&h.cnt, counts + r);
+        cp_async_arrive(bars + st);
+    };
     // prologue
-    if (lane == 0)
-        for (int st = 0; st < kStages - 1; ++st) {
-            const uint64_t i = w0 + st * warps_total;
-            if (i < n) issue(i, st);
+    for (int st = 0; st < kStages - 1; ++st) {
+        const uint64_t i = w0 + st * warps_total;
+        if (i < n) {
+            if (kHdr) {
+                const uint64_t r = ray_of(i);
+                if (lane == 0) issue(r, st);
+                issue_hdr(r, st);
+            } else if (lane == 0) {
+                issue(ray_of(i), st);
+            }
         }
+    }
+    // kHdr: the id of the next ray to stream, loaded one iteration before it is issued
+    uint64_t pf_i = w0 + (kStages - 1) * warps_total;
+    uint64_t r_pf = (kHdr && pf_i < n) ? ray_of(pf_i) : 0;
     const float ih = static_cast<float>(g.inv_h);
     uint32_t phase = 0;  // bit st = parity of stage st
     int st = 0;
@@ -1187,18 +1225,44 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
         {  // keep kStages-1 rays in flight: refill the stage released last iteration
             const uint64_t nxt = i + (kStages - 1) * warps_total;
             const int nst = (st + kStages - 1) % kStages;
-            if (lane == 0 && nxt < n) issue(nxt, nst);
+            if (kHdr) {
+                if (nxt < n) {
+                    if (lane == 0) issue(r_pf, nst);
+                    issue_hdr(r_pf, nst);
+                }
+                pf_i += warps_total;
+                if (pf_i < n) r_pf = ray_of(pf_i);
+            } else if (lane == 0 && nxt < n) {
+                issue(ray_of(nxt), nst);
+            }
         }
-        const uint64_t r = ray_of(i);
-        const uint32_t cnt = counts[r];
-        const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-        const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
-        const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
-        const float dD = d_depth[r];
-        const float dN[3] = {d_normal[3 * r], d_normal[3 * r + 1], d_normal[3 * r + 2]};
+        uint32_t cnt;
+        double o_r[3], d_r[3];
+        float dC[3], dD, dN[3];
+        const double* o = o_r;
+        const double* d = d_r;
+        if (!kHdr) {
+            const uint64_t r = ray_of(i);
+            cnt = counts[r];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                o_r[a] = O[3 * r + a], d_r[a] = D[3 * r + a];
+                dC[a] = d_rgb[3 * r + a], dN[a] = d_normal[3 * r + a];
+            }
+            dD = d_depth[r];
+        }
         mbar_wait(bars + st, (phase >> st) & 1u);
         phase ^= 1u << st;
         const PipeSlot& sl = slots[st];
+        if (kHdr) {
+            const PipeHdr& h = sl.hdr;
+            cnt = h.cnt;
+            o = h.o;
+            d = h.d;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) dC[a] = h.dC[a], dN[a] = h.dN[a];
+            dD = h.dD;
+        }
         if (cnt) {
             const uint32_t k0 = 2 * lane, k1 = k0 + 1;
             PairT p;
@@ -1750,7 +1814,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
                                  const uint32_t* order, const uint32_t* counts, const double* t,
                                  uint32_t S, double step, double beta, const float* d_rgb,
                                  const float* d_depth, const float* d_normal, const float4* rec,
-                                 cudaStream_t s, int min_blocks, int num_sms, bool agg) {
+                                 cudaStream_t s, int min_blocks, int num_sms, bool agg, bool hdr) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
     const int stages = (min_blocks == 4 || min_blocks == 5) ? 2 : kPipeStages;
@@ -1763,6 +1827,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     const uint64_t warps_total = ctas * kPipeWarps;
 #define SVR_COMMA2(a, b) a, b
 #define SVR_COMMA3(a, b, c) a, b, c
+#define SVR_COMMA4(a, b, c, e) a, b, c, e
 #define SVR_SEQ(MB, ST)                                                                           \
     do {                                                                                          \
         const size_t sm = sizeof(PipeSlot) * (ST) * kPipeWarps + 8 * (ST) * kPipeWarps;           \
@@ -1794,10 +1859,12 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
         case 602: SVR_SEQ(4, 2); break;
         case 603: SVR_SEQ(5, 2); break;
         default:
-            if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
+            if (agg && hdr) SVR_PIPE(SVR_COMMA4(3, 3, 3, true));
+            else if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
             else SVR_PIPE(3);
             break;
     }
+#undef SVR_COMMA4
 #undef SVR_PIPE
 #undef SVR_SEQ
 #undef SVR_COMMA2

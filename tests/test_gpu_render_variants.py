@@ -87,16 +87,18 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
     _check_fwd_bwd(g, case, 64)
 
 
-@pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe",
-                         [(2, 1, 1), (3, 1, 1), (3, 0, 1), (3, 1, 0), (3, 0, 0), (4, 1, 1),
-                          (601, 1, 1), (602, 1, 1)])
-def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe):
-    """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward."""
+@pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe,bwd_hdr",
+                         [(2, 1, 1, 0), (3, 1, 1, 0), (3, 1, 1, 1), (3, 0, 1, 0), (3, 1, 0, 0), (3, 0, 0, 0),
+                          (4, 1, 1, 0), (601, 1, 1, 0), (602, 1, 1, 0)])
+def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe, bwd_hdr):
+    """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward,
+    ray scalars streamed through the ring (bwd_hdr) or loaded per ray."""
     for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):  # + invalid samples inside runs
         g = gpu_grid_from(c)
         g.set_tuning("pipe_min_blocks", pipe_min_blocks)
         g.set_tuning("warp_agg", warp_agg)
         g.set_tuning("bwd_pipe", bwd_pipe)
+        g.set_tuning("bwd_hdr", bwd_hdr)
         _check_fwd_bwd(g, c, 64)
 
 
