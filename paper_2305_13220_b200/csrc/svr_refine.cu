@@ -69,34 +69,47 @@ __global__ void __launch_bounds__(256) k_sample_frame_rays(RayBatchArgs a) {
 }
 
 // |sdf| < band per sample of the retained forward (records hold the fp32 interpolated sdf)
+// Warp per ray, lane per sample (coalesced record reads); the band flags of 32 samples are
+// counted / placed with one ballot, so the points keep (ray, sample) order.
+__device__ __forceinline__ bool band_flag(const float4* __restrict__ rec, uint64_t r, uint32_t S, uint32_t k,
+                                          uint32_t cnt, float band) {
+    if (k >= cnt) return false;
+    const float* q = reinterpret_cast<const float*>(rec + (r * S + k) * 2);
+    return __float_as_uint(__ldg(q + 7)) != kInvalid && fabsf(__ldg(q)) < band;  // entry, sdf
+}
+
 __global__ void __launch_bounds__(256) k_band_count(const uint32_t* __restrict__ counts, const float4* __restrict__ rec,
                                                     uint64_t n, uint32_t S, float band, uint32_t* out) {
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     if (r >= n) return;
     const uint32_t cnt = counts[r];
     uint32_t m = 0;
-    for (uint32_t k = 0; k < cnt; ++k) {
-        const float4 a = rec[(r * S + k) * 2], b = rec[(r * S + k) * 2 + 1];
-        if (__float_as_uint(b.w) != kInvalid && fabsf(a.x) < band) ++m;
-    }
-    out[r] = m;
+    for (uint32_t base = 0; base < cnt; base += 32)
+        m += __popc(__ballot_sync(0xFFFFFFFFu, band_flag(rec, r, S, base + lane, cnt, band)));
+    if (lane == 0) out[r] = m;
 }
 
 __global__ void __launch_bounds__(256) k_band_write(const double* __restrict__ O, const double* __restrict__ D,
                                                     const uint32_t* __restrict__ counts, const double* __restrict__ T,
                                                     const float4* __restrict__ rec, uint64_t n, uint32_t S, float band,
                                                     const uint32_t* __restrict__ off, uint64_t cap, double* pts) {
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t r = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
     if (r >= n) return;
     const uint32_t cnt = counts[r];
     uint64_t j = off[r];
-    for (uint32_t k = 0; k < cnt && j < cap; ++k) {
-        const float4 a = rec[(r * S + k) * 2], b = rec[(r * S + k) * 2 + 1];
-        if (__float_as_uint(b.w) == kInvalid || !(fabsf(a.x) < band)) continue;
-        const double t = T[r * S + k];
+    for (uint32_t base = 0; base < cnt && j < cap; base += 32) {
+        const uint32_t k = base + lane;
+        const bool f = band_flag(rec, r, S, k, cnt, band);
+        const uint32_t bal = __ballot_sync(0xFFFFFFFFu, f);
+        const uint64_t pos = j + __popc(bal & ((1u << lane) - 1u));
+        if (f && pos < cap) {
+            const double t = T[r * S + k];
 #pragma unroll
-        for (int q = 0; q < 3; ++q) pts[3 * j + q] = __dadd_rn(O[3 * r + q], __dmul_rn(t, D[3 * r + q]));
-        ++j;
+            for (int q = 0; q < 3; ++q) pts[3 * pos + q] = __dadd_rn(O[3 * r + q], __dmul_rn(t, D[3 * r + q]));
+        }
+        j += __popc(bal);
     }
 }
 
@@ -120,7 +133,7 @@ uint64_t band_points(const double* o, const double* d, const uint32_t* counts, c
                      const float4* rec, uint64_t n, uint32_t S, float band, uint32_t* scratch, void* tmp,
                      size_t tmp_bytes, uint64_t cap, double* pts, cudaStream_t s) {
     if (!n) return 0;
-    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    const unsigned grid = static_cast<unsigned>((n * 32 + 255) / 256);  // warp per ray
     uint32_t* cnt = scratch;
     uint32_t* off = scratch + n;
     k_band_count<<<grid, 256, 0, s>>>(counts, rec, n, S, band, cnt);
