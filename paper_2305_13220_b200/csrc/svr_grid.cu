@@ -463,7 +463,9 @@ int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double 
         double* dt = st.out(t, nt);
         if (!dt && nt) dt = static_cast<double*>(st.alloc(8 * nt));
         double* dl = st.out(delta, nt);
-        svr_internal::launch_march(g->view(), dO, dD, n, nullptr, step, max_samples, dc, dt, dl, g->stream);
+        // the renderer's march kernel (march_variant), so the march parity tests cover it
+        svr_internal::launch_march(g->view(), dO, dD, n, nullptr, step, max_samples, dc, dt, dl, g->stream,
+                                   g->march_variant);
         st.finish();
     });
 }
