@@ -580,6 +580,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "traffic": traffic.get(dom) if traffic else None,
                      "bytes_model": "SURVEY.md 8(d): fwd 182.8 B/valid sample + 80 B/ray; "
                                     "bwd 256 B/valid sample + 28 B/ray",
+                     # measured DRAM traffic of the same kernel over its duration: the byte model
+                     # charges every corner read-modify-write to HBM, L2 serves most of them, so
+                     # frac (model) can exceed 1 while the DRAM itself runs at dram_frac
+                     "dram_achieved": (traffic[dom] / (dom_ms * 1e-3) / 1e9) if traffic.get(dom) else None,
+                     "dram_frac": (traffic[dom] / (dom_ms * 1e-3) / 1e9 / peak) if traffic.get(dom) else None,
                      "kernel_ms": dom_ms, "fwd_call_ms": fwd_ms, "bwd_ms": bwd_ms,
                      "fwd_call_frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / peak,
                      "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
