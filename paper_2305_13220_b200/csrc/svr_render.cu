@@ -1817,10 +1817,16 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
                                  cudaStream_t s, int min_blocks, int num_sms, bool agg, bool hdr) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
-    const int stages = (min_blocks == 4 || min_blocks == 5) ? 2 : kPipeStages;
+    // the default (agg + ray scalars in the ring) runs a 2-stage ring: one ray of look-ahead
+    // covers the loads once the scalars travel with the rows, and the smaller ring leaves
+    // more of the SM's 256 KB to L1 (2.40 vs 2.45 ms with 3 stages)
+    const bool def2 = agg && hdr && (min_blocks == 3 || min_blocks == 0 || min_blocks > 5) && min_blocks != 203 &&
+                      min_blocks != 310 && min_blocks != 311 && min_blocks < 600;
+    const int stages = (min_blocks == 4 || min_blocks == 5 || def2) ? 2 : (min_blocks == 311 ? 4 : kPipeStages);
     const size_t smem = sizeof(PipeSlot) * stages * kPipeWarps + 8 * stages * kPipeWarps;
     const float ib = static_cast<float>(1.0 / beta);
-    const int mb_eff = min_blocks >= 600 ? (min_blocks == 601 ? 3 : (min_blocks == 602 ? 4 : 5)) : min_blocks % 100;
+    const int mb_eff = min_blocks == 310 ? 3 : min_blocks == 311 ? 2
+                       : min_blocks >= 600 ? (min_blocks == 601 ? 3 : (min_blocks == 602 ? 4 : 5)) : min_blocks % 100;
     uint64_t ctas = static_cast<uint64_t>(num_sms) * mb_eff;
     const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
     if (ctas > need) ctas = need;
@@ -1855,11 +1861,13 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
         case 4: SVR_PIPE(SVR_COMMA3(4, 3, 2)); break;  // 2-stage ring, 64 registers
         case 5: SVR_PIPE(SVR_COMMA3(5, 3, 2)); break;
         case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
+        case 310: SVR_PIPE(SVR_COMMA4(3, 3, 3, true)); break;  // 3-stage ring with the ray scalars
+        case 311: SVR_PIPE(SVR_COMMA4(2, 3, 4, true)); break;  // experiment: 4-stage ring, 2 CTAs
         case 601: SVR_SEQ(3, 3); break;  // one sample per lane per pass
         case 602: SVR_SEQ(4, 2); break;
         case 603: SVR_SEQ(5, 2); break;
         default:
-            if (agg && hdr) SVR_PIPE(SVR_COMMA4(3, 3, 3, true));
+            if (agg && hdr) SVR_PIPE(SVR_COMMA4(3, 3, 2, true));
             else if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
             else SVR_PIPE(3);
             break;

@@ -88,8 +88,8 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
 
 
 @pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe,bwd_hdr",
-                         [(2, 1, 1, 0), (3, 1, 1, 0), (3, 1, 1, 1), (3, 0, 1, 0), (3, 1, 0, 0), (3, 0, 0, 0),
-                          (4, 1, 1, 0), (601, 1, 1, 0), (602, 1, 1, 0)])
+                         [(2, 1, 1, 0), (3, 1, 1, 0), (3, 1, 1, 1), (310, 1, 1, 1), (311, 1, 1, 1), (3, 0, 1, 0),
+                          (3, 1, 0, 0), (3, 0, 0, 0), (4, 1, 1, 0), (601, 1, 1, 0), (602, 1, 1, 0)])
 def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe, bwd_hdr):
     """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward,
     ray scalars streamed through the ring (bwd_hdr) or loaded per ray."""
