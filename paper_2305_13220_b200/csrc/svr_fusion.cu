@@ -259,11 +259,15 @@ __host__ __device__ constexpr size_t denoise_smem_bytes(int r) {
            static_cast<size_t>((8 + 2 * r) * (8 + 2 * r) * 8) * 40 + static_cast<size_t>((8 + 2 * r) * 64) * 40;
 }
 
+// The radius is a template parameter (0..4, the Gaussian table holds 2r + 1 <= 9 taps): the
+// halo extent S is a compile-time constant, so the halo index arithmetic (div / mod by S)
+// becomes multiply-shift and every tap loop unrolls.
+template <int kR>
 __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint32_t s_nb[27];
     __shared__ double s_gw[9];
-    const int r = a.r, S = 8 + 2 * r, S3 = S * S * S, NX = S * S * 8, NY = S * 64;
+    constexpr int r = kR, S = 8 + 2 * r, S3 = S * S * S, NX = S * S * 8, NY = S * 64;
     float4* halo = reinterpret_cast<float4*>(smem);
     unsigned char* hval = smem + static_cast<size_t>(S3) * 16;
     double* tx = reinterpret_cast<double*>(smem + ((static_cast<size_t>(S3) * 17 + 15) & ~size_t(15)));
@@ -295,10 +299,14 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
                 } else {
                     const int k0 = 4 * (grp - 1);
                     const float* lp = a.g.logits + gi * C + k0;
-                    val.x = __ldg(lp);
-                    if (k0 + 1 < C) val.y = __ldg(lp + 1);
-                    if (k0 + 2 < C) val.z = __ldg(lp + 2);
-                    if (k0 + 3 < C) val.w = __ldg(lp + 3);
+                    if ((C & 3) == 0) {  // 16 B aligned: one vector load
+                        val = __ldg(reinterpret_cast<const float4*>(lp));
+                    } else {
+                        val.x = __ldg(lp);
+                        if (k0 + 1 < C) val.y = __ldg(lp + 1);
+                        if (k0 + 2 < C) val.z = __ldg(lp + 2);
+                        if (k0 + 3 < C) val.w = __ldg(lp + 3);
+                    }
                 }
             }
             halo[i] = val;
@@ -319,7 +327,8 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
                 n3 = __dadd_rn(n3, __dmul_rn(w, static_cast<double>(v.w)));
                 if (grp == 0) dd = __dadd_rn(dd, __dmul_rn(w, hval[hi] ? 1.0 : 0.0));
             }
-            tx[i] = n0, tx[NX + i] = n1, tx[2 * NX + i] = n2, tx[3 * NX + i] = n3, tx[4 * NX + i] = dd;
+            tx[i] = n0, tx[NX + i] = n1, tx[2 * NX + i] = n2, tx[3 * NX + i] = n3;
+            if (grp == 0) tx[4 * NX + i] = dd;  // the denominator: group 0 only
         }
         __syncthreads();
         // pass Y: planes hz, (y, x) in [0, 8)^2
@@ -330,10 +339,12 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
                 const int ti = (hz * S + y + dy) * 8 + x;
                 const double w = s_gw[dy];
 #pragma unroll
-                for (int k = 0; k < 5; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(w, tx[k * NX + ti]));
+                for (int k = 0; k < 5; ++k)
+                    if (k < 4 || grp == 0) acc[k] = __dadd_rn(acc[k], __dmul_rn(w, tx[k * NX + ti]));
             }
 #pragma unroll
-            for (int k = 0; k < 5; ++k) ty[k * NY + i] = acc[k];
+            for (int k = 0; k < 5; ++k)
+                if (k < 4 || grp == 0) ty[k * NY + i] = acc[k];
         }
         __syncthreads();
         // pass Z + output
@@ -346,7 +357,8 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
                 const int ti = ((z + dz) * 8 + y) * 8 + x;
                 const double w = s_gw[dz];
 #pragma unroll
-                for (int k = 0; k < 5; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(w, ty[k * NY + ti]));
+                for (int k = 0; k < 5; ++k)
+                    if (k < 4 || grp == 0) acc[k] = __dadd_rn(acc[k], __dmul_rn(w, ty[k * NY + ti]));
             }
             if (grp == 0) den[j] = acc[4];
             const int hc = ((z + r) * S + y + r) * S + x + r;
@@ -428,8 +440,17 @@ void launch_denoise(const GridView& g, const int32_t* coords4, float4* pay_out, 
     a.r = radius;
     for (int i = 0; i <= 2 * radius; ++i) a.gw[i] = gw[i];
     const size_t smem = denoise_smem_bytes(radius);
-    cudaFuncSetAttribute(k_denoise, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_denoise<<<g.n_blocks, kDnThreads, smem, s>>>(a);
+#define SVR_DN(R)                                                                                       \
+    cudaFuncSetAttribute(k_denoise<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    k_denoise<R><<<g.n_blocks, kDnThreads, smem, s>>>(a)
+    switch (radius) {
+        case 0: SVR_DN(0); break;
+        case 1: SVR_DN(1); break;
+        case 2: SVR_DN(2); break;
+        case 3: SVR_DN(3); break;
+        default: SVR_DN(4); break;
+    }
+#undef SVR_DN
 }
 
 }  // namespace svr_internal
