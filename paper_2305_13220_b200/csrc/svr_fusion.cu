@@ -285,11 +285,27 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
     const int C = a.g.C, groups = 1 + (C + 3) / 4;
     for (int grp = 0; grp < groups; ++grp) {
         // stage the halo of this channel group: group 0 = (sdf, r, g, b), group k = logits 4k-4..
+        // 16 B channel groups go global -> shared with cp.async (zero-filled for a missing
+        // block), so no load round-trips through registers; the validity bit is applied
+        // where the halo is read (pass X)
+        const bool vec = grp == 0 || (C & 3) == 0;
         for (int i = threadIdx.x; i < S3; i += kDnThreads) {
             const int hx = i % S - r, hy = (i / S) % S - r, hz = i / (S * S) - r;
             const int nbi = ((hx >> 3) + 1) + 3 * ((hy >> 3) + 1) + 9 * ((hz >> 3) + 1);
             const uint32_t e = s_nb[nbi];
             const uint32_t local = (hx & 7) + 8 * (hy & 7) + 64 * (hz & 7);
+            if (vec) {
+                const bool blk = e != kInvalid;
+                const size_t gi = blk ? static_cast<size_t>(e & ~kFullBit) * kVox + local : 0;
+                const void* src = grp == 0 ? static_cast<const void*>(a.g.pay + gi)
+                                           : static_cast<const void*>(a.g.logits + gi * C + 4 * (grp - 1));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(halo + i))),
+                             "l"(src), "r"(blk ? 16u : 0u)
+                             : "memory");
+                if (grp == 0) hval[i] = blk && voxel_valid(a.g, e, local);
+                continue;
+            }
             const bool ok = e != kInvalid && voxel_valid(a.g, e, local);
             float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
             if (ok) {
@@ -310,8 +326,8 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
                 }
             }
             halo[i] = val;
-            if (grp == 0) hval[i] = ok;
         }
+        asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
         // pass X: rows (hz, hy) over the halo, x in [0, 8)
         for (int i = threadIdx.x; i < NX; i += kDnThreads) {
@@ -320,12 +336,14 @@ __global__ void __launch_bounds__(kDnThreads) k_denoise(DenoiseArgs a) {
             for (int dx = 0; dx <= 2 * r; ++dx) {
                 const int hi = row * S + x + dx;
                 const double w = s_gw[dx];
-                const float4 v = halo[hi];
+                const bool hv = hval[hi];
+                const float4 hr = halo[hi];
+                const float4 v = hv ? hr : make_float4(0.f, 0.f, 0.f, 0.f);  // unobserved: zero
                 n0 = __dadd_rn(n0, __dmul_rn(w, static_cast<double>(v.x)));
                 n1 = __dadd_rn(n1, __dmul_rn(w, static_cast<double>(v.y)));
                 n2 = __dadd_rn(n2, __dmul_rn(w, static_cast<double>(v.z)));
                 n3 = __dadd_rn(n3, __dmul_rn(w, static_cast<double>(v.w)));
-                if (grp == 0) dd = __dadd_rn(dd, __dmul_rn(w, hval[hi] ? 1.0 : 0.0));
+                if (grp == 0) dd = __dadd_rn(dd, __dmul_rn(w, hv ? 1.0 : 0.0));
             }
             tx[i] = n0, tx[NX + i] = n1, tx[2 * NX + i] = n2, tx[3 * NX + i] = n3;
             if (grp == 0) tx[4 * NX + i] = dd;  // the denominator: group 0 only
