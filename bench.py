@@ -438,10 +438,10 @@ def run_ours(args, cfg, rank, world, local_rank):
             best = "peer"
         reducer["fn"], reducer["used"] = variants[best], best
 
-    # ours per step: k_ray_keys_dir, k_march, k_ray_keys, k_forward, k_backward,
+    # ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward, k_backward,
     # k_active_count/scan/write, k_grad_zero_active (+ k_active_* / pack / unpack for N > 1);
     # plus 2 CUB radix sorts (5 library kernels each) that only reorder rays
-    launches_per_step = 9 + (5 if world > 1 else 0)
+    launches_per_step = 8 + (5 if world > 1 else 0)
     library_launches_per_step = 10  # 2 CUB radix sorts of 24-bit keys: histogram + scan + 3 onesweep passes each
     for _ in range(max(args.warmup, 3)):
         step(False)

@@ -120,6 +120,8 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * loaded one pass ahead; 2: the same without the t prefetch; 1: lane l owns samples l and
  * 32 + l; 0: samples 2l and 2l + 1), "ray_hdr" (0/1, default 0: with fwd_split 3 and sorted rays, a
  * k_ray_headers pass hands the forward {id, count} in sorted order -- measured neutral),
+ * "march_keys" (0/1, default 1: the march writes each ray's post-march sort key from the first
+ * sample it emits, instead of a separate key pass re-reading the t rows),
  * "bwd_hdr" (0/1, default 1: the pipelined backward streams each ray's origin, direction,
  * upstream gradients and sample count into its ring slot with cp.async, completed on the
  * slot's mbarrier, instead of loading them when the ray starts), "march_jump" (0/1, default 1: exact

@@ -50,9 +50,25 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
         }
     };
     if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
+    // march_keys: the march itself writes the post-march sort keys (no k_ray_keys pass)
+    const bool mkeys = cub_sort && (g->ray_sort & 1) && g->ray_key == 0 && g->march_keys;
+    uint32_t* k2 = nullptr;
+    uint32_t* id2 = nullptr;
+    if (mkeys) {
+        g->ord_keys2.ensure(8 * n);
+        g->ord_ids2.ensure(8 * n);
+        k2 = g->ord_keys2.as<uint32_t>();
+        id2 = g->ord_ids2.as<uint32_t>();
+    }
     svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples, g->counts.as<uint32_t>(),
-                               g->tbuf.as<double>(), nullptr, g->stream, g->march_variant);
-    if (sort && (g->ray_sort & 1)) order_rays(true);   // post-march: first-sample block
+                               g->tbuf.as<double>(), nullptr, g->stream, g->march_variant, k2, id2);
+    if (mkeys) {
+        svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), nullptr, max_samples, k2, id2,
+                                       k2 + n, id2 + n, g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream,
+                                       0);
+    } else if (sort && (g->ray_sort & 1)) {
+        order_rays(true);  // post-march: first-sample block
+    }
     g->ctx_rec = g->use_records;
     if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
     float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;

@@ -156,6 +156,8 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->zero_async = static_cast<int>(value);
         } else if (k == "bwd_hdr") {
             g->bwd_hdr = value != 0;
+        } else if (k == "march_keys") {
+            g->march_keys = value != 0;
         } else if (k == "ray_hdr") {
             g->ray_hdr = value != 0;
         } else if (k == "fwd_split") {

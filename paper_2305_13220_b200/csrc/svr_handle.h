@@ -194,6 +194,8 @@ struct svr_grid {
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
     DevBuf ord_keys, ord_ids, ord_tmp;  // ray ordering (Morton key of the first sample block)
     DevBuf ord_hdr;                     // {id, count} per sorted ray (fwd_split 3 + ray_hdr)
+    DevBuf ord_keys2, ord_ids2;         // post-march keys written by the march (march_keys)
+    int march_keys = 1;  // the march writes the post-march sort keys (saves the k_ray_keys pass)
     DevBuf rec;                         // per-sample forward records for the backward
     bool ctx_rec = false;
     uint32_t* ctx_order = nullptr;

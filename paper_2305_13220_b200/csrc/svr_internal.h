@@ -24,7 +24,8 @@ void launch_query(const svr_dev::GridView& g, const double* x, uint64_t n, doubl
                   double* grad, double* rgb, double* logits, uint8_t* valid, cudaStream_t s);
 void launch_march(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
                   const uint32_t* order, double step, uint32_t max_samples, uint32_t* counts,
-                  double* t, double* delta, cudaStream_t s, int variant = 0);
+                  double* t, double* delta, cudaStream_t s, int variant = 0, uint32_t* pkeys = nullptr,
+                  uint32_t* pids = nullptr);
 void launch_render_forward(const svr_dev::GridView& g, const double* o, const double* d,
                            uint64_t n, const uint32_t* order, const uint32_t* counts,
                            const double* t, uint32_t S, double step, double beta, float* rgb,

@@ -262,16 +262,36 @@ struct StridedVec {
     __device__ __forceinline__ double operator[](int a) const { return base[a * stride]; }
 };
 
+__device__ __forceinline__ uint32_t spread3(uint32_t v);
+// Morton code of the block holding a ray's first sample (k_ray_keys mode 0), computed by the
+// march from the t it has just emitted; rays without samples sort last.
+template <typename V>
+__device__ __forceinline__ uint32_t first_sample_key(const GridView& g, const V& o, const V& d, uint32_t cnt,
+                                                     double t) {
+    if (!cnt) return 0xFFFFFFFFu;
+    uint32_t b[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double x = o[a] + t * d[a];
+        int32_t v = static_cast<int32_t>(floor(x / g.L)) - g.lo[a];
+        v = v < 0 ? 0 : (v > 1023 ? 1023 : v);
+        b[a] = static_cast<uint32_t>(v);
+    }
+    return spread3(b[0]) | (spread3(b[1]) << 1) | (spread3(b[2]) << 2);
+}
+
 template <int kMinBlocks, bool kSmem, int kThreads = 128>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_march(GridView g, const double* __restrict__ O,
                                                const double* __restrict__ D, uint64_t n,
                                                const uint32_t* __restrict__ order, double step,
-                                               uint32_t S, uint32_t* counts, double* T, double* delta) {
+                                               uint32_t S, uint32_t* counts, double* T, double* delta,
+                                               uint32_t* pkeys = nullptr, uint32_t* pids = nullptr) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint64_t r = order ? order[i] : i;
     double* tr = T + r * S;
-    uint32_t cnt;
+    uint32_t cnt, key = 0xFFFFFFFFu;
+    double t_first = 0.0;
     if (kSmem) {
         __shared__ double s_od[6][kThreads];
 #pragma unroll
@@ -280,13 +300,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_march(GridView g, cons
             s_od[3 + a][threadIdx.x] = D[3 * r + a];
         }
         const StridedVec o{&s_od[0][threadIdx.x], kThreads}, d{&s_od[3][threadIdx.x], kThreads};
-        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
+            tr[k] = t;
+            if (k == 0) t_first = t;
+        });
+        if (pkeys) key = first_sample_key(g, o, d, cnt, t_first);
     } else {
         const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
         const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
-        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) { tr[k] = t; });
+        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
+            tr[k] = t;
+            if (k == 0) t_first = t;
+        });
+        if (pkeys) key = first_sample_key(g, o, d, cnt, t_first);
     }
     counts[r] = cnt;
+    if (pkeys) {  // the post-march sort key (k_ray_keys mode 0) without re-reading the t row
+        pkeys[r] = key;
+        pids[r] = static_cast<uint32_t>(r);
+    }
     if (delta) {
         double* dr = delta + r * S;
         for (uint32_t k = 0; k < cnt; ++k)
@@ -1638,9 +1670,13 @@ void launch_query(const GridView& g, const double* x, uint64_t n, double* sdf, d
 
 void launch_march(const GridView& g, const double* o, const double* d, uint64_t n,
                   const uint32_t* order, double step, uint32_t S, uint32_t* counts, double* t,
-                  double* delta, cudaStream_t s, int variant) {
+                  double* delta, cudaStream_t s, int variant, uint32_t* pkeys, uint32_t* pids) {
     if (!n) return;
     const unsigned grid = grid_for(n, 128);
+    if (pkeys) {  // the default kernel, also writing the post-march sort keys
+        k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta, pkeys, pids);
+        return;
+    }
     switch (variant) {
         case 1: k_march<8, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
         case 2: k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
@@ -1790,10 +1826,11 @@ void launch_ray_order(const GridView& g, const double* o, const double* d, uint6
                       uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
                       size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s, int key_mode) {
     if (!n) return;
-    if (counts)  // post-march: first-sample block
+    if (counts && t)  // post-march: first-sample block
         k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids, key_mode);
-    else         // pre-march: origin + direction
+    else if (!counts)  // pre-march: origin + direction
         k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
+    // (counts && !t: the march already wrote the post-march keys / ids)
     // sort only the key bits in use: 24 for the pre-march key; 3 x (bits per axis of the
     // block AABB) for the post-march Morton key (empty rays carry all ones and sort last)
     int end_bit = 24;

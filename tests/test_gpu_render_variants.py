@@ -206,3 +206,13 @@ def test_small_batches_skip_the_ordering():
     assert_close(res[1][1][0], res[0][1][0], what="grad_sdf")
     assert_close(res[1][1][1], res[0][1][1], what="grad_rgb")
     assert np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("march_keys", [0, 1])
+def test_march_written_sort_keys_match_oracle(march_keys):
+    """march_keys: the march writes the post-march sort keys itself (no k_ray_keys pass);
+    results must not depend on it."""
+    for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
+        g = gpu_grid_from(c)
+        g.set_tuning("march_keys", march_keys)
+        _check_fwd_bwd(g, c, 64)
