@@ -316,7 +316,7 @@ def traffic_from_profiles(workload, rays_per_gpu):
         return {}
     for e in entries:
         if e.get("workload") == workload and e.get("rays_per_gpu") == rays_per_gpu:
-            return e["bytes"]
+            return dict(e["bytes"], _l2_hit_pct=e.get("l2_hit_pct", {}))
     return {}
 
 
@@ -585,6 +585,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      # frac (model) can exceed 1 while the DRAM itself runs at dram_frac
                      "dram_achieved": (traffic[dom] / (dom_ms * 1e-3) / 1e9) if traffic.get(dom) else None,
                      "dram_frac": (traffic[dom] / (dom_ms * 1e-3) / 1e9 / peak) if traffic.get(dom) else None,
+                     "l2_hit_pct": traffic.get("_l2_hit_pct", {}).get(dom) if traffic else None,
                      "kernel_ms": dom_ms, "fwd_call_ms": fwd_ms, "bwd_ms": bwd_ms,
                      "fwd_call_frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / peak,
                      "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
