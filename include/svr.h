@@ -116,7 +116,7 @@ int svr_grid_set_lookup(svr_grid* g, int32_t mode);
  * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
  * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
  * "pipe_min_blocks", "fwd_split" (forward lane layout, default 3: one sample per lane per 32-sample
- * pass with the ray's o / d in shared memory, 64-thread CTAs, 32 warps per SM, each lane's t
+ * pass with the ray's o / d in shared memory, one-warp CTAs, 32 warps per SM, each lane's t
  * loaded one pass ahead; 2: the same without the t prefetch; 1: lane l owns samples l and
  * 32 + l; 0: samples 2l and 2l + 1), "ray_hdr" (0/1, default 0: with fwd_split 3 and sorted rays, a
  * k_ray_headers pass hands the forward {id, count} in sorted order -- measured neutral),

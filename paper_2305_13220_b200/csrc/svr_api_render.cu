@@ -79,7 +79,7 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
                                                                 g->num_sms);
     if (!piped) {
         const int fcase = g->fwd_min_blocks != 3 ? g->fwd_min_blocks
-                          : g->fwd_split == 3    ? 119
+                          : g->fwd_split == 3    ? 122  // one-warp CTAs, 32 per SM (0.3 % over 64-thread CTAs)
                           : g->fwd_split == 2    ? 113
                           : g->fwd_split == 1    ? 104
                                                  : 3;
