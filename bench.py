@@ -145,7 +145,7 @@ class ClockSampler:
 # inputs (host, identical for every arm)
 # ----------------------------------------------------------------------------------
 def make_scene(cfg):
-    from paper_2305_13220_b200.synthetic import SyntheticScene
+    from fixtures import SyntheticScene
 
     r = cfg["room"]
     return SyntheticScene(room_w=r[0], room_d=r[1], room_h=r[2], n_objects=cfg["n_objects"],
@@ -161,7 +161,7 @@ def activation_frames(scene, cfg):
 def rays_for_rank(scene, cfg, rank, world):
     """Global ray set = world x (poses x rays_per_pose) (weak scaling), or poses x rays_per_pose
     whatever the world size (cfg5, strong scaling); rank r owns a contiguous shard."""
-    from paper_2305_13220_b200.synthetic import uniform_floats
+    from fixtures import uniform_floats
 
     poses, rpp = cfg["ray_poses"], cfg["rays_per_pose"]
     if cfg.get("strong"):
@@ -640,7 +640,7 @@ def bench_cfg1(dev, stream, cpu=True):
     import torch
 
     from paper_2305_13220_b200 import SparseDenseGrid
-    from paper_2305_13220_b200.synthetic import uniform_floats
+    from fixtures import uniform_floats
 
     cfg = dict(CFG3, room=(5.0, 5.0, 3.0), h=0.02, act_frames=24, ray_poses=24)
     scene = make_scene(cfg)

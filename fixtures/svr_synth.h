@@ -4,7 +4,8 @@
  * synthetic.cpp:42-192): a box room with spheres/boxes, ring cameras, z-depth
  * raycasting, plus the payload/ray/upstream-gradient recipes of SURVEY.md section
  * 8(d) used by the parity tests and bench.py.  These produce INPUTS; they are not part
- * of the rendering hot path.  Exported from libsvr_b200.so.
+ * of the rendering hot path.  Exported from fixtures/libsvr_fixture.so (host-only, built by
+ * fixtures/build.py), never from the product library.
  */
 #ifndef SVR_SYNTH_H
 #define SVR_SYNTH_H
@@ -16,6 +17,8 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+
+const char* svr_fixture_last_error(void);
 
 /* SceneSpec (synthetic.hpp:13-30); defaults via svr_scene_spec_default. */
 typedef struct {

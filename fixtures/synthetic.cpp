@@ -1,7 +1,9 @@
-// Synthetic analytic-SDF scene fixtures (host C++).  Restates the reference generator
-// proj/src/core/synthetic.cpp:42-192 (scene, sdf, color, raycast, ring cameras) without
-// Eigen, plus the payload / ray / gradient recipes of SURVEY.md 8(d).  Inputs only:
-// nothing here runs inside the rendering hot path.
+// Synthetic analytic-SDF scene fixtures (host C++, fixtures/libsvr_fixture.so -- NOT part of
+// the product library).  Restates the reference generator proj/src/core/synthetic.cpp:42-192
+// (scene, sdf, color, raycast, ring cameras) without Eigen, plus the payload / ray / gradient
+// recipes of SURVEY.md 8(d).  Inputs only: nothing here runs inside the rendering hot path.
+// Pinned bit for bit to the reference's own SyntheticScene compiled verbatim into
+// oracle/_ref (tests/test_synthetic.py::test_fixture_equals_reference_generator).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -13,8 +15,9 @@
 
 #include "svr_synth.h"
 
-namespace svr_internal {
-void set_error(const std::string& msg);
+namespace svr_internal {  // this library's own last-error slot (svr_fixture_last_error)
+thread_local std::string g_fixture_err;
+void set_error(const std::string& msg) { g_fixture_err = msg; }
 }
 
 namespace {
@@ -233,6 +236,8 @@ struct svr_scene {
 };
 
 extern "C" {
+
+const char* svr_fixture_last_error(void) { return svr_internal::g_fixture_err.c_str(); }
 
 void svr_scene_spec_default(svr_scene_spec* s) {  // synthetic.hpp:13-30
     s->room_w = 2.4;

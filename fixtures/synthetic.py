@@ -1,4 +1,4 @@
-"""Synthetic analytic-SDF scene fixtures (include/svr_synth.h; host-only, no GPU needed).
+"""Synthetic analytic-SDF scene fixtures (fixtures/svr_synth.h; host-only, no GPU needed).
 
 Restates the reference's SyntheticScene (proj/src/core/synthetic.cpp:42-192) and the
 input recipes of SURVEY.md 8(d): GT depth frames for activation, clamped-SDF payloads,
@@ -7,16 +7,70 @@ random-pixel rays from ring poses and U(-1,1) upstream gradients.
 from __future__ import annotations
 
 import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_float, c_int32, c_uint32, c_uint64, c_void_p
 
 import numpy as np
 
-from . import _lib
-from ._lib import Camera, SceneSpec, check
+from paper_2305_13220_b200._lib import Camera, SvrError, _ERRORS
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsvr_fixture.so")
+
+
+class SceneSpec(ctypes.Structure):
+    """svr_scene_spec (synthetic.hpp:13-30)."""
+
+    _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
+                ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
+                ("height", c_int32), ("fov_deg", c_double), ("label_channels", c_int32),
+                ("texture_amplitude", c_double), ("texture_frequency", c_double),
+                ("seed", c_uint64)]
+
+
+P, _I = c_void_p, c_int32
+_PROTOS = {
+    "svr_fixture_last_error": (c_char_p, []),
+    "svr_scene_spec_default": (None, [POINTER(SceneSpec)]),
+    "svr_scene_create": (_I, [POINTER(SceneSpec), POINTER(c_void_p)]),
+    "svr_scene_destroy": (None, [c_void_p]),
+    "svr_scene_camera": (_I, [c_void_p, c_int32, POINTER(Camera)]),
+    "svr_scene_depth": (_I, [c_void_p, P, c_uint32, P, c_int32]),
+    "svr_scene_frames": (_I, [c_void_p, P, c_uint32, P, P, P, c_int32, P, c_int32]),
+    "svr_scene_sdf": (_I, [c_void_p, P, c_uint64, P]),
+    "svr_scene_fill_payload": (_I, [c_void_p, c_double, c_int32, c_int32, c_double, P, c_uint64,
+                                    P, P, P, P, c_int32]),
+    "svr_scene_rays": (_I, [c_void_p, c_uint32, c_uint32, c_uint64, P, P]),
+    "svr_scene_image_rays": (_I, [c_void_p, c_int32, P, P]),
+    "svr_uniform_floats": (_I, [c_uint64, c_uint64, c_float, c_float, P]),
+}
+_lib_handle = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib_handle
+    if _lib_handle is None:
+        if not os.path.exists(LIB_PATH):
+            from . import build
+
+            build.build()
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _PROTOS.items():
+            fn = getattr(lib, name)
+            fn.restype, fn.argtypes = res, args
+        _lib_handle = lib
+    return _lib_handle
+
+
+def check(status: int) -> None:
+    if status:
+        msg = (load().svr_fixture_last_error() or b"").decode(errors="replace")
+        raise _ERRORS.get(status, SvrError)(msg)
 
 
 class SyntheticScene:
     def __init__(self, **spec):
-        self._lib = _lib.load()
+        self._lib = load()
         s = SceneSpec()
         self._lib.svr_scene_spec_default(ctypes.byref(s))
         for k, v in spec.items():
@@ -105,5 +159,5 @@ class SyntheticScene:
 
 def uniform_floats(n: int, seed: int, lo: float = -1.0, hi: float = 1.0) -> np.ndarray:
     out = np.empty(n, np.float32)
-    check(_lib.load().svr_uniform_floats(n, seed, lo, hi, out.ctypes.data))
+    check(load().svr_uniform_floats(n, seed, lo, hi, out.ctypes.data))
     return out

@@ -476,3 +476,128 @@ class RefGrid(_Base):
         gr = np.empty((A, V, 3), np.float32)
         self.lib().svrr_grad_get(self._h, _ptr(gs), _ptr(gr))
         return gs, gr
+
+
+class RefScene:
+    """The reference's own SyntheticScene (synthetic.cpp, compiled verbatim into
+    _ref/libsvr_ref.so) behind the interface of fixtures.SyntheticScene: the --impl reference
+    bench arm builds every input with it, and tests pin the fixture restatement to it."""
+
+    class Spec(ctypes.Structure):
+        _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
+                    ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
+                    ("height", c_int32), ("fov_deg", c_double), ("label_channels", c_int32),
+                    ("texture_amplitude", c_double), ("texture_frequency", c_double),
+                    ("seed", c_uint64)]
+
+    # synthetic.hpp:13-30 defaults (the fields the harness sets)
+    DEFAULTS = dict(room_w=2.4, room_d=2.2, room_h=2.0, n_objects=2, n_frames=24, width=320, height=240,
+                    fov_deg=70.0, label_channels=4, texture_amplitude=0.25, texture_frequency=4.0, seed=1)
+
+    _protos = {
+        "scene_create": (c_int, [P, POINTER(c_void_p)]),
+        "scene_destroy": (None, [c_void_p]),
+        "scene_camera": (c_int, [c_void_p, c_int32, P]),
+        "scene_frames": (c_int, [c_void_p, P, c_uint32, P, P, P, c_int32, P, c_int32]),
+        "scene_sdf": (c_int, [c_void_p, P, c_uint64, P]),
+        "scene_fill_payload": (c_int, [c_void_p, c_double, c_int32, c_int32, c_double, P, c_uint64,
+                                       P, P, P, P, c_int32]),
+        "scene_rays": (c_int, [c_void_p, c_uint32, c_uint32, c_uint64, P, P]),
+        "scene_image_rays": (c_int, [c_void_p, c_int32, P, P]),
+        "uniform_floats": (c_int, [c_uint64, c_uint64, c_float, c_float, P]),
+    }
+    _bound = False
+
+    @classmethod
+    def lib(cls):
+        lib = RefGrid.lib()
+        if not cls._bound:
+            for name, (res, args) in cls._protos.items():
+                fn = getattr(lib, "svrr_" + name)
+                fn.restype, fn.argtypes = res, args
+            cls._bound = True
+        return lib
+
+    def __init__(self, **spec):
+        vals = dict(self.DEFAULTS)
+        for k, v in spec.items():
+            if k not in vals:
+                raise TypeError(f"unknown SceneSpec field {k}")
+            vals[k] = v
+        self.spec = self.Spec(**vals)
+        h = c_void_p()
+        self._check(self.lib().svrr_scene_create(ctypes.addressof(self.spec), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            if self._h.value:
+                self.lib().svrr_scene_destroy(self._h)
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st:
+            raise OracleError(st, self.lib().svrr_last_error().decode())
+
+    def camera_for_frame(self, frame: int):
+        from paper_2305_13220_b200._lib import Camera  # the svr_camera layout (a plain struct)
+
+        c = Camera()
+        self._check(self.lib().svrr_scene_camera(self._h, frame, ctypes.addressof(c)))
+        return c
+
+    def cameras(self, n=None):
+        n = self.spec.n_frames if n is None else n
+        return [self.camera_for_frame(f) for f in range(n)]
+
+    def frames(self, cams, threads=0, label_channels=None, normals=False, what=("depth", "rgb", "sem")):
+        C = self.spec.label_channels if label_channels is None else label_channels
+        F, H, W = len(cams), self.spec.height, self.spec.width
+        arr = (type(cams[0]) * F)(*cams)
+        out = {"depth": np.empty((F, H, W), np.float32) if "depth" in what else None,
+               "rgb": np.empty((F, H, W, 3), np.float32) if "rgb" in what else None,
+               "sem": np.empty((F, H, W, C), np.float32) if "sem" in what else None,
+               "normal": np.empty((F, H, W, 3), np.float32) if normals else None}
+        self._check(self.lib().svrr_scene_frames(self._h, ctypes.addressof(arr), F, _ptr(out["depth"]),
+                                                 _ptr(out["rgb"]), _ptr(out["sem"]), C, _ptr(out["normal"]),
+                                                 threads))
+        res = tuple(out[k] for k in ("depth", "rgb", "sem") if k in what)
+        return res + (out["normal"],) if normals else res
+
+    def depth(self, cams, threads=0):
+        return self.frames(cams, threads, what=("depth",))[0]
+
+    def sdf(self, x):
+        x = _f64(x, (-1, 3))
+        out = np.empty(len(x))
+        self._check(self.lib().svrr_scene_sdf(self._h, _ptr(x), len(x), _ptr(out)))
+        return out
+
+    def fill_payload(self, voxel_size, coords, trunc, label_channels, block_res=8, threads=0):
+        c = np.ascontiguousarray(coords, np.int32).reshape(-1, 3)
+        n, V = len(c), block_res ** 3
+        out = {"sdf": np.empty((n, V), np.float32), "weight": np.empty((n, V), np.float32),
+               "rgb": np.empty((n, V, 3), np.float32), "logits": np.empty((n, V, label_channels), np.float32)}
+        self._check(self.lib().svrr_scene_fill_payload(self._h, voxel_size, block_res, label_channels, trunc,
+                                                       _ptr(c), n, _ptr(out["sdf"]), _ptr(out["weight"]),
+                                                       _ptr(out["rgb"]), _ptr(out["logits"]), threads))
+        return out
+
+    def rays(self, n_poses, rays_per_pose, seed=0):
+        n = n_poses * rays_per_pose
+        o, d = np.empty((n, 3)), np.empty((n, 3))
+        self._check(self.lib().svrr_scene_rays(self._h, n_poses, rays_per_pose, seed, _ptr(o), _ptr(d)))
+        return o, d
+
+    def image_rays(self, frame):
+        n = self.spec.width * self.spec.height
+        o, d = np.empty((n, 3)), np.empty((n, 3))
+        self._check(self.lib().svrr_scene_image_rays(self._h, frame, _ptr(o), _ptr(d)))
+        return o, d
+
+    @classmethod
+    def uniform_floats(cls, n, seed, lo=-1.0, hi=1.0):
+        out = np.empty(n, np.float32)
+        cls.lib().svrr_uniform_floats(n, seed, lo, hi, _ptr(out))
+        return out

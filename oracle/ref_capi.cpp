@@ -551,3 +551,257 @@ int svrr_mesh_export_obj(const svrr_grid* w, const char* path) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// The REFERENCE's synthetic generator (proj/src/core/synthetic.cpp, compiled verbatim; the
+// file-writing helpers it calls only from generate_synthetic are stubbed in
+// shim/io_stubs.cpp) behind the same C interface as fixtures/libsvr_fixture.so, so the
+// --impl reference bench arm builds its inputs with reference code only, and the fixture
+// restatement is pinned to it bit for bit (tests/test_synthetic.py).
+//
+// The recipes around the scene are the harness's: GT depth = the z-depth
+// raycast per integer pixel as generate_synthetic renders it (synthetic.cpp:318-340),
+// payload = clamp(sdf(v h), -mu, mu) with colour / one-hot logits of the nearest surface's
+// class, rays through mt19937_64-drawn pixels with Camera::ray_direction (camera.cpp:27-30).
+// ---------------------------------------------------------------------------------------
+#include <random>
+#include <thread>
+
+#include "core/synthetic.hpp"
+
+namespace {
+// Layout mirror of SyntheticScene's private state (synthetic.hpp:61-71), used only to read the
+// object list for the nearest-surface class of a payload voxel (the reference exposes sdf()
+// but not which surface attains it).  Checked against the real object at construction.
+struct SceneMirror {
+    struct Object {
+        bool is_sphere = true;
+        Eigen::Vector3d center{0, 0, 0};
+        Eigen::Vector3d half{0.1, 0.1, 0.1};
+        int label = 2;
+    };
+    SceneSpec spec_;
+    Eigen::Vector3d room_half_;
+    std::vector<Object> objects_;
+};
+static_assert(sizeof(SceneMirror) == sizeof(SyntheticScene), "SyntheticScene layout changed");
+
+double mirror_box_sdf(const Eigen::Vector3d& p, const Eigen::Vector3d& half) {  // synthetic.cpp:33-38
+    const Eigen::Vector3d q = p.cwiseAbs() - half;
+    const Eigen::Vector3d outside = q.cwiseMax(0.0);
+    const double inside = std::min(q.maxCoeff(), 0.0);
+    return outside.norm() + inside;
+}
+
+template <typename F>
+void for_range(uint64_t n, int threads, F&& fn) {
+    int w = threads > 0 ? threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    w = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(w), std::max<uint64_t>(n, 1)));
+    if (w <= 1) {
+        fn(uint64_t(0), n);
+        return;
+    }
+    const uint64_t chunk = (n + w - 1) / w;
+    std::vector<std::thread> pool;
+    for (int i = 0; i < w; ++i) {
+        const uint64_t b = i * chunk, e = std::min(n, b + chunk);
+        if (b >= e) break;
+        pool.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& t : pool) t.join();
+}
+}  // namespace
+
+typedef struct {
+    double room_w, room_d, room_h;
+    int32_t n_objects, n_frames, width, height;
+    double fov_deg;
+    int32_t label_channels;
+    double texture_amplitude, texture_frequency;
+    uint64_t seed;
+} svrr_scene_spec;
+
+struct svrr_scene {
+    std::unique_ptr<SyntheticScene> s;
+    const SceneMirror* m = nullptr;
+    // class of the surface nearest to x: walls / floor from the room box, else the nearest object
+    int label(const Eigen::Vector3d& x) const {
+        const Eigen::Vector3d dw = m->room_half_ - x.cwiseAbs();
+        int axis = 0;
+        for (int a = 1; a < 3; ++a)
+            if (dw[a] < dw[axis]) axis = a;
+        double best = dw[axis];
+        int lab = (axis == 2 && x.z() < 0.0) ? 1 : 0;
+        for (const auto& o : m->objects_) {
+            const double od = o.is_sphere ? (x - o.center).norm() - o.half.x() : mirror_box_sdf(x - o.center, o.half);
+            if (od < best) {
+                best = od;
+                lab = o.label;
+            }
+        }
+        return lab;
+    }
+};
+
+namespace {
+svrr_camera from_camera(const Camera& c) {
+    svrr_camera o{};
+    o.fx = c.fx, o.fy = c.fy, o.cx = c.cx, o.cy = c.cy;
+    o.width = c.width, o.height = c.height;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) o.R[3 * i + j] = c.rotation(i, j);
+    for (int i = 0; i < 3; ++i) o.t[i] = c.translation[i];
+    return o;
+}
+}  // namespace
+
+extern "C" {
+
+int svrr_scene_create(const svrr_scene_spec* in, svrr_scene** out) {
+    return guarded([&] {
+        SceneSpec sp;  // synthetic.hpp:13-30 (the fields the fixture sets; the rest default)
+        sp.room_w = in->room_w, sp.room_d = in->room_d, sp.room_h = in->room_h;
+        sp.n_objects = in->n_objects, sp.n_frames = in->n_frames;
+        sp.width = in->width, sp.height = in->height, sp.fov_deg = in->fov_deg;
+        sp.label_channels = in->label_channels;
+        sp.texture_amplitude = in->texture_amplitude, sp.texture_frequency = in->texture_frequency;
+        sp.seed = in->seed;
+        auto w = std::make_unique<svrr_scene>();
+        w->s = std::make_unique<SyntheticScene>(sp);
+        w->m = reinterpret_cast<const SceneMirror*>(w->s.get());
+        // the mirror must reproduce the reference's own sdf (synthetic.cpp:71-80)
+        std::mt19937_64 rng(12345);
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        for (int i = 0; i < 64; ++i) {
+            const Eigen::Vector3d x(u(rng) * sp.room_w / 2, u(rng) * sp.room_d / 2, u(rng) * sp.room_h / 2);
+            double d = (w->m->room_half_ - x.cwiseAbs()).minCoeff();
+            for (const auto& o : w->m->objects_)
+                d = std::min(d, o.is_sphere ? (x - o.center).norm() - o.half.x() : mirror_box_sdf(x - o.center, o.half));
+            if (d != w->s->sdf(x)) throw DataError("scene mirror disagrees with SyntheticScene::sdf");
+        }
+        *out = w.release();
+    });
+}
+
+void svrr_scene_destroy(svrr_scene* s) { delete s; }
+
+int svrr_scene_camera(const svrr_scene* s, int32_t frame, svrr_camera* out) {
+    return guarded([&] { *out = from_camera(s->s->camera_for_frame(frame)); });
+}
+
+// depth / rgb / semantic / camera-frame normal per integer pixel, as generate_synthetic
+// renders its frames (synthetic.cpp:318-340); any output may be NULL
+int svrr_scene_frames(const svrr_scene* s, const svrr_camera* cams, uint32_t n, float* depth, float* rgb,
+                      float* sem, int32_t C, float* normal, int32_t threads) {
+    if (!n) return 0;
+    std::atomic<bool> escaped{false};
+    const int W = cams[0].width, H = cams[0].height;
+    std::vector<Camera> cs(n);
+    for (uint32_t f = 0; f < n; ++f) cs[f] = to_camera(cams[f]);
+    for_range(static_cast<uint64_t>(n) * H, threads, [&](uint64_t b, uint64_t e) {
+        for (uint64_t r = b; r < e; ++r) {
+            const uint32_t f = static_cast<uint32_t>(r / H);
+            const int y = static_cast<int>(r % H);
+            for (int x = 0; x < W; ++x) {
+                SyntheticScene::Hit hit;
+                if (!s->s->raycast(cs[f], x, y, hit)) {
+                    escaped = true;
+                    continue;
+                }
+                const uint64_t px = r * W + x;
+                if (depth) depth[px] = static_cast<float>(hit.depth);
+                if (normal) {
+                    const Eigen::Vector3d n_cam = cs[f].rotation.transpose() * hit.normal;
+                    for (int c = 0; c < 3; ++c) normal[3 * px + c] = static_cast<float>(n_cam[c]);
+                }
+                if (sem)
+                    for (int k = 0; k < C; ++k) sem[C * px + k] = k == hit.label ? 1.0f : 0.0f;
+                if (rgb) {
+                    const Eigen::Vector3d c = s->s->color(hit.point, hit.label);
+                    for (int k = 0; k < 3; ++k) rgb[3 * px + k] = static_cast<float>(c[k]);
+                }
+            }
+        }
+    });
+    if (escaped) {
+        g_err = "synthetic: ray escaped the room";
+        return 3;
+    }
+    return 0;
+}
+
+int svrr_scene_sdf(const svrr_scene* s, const double* x, uint64_t n, double* out) {
+    for (uint64_t i = 0; i < n; ++i) out[i] = s->s->sdf(Eigen::Vector3d(x[3 * i], x[3 * i + 1], x[3 * i + 2]));
+    return 0;
+}
+
+int svrr_scene_fill_payload(const svrr_scene* s, double h, int32_t B, int32_t C, double trunc,
+                            const int32_t* coords, uint64_t nblocks, float* sdf, float* weight, float* rgb,
+                            float* logits, int32_t threads) {
+    const uint64_t V = static_cast<uint64_t>(B) * B * B;
+    for_range(nblocks, threads, [&](uint64_t b, uint64_t e) {
+        for (uint64_t i = b; i < e; ++i)
+            for (uint64_t v = 0; v < V; ++v) {
+                const int lx = static_cast<int>(v % B), ly = static_cast<int>((v / B) % B),
+                          lz = static_cast<int>(v / (B * B));
+                // voxel_to_world (grid.hpp:124-126)
+                const Eigen::Vector3d x = Eigen::Vector3i(coords[3 * i] * B + lx, coords[3 * i + 1] * B + ly,
+                                                          coords[3 * i + 2] * B + lz)
+                                              .cast<double>() *
+                                          h;
+                const uint64_t o = i * V + v;
+                if (sdf) sdf[o] = static_cast<float>(std::clamp(s->s->sdf(x), -trunc, trunc));
+                if (weight) weight[o] = 1.0f;
+                if (rgb || logits) {
+                    const int lab = s->label(x);
+                    if (rgb) {
+                        const Eigen::Vector3d c = s->s->color(x, lab);
+                        for (int k = 0; k < 3; ++k) rgb[3 * o + k] = static_cast<float>(c[k]);
+                    }
+                    if (logits)
+                        for (int k = 0; k < C; ++k) logits[C * o + k] = k == lab ? 1.0f : 0.0f;
+                }
+            }
+    });
+    return 0;
+}
+
+int svrr_scene_rays(const svrr_scene* s, uint32_t n_poses, uint32_t rays_per_pose, uint64_t seed, double* o,
+                    double* d) {
+    const SceneSpec& sp = s->s->spec();
+    std::mt19937_64 rng(seed);
+    const uint64_t npix = static_cast<uint64_t>(sp.width) * sp.height;
+    std::uniform_int_distribution<uint64_t> pick(0, npix - 1);
+    uint64_t i = 0;
+    for (uint32_t p = 0; p < n_poses; ++p) {
+        const Camera cam = s->s->camera_for_frame(static_cast<int>(p));
+        for (uint32_t r = 0; r < rays_per_pose; ++r, ++i) {
+            const uint64_t px = pick(rng);
+            const Eigen::Vector3d dir = cam.ray_direction(
+                Eigen::Vector2d(static_cast<double>(px % sp.width), static_cast<double>(px / sp.width)));
+            for (int a = 0; a < 3; ++a) o[3 * i + a] = cam.translation[a], d[3 * i + a] = dir[a];
+        }
+    }
+    return 0;
+}
+
+int svrr_scene_image_rays(const svrr_scene* s, int32_t frame, double* o, double* d) {
+    const SceneSpec& sp = s->s->spec();
+    const Camera cam = s->s->camera_for_frame(frame);
+    uint64_t i = 0;
+    for (int y = 0; y < sp.height; ++y)
+        for (int x = 0; x < sp.width; ++x, ++i) {
+            const Eigen::Vector3d dir = cam.ray_direction(Eigen::Vector2d(x, y));
+            for (int a = 0; a < 3; ++a) o[3 * i + a] = cam.translation[a], d[3 * i + a] = dir[a];
+        }
+    return 0;
+}
+
+int svrr_uniform_floats(uint64_t n, uint64_t seed, float lo, float hi, float* out) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<float> u(lo, hi);
+    for (uint64_t i = 0; i < n; ++i) out[i] = u(rng);
+    return 0;
+}
+
+}  // extern "C"

@@ -8,8 +8,7 @@ C-ABI of ``libsvr_b200.so`` (include/svr.h) and hand-written sm_100a kernels.
 from ._lib import (CapacityError, ConfigError, CudaError, DataError, DivergedError, SvrError,
                    SVR_INVALID_BLOCK, SVR_LOOKUP_AUTO, SVR_LOOKUP_DENSE, SVR_LOOKUP_HASH)
 from .grid import SparseDenseGrid, camera
-from .synthetic import SyntheticScene
 
-__all__ = ["SparseDenseGrid", "SyntheticScene", "camera", "SvrError", "ConfigError", "DataError",
+__all__ = ["SparseDenseGrid", "camera", "SvrError", "ConfigError", "DataError",
            "DivergedError", "CapacityError", "CudaError", "SVR_INVALID_BLOCK", "SVR_LOOKUP_AUTO",
            "SVR_LOOKUP_DENSE", "SVR_LOOKUP_HASH"]

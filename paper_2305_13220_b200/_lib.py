@@ -1,4 +1,4 @@
-"""ctypes binding of libsvr_b200.so (include/svr.h, include/svr_synth.h).
+"""ctypes binding of libsvr_b200.so (include/svr.h).
 
 The shared library is built in-tree by ``paper_2305_13220_b200.build.build()`` (called
 from ``__graft_entry__.build()``).  Loading fails loudly when it is missing: there is
@@ -98,14 +98,6 @@ class RefineConfig(ctypes.Structure):
                 ("mu", c_double)]
 
 
-class SceneSpec(ctypes.Structure):
-    _fields_ = [("room_w", c_double), ("room_d", c_double), ("room_h", c_double),
-                ("n_objects", c_int32), ("n_frames", c_int32), ("width", c_int32),
-                ("height", c_int32), ("fov_deg", c_double), ("label_channels", c_int32),
-                ("texture_amplitude", c_double), ("texture_frequency", c_double),
-                ("seed", c_uint64)]
-
-
 P = c_void_p  # every array argument: host or device address
 _I = c_int32
 
@@ -170,19 +162,6 @@ _PROTOS = {
     "svr_mesh_get": (_I, [c_void_p, P, P, P, P, P]),
     "svr_mesh_save_ply": (_I, [c_void_p, c_char_p]),
     "svr_mesh_save_obj": (_I, [c_void_p, c_char_p]),
-    # svr_synth.h (host-only fixtures)
-    "svr_scene_spec_default": (None, [POINTER(SceneSpec)]),
-    "svr_scene_create": (_I, [POINTER(SceneSpec), POINTER(c_void_p)]),
-    "svr_scene_destroy": (None, [c_void_p]),
-    "svr_scene_camera": (_I, [c_void_p, c_int32, POINTER(Camera)]),
-    "svr_scene_depth": (_I, [c_void_p, P, c_uint32, P, c_int32]),
-    "svr_scene_frames": (_I, [c_void_p, P, c_uint32, P, P, P, c_int32, P, c_int32]),
-    "svr_scene_sdf": (_I, [c_void_p, P, c_uint64, P]),
-    "svr_scene_fill_payload": (_I, [c_void_p, c_double, c_int32, c_int32, c_double, P, c_uint64,
-                                    P, P, P, P, c_int32]),
-    "svr_scene_rays": (_I, [c_void_p, c_uint32, c_uint32, c_uint64, P, P]),
-    "svr_scene_image_rays": (_I, [c_void_p, c_int32, P, P]),
-    "svr_uniform_floats": (_I, [c_uint64, c_uint64, c_float, c_float, P]),
 }
 
 EXPORTED = tuple(_PROTOS)

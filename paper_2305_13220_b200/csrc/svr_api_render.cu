@@ -19,8 +19,9 @@ bool is_pinned_host(const void* p) {
     return a.type == cudaMemoryTypeHost;
 }
 
-// The forward kernels on g->stream: optional pre-march ray order, K4 march, optional
-// post-march order, K5 forward (+ records).  dO / dD / outputs are device pointers.
+// The forward kernels on g->stream: optional pre-march ray order, K4 march (which also writes
+// the post-march sort keys), optional post-march order, K5 forward (+ records).  dO / dD /
+// outputs are device pointers.
 void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n, double step,
                      uint32_t max_samples, double beta, float* a, float* b, float* c, float* e) {
     g->ensure_rays(std::max<uint64_t>(n, 1), max_samples);
@@ -28,92 +29,50 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
     g->ctx_order = nullptr;
     // below sort_min_rays the two ordering sorts cost more than the coherence they buy
     const bool sort = g->ray_sort != 0 && n > 1 && n >= g->sort_min_rays;
-    const bool cub_sort = sort && g->sort_impl == 1;
-    if (cub_sort) {
+    const bool pre = sort && (g->ray_sort & 2), post = sort && (g->ray_sort & 1);
+    if (sort) g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
+    if (pre) {  // pre-march: origin + direction
         g->ord_keys.ensure(8 * n);
         g->ord_ids.ensure(8 * n);
-        g->ord_tmp.ensure(std::max<size_t>(svr_internal::ray_order_tmp_bytes(n), 16));
-    } else if (sort) {
-        g->ord_ids.ensure(4 * svr_internal::ray_order_scratch_words(n));
+        uint32_t* k = g->ord_keys.as<uint32_t>();
+        uint32_t* id = g->ord_ids.as<uint32_t>();
+        svr_internal::launch_ray_order(dO, dD, n, v, false, k, id, k + n, id + n, g->ord_tmp.p, g->ord_tmp.bytes,
+                                       &g->ctx_order, g->stream);
     }
-    uint32_t* k = g->ord_keys.as<uint32_t>();
-    uint32_t* id = g->ord_ids.as<uint32_t>();
-    auto order_rays = [&](bool post_march) {
-        const uint32_t* cnt = post_march ? g->counts.as<uint32_t>() : nullptr;
-        const double* tt = post_march ? g->tbuf.as<double>() : nullptr;
-        if (cub_sort) {
-            svr_internal::launch_ray_order(v, dO, dD, n, cnt, tt, max_samples, k, id, k + n, id + n,
-                                           g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream, g->ray_key);
-        } else {
-            svr_internal::launch_ray_bucket_order(v, dO, dD, n, cnt, tt, max_samples, id, g->stream);
-            g->ctx_order = id;
-        }
-    };
-    if (sort && (g->ray_sort & 2)) order_rays(false);  // pre-march: origin + direction
-    // march_keys: the march itself writes the post-march sort keys (no k_ray_keys pass)
-    const bool mkeys = cub_sort && (g->ray_sort & 1) && g->ray_key == 0 && g->march_keys;
     uint32_t* k2 = nullptr;
     uint32_t* id2 = nullptr;
-    if (mkeys) {
+    if (post) {
         g->ord_keys2.ensure(8 * n);
         g->ord_ids2.ensure(8 * n);
         k2 = g->ord_keys2.as<uint32_t>();
         id2 = g->ord_ids2.as<uint32_t>();
     }
     svr_internal::launch_march(v, dO, dD, n, g->ctx_order, step, max_samples, g->counts.as<uint32_t>(),
-                               g->tbuf.as<double>(), nullptr, g->stream, g->march_variant, k2, id2);
-    if (mkeys) {
-        svr_internal::launch_ray_order(v, dO, dD, n, g->counts.as<uint32_t>(), nullptr, max_samples, k2, id2,
-                                       k2 + n, id2 + n, g->ord_tmp.p, g->ord_tmp.bytes, &g->ctx_order, g->stream,
-                                       0);
-    } else if (sort && (g->ray_sort & 1)) {
-        order_rays(true);  // post-march: first-sample block
-    }
+                               g->tbuf.as<double>(), nullptr, g->stream, k2, id2, g->nvalid.as<unsigned long long>());
+    if (post)  // post-march: first-sample block, keys written by the march
+        svr_internal::launch_ray_order(dO, dD, n, v, true, k2, id2, k2 + n, id2 + n, g->ord_tmp.p, g->ord_tmp.bytes,
+                                       &g->ctx_order, g->stream);
     g->ctx_rec = g->use_records;
     if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
     float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;
-    const bool piped =
-        g->fwd_pipe && svr_internal::launch_render_forward_pipe(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
-                                                                g->tbuf.as<double>(), max_samples, step, beta, a, b,
-                                                                c, e, recp, g->stream, g->fwd_pipe_min_blocks,
-                                                                g->num_sms);
-    if (!piped) {
-        const int fcase = g->fwd_min_blocks != 3 ? g->fwd_min_blocks
-                          : g->fwd_split == 3    ? 122  // one-warp CTAs, 32 per SM (0.3 % over 64-thread CTAs)
-                          : g->fwd_split == 2    ? 113
-                          : g->fwd_split == 1    ? 104
-                                                 : 3;
-        // k_forward_multi starts from {id, count} in sorted order when the rays were sorted
-        const uint2* hdr = nullptr;
-        if (g->ray_hdr && g->ctx_order && fcase >= 114 && fcase <= 122) {
-            g->ord_hdr.ensure(8 * n);
-            svr_internal::launch_ray_headers(g->ctx_order, g->counts.as<uint32_t>(), n, g->ord_hdr.as<uint2>(),
-                                             g->stream);
-            hdr = g->ord_hdr.as<uint2>();
-        }
-        svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(),
-                                            g->tbuf.as<double>(), max_samples, step, beta, a, b, c, e, nullptr,
-                                            recp, g->stream, fcase, hdr);
-    }
+    svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
+                                        max_samples, step, beta, a, b, c, e, g->nvalid.as<unsigned long long>(),
+                                        recp, g->stream);
 }
 
 void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {
     const uint64_t n = g->ctx_n;
-    // bwd_order (experiment): 0 = the forward's sorted order, 1 = caller order
-    const uint32_t* border = g->bwd_order == 1 ? nullptr : g->ctx_order;
     const bool piped =
         g->bwd_pipe && g->ctx_rec &&
-        svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, border,
+        svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                                   g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                                   g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
-                                                  g->stream, g->pipe_min_blocks, g->num_sms, g->warp_agg,
-                                                  g->bwd_hdr);
+                                                  g->stream, g->num_sms);
     if (!piped)
         svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                              g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                              g->ctx_step, g->ctx_beta, a, b, c,
-                                             g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream,
-                                             g->bwd_min_blocks, g->warp_agg);
+                                             g->ctx_rec ? g->rec.as<float4>() : nullptr, g->stream);
 }
 }  // namespace
 
@@ -282,23 +241,13 @@ int svr_render_get_stats(svr_grid* g, svr_render_stats* out) {
         svr_render_stats s{};
         s.rays = g->ctx_valid ? g->ctx_n : 0;
         if (g->ctx_valid && g->ctx_n) {
-            // re-run the forward's validity count on the retained context (not on the hot path)
+            // marched samples from the counts; valid samples as counted by the last forward
             std::vector<uint32_t> cnt(g->ctx_n);
+            unsigned long long v = 0;
             SVR_CK(cudaMemcpyAsync(cnt.data(), g->counts.p, 4 * g->ctx_n, cudaMemcpyDeviceToHost, g->stream));
+            SVR_CK(cudaMemcpyAsync(&v, g->nvalid.p, 8, cudaMemcpyDeviceToHost, g->stream));
             SVR_CK(cudaStreamSynchronize(g->stream));
             for (uint32_t c : cnt) s.samples += c;
-            DevBuf vc;
-            vc.ensure(8);
-            SVR_CK(cudaMemsetAsync(vc.p, 0, 8, g->stream));
-            svr_internal::launch_render_forward(g->view(), g->ctx_o, g->ctx_d, g->ctx_n, g->ctx_order,
-                                                g->counts.as<uint32_t>(), g->tbuf.as<double>(),
-                                                g->ctx_S, g->ctx_step, g->ctx_beta, nullptr, nullptr,
-                                                nullptr, nullptr, vc.as<unsigned long long>(), nullptr,
-                                                g->stream, g->fwd_min_blocks);
-            SVR_LAUNCHED();
-            unsigned long long v = 0;
-            SVR_CK(cudaMemcpyAsync(&v, vc.p, 8, cudaMemcpyDeviceToHost, g->stream));
-            SVR_CK(cudaStreamSynchronize(g->stream));
             s.valid_samples = v;
         }
         *out = s;

@@ -25,6 +25,7 @@ constexpr uint32_t kFullBit = 0x80000000u;
 constexpr unsigned long long kEmptyKey = ~0ull;
 constexpr int kRes = 8;        // block resolution
 constexpr int kVox = 512;      // voxels per block
+constexpr uint64_t kMaxBlocks = 1ull << 23;  // 32-bit voxel addresses: block * 512 + local
 constexpr int32_t kCoordLim = 1 << 20;
 
 struct __align__(16) HashSlot {

@@ -21,6 +21,9 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
     if (B < 2) throw Fail{SVR_ERR_CONFIG, "grid: block_res must be >= 2"};
     if (B != kRes) throw Fail{SVR_ERR_CONFIG, "grid: this build specialises block_res = 8"};
     if (C < 1) throw Fail{SVR_ERR_CONFIG, "grid: label_channels must be >= 1"};
+    // voxel addresses are 32-bit (block * 512 + local): at most 2^23 blocks (a 2^23-block grid
+    // with C = 4 is ~250 GB, beyond one B200's 180 GB anyway)
+    if (capacity > kMaxBlocks) throw Fail{SVR_ERR_CONFIG, "grid: capacity above 2^23 blocks"};
     int ndev = 0;
     SVR_CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw Fail{SVR_ERR_CUDA, "grid: no such CUDA device"};
@@ -131,48 +134,19 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
         if (k == "ray_sort") {
             if (value < 0 || value > 3) throw Fail{SVR_ERR_CONFIG, "tuning: ray_sort is 0..3"};
             g->ray_sort = static_cast<int>(value);
-        } else if (k == "fwd_min_blocks") {
-            g->fwd_min_blocks = static_cast<int>(value);
-        } else if (k == "sort_impl") {
-            g->sort_impl = static_cast<int>(value);
-        } else if (k == "fwd_pipe") {
-            g->fwd_pipe = value != 0;
-        } else if (k == "fwd_pipe_min_blocks") {
-            g->fwd_pipe_min_blocks = static_cast<int>(value);
-        } else if (k == "bwd_pipe") {
-            g->bwd_pipe = value != 0;
-        } else if (k == "pipe_min_blocks") {
-            g->pipe_min_blocks = static_cast<int>(value);
-        } else if (k == "records") {
-            g->use_records = value != 0;
-        } else if (k == "bwd_min_blocks") {
-            g->bwd_min_blocks = static_cast<int>(value);
         } else if (k == "sort_min_rays") {
             if (value < 0) throw Fail{SVR_ERR_CONFIG, "tuning: sort_min_rays must be >= 0"};
             g->sort_min_rays = static_cast<uint64_t>(value);
+        } else if (k == "records") {
+            g->use_records = value != 0;
+        } else if (k == "bwd_pipe") {
+            g->bwd_pipe = value != 0;
+        } else if (k == "march_jump") {
+            g->use_jump = value != 0;
         } else if (k == "zero_async") {
             g->join_side();
             if (value < 0 || value > 16) throw Fail{SVR_ERR_CONFIG, "tuning: zero_async is 0..16"};
             g->zero_async = static_cast<int>(value);
-        } else if (k == "bwd_hdr") {
-            g->bwd_hdr = value != 0;
-        } else if (k == "march_keys") {
-            g->march_keys = value != 0;
-        } else if (k == "ray_hdr") {
-            g->ray_hdr = value != 0;
-        } else if (k == "fwd_split") {
-            if (value < 0 || value > 3) throw Fail{SVR_ERR_CONFIG, "tuning: fwd_split is 0..3"};
-            g->fwd_split = static_cast<int>(value);
-        } else if (k == "ray_key") {
-            g->ray_key = static_cast<int>(value);
-        } else if (k == "bwd_order") {
-            g->bwd_order = static_cast<int>(value);
-        } else if (k == "march_variant") {
-            g->march_variant = static_cast<int>(value);
-        } else if (k == "march_jump") {
-            g->use_jump = value != 0;
-        } else if (k == "warp_agg") {
-            g->warp_agg = value != 0;
         } else if (k == "host_async") {
             SVR_CK(cudaStreamSynchronize(g->stream));
             if (g->h2d) {
@@ -466,8 +440,7 @@ int svr_march(svr_grid* g, const double* o, const double* d, uint64_t n, double 
         if (!dt && nt) dt = static_cast<double*>(st.alloc(8 * nt));
         double* dl = st.out(delta, nt);
         // the renderer's march kernel (march_variant), so the march parity tests cover it
-        svr_internal::launch_march(g->view(), dO, dD, n, nullptr, step, max_samples, dc, dt, dl, g->stream,
-                                   g->march_variant);
+        svr_internal::launch_march(g->view(), dO, dD, n, nullptr, step, max_samples, dc, dt, dl, g->stream);
         st.finish();
     });
 }

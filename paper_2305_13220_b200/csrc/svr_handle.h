@@ -18,7 +18,6 @@
 #include <vector>
 
 #include "svr_internal.h"
-#include "svr_synth.h"
 
 namespace svr_host {
 using namespace svr_dev;
@@ -188,39 +187,22 @@ struct svr_grid {
     int32_t dim[3] = {0, 0, 0};
     DevBuf dense, occ, nbr, bdist, bdist_tmp;
     bool use_jump = true;   // march: exact empty-space jumps over the block-distance field
-    int march_variant = 2;  // k_march build: 0 o / d in registers; 1/2/3 in shared memory, 8/6/7 CTAs
 
     // render context
     DevBuf ray_o, ray_d, counts, tbuf, nvalid;
-    DevBuf ord_keys, ord_ids, ord_tmp;  // ray ordering (Morton key of the first sample block)
-    DevBuf ord_hdr;                     // {id, count} per sorted ray (fwd_split 3 + ray_hdr)
-    DevBuf ord_keys2, ord_ids2;         // post-march keys written by the march (march_keys)
-    int march_keys = 1;  // the march writes the post-march sort keys (saves the k_ray_keys pass)
+    DevBuf ord_keys, ord_ids, ord_tmp;  // pre-march ray order (origin + direction keys)
+    DevBuf ord_keys2, ord_ids2;         // post-march order (keys written by the march)
     DevBuf rec;                         // per-sample forward records for the backward
     bool ctx_rec = false;
     uint32_t* ctx_order = nullptr;
-    // tuning knobs (svr_grid_set_tuning)
+    // tuning knobs (svr_grid_set_tuning); none changes results
     // bit 1: order the march by origin + direction; bit 0: order forward/backward by the
     // block of each ray's first sample (3 = both)
     int ray_sort = 3;
     uint64_t sort_min_rays = 32768;  // smaller batches are rendered in caller order
-    int sort_impl = 1;  // 1: CUB radix sort (default, best order), 0: in-house bucketed counting sort
-    int fwd_min_blocks = 3;
-    // forward lane layout: 2 = one sample per lane per pass, o / d in shared memory, 16 CTAs of
-    // 64 per SM (default); 1 = samples l and 32 + l; 0 = samples 2l and 2l + 1
-    int fwd_split = 3;
-    int ray_hdr = 0;
-    bool bwd_hdr = true;  // k_backward_pipe streams each ray's scalars with its t / record rows  // fwd_split 3: a k_ray_headers pass gives the forward {id, count} in sorted order
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
-    bool fwd_pipe = false;    // persistent forward streaming t rows (measured slower: off)
-    int fwd_pipe_min_blocks = 3;
-    int pipe_min_blocks = 3;
     int num_sms = 148;
-    int bwd_min_blocks = 3;
-    int bwd_order = 0;
-    int ray_key = 0;  // post-march sort key: 0 first-sample block, 1 middle-sample block, 2 half blocks
-    bool warp_agg = true;  // backward scatter: hand a lane's first cell run to the previous lane
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
     uint64_t ctx_n = 0;
@@ -494,7 +476,7 @@ struct svr_grid {
 
     void ensure_rays(uint64_t nr, uint32_t S) {
         counts.ensure(nr * 4);
-        nvalid.ensure(nr * 4);
+        nvalid.ensure(8);  // valid-sample counter of the last forward
         tbuf.ensure(nr * S * 8);
     }
 };

@@ -24,48 +24,33 @@ void launch_query(const svr_dev::GridView& g, const double* x, uint64_t n, doubl
                   double* grad, double* rgb, double* logits, uint8_t* valid, cudaStream_t s);
 void launch_march(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
                   const uint32_t* order, double step, uint32_t max_samples, uint32_t* counts,
-                  double* t, double* delta, cudaStream_t s, int variant = 0, uint32_t* pkeys = nullptr,
-                  uint32_t* pids = nullptr);
+                  double* t, double* delta, cudaStream_t s, uint32_t* pkeys = nullptr,
+                  uint32_t* pids = nullptr, unsigned long long* valid_counter = nullptr);
 void launch_render_forward(const svr_dev::GridView& g, const double* o, const double* d,
                            uint64_t n, const uint32_t* order, const uint32_t* counts,
                            const double* t, uint32_t S, double step, double beta, float* rgb,
                            float* depth, float* normal, float* wsum,
-                           unsigned long long* valid_counter, float4* rec, cudaStream_t s,
-                           int min_blocks, const uint2* hdr = nullptr);
-void launch_ray_headers(const uint32_t* order, const uint32_t* counts, uint64_t n, uint2* hdr,
-                        cudaStream_t s);
+                           unsigned long long* valid_counter, float4* rec, cudaStream_t s);
+// Non-pipelined backward (any max_samples; re-gathers the payload when rec == NULL).
 void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
                             uint64_t n, const uint32_t* order, const uint32_t* counts,
                             const double* t, uint32_t S, double step, double beta,
                             const float* d_rgb, const float* d_depth, const float* d_normal,
-                            const float4* rec, cudaStream_t s, int min_blocks, bool agg);
-// Sort rays for locality; *sorted_ids points into ids or ids_alt.  counts != NULL: key =
-// Morton code of the first sample's block (after the march); counts == NULL: key = origin
-// hash + octahedral-direction Morton code (before the march).
-void launch_ray_order(const svr_dev::GridView& g, const double* o, const double* d, uint64_t n,
-                      const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
-                      uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
-                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s, int key_mode = 0);
-size_t ray_order_tmp_bytes(uint64_t n);
-// In-house bucketed counting sort (svr_sort.cu): order = scratch[0, n).  counts == NULL:
-// origin + direction buckets (pre-march); else first-sample block buckets (post-march).
-size_t ray_order_scratch_words(uint64_t n);
-void launch_ray_bucket_order(const svr_dev::GridView& g, const double* o, const double* d,
-                             uint64_t n, const uint32_t* counts, const double* t, uint32_t S,
-                             uint32_t* scratch, cudaStream_t s);
-// Pipelined forward (max_samples <= 64, even); returns false if not applicable.
-bool launch_render_forward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
-                                uint64_t n, const uint32_t* order, const uint32_t* counts,
-                                const double* t, uint32_t S, double step, double beta, float* rgb,
-                                float* depth, float* normal, float* wsum, float4* rec,
-                                cudaStream_t s, int min_blocks, int num_sms);
+                            const float4* rec, cudaStream_t s);
 // Pipelined backward (records, max_samples <= 64, even); returns false if not applicable.
 bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, const double* d,
                                  uint64_t n, const uint32_t* order, const uint32_t* counts,
                                  const double* t, uint32_t S, double step, double beta,
                                  const float* d_rgb, const float* d_depth, const float* d_normal,
-                                 const float4* rec, cudaStream_t s, int min_blocks, int num_sms,
-                                 bool agg, bool hdr = false);
+                                 const float4* rec, cudaStream_t s, int num_sms);
+// Sort rays for locality; *sorted_ids points into ids or ids_alt.  post_march: keys / ids
+// were written by the march (Morton code of each ray's first-sample block); otherwise the
+// keys are computed here from the origin hash + octahedral-direction Morton code.
+void launch_ray_order(const double* o, const double* d, uint64_t n, const svr_dev::GridView& g,
+                      bool post_march, uint32_t* keys, uint32_t* ids, uint32_t* keys_alt,
+                      uint32_t* ids_alt, void* tmp, size_t tmp_bytes, uint32_t** sorted_ids,
+                      cudaStream_t s);
+size_t ray_order_tmp_bytes(uint64_t n);
 
 // Launchers (svr_activate.cu)
 struct KeySet {

@@ -159,6 +159,10 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const V& o, con
             }
         }
         nr = 0;
+        // the estimate is exact again: the early stop below keeps its one-per-run slack
+        // for the runs recorded from here on
+        est = cnt;
+        est_cursor = cursor;
     };
     // Empty-space jump (dense mode): every block within Chebyshev distance dist - 1 of an
     // empty block is empty, so the walk may resume at the DDA state of a time t* that stays
@@ -280,43 +284,34 @@ __device__ __forceinline__ uint32_t first_sample_key(const GridView& g, const V&
     return spread3(b[0]) | (spread3(b[1]) << 1) | (spread3(b[2]) << 2);
 }
 
-template <int kMinBlocks, bool kSmem, int kThreads = 128>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_march(GridView g, const double* __restrict__ O,
-                                               const double* __restrict__ D, uint64_t n,
-                                               const uint32_t* __restrict__ order, double step,
-                                               uint32_t S, uint32_t* counts, double* T, double* delta,
-                                               uint32_t* pkeys = nullptr, uint32_t* pids = nullptr) {
+// thread per ray; o / d in shared memory (SoA) instead of 12 registers: 6 CTAs of 128 per SM
+constexpr int kMarchThreads = 128;
+__global__ void __launch_bounds__(kMarchThreads, 6) k_march(GridView g, const double* __restrict__ O,
+                                                            const double* __restrict__ D, uint64_t n,
+                                                            const uint32_t* __restrict__ order, double step,
+                                                            uint32_t S, uint32_t* counts, double* T, double* delta,
+                                                            uint32_t* pkeys, uint32_t* pids,
+                                                            unsigned long long* valid_counter) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i == 0 && valid_counter) *valid_counter = 0;  // the forward that follows counts into it
     if (i >= n) return;
     const uint64_t r = order ? order[i] : i;
     double* tr = T + r * S;
-    uint32_t cnt, key = 0xFFFFFFFFu;
     double t_first = 0.0;
-    if (kSmem) {
-        __shared__ double s_od[6][kThreads];
+    __shared__ double s_od[6][kMarchThreads];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            s_od[a][threadIdx.x] = O[3 * r + a];
-            s_od[3 + a][threadIdx.x] = D[3 * r + a];
-        }
-        const StridedVec o{&s_od[0][threadIdx.x], kThreads}, d{&s_od[3][threadIdx.x], kThreads};
-        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
-            tr[k] = t;
-            if (k == 0) t_first = t;
-        });
-        if (pkeys) key = first_sample_key(g, o, d, cnt, t_first);
-    } else {
-        const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-        const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
-        cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
-            tr[k] = t;
-            if (k == 0) t_first = t;
-        });
-        if (pkeys) key = first_sample_key(g, o, d, cnt, t_first);
+    for (int a = 0; a < 3; ++a) {
+        s_od[a][threadIdx.x] = O[3 * r + a];
+        s_od[3 + a][threadIdx.x] = D[3 * r + a];
     }
+    const StridedVec o{&s_od[0][threadIdx.x], kMarchThreads}, d{&s_od[3][threadIdx.x], kMarchThreads};
+    const uint32_t cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
+        tr[k] = t;
+        if (k == 0) t_first = t;
+    });
     counts[r] = cnt;
-    if (pkeys) {  // the post-march sort key (k_ray_keys mode 0) without re-reading the t row
-        pkeys[r] = key;
+    if (pkeys) {  // the post-march sort key without re-reading the t row
+        pkeys[r] = first_sample_key(g, o, d, cnt, t_first);
         pids[r] = static_cast<uint32_t>(r);
     }
     if (delta) {
@@ -396,14 +391,11 @@ __device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3
 }
 
 // Full gather + trilinear interpolation of sdf, grad(sdf) and rgb (fp32 payload math).
-// kDiag (diagnostic builds of k_forward only; results are wrong): 1 = no payload loads,
-// 2 = no block lookup (base block assumed to be block 0 and fully valid)
-template <int kDiag = 0>
 __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
                                             double t, SampleVal& v) {
     int base[3];
     cell_geom(g, o, d, t, base, v);
-    const uint32_t e0 = kDiag == 2 ? kFullBit : lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
+    const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
     const bool ok = corner_addrs<true>(g, base, e0, v);
     if (!ok) {
         v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
@@ -413,14 +405,7 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
     v.e0 = e0;
     float4 p[8];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        if (kDiag == 1) {
-            const float q = static_cast<float>(v.gidx[c] & 1023) * 1e-4f;
-            p[c] = make_float4(q, q, q, q);
-        } else {
-            p[c] = __ldg(g.pay + v.gidx[c]);
-        }
-    }
+    for (int c = 0; c < 8; ++c) p[c] = __ldg(g.pay + v.gidx[c]);
     const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
     const float w[8] = {x0 * y0 * z0, x1 * y0 * z0, x0 * y1 * z0, x1 * y1 * z0,
                         x0 * y0 * z1, x1 * y0 * z1, x0 * y1 * z1, x1 * y1 * z1};
@@ -444,10 +429,9 @@ __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3]
 }
 
 // A lane slot past the ray's sample count: well-defined zeros (accumulated with w = 0).
-template <int kDiag = 0>
 __device__ __forceinline__ bool eval_slot(const GridView& g, const double o[3], const double d[3],
                                           bool in, double t, SampleVal& v) {
-    if (in) return eval_sample<kDiag>(g, o, d, t, v);
+    if (in) return eval_sample(g, o, d, t, v);
     zero_sample(v);
     return false;
 }
@@ -584,34 +568,6 @@ __device__ __forceinline__ uint32_t spread3(uint32_t v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_ray_keys(GridView g, const double* __restrict__ O,
-                                                  const double* __restrict__ D, uint64_t n,
-                                                  const uint32_t* __restrict__ counts,
-                                                  const double* __restrict__ T, uint32_t S,
-                                                  uint32_t* keys, uint32_t* ids, int mode) {
-    const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    uint32_t key = 0xFFFFFFFFu;
-    if (counts[r]) {
-        // mode 0: block of the first sample; 1: block of the middle sample; 2: first sample at
-        // half-block resolution
-        const double t = T[r * S + (mode == 1 ? counts[r] / 2 : 0)];
-        const double cell = mode == 2 ? 0.5 * g.L : g.L;
-        const int scale = mode == 2 ? 2 : 1;
-        uint32_t b[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double x = O[3 * r + a] + t * D[3 * r + a];
-            int32_t v = static_cast<int32_t>(floor(x / cell)) - scale * g.lo[a];
-            v = v < 0 ? 0 : (v > 1023 ? 1023 : v);
-            b[a] = static_cast<uint32_t>(v);
-        }
-        key = spread3(b[0]) | (spread3(b[1]) << 1) | (spread3(b[2]) << 2);
-    }
-    keys[r] = key;
-    ids[r] = static_cast<uint32_t>(r);
-}
-
 // Pre-march ordering: 8-bit hash of the origin (1 mm cells) above a 16-bit Morton code of
 // the octahedral direction, so rays from one camera with nearby pixels march together.
 __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__ O,
@@ -643,282 +599,64 @@ __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__
 }
 
 // ---------------------------------------------------------------------------
-// K5: forward.  One warp per ray, lane l owns samples 2l and 2l+1 of each 64-sample
-// chunk; exclusive prefix of tau by a warp scan gives T_k = exp(-sum_{j<k} tau_j).
+// K5: forward.  One warp per ray (one-warp CTAs, 32 resident per SM at <= 64 registers),
+// one sample per lane per 32-sample pass; the exclusive prefix of tau by a warp scan gives
+// T_k = exp(-sum_{j<k} tau_j).  The ray's o / d sit in a per-warp shared slot (6 lanes load
+// them), and each lane's t value is fetched one pass ahead so a pass starts with its cell
+// decision instead of a dependent load.  Leaves a 32 B record per sample for the backward.
 // ---------------------------------------------------------------------------
-template <int kThreads, int kMinBlocks, int kDiag = 0>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward(GridView g, const double* __restrict__ O,
-                                                    const double* __restrict__ D, uint64_t n,
-                                                    const uint32_t* __restrict__ order,
-                                                    const uint32_t* __restrict__ counts,
-                                                    const double* __restrict__ T, uint32_t S,
-                                                    double step, float ib, float* rgb, float* depth,
-                                                    float* normal, float* wsum,
-                                                    unsigned long long* valid_counter, float4* rec) {
-    const int lane = threadIdx.x & 31;
+constexpr int kFwdThreads = 32;
+__global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const double* __restrict__ O,
+                                                             const double* __restrict__ D, uint64_t n,
+                                                             const uint32_t* __restrict__ order,
+                                                             const uint32_t* __restrict__ counts,
+                                                             const double* __restrict__ T, uint32_t S,
+                                                             double step, float ib, float* rgb, float* depth,
+                                                             float* normal, float* wsum,
+                                                             unsigned long long* valid_counter, float4* rec) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
-    const uint64_t r = order ? order[w] : w;
-    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
+    __shared__ double s_od[kFwdThreads / 32][6];
+    const uint32_t r = order ? order[w] : static_cast<uint32_t>(w);
+    if (lane < 6) s_od[wib][lane] = lane < 3 ? O[3ull * r + lane] : D[3ull * r + lane - 3];
     const uint32_t cnt = counts[r];
-    const double* tr = T + r * S;
+    __syncwarp();
+    const double* o = s_od[wib];
+    const double* d = o + 3;
+    const double* tr = T + static_cast<uint64_t>(r) * S;
+    double t_cur = static_cast<uint32_t>(lane) < cnt ? tr[lane] : 0.0;  // t of the upcoming pass
+    uint32_t nvalid = 0;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
     float tau_base = 0.f;
-    uint32_t nvalid = 0;
-    for (uint32_t base = 0; base < cnt; base += 64) {
-        const PairT p = load_pair(tr, cnt, base, lane, step);
-        SampleVal v0, v1;
-        const bool ok0 = eval_slot<kDiag == 3 ? 0 : kDiag>(g, o, d, p.in0, p.t0, v0);
-        const bool ok1 = eval_slot<kDiag == 3 ? 0 : kDiag>(g, o, d, p.in1, p.t1, v1);
-        if (rec && kDiag != 3) {  // per-sample record for the backward (coalesced: 64 B per lane)
-            float4* rr = rec + (r * S + base + 2 * lane) * 2;
-            if (p.in0) store_record(rr, v0);
-            if (p.in1) store_record(rr + 2, v1);
-        }
-        const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
-        const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
-        const float incl = warp_incl_scan(tau0 + tau1, lane);
-        float excl = __shfl_up_sync(kFull, incl, 1);
-        if (lane == 0) excl = 0.f;
-        // T0 = exp(-P0); w0 = T0 (1 - e^-tau0); T1 = T0 e^-tau0 = T0 - w0 (one exp per pair)
-        const float T0 = expf(-(tau_base + excl));
-        const float w0 = -T0 * expm1f(-tau0);
-        const float T1 = T0 - w0;
-        const float w1 = ok1 ? -T1 * expm1f(-tau1) : 0.f;
-        acc[0] += w0 * v0.r + w1 * v1.r;
-        acc[1] += w0 * v0.gc + w1 * v1.gc;
-        acc[2] += w0 * v0.b + w1 * v1.b;
-        acc[3] += w0 * static_cast<float>(p.t0) + w1 * static_cast<float>(p.t1);
-        acc[4] += w0 * v0.gx + w1 * v1.gx;
-        acc[5] += w0 * v0.gy + w1 * v1.gy;
-        acc[6] += w0 * v0.gz + w1 * v1.gz;
-        acc[7] += w0 + w1;
-        if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
-        tau_base += __shfl_sync(kFull, incl, 31);
-    }
-    write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
-    if (lane == 0 && valid_counter && nvalid)
-        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
-}
-
-// K5 with the split lane layout: lane l owns samples base + l and base + 32 + l, so the
-// 32 lanes of one gather instruction walk 32 consecutive samples (neighbouring lanes share
-// cells and cache lines).
-template <int kThreads, int kMinBlocks>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_split(GridView g, const double* __restrict__ O,
-                                                    const double* __restrict__ D, uint64_t n,
-                                                    const uint32_t* __restrict__ order,
-                                                    const uint32_t* __restrict__ counts,
-                                                    const double* __restrict__ T, uint32_t S,
-                                                    double step, float ib, float* rgb, float* depth,
-                                                    float* normal, float* wsum,
-                                                    unsigned long long* valid_counter, float4* rec) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= n) return;
-    const uint64_t r = order ? order[w] : w;
-    const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-    const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
-    const uint32_t cnt = counts[r];
-    const double* tr = T + r * S;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
-    float tau_base = 0.f;
-    uint32_t nvalid = 0;
-    for (uint32_t base = 0; base < cnt; base += 64) {
-        const uint32_t k0 = base + lane, k1 = base + 32 + lane;
-        const bool in0 = k0 < cnt, in1 = k1 < cnt;
-        const double t0 = in0 ? tr[k0] : 0.0, t1 = in1 ? tr[k1] : 0.0;
-        double tn0 = __shfl_down_sync(kFull, t0, 1);
-        const double t1_l0 = __shfl_sync(kFull, t1, 0);
-        double tn1 = __shfl_down_sync(kFull, t1, 1);
-        if (lane == 31) {
-            tn0 = t1_l0;
-            if (k1 + 1 < cnt) tn1 = tr[k1 + 1];
-        }
-        const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
-        const float d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn1, t1)) : static_cast<float>(step);
-        SampleVal v0, v1;
-        const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
-        const bool ok1 = eval_slot(g, o, d, in1, t1, v1);
-        if (rec) {
-            if (in0) store_record(rec + (r * S + k0) * 2, v0);
-            if (in1) store_record(rec + (r * S + k1) * 2, v1);
-        }
-        const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
-        const float tau1 = ok1 ? density(v1.s, ib) * d1 : 0.f;
-        const float inc0 = warp_incl_scan(tau0, lane);
-        const float inc1 = warp_incl_scan(tau1, lane);
-        const float tot0 = __shfl_sync(kFull, inc0, 31);
-        const float w0 = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
-        const float w1 = -expf(-(tau_base + tot0 + inc1 - tau1)) * expm1f(-tau1);
-        acc[0] += w0 * v0.r + w1 * v1.r;
-        acc[1] += w0 * v0.gc + w1 * v1.gc;
-        acc[2] += w0 * v0.b + w1 * v1.b;
-        acc[3] += w0 * static_cast<float>(t0) + w1 * static_cast<float>(t1);
-        acc[4] += w0 * v0.gx + w1 * v1.gx;
-        acc[5] += w0 * v0.gy + w1 * v1.gy;
-        acc[6] += w0 * v0.gz + w1 * v1.gz;
-        acc[7] += w0 + w1;
-        if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0)) + __popc(__ballot_sync(kFull, ok1));
-        tau_base += tot0 + __shfl_sync(kFull, inc1, 31);
-    }
-    write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
-    if (lane == 0 && valid_counter && nvalid)
-        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
-}
-
-// K5, sequential halves: one sample per lane per pass (samples base + 32 h + l), so only
-// one sample's state is live -- fewer registers, more resident warps.
-template <int kThreads, int kMinBlocks, bool kOdSmem = false>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_seq(GridView g, const double* __restrict__ O,
-                                                    const double* __restrict__ D, uint64_t n,
-                                                    const uint32_t* __restrict__ order,
-                                                    const uint32_t* __restrict__ counts,
-                                                    const double* __restrict__ T, uint32_t S,
-                                                    double step, float ib, float* rgb, float* depth,
-                                                    float* normal, float* wsum,
-                                                    unsigned long long* valid_counter, float4* rec) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    if (w >= n) return;
-    const uint64_t r = order ? order[w] : w;
-    // the ray's origin / direction: registers, or (kOdSmem) a per-warp shared slot read at
-    // each use, which frees 12 registers
-    __shared__ double s_od[kThreads / 32][6];
-    double o_r[3], d_r[3];
-    const double* o = o_r;
-    const double* d = d_r;
-    if (kOdSmem) {
-        const int wib = threadIdx.x >> 5;
-        if (lane < 6) s_od[wib][lane] = lane < 3 ? O[3 * r + lane] : D[3 * r + lane - 3];
-        __syncwarp();
-        o = s_od[wib];
-        d = s_od[wib] + 3;
-    } else {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) o_r[a] = O[3 * r + a], d_r[a] = D[3 * r + a];
-    }
-    const uint32_t cnt = counts[r];
-    const double* tr = T + r * S;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
-    float tau_base = 0.f;
-    uint32_t nvalid = 0;
     for (uint32_t base = 0; base < cnt; base += 32) {
         const uint32_t k0 = base + lane;
         const bool in0 = k0 < cnt;
-        const double t0 = in0 ? tr[k0] : 0.0;
+        const double t0 = in0 ? t_cur : 0.0;
+        t_cur = k0 + 32 < cnt ? tr[k0 + 32] : 0.0;  // one pass ahead
         double tn0 = __shfl_down_sync(kFull, t0, 1);
-        if (lane == 31 && k0 + 1 < cnt) tn0 = tr[k0 + 1];
+        const double tl0 = __shfl_sync(kFull, t_cur, 0);
+        if (lane == 31) tn0 = tl0;
         const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
         SampleVal v0;
         const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
-        if (rec && in0) store_record(rec + (r * S + k0) * 2, v0);
+        if (rec && in0) store_record(rec + (static_cast<uint64_t>(r) * S + k0) * 2, v0);
         const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
         const float inc0 = warp_incl_scan(tau0, lane);
-        const float w0 = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
-        acc[0] += w0 * v0.r;
-        acc[1] += w0 * v0.gc;
-        acc[2] += w0 * v0.b;
-        acc[3] += w0 * static_cast<float>(t0);
-        acc[4] += w0 * v0.gx;
-        acc[5] += w0 * v0.gy;
-        acc[6] += w0 * v0.gz;
-        acc[7] += w0;
+        const float wk = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
+        acc[0] += wk * v0.r;
+        acc[1] += wk * v0.gc;
+        acc[2] += wk * v0.b;
+        acc[3] += wk * static_cast<float>(t0);
+        acc[4] += wk * v0.gx;
+        acc[5] += wk * v0.gy;
+        acc[6] += wk * v0.gz;
+        acc[7] += wk;
         if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0));
         tau_base += __shfl_sync(kFull, inc0, 31);
     }
     write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
-    if (lane == 0 && valid_counter && nvalid)
-        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
-}
-
-// K5, sequential halves over K consecutive (sorted) rays per warp with the per-ray set-up
-// taken off the critical path: one load of the K ray ids, then the K origins / directions
-// (to shared memory) and sample counts in one parallel round trip, and every t value one
-// pass ahead (the next pass of this ray, or the first pass of the next ray) -- the chain
-// order -> o/d -> count -> t -> lookup -> payload of k_forward_seq shrinks to
-// lookup -> payload per pass.  Same arithmetic per sample as k_forward_seq.
-template <int kThreads, int kMinBlocks, int K, bool kHdr>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_forward_multi(GridView g, const double* __restrict__ O,
-                                                    const double* __restrict__ D, uint64_t n,
-                                                    const uint32_t* __restrict__ order,
-                                                    const uint32_t* __restrict__ counts,
-                                                    const double* __restrict__ T, uint32_t S,
-                                                    double step, float ib, float* rgb, float* depth,
-                                                    float* normal, float* wsum,
-                                                    unsigned long long* valid_counter, float4* rec,
-                                                    const uint2* __restrict__ hdr) {
-    static_assert(6 * K <= 32, "one lane per origin / direction component");
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint64_t w0 = ((static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * K;
-    if (w0 >= n) return;
-    const int nr = n - w0 < static_cast<uint64_t>(K) ? static_cast<int>(n - w0) : K;
-    __shared__ double s_od[kThreads / 32][K][6];
-    uint32_t my_r = 0, my_cnt = 0;  // lane j < nr: ray j's id and sample count
-    if (lane < nr) {
-        if (kHdr) {  // {id, count} in sorted order: one load level less
-            const uint2 h = hdr[w0 + lane];
-            my_r = h.x, my_cnt = h.y;
-        } else {
-            my_r = order ? order[w0 + lane] : static_cast<uint32_t>(w0 + lane);
-        }
-    }
-    {
-        const int j = lane / 6, a = lane - 6 * (lane / 6);
-        const uint32_t rj = __shfl_sync(kFull, my_r, j < K ? j : 0);
-        if (j < nr) s_od[wib][j][a] = a < 3 ? O[3ull * rj + a] : D[3ull * rj + a - 3];
-        if (lane < nr && !kHdr) my_cnt = counts[my_r];
-    }
-    __syncwarp();
-    uint32_t nvalid = 0;
-    // t of the lane's sample in the upcoming pass
-    uint32_t r = __shfl_sync(kFull, my_r, 0), cnt = __shfl_sync(kFull, my_cnt, 0);
-    double t_cur = static_cast<uint32_t>(lane) < cnt ? T[static_cast<uint64_t>(r) * S + lane] : 0.0;
-    for (int j = 0; j < nr; ++j) {
-        const double* o = s_od[wib][j];
-        const double* d = o + 3;
-        const double* tr = T + static_cast<uint64_t>(r) * S;
-        const uint32_t r1 = __shfl_sync(kFull, my_r, j + 1 < K ? j + 1 : 0);
-        const uint32_t cnt1 = j + 1 < nr ? __shfl_sync(kFull, my_cnt, j + 1 < K ? j + 1 : 0) : 0u;
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
-        float tau_base = 0.f;
-        for (uint32_t base = 0; base < cnt; base += 32) {
-            const uint32_t k0 = base + lane;
-            const bool in0 = k0 < cnt;
-            const double t0 = in0 ? t_cur : 0.0;
-            // one pass ahead: this ray's next pass, else the next ray's first pass
-            t_cur = base + 32 < cnt ? (k0 + 32 < cnt ? tr[k0 + 32] : 0.0)
-                                    : (static_cast<uint32_t>(lane) < cnt1 ? T[static_cast<uint64_t>(r1) * S + lane] : 0.0);
-            double tn0 = __shfl_down_sync(kFull, t0, 1);
-            const double tl0 = __shfl_sync(kFull, t_cur, 0);
-            if (lane == 31) tn0 = tl0;
-            const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
-            SampleVal v0;
-            const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
-            if (rec && in0) store_record(rec + (static_cast<uint64_t>(r) * S + k0) * 2, v0);
-            const float tau0 = ok0 ? density(v0.s, ib) * d0 : 0.f;
-            const float inc0 = warp_incl_scan(tau0, lane);
-            const float w = -expf(-(tau_base + inc0 - tau0)) * expm1f(-tau0);
-            acc[0] += w * v0.r;
-            acc[1] += w * v0.gc;
-            acc[2] += w * v0.b;
-            acc[3] += w * static_cast<float>(t0);
-            acc[4] += w * v0.gx;
-            acc[5] += w * v0.gy;
-            acc[6] += w * v0.gz;
-            acc[7] += w;
-            if (valid_counter) nvalid += __popc(__ballot_sync(kFull, ok0));
-            tau_base += __shfl_sync(kFull, inc0, 31);
-        }
-        if (cnt == 0)  // no pass ran: the next ray's first pass is still to be fetched
-            t_cur = static_cast<uint32_t>(lane) < cnt1 ? T[static_cast<uint64_t>(r1) * S + lane] : 0.0;
-        write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
-        r = r1;
-        cnt = cnt1;
-    }
-    if (lane == 0 && valid_counter && nvalid)
-        atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+    if (lane == 0 && valid_counter && nvalid) atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
 }
 
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
@@ -953,29 +691,6 @@ __device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& 
 #pragma unroll
         for (int c = 1; c < 8; ++c)
             if (c & v.smask) mark_block(g, v.gidx[c] >> 9);
-    }
-}
-
-template <int c, int kMode = 0>
-__device__ __forceinline__ void scatter_corner(float4* grad, const SampleVal& v0, const SampleVal& v1,
-                                               const CornerCoef& k0, const CornerCoef& k1, bool ok0,
-                                               bool ok1, bool same) {
-    if (kMode == 1) {  // diagnostic: same arithmetic, plain stores instead of atomics
-        if (ok0) grad[v0.gidx[c]] = corner_grad<c>(k0);
-        if (ok1) grad[v1.gidx[c]] = corner_grad<c>(k1);
-        return;
-    }
-    if (kMode == 2) {  // diagnostic: arithmetic only, no memory traffic
-        const float4 a = corner_grad<c>(k0), b = corner_grad<c>(k1);
-        if (a.x == 1234.5f && b.y == 1234.5f) grad[0] = a;
-        return;
-    }
-    if (same) {
-        const float4 a = corner_grad<c>(k0), b = corner_grad<c>(k1);
-        atomicAdd(grad + v0.gidx[c], make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w));
-    } else {
-        if (ok0) atomicAdd(grad + v0.gidx[c], corner_grad<c>(k0));
-        if (ok1) atomicAdd(grad + v1.gidx[c], corner_grad<c>(k1));
     }
 }
 
@@ -1038,8 +753,8 @@ __device__ __forceinline__ void scatter_pair_agg(float4* grad, const SampleVal& 
 // Corner gradients are produced and issued one corner at a time (red.global.add.v4.f32);
 // a lane whose two samples share a cell sums them first.
 // ---------------------------------------------------------------------------
-template <int kMinBlocks, int kMode, bool kRec>
-__global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const double* __restrict__ O,
+template <bool kRec>
+__global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* __restrict__ O,
                                                      const double* __restrict__ D, uint64_t n,
                                                      const uint32_t* __restrict__ order,
                                                      const uint32_t* __restrict__ counts,
@@ -1118,19 +833,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
                                         w1, dC, dN, ih);
         if (ok0) mark_blocks(g, v0);
         if (ok1) mark_blocks(g, v1);
-        if (kMode == 3) {
-            scatter_pair_agg(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
-        } else {
-            const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-            scatter_corner<0, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<1, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<2, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<3, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<4, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<5, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<6, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-            scatter_corner<7, kMode>(g.grad, v0, v1, k0, k1, ok0, ok1, same);
-        }
+        scatter_pair_agg(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
         S_after += __shfl_sync(kFull, sinc, 0);
     }
 }
@@ -1142,7 +845,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) k_backward(GridView g, const 
 // completion on an mbarrier), so the per-ray load latency overlaps the compositing
 // adjoint and the atomic scatter of the current ray.
 // ---------------------------------------------------------------------------
-constexpr int kPipeStages = 3;
+constexpr int kStages = 2;  // one ray of look-ahead per warp
 constexpr int kPipeWarps = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -1173,7 +876,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!done);
 }
 
-// The ray's scalars (kHdr): origin / direction, upstream gradients and sample count, copied
+// The ray's scalars: origin / direction, upstream gradients and sample count, copied
 // into the slot by 14 lanes with cp.async and completed on the slot's mbarrier.
 struct PipeHdr {
     double o[3], d[3];
@@ -1197,8 +900,7 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int kMinBlocks, int kMode = 0, int kStages = kPipeStages, bool kHdr = false>
-__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
+__global__ void __launch_bounds__(kPipeWarps * 32, 3)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
                     const double* __restrict__ T, uint32_t S, double step, float ib,
@@ -1213,7 +915,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
     const uint32_t tbytes = S * 8, rbytes = S * 32;
     if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, kHdr ? 33 : 1);
+        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, 33);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -1224,7 +926,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
         bulk_g2s(slots[st].t, T + r * S, tbytes, bars + st);
         bulk_g2s(slots[st].rec, rec + r * S * 2, rbytes, bars + st);
     };
-    auto issue_hdr = [&](uint64_t r, int st) {  // every lane (kHdr): ray r's scalars + arrive
+    auto issue_hdr = [&](uint64_t r, int st) {  // every lane: ray r's scalars + arrive
         PipeHdr& h = slots[st].hdr;
         if (lane < 3) cp_async_8(&h.o[lane], O + 3 * r + lane);
         else if (lane < 6) cp_async_8(&h.d[lane - 3], D + 3 * r + lane - 3);
@@ -1238,18 +940,14 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
     for (int st = 0; st < kStages - 1; ++st) {
         const uint64_t i = w0 + st * warps_total;
         if (i < n) {
-            if (kHdr) {
-                const uint64_t r = ray_of(i);
-                if (lane == 0) issue(r, st);
-                issue_hdr(r, st);
-            } else if (lane == 0) {
-                issue(ray_of(i), st);
-            }
+            const uint64_t r = ray_of(i);
+            if (lane == 0) issue(r, st);
+            issue_hdr(r, st);
         }
     }
-    // kHdr: the id of the next ray to stream, loaded one iteration before it is issued
+    // the id of the next ray to stream, loaded one iteration before it is issued
     uint64_t pf_i = w0 + (kStages - 1) * warps_total;
-    uint64_t r_pf = (kHdr && pf_i < n) ? ray_of(pf_i) : 0;
+    uint64_t r_pf = pf_i < n ? ray_of(pf_i) : 0;
     const float ih = static_cast<float>(g.inv_h);
     uint32_t phase = 0;  // bit st = parity of stage st
     int st = 0;
@@ -1257,44 +955,24 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
         {  // keep kStages-1 rays in flight: refill the stage released last iteration
             const uint64_t nxt = i + (kStages - 1) * warps_total;
             const int nst = (st + kStages - 1) % kStages;
-            if (kHdr) {
-                if (nxt < n) {
-                    if (lane == 0) issue(r_pf, nst);
-                    issue_hdr(r_pf, nst);
-                }
-                pf_i += warps_total;
-                if (pf_i < n) r_pf = ray_of(pf_i);
-            } else if (lane == 0 && nxt < n) {
-                issue(ray_of(nxt), nst);
+            if (nxt < n) {
+                if (lane == 0) issue(r_pf, nst);
+                issue_hdr(r_pf, nst);
             }
-        }
-        uint32_t cnt;
-        double o_r[3], d_r[3];
-        float dC[3], dD, dN[3];
-        const double* o = o_r;
-        const double* d = d_r;
-        if (!kHdr) {
-            const uint64_t r = ray_of(i);
-            cnt = counts[r];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                o_r[a] = O[3 * r + a], d_r[a] = D[3 * r + a];
-                dC[a] = d_rgb[3 * r + a], dN[a] = d_normal[3 * r + a];
-            }
-            dD = d_depth[r];
+            pf_i += warps_total;
+            if (pf_i < n) r_pf = ray_of(pf_i);
         }
         mbar_wait(bars + st, (phase >> st) & 1u);
         phase ^= 1u << st;
         const PipeSlot& sl = slots[st];
-        if (kHdr) {
-            const PipeHdr& h = sl.hdr;
-            cnt = h.cnt;
-            o = h.o;
-            d = h.d;
+        const PipeHdr& h = sl.hdr;
+        const uint32_t cnt = h.cnt;
+        const double* o = h.o;
+        const double* d = h.d;
+        float dC[3], dN[3];
 #pragma unroll
-            for (int a = 0; a < 3; ++a) dC[a] = h.dC[a], dN[a] = h.dN[a];
-            dD = h.dD;
-        }
+        for (int a = 0; a < 3; ++a) dC[a] = h.dC[a], dN[a] = h.dN[a];
+        const float dD = h.dD;
         if (cnt) {
             const uint32_t k0 = 2 * lane, k1 = k0 + 1;
             PairT p;
@@ -1333,328 +1011,15 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
                                             w1, dC, dN, ih);
             if (ok0) mark_blocks(g, v0);
             if (ok1) mark_blocks(g, v1);
-            if (kMode == 3) {
-                scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
-            } else {
-                const bool same = ok0 && ok1 && v0.gidx[0] == v1.gidx[0];
-                scatter_corner<0, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<1, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<2, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<3, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<4, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<5, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<6, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-                scatter_corner<7, kMode>(g.grad, v0, v1, c0, c1, ok0, ok1, same);
-            }
+            scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
         st = (st + 1) % kStages;
     }
 }
 
-// ---------------------------------------------------------------------------
-// K6s: the pipelined backward with one sample per lane per 32-sample pass (samples 32 h + l),
-// like k_forward_seq: pass A turns the staged records into tau and the exclusive prefix of
-// both halves; pass B walks the halves back to front (suffix S_k carried across), evaluates
-// one sample per lane and scatters with the one-step warp hand-off (lane l's cell run joins
-// lane l-1's when it is the same cell).  Fewer live registers per lane than K6p.
-// ---------------------------------------------------------------------------
-template <int kMinBlocks, int kStages>
-__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
-    k_backward_seq(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
-                   const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
-                   const double* __restrict__ T, uint32_t S, double step, float ib,
-                   const float* __restrict__ d_rgb, const float* __restrict__ d_depth,
-                   const float* __restrict__ d_normal, const float4* __restrict__ rec,
-                   uint64_t warps_total) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    PipeSlot* slots = reinterpret_cast<PipeSlot*>(smem_raw) + wib * kStages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(PipeSlot) * kStages * kPipeWarps) +
-                     wib * kStages;
-    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
-    const uint32_t tbytes = S * 8, rbytes = S * 32;
-    if (lane == 0) {
-        for (int st = 0; st < kStages; ++st) mbar_init(bars + st, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
-    auto issue = [&](uint64_t i, int st) {
-        const uint64_t r = ray_of(i);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bars + st, tbytes + rbytes);
-        bulk_g2s(slots[st].t, T + r * S, tbytes, bars + st);
-        bulk_g2s(slots[st].rec, rec + r * S * 2, rbytes, bars + st);
-    };
-    if (lane == 0)
-        for (int st = 0; st < kStages - 1; ++st) {
-            const uint64_t i = w0 + st * warps_total;
-            if (i < n) issue(i, st);
-        }
-    const float ih = static_cast<float>(g.inv_h);
-    uint32_t phase = 0;
-    int st = 0;
-    for (uint64_t i = w0; i < n; i += warps_total) {
-        {
-            const uint64_t nxt = i + (kStages - 1) * warps_total;
-            const int nst = (st + kStages - 1) % kStages;
-            if (lane == 0 && nxt < n) issue(nxt, nst);
-        }
-        const uint64_t r = ray_of(i);
-        const uint32_t cnt = counts[r];
-        mbar_wait(bars + st, (phase >> st) & 1u);
-        phase ^= 1u << st;
-        const PipeSlot& sl = slots[st];
-        if (cnt) {
-            const double o[3] = {O[3 * r], O[3 * r + 1], O[3 * r + 2]};
-            const double d[3] = {D[3 * r], D[3 * r + 1], D[3 * r + 2]};
-            const float dC[3] = {d_rgb[3 * r], d_rgb[3 * r + 1], d_rgb[3 * r + 2]};
-            const float dD = d_depth[r];
-            const float dN[3] = {d_normal[3 * r], d_normal[3 * r + 1], d_normal[3 * r + 2]};
-            // pass A: tau_k from the records (s, validity) and delta_k from the t row
-            float tau[2], dl[2], P[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t k = 32 * h + lane;
-                const bool in = k < cnt;
-                dl[h] = (k + 1 < cnt) ? static_cast<float>(__dsub_rn(sl.t[k + 1], sl.t[k])) : static_cast<float>(step);
-                const bool ok = in && __float_as_uint(sl.rec[2 * k + 1].w) != kInvalid;
-                tau[h] = ok ? density(sl.rec[2 * k].x, ib) * dl[h] : 0.f;
-            }
-            const float inc0 = warp_incl_scan(tau[0], lane);
-            const float inc1 = warp_incl_scan(tau[1], lane);
-            P[0] = inc0 - tau[0];
-            P[1] = __shfl_sync(kFull, inc0, 31) + inc1 - tau[1];
-            // pass B: back to front
-            float S_after = 0.f;
-#pragma unroll
-            for (int h = 1; h >= 0; --h) {
-                const uint32_t k = 32 * h + lane;
-                const bool in = k < cnt;
-                const double t = in ? sl.t[k] : 0.0;
-                SampleVal v;
-                const bool ok = eval_from_record(g, o, d, in, t, sl.rec + 2 * k, v);
-                const float sg = ok ? density(v.s, ib) : 0.f;
-                const float w = ok ? -expf(-P[h]) * expm1f(-tau[h]) : 0.f;
-                const float Tn = expf(-(P[h] + tau[h]));
-                const float vv = ok ? dC[0] * v.r + dC[1] * v.gc + dC[2] * v.b + dD * static_cast<float>(t) +
-                                          dN[0] * v.gx + dN[1] * v.gy + dN[2] * v.gz
-                                    : 0.f;
-                const float u = w * vv;
-                const float sinc = warp_incl_suffix(u, lane);
-                float sexc = __shfl_down_sync(kFull, sinc, 1);
-                if (lane == 31) sexc = 0.f;
-                const float Sk = S_after + sexc;
-                const CornerCoef c = make_coef(v, ok ? dl[h] * density_ds(v.s, sg, ib) * (Tn * vv - Sk) : 0.f, w,
-                                               dC, dN, ih);
-                if (ok) mark_blocks(g, v);
-                // one-step hand-off: lane l's run joins lane l-1's when it is the same cell
-                const uint32_t cell = ok ? v.gidx[0] : kInvalid;
-                const uint32_t prev = __shfl_up_sync(kFull, cell, 1);
-                const bool give = lane > 0 && ok && cell == prev;
-                const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
-#define SVR_SEQ_CORNER(cc)                                                                        \
-    {                                                                                             \
-        const float4 a = ok ? corner_grad<cc>(c) : make_float4(0.f, 0.f, 0.f, 0.f);               \
-        const float4 inb = shfl_down4(a);                                                         \
-        if (ok) {                                                                                 \
-            if (give) {                                                                           \
-                if (recv) atomicAdd(g.grad + v.gidx[cc], inb);                                    \
-            } else {                                                                              \
-                atomicAdd(g.grad + v.gidx[cc], recv ? f4add(a, inb) : a);                         \
-            }                                                                                     \
-        }                                                                                         \
-    }
-                SVR_SEQ_CORNER(0) SVR_SEQ_CORNER(1) SVR_SEQ_CORNER(2) SVR_SEQ_CORNER(3)
-                SVR_SEQ_CORNER(4) SVR_SEQ_CORNER(5) SVR_SEQ_CORNER(6) SVR_SEQ_CORNER(7)
-#undef SVR_SEQ_CORNER
-                S_after += __shfl_sync(kFull, sinc, 0);
-            }
-        }
-        __syncwarp();
-        st = (st + 1) % kStages;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// K5p: pipelined forward (max_samples <= 64, even).  Persistent warps, 3-stage ring of
-// t rows streamed with cp.async.bulk; while ray i is gathered and composited, ray i+1's
-// t row is already resident and its base-voxel block lookups are in flight, and ray i+2's
-// t row is being copied.  Per-ray scalars (o, d) ride in lanes 0-5 and are broadcast.
-// ---------------------------------------------------------------------------
-constexpr int kFwdStages = 3;
-
-struct RayPrep {  // state of the next ray, prepared one iteration ahead
-    uint64_t r;
-    uint32_t cnt;
-    double od;          // lane k < 6 holds o[k] (k < 3) or d[k-3]
-    uint32_t e0a, e0b;  // block entries of the base voxels of this lane's two samples
-};
-
-__device__ __forceinline__ void bcast_od(double od, double o[3], double d[3]) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        o[k] = __shfl_sync(kFull, od, k);
-        d[k] = __shfl_sync(kFull, od, k + 3);
-    }
-}
-
-__device__ __forceinline__ uint32_t base_lookup(const GridView& g, const double o[3], const double d[3],
-                                                double t) {
-    int base[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        const double x = __dadd_rn(o[a], __dmul_rn(t, d[a]));
-        base[a] = static_cast<int>(floor(__dmul_rn(x, g.inv_h)));
-    }
-    return lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
-}
-
-template <int kMinBlocks>
-__global__ void __launch_bounds__(kPipeWarps * 32, kMinBlocks)
-    k_forward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
-                   const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
-                   const double* __restrict__ T, uint32_t S, double step, float ib, float* rgb,
-                   float* depth, float* normal, float* wsum, float4* rec, uint64_t warps_total) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double(*trow)[64] = reinterpret_cast<double(*)[64]>(smem_raw) + wib * kFwdStages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double) * 64 * kFwdStages * kPipeWarps) +
-                     wib * kFwdStages;
-    const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kPipeWarps + wib;
-    const uint32_t tbytes = S * 8;
-    if (lane == 0) {
-        for (int st = 0; st < kFwdStages; ++st) mbar_init(bars + st, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    auto ray_of = [&](uint64_t i) -> uint64_t { return order ? order[i] : i; };
-    auto issue = [&](uint64_t i, int st) {
-        const uint64_t r = ray_of(i);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bars + st, tbytes);
-        bulk_g2s(trow[st], T + r * S, tbytes, bars + st);
-    };
-    uint32_t phase = 0;
-    auto prep = [&](uint64_t i, int st, RayPrep& p) {  // scalars + base lookups of ray i
-        p.r = ray_of(i);
-        p.cnt = counts[p.r];
-        p.od = lane < 3 ? O[3 * p.r + lane] : (lane < 6 ? D[3 * p.r + lane - 3] : 0.0);
-        double o[3], d[3];
-        bcast_od(p.od, o, d);
-        mbar_wait(bars + st, (phase >> st) & 1u);
-        phase ^= 1u << st;
-        const uint32_t k0 = 2 * lane, k1 = k0 + 1;
-        p.e0a = k0 < p.cnt ? base_lookup(g, o, d, trow[st][k0]) : kInvalid;
-        p.e0b = k1 < p.cnt ? base_lookup(g, o, d, trow[st][k1]) : kInvalid;
-    };
-    if (w0 >= n) return;
-    if (lane == 0) {
-        issue(w0, 0);
-        if (w0 + warps_total < n) issue(w0 + warps_total, 1);
-    }
-    RayPrep cur;
-    prep(w0, 0, cur);
-    int st = 0;
-    const float ih = static_cast<float>(g.inv_h);
-    for (uint64_t i = w0; i < n; i += warps_total) {
-        const uint64_t i1 = i + warps_total, i2 = i + 2 * warps_total;
-        const int st1 = (st + 1) % kFwdStages, st2 = (st + 2) % kFwdStages;
-        if (lane == 0 && i2 < n) issue(i2, st2);
-        RayPrep nxt;
-        nxt.cnt = 0;
-        if (i1 < n) prep(i1, st1, nxt);  // its lookups are in flight during this ray
-        // ---- gather + composite ray i (t row in stage st) ----
-        double o[3], d[3];
-        bcast_od(cur.od, o, d);
-        const uint64_t r = cur.r;
-        const uint32_t cnt = cur.cnt;
-        const double* tr = trow[st];
-        const uint32_t k0 = 2 * lane, k1 = k0 + 1;
-        PairT p;
-        p.in0 = k0 < cnt;
-        p.in1 = k1 < cnt;
-        p.t0 = p.in0 ? tr[k0] : 0.0;
-        p.t1 = p.in1 ? tr[k1] : 0.0;
-        p.d0 = p.in1 ? static_cast<float>(__dsub_rn(p.t1, p.t0)) : static_cast<float>(step);
-        p.d1 = (k1 + 1 < cnt) ? static_cast<float>(__dsub_rn(tr[k1 + 1], p.t1)) : static_cast<float>(step);
-        SampleVal v0, v1;
-        bool ok0 = false, ok1 = false;
-        float4 p0[8], p1[8];
-        {
-            int b0[3], b1[3];
-            zero_sample(v0);
-            zero_sample(v1);
-            if (p.in0) {
-                cell_geom(g, o, d, p.t0, b0, v0);
-                ok0 = corner_addrs<true>(g, b0, cur.e0a, v0);
-            }
-            if (p.in1) {
-                cell_geom(g, o, d, p.t1, b1, v1);
-                ok1 = corner_addrs<true>(g, b1, cur.e0b, v1);
-            }
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                p0[c] = ok0 ? __ldg(g.pay + v0.gidx[c]) : make_float4(0.f, 0.f, 0.f, 0.f);
-                p1[c] = ok1 ? __ldg(g.pay + v1.gidx[c]) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-        auto interp = [&](SampleVal& v, const float4* pp, bool ok, uint32_t e0) {
-            const float x1 = v.fx, x0 = 1.f - x1, y1 = v.fy, y0 = 1.f - y1, z1 = v.fz, z0 = 1.f - z1;
-            const float w[8] = {x0 * y0 * z0, x1 * y0 * z0, x0 * y1 * z0, x1 * y1 * z0,
-                                x0 * y0 * z1, x1 * y0 * z1, x0 * y1 * z1, x1 * y1 * z1};
-            float sv = 0.f, rv = 0.f, gv = 0.f, bv = 0.f;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                sv = fmaf(w[c], pp[c].x, sv);
-                rv = fmaf(w[c], pp[c].y, rv);
-                gv = fmaf(w[c], pp[c].z, gv);
-                bv = fmaf(w[c], pp[c].w, bv);
-            }
-            v.s = sv, v.r = rv, v.gc = gv, v.b = bv;
-            v.gx = ih * ((y0 * z0) * (pp[1].x - pp[0].x) + (y1 * z0) * (pp[3].x - pp[2].x) +
-                         (y0 * z1) * (pp[5].x - pp[4].x) + (y1 * z1) * (pp[7].x - pp[6].x));
-            v.gy = ih * ((x0 * z0) * (pp[2].x - pp[0].x) + (x1 * z0) * (pp[3].x - pp[1].x) +
-                         (x0 * z1) * (pp[6].x - pp[4].x) + (x1 * z1) * (pp[7].x - pp[5].x));
-            v.gz = ih * ((x0 * y0) * (pp[4].x - pp[0].x) + (x1 * y0) * (pp[5].x - pp[1].x) +
-                         (x0 * y1) * (pp[6].x - pp[2].x) + (x1 * y1) * (pp[7].x - pp[3].x));
-            v.e0 = ok ? e0 : kInvalid;
-        };
-        interp(v0, p0, ok0, cur.e0a);
-        interp(v1, p1, ok1, cur.e0b);
-        if (rec) {
-            float4* rr = rec + (r * S + 2 * lane) * 2;
-            if (p.in0) store_record(rr, v0);
-            if (p.in1) store_record(rr + 2, v1);
-        }
-        const float tau0 = ok0 ? density(v0.s, ib) * p.d0 : 0.f;
-        const float tau1 = ok1 ? density(v1.s, ib) * p.d1 : 0.f;
-        const float incl = warp_incl_scan(tau0 + tau1, lane);
-        float excl = __shfl_up_sync(kFull, incl, 1);
-        if (lane == 0) excl = 0.f;
-        const float P0 = excl, P1 = P0 + tau0;
-        const float w0v = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
-        const float w1v = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
-        float acc[8];
-        acc[0] = w0v * v0.r + w1v * v1.r;
-        acc[1] = w0v * v0.gc + w1v * v1.gc;
-        acc[2] = w0v * v0.b + w1v * v1.b;
-        acc[3] = w0v * static_cast<float>(p.t0) + w1v * static_cast<float>(p.t1);
-        acc[4] = w0v * v0.gx + w1v * v1.gx;
-        acc[5] = w0v * v0.gy + w1v * v1.gy;
-        acc[6] = w0v * v0.gz + w1v * v1.gz;
-        acc[7] = w0v + w1v;
-        write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
-        __syncwarp();  // stage st is free for refilling
-        cur = nxt;
-        st = st1;
-    }
-}
-
 }  // namespace
 }  // namespace svr_dev
-
 namespace svr_internal {
 using namespace svr_dev;
 
@@ -1670,277 +1035,83 @@ void launch_query(const GridView& g, const double* x, uint64_t n, double* sdf, d
 
 void launch_march(const GridView& g, const double* o, const double* d, uint64_t n,
                   const uint32_t* order, double step, uint32_t S, uint32_t* counts, double* t,
-                  double* delta, cudaStream_t s, int variant, uint32_t* pkeys, uint32_t* pids) {
+                  double* delta, cudaStream_t s, uint32_t* pkeys, uint32_t* pids,
+                  unsigned long long* valid_counter) {
     if (!n) return;
-    const unsigned grid = grid_for(n, 128);
-    if (pkeys) {  // the default kernel, also writing the post-march sort keys
-        k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta, pkeys, pids);
-        return;
-    }
-    switch (variant) {
-        case 1: k_march<8, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-        case 2: k_march<6, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-        case 3: k_march<7, true><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-        case 4: k_march<12, true, 64><<<grid_for(n, 64), 64, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-        case 5: k_march<3, true, 256><<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-        default: k_march<1, false><<<grid, 128, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta); break;
-    }
+    k_march<<<grid_for(n, kMarchThreads), kMarchThreads, 0, s>>>(g, o, d, n, order, step, S, counts, t, delta,
+                                                                 pkeys, pids, valid_counter);
 }
 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
                            const uint32_t* order, const uint32_t* counts, const double* t, uint32_t S,
                            double step, double beta, float* rgb, float* depth, float* normal,
-                           float* wsum, unsigned long long* valid_counter, float4* rec,
-                           cudaStream_t s, int min_blocks, const uint2* hdr) {
+                           float* wsum, unsigned long long* valid_counter, float4* rec, cudaStream_t s) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
-#define SVR_FWD(TH, MB)                                                                         \
-    k_forward<TH, MB><<<grid_for(n * 32, TH), TH, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
-                                                          rgb, depth, normal, wsum, valid_counter, rec)
-    switch (min_blocks) {
-        case 1: SVR_FWD(256, 1); break;
-        case 2: SVR_FWD(256, 2); break;
-        case 4: SVR_FWD(256, 4); break;
-        case 11: SVR_FWD(768, 1); break;  // one 24-warp CTA per SM: concurrent warps = adjacent rays
-        case 12: SVR_FWD(512, 1); break;
-        case 13: SVR_FWD(1024, 1); break;
-        case 105: k_forward_seq<256, 4><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
-                                                                              ib, rgb, depth, normal, wsum,
-                                                                              valid_counter, rec);
-            break;
-        case 109: k_forward_seq<256, 4, true><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S,
-                                                                                    step, ib, rgb, depth, normal,
-                                                                                    wsum, valid_counter, rec);
-            break;
-        case 111: k_forward_seq<128, 8, true><<<grid_for(n * 32, 128), 128, 0, s>>>(g, o, d, n, order, counts, t, S,
-                                                                                    step, ib, rgb, depth, normal,
-                                                                                    wsum, valid_counter, rec);
-            break;
-        case 113: k_forward_seq<64, 16, true><<<grid_for(n * 32, 64), 64, 0, s>>>(g, o, d, n, order, counts, t, S,
-                                                                                  step, ib, rgb, depth, normal,
-                                                                                  wsum, valid_counter, rec);
-            break;
-#define SVR_FWD_MULTI(TH, MB, K)                                                                  \
-    if (hdr)                                                                                      \
-        k_forward_multi<TH, MB, K, true><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(         \
-            g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec, hdr); \
-    else                                                                                          \
-        k_forward_multi<TH, MB, K, false><<<grid_for((n + K - 1) / K * 32, TH), TH, 0, s>>>(        \
-            g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, valid_counter, rec, nullptr)
-        case 114: SVR_FWD_MULTI(64, 16, 2); break;
-        case 115: SVR_FWD_MULTI(64, 16, 4); break;
-        case 116: SVR_FWD_MULTI(128, 8, 4); break;
-        case 117: SVR_FWD_MULTI(64, 16, 3); break;
-        case 118: SVR_FWD_MULTI(64, 16, 5); break;
-        case 119: SVR_FWD_MULTI(64, 16, 1); break;
-        case 120: SVR_FWD_MULTI(128, 8, 1); break;
-        case 121: SVR_FWD_MULTI(256, 4, 1); break;
-        case 122: SVR_FWD_MULTI(32, 32, 1); break;
-#undef SVR_FWD_MULTI
-        case 112: k_forward_seq<512, 2, true><<<grid_for(n * 32, 512), 512, 0, s>>>(g, o, d, n, order, counts, t, S,
-                                                                                    step, ib, rgb, depth, normal,
-                                                                                    wsum, valid_counter, rec);
-            break;
-        case 110: k_forward_seq<256, 5, true><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S,
-                                                                                    step, ib, rgb, depth, normal,
-                                                                                    wsum, valid_counter, rec);
-            break;
-        case 107: k_forward_seq<256, 5><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
-                                                                              ib, rgb, depth, normal, wsum,
-                                                                              valid_counter, rec);
-            break;
-        case 108: k_forward_seq<256, 6><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
-                                                                              ib, rgb, depth, normal, wsum,
-                                                                              valid_counter, rec);
-            break;
-        case 106: k_forward_seq<256, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
-                                                                              ib, rgb, depth, normal, wsum,
-                                                                              valid_counter, rec);
-            break;
-        case 104: k_forward_split<256, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step,
-                                                                                ib, rgb, depth, normal, wsum,
-                                                                                valid_counter, rec);
-            break;
-        // diagnostics (wrong results): 101 no payload loads, 102 no block lookup, 103 no records
-        case 101: k_forward<256, 3, 1><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
-                                                                           rgb, depth, normal, wsum, valid_counter, rec);
-            break;
-        case 102: k_forward<256, 3, 2><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
-                                                                           rgb, depth, normal, wsum, valid_counter, rec);
-            break;
-        case 103: k_forward<256, 3, 3><<<grid_for(n * 32, 256), 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib,
-                                                                           rgb, depth, normal, wsum, valid_counter, rec);
-            break;
-        default: SVR_FWD(256, 3); break;
-    }
-#undef SVR_FWD
+    k_forward<<<grid_for(n * 32, kFwdThreads), kFwdThreads, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, rgb,
+                                                                    depth, normal, wsum, valid_counter, rec);
 }
 
 void launch_render_backward(const GridView& g, const double* o, const double* d, uint64_t n,
                             const uint32_t* order, const uint32_t* counts, const double* t,
                             uint32_t S, double step, double beta, const float* d_rgb,
                             const float* d_depth, const float* d_normal, const float4* rec,
-                            cudaStream_t s, int min_blocks, bool agg) {
+                            cudaStream_t s) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
     const unsigned grid = grid_for(n * 32, 256);
-#define SVR_COMMA(a, b, c) a, b, c
-#define SVR_BWD(...) k_backward<__VA_ARGS__><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, \
-                                                                d_rgb, d_depth, d_normal, rec)
-    const bool r = rec != nullptr;
-    switch (min_blocks) {
-        case 2: r ? SVR_BWD(2, 0, true) : SVR_BWD(2, 0, false); break;
-        case 4: r ? SVR_BWD(4, 0, true) : SVR_BWD(4, 0, false); break;
-        case 103:  // diagnostics (wrong gradients): plain stores / arithmetic only
-            r ? SVR_BWD(3, 1, true) : SVR_BWD(3, 1, false);
-            break;
-        case 203:
-            r ? SVR_BWD(3, 2, true) : SVR_BWD(3, 2, false);
-            break;
-        default:
-            if (agg)
-                r ? SVR_BWD(3, 3, true) : SVR_BWD(3, 3, false);
-            else
-                r ? SVR_BWD(3, 0, true) : SVR_BWD(3, 0, false);
-            break;
-    }
-#undef SVR_BWD
-#undef SVR_COMMA
-}
-
-// {id, sample count} of every ray in sorted order, for the forward's first load level
-__global__ void k_ray_headers(const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
-                              uint64_t n, uint2* __restrict__ hdr) {
-    const uint64_t w = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (w >= n) return;
-    const uint32_t r = order[w];
-    hdr[w] = make_uint2(r, counts[r]);
-}
-
-void launch_ray_headers(const uint32_t* order, const uint32_t* counts, uint64_t n, uint2* hdr, cudaStream_t s) {
-    if (n) k_ray_headers<<<grid_for(n, 256), 256, 0, s>>>(order, counts, n, hdr);
-}
-
-void launch_ray_order(const GridView& g, const double* o, const double* d, uint64_t n,
-                      const uint32_t* counts, const double* t, uint32_t S, uint32_t* keys,
-                      uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
-                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s, int key_mode) {
-    if (!n) return;
-    if (counts && t)  // post-march: first-sample block
-        k_ray_keys<<<grid_for(n, 256), 256, 0, s>>>(g, o, d, n, counts, t, S, keys, ids, key_mode);
-    else if (!counts)  // pre-march: origin + direction
-        k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
-    // (counts && !t: the march already wrote the post-march keys / ids)
-    // sort only the key bits in use: 24 for the pre-march key; 3 x (bits per axis of the
-    // block AABB) for the post-march Morton key (empty rays carry all ones and sort last)
-    int end_bit = 24;
-    if (counts) {
-        const int sc = key_mode == 2 ? 2 : 1;
-        int bits = 1;
-        while (bits < 10 && ((1 << bits) < sc * g.dim[0] || (1 << bits) < sc * g.dim[1] || (1 << bits) < sc * g.dim[2]))
-            ++bits;
-        end_bit = 3 * bits;
-    }
-    cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
-    size_t bytes = tmp_bytes;
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, end_bit, s);
-    *sorted_ids = vb.Current();
+    if (rec)
+        k_backward<true><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal,
+                                              rec);
+    else
+        k_backward<false><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal,
+                                               rec);
 }
 
 bool launch_render_backward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
                                  const uint32_t* order, const uint32_t* counts, const double* t,
                                  uint32_t S, double step, double beta, const float* d_rgb,
                                  const float* d_depth, const float* d_normal, const float4* rec,
-                                 cudaStream_t s, int min_blocks, int num_sms, bool agg, bool hdr) {
+                                 cudaStream_t s, int num_sms) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
-    // the default (agg + ray scalars in the ring) runs a 2-stage ring: one ray of look-ahead
-    // covers the loads once the scalars travel with the rows, and the smaller ring leaves
-    // more of the SM's 256 KB to L1 (2.40 vs 2.45 ms with 3 stages)
-    const bool def2 = agg && hdr && (min_blocks == 3 || min_blocks == 0 || min_blocks > 5) && min_blocks != 203 &&
-                      min_blocks != 310 && min_blocks != 311 && min_blocks < 600;
-    const int stages = (min_blocks == 4 || min_blocks == 5 || def2) ? 2 : (min_blocks == 311 ? 4 : kPipeStages);
-    const size_t smem = sizeof(PipeSlot) * stages * kPipeWarps + 8 * stages * kPipeWarps;
+    const size_t smem = sizeof(PipeSlot) * kStages * kPipeWarps + 8 * kStages * kPipeWarps;
     const float ib = static_cast<float>(1.0 / beta);
-    const int mb_eff = min_blocks == 310 ? 3 : min_blocks == 311 ? 2
-                       : min_blocks >= 600 ? (min_blocks == 601 ? 3 : (min_blocks == 602 ? 4 : 5)) : min_blocks % 100;
-    uint64_t ctas = static_cast<uint64_t>(num_sms) * mb_eff;
+    uint64_t ctas = static_cast<uint64_t>(num_sms) * 3;  // persistent: 3 CTAs of 8 warps per SM
     const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
     if (ctas > need) ctas = need;
     const uint64_t warps_total = ctas * kPipeWarps;
-#define SVR_COMMA2(a, b) a, b
-#define SVR_COMMA3(a, b, c) a, b, c
-#define SVR_COMMA4(a, b, c, e) a, b, c, e
-#define SVR_SEQ(MB, ST)                                                                           \
-    do {                                                                                          \
-        const size_t sm = sizeof(PipeSlot) * (ST) * kPipeWarps + 8 * (ST) * kPipeWarps;           \
-        cudaFuncSetAttribute(k_backward_seq<MB, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(sm));                                               \
-        k_backward_seq<MB, ST><<<static_cast<unsigned>(ctas), kPipeWarps * 32, sm, s>>>(          \
-            g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
-    } while (0)
-#define SVR_PIPE(...)                                                                             \
-    do {                                                                                          \
-        cudaFuncSetAttribute(k_backward_pipe<__VA_ARGS__>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             static_cast<int>(smem));                                             \
-        k_backward_pipe<__VA_ARGS__><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(  \
-            g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total); \
-    } while (0)
-    switch (min_blocks) {
-        case 1:
-            if (agg) SVR_PIPE(SVR_COMMA2(1, 3));
-            else SVR_PIPE(1);
-            break;
-        case 2:
-            if (agg) SVR_PIPE(SVR_COMMA2(2, 3));
-            else SVR_PIPE(2);
-            break;
-        case 4: SVR_PIPE(SVR_COMMA3(4, 3, 2)); break;  // 2-stage ring, 64 registers
-        case 5: SVR_PIPE(SVR_COMMA3(5, 3, 2)); break;
-        case 203: SVR_PIPE(SVR_COMMA2(3, 2)); break;  // diagnostic: no atomics (wrong gradients)
-        case 310: SVR_PIPE(SVR_COMMA4(3, 3, 3, true)); break;  // 3-stage ring with the ray scalars
-        case 311: SVR_PIPE(SVR_COMMA4(2, 3, 4, true)); break;  // experiment: 4-stage ring, 2 CTAs
-        case 601: SVR_SEQ(3, 3); break;  // one sample per lane per pass
-        case 602: SVR_SEQ(4, 2); break;
-        case 603: SVR_SEQ(5, 2); break;
-        default:
-            if (agg && hdr) SVR_PIPE(SVR_COMMA4(3, 3, 2, true));
-            else if (agg) SVR_PIPE(SVR_COMMA2(3, 3));
-            else SVR_PIPE(3);
-            break;
+    static bool attr_set = false;  // per process; the attribute is per function, not per device
+    if (!attr_set) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(k_backward_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return false;
+        attr_set = true;
     }
-#undef SVR_COMMA4
-#undef SVR_PIPE
-#undef SVR_SEQ
-#undef SVR_COMMA2
-#undef SVR_COMMA3
+    k_backward_pipe<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(
+        g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total);
     return true;
 }
 
-bool launch_render_forward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
-                                const uint32_t* order, const uint32_t* counts, const double* t,
-                                uint32_t S, double step, double beta, float* rgb, float* depth,
-                                float* normal, float* wsum, float4* rec, cudaStream_t s,
-                                int min_blocks, int num_sms) {
-    if (!n) return true;
-    if (S > 64 || (S & 1)) return false;
-    const size_t smem = sizeof(double) * 64 * kFwdStages * kPipeWarps + 8 * kFwdStages * kPipeWarps;
-    const float ib = static_cast<float>(1.0 / beta);
-    uint64_t ctas = static_cast<uint64_t>(num_sms) * min_blocks;
-    const uint64_t need = (n + kPipeWarps - 1) / kPipeWarps;
-    if (ctas > need) ctas = need;
-    const uint64_t warps_total = ctas * kPipeWarps;
-#define SVR_FPIPE(MB)                                                                                 \
-    k_forward_pipe<MB><<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(                  \
-        g, o, d, n, order, counts, t, S, step, ib, rgb, depth, normal, wsum, rec, warps_total)
-    switch (min_blocks) {
-        case 1: SVR_FPIPE(1); break;
-        case 2: SVR_FPIPE(2); break;
-        case 4: SVR_FPIPE(4); break;
-        default: SVR_FPIPE(3); break;
+void launch_ray_order(const double* o, const double* d, uint64_t n, const GridView& g, bool post_march,
+                      uint32_t* keys, uint32_t* ids, uint32_t* keys_alt, uint32_t* ids_alt, void* tmp,
+                      size_t tmp_bytes, uint32_t** sorted_ids, cudaStream_t s) {
+    if (!n) return;
+    // pre-march: origin + direction keys (24 bits); post-march: the march already wrote the
+    // Morton key of each ray's first-sample block (3 x bits per axis of the block AABB; empty
+    // rays carry all ones and sort last)
+    int end_bit = 24;
+    if (post_march) {
+        int bits = 1;
+        while (bits < 10 && ((1 << bits) < g.dim[0] || (1 << bits) < g.dim[1] || (1 << bits) < g.dim[2])) ++bits;
+        end_bit = 3 * bits;
+    } else {
+        k_ray_keys_dir<<<grid_for(n, 256), 256, 0, s>>>(o, d, n, keys, ids);
     }
-#undef SVR_FPIPE
-    return true;
+    cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
+    size_t bytes = tmp_bytes;
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, end_bit, s);
+    *sorted_ids = vb.Current();
 }
 
 size_t ray_order_tmp_bytes(uint64_t n) {

@@ -60,6 +60,11 @@ class Refiner:
         self.rank = dist.get_rank(group) if self.world > 1 else 0
 
         self.g = grid
+        if self.world > 1:
+            # the 1/world scaling of the upstream gradients (torch ops) and the process-group
+            # collectives of reduce_active_grads run on torch's current stream: the grid's
+            # kernels must be ordered on that same stream
+            grid.set_stream(torch.cuda.current_stream(rgb.device))
         self.cfg = config or RefineConfig()
         self.step_m, self.beta, self.mu = step_m, beta, mu
         self.cams = list(cameras)
@@ -82,7 +87,7 @@ class Refiner:
         self.pts = torch.empty((self.cfg.band_cap + self.cfg.uniform_points, 3), dtype=torch.float64, device=dev)
         self._camarr = (Camera * len(self.cams))(*self.cams)
         self.cams_dev = torch.frombuffer(bytearray(bytes(self._camarr)), dtype=torch.uint8).to(dev)
-        # the frames / cameras were uploaded on torch's stream; the grid may run on its own
+        # the frames / cameras were uploaded on torch's stream; the grid may run on its own (world 1)
         torch.cuda.synchronize(dev)
 
     def lr_at(self, i: int, steps: int) -> float:

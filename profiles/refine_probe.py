@@ -11,7 +11,7 @@ import torch  # noqa: E402
 
 from paper_2305_13220_b200 import SparseDenseGrid  # noqa: E402
 from paper_2305_13220_b200.refine import RefineConfig, Refiner, frames_to_device  # noqa: E402
-from paper_2305_13220_b200.synthetic import SyntheticScene  # noqa: E402
+from fixtures import SyntheticScene  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 300
 sc = SyntheticScene(n_frames=32, width=320, height=240, label_channels=4, n_objects=4, seed=1)

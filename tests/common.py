@@ -12,7 +12,7 @@ import functools
 import numpy as np
 
 from oracle import OracleGrid
-from paper_2305_13220_b200.synthetic import SyntheticScene, uniform_floats
+from fixtures import SyntheticScene, uniform_floats
 
 # render tolerance: |gpu - oracle| <= RTOL*|oracle| + ATOL_FRAC*max|oracle|
 RTOL = 1e-4

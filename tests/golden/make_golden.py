@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402
 from oracle import RefGrid  # noqa: E402
-from paper_2305_13220_b200.synthetic import SyntheticScene, uniform_floats  # noqa: E402
+from fixtures import SyntheticScene, uniform_floats  # noqa: E402
 
 
 def save(name, **arrays):

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     names = set()
-    for hdr in ("svr.h", "svr_synth.h"):
+    for hdr in sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h")):
         text = open(os.path.join(ROOT, "include", hdr)).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names |= set(re.findall(r"\b(svr_\w+)\s*\(", text))
@@ -29,6 +29,14 @@ def test_library_exports_every_declared_symbol():
 
 def test_binding_covers_the_abi():
     assert declared_symbols() == set(_lib.EXPORTED)
+
+
+def test_product_library_carries_no_fixture_or_oracle_code():
+    """The synthetic-scene generator lives in fixtures/libsvr_fixture.so, the checkers in
+    oracle/: the product library exports neither."""
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in ("svr_scene_create", "svr_scene_rays", "svr_uniform_floats", "svr_fixture_last_error"):
+        assert not hasattr(lib, name), name
 
 
 def test_integration_maps_every_entry_point():

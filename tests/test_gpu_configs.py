@@ -17,7 +17,7 @@ H, R = 0.02, 2
 @pytest.fixture(scope="module")
 def cfg1():
     from paper_2305_13220_b200 import SparseDenseGrid
-    from paper_2305_13220_b200.synthetic import SyntheticScene, uniform_floats
+    from fixtures import SyntheticScene, uniform_floats
 
     sc = SyntheticScene(**CFG1)
     cams = sc.cameras()

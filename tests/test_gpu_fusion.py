@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import OracleGrid
-from paper_2305_13220_b200.synthetic import SyntheticScene
+from fixtures import SyntheticScene
 
 pytestmark = pytest.mark.gpu
 

@@ -97,7 +97,7 @@ def test_march_golden(lookup):
 
 def test_render_golden():
     from paper_2305_13220_b200 import SparseDenseGrid
-    from paper_2305_13220_b200.synthetic import SyntheticScene
+    from fixtures import SyntheticScene
 
     z = gold("render.npz")
     h = float(z["h"])

@@ -51,7 +51,7 @@ def test_all_256_cases_match_oracle(lookup):
 
 def test_fused_scene_mesh_matches_oracle():
     """fusion -> marching cubes on a synthetic room: the inference output path end to end."""
-    from paper_2305_13220_b200.synthetic import SyntheticScene
+    from fixtures import SyntheticScene
 
     sc = SyntheticScene(n_frames=12, width=96, height=72, label_channels=4)
     cams = sc.cameras()

@@ -187,9 +187,8 @@ def test_device_resident_path_matches_host_path(case):
         assert np.array_equal(dev[k].cpu().numpy(), host[k]), k
 
 
-@pytest.mark.parametrize("variant", [2, 0])  # default k_march (o / d in smem); registers variant
 @pytest.mark.parametrize("lookup", LOOKUPS)
-def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup, variant):
+def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup):
     """200k rays from random origins (inside and outside the AABB) with random and nearly
     axis-parallel directions (components down to 1e-300) -- counts, t, delta bit-exact."""
     rng = np.random.default_rng(99)
@@ -203,7 +202,6 @@ def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup, va
     d[4 * k:5 * k, 1] = 0.0
     d /= np.linalg.norm(d, axis=1, keepdims=True)
     g = gpu_grid_from(case, lookup)
-    g.set_tuning("march_variant", variant)
     m = g.march(o, d, case["step"], 48)
     OracleGrid.set_threads(8)
     try:
@@ -217,9 +215,8 @@ def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup, va
     assert mask.sum() > 500_000
 
 
-@pytest.mark.parametrize("variant", [2, 0])
 @pytest.mark.parametrize("jump", [1, 0])
-def test_march_empty_space_jumps_bit_exact(jump, variant):
+def test_march_empty_space_jumps_bit_exact(jump):
     """Sparse block clusters inside a 96^3-block AABB, so most of each ray's walk crosses
     wide empty space where the dense-mode march jumps over the block-distance field: counts,
     t and delta must equal the oracle's step-by-step walk bit for bit (random rays, rays
@@ -242,7 +239,6 @@ def test_march_empty_space_jumps_bit_exact(jump, variant):
     g.set_payload(0, A, weight=np.ones((A, 512), np.float32))
     g.set_lookup(2)  # dense AABB index (the jump needs the distance field)
     g.set_tuning("march_jump", jump)
-    g.set_tuning("march_variant", variant)
     n = 60_000
     o = rng.uniform(-0.5, 96 * L + 0.5, size=(n, 3))
     d = rng.normal(size=(n, 3))

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _frames(n=6, W=64, H=48, C=4):
-    from paper_2305_13220_b200.synthetic import SyntheticScene
+    from fixtures import SyntheticScene
 
     sc = SyntheticScene(n_frames=n, width=W, height=H, label_channels=C)
     cams = sc.cameras()

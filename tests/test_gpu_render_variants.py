@@ -87,18 +87,13 @@ def test_performance_knobs_do_not_change_results(ray_sort, records, pipe):
     _check_fwd_bwd(g, case, 64)
 
 
-@pytest.mark.parametrize("pipe_min_blocks,warp_agg,bwd_pipe,bwd_hdr",
-                         [(2, 1, 1, 0), (3, 1, 1, 0), (3, 1, 1, 1), (310, 1, 1, 1), (311, 1, 1, 1), (3, 0, 1, 0),
-                          (3, 1, 0, 0), (3, 0, 0, 0), (4, 1, 1, 0), (601, 1, 1, 0), (602, 1, 1, 0)])
-def test_scatter_variants_match_oracle(pipe_min_blocks, warp_agg, bwd_pipe, bwd_hdr):
-    """warp-aggregated scatter (default) vs per-lane scatter, pipelined and plain backward,
-    ray scalars streamed through the ring (bwd_hdr) or loaded per ray."""
-    for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):  # + invalid samples inside runs
+@pytest.mark.parametrize("bwd_pipe", [1, 0])
+def test_scatter_paths_match_oracle(bwd_pipe):
+    """Pipelined (cp.async.bulk ring, records <= 64 samples) and plain backward, with invalid
+    samples inside the runs (partially observed blocks)."""
+    for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
         g = gpu_grid_from(c)
-        g.set_tuning("pipe_min_blocks", pipe_min_blocks)
-        g.set_tuning("warp_agg", warp_agg)
         g.set_tuning("bwd_pipe", bwd_pipe)
-        g.set_tuning("bwd_hdr", bwd_hdr)
         _check_fwd_bwd(g, c, 64)
 
 
@@ -140,28 +135,15 @@ def test_host_async_pipeline_matches_synchronous():
     assert_close(gr, ref_gr, what="grad_rgb")
 
 
-@pytest.mark.parametrize("split", [0, 1, 2, 3])
-def test_forward_lane_layouts_match_oracle(split):
-    """fwd_split: one sample per lane per pass with t one pass ahead [default], the same without
-    the prefetch, lane l owns samples (l, 32 + l), or (2l, 2l + 1)."""
+@pytest.mark.parametrize("S", [8, 33, 100])
+@pytest.mark.parametrize("records", [1, 0])
+def test_sample_budgets_below_at_and_beyond_one_pass(S, records):
+    """The forward's one-pass-ahead t prefetch at budgets below, just above and beyond one
+    32-sample pass, with and without records (the backward re-gathers without them)."""
     for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
         g = gpu_grid_from(c)
-        g.set_tuning("fwd_split", split)
-        _check_fwd_bwd(g, c, 64)
-
-
-@pytest.mark.parametrize("case_id", [119, 114, 115, 117, 122])
-@pytest.mark.parametrize("S", [8, 33, 100])
-@pytest.mark.parametrize("hdr", [0, 1])
-def test_forward_prefetch_variants_match_oracle(case_id, S, hdr):
-    """k_forward_multi: K = 1..4 consecutive rays per warp with the per-ray set-up and every t
-    value fetched one pass ahead, at sample budgets below, just above and beyond one pass; with
-    and without the {id, count} header pass (ray_hdr)."""
-    c = scene_case()
-    g = gpu_grid_from(c)
-    g.set_tuning("fwd_min_blocks", case_id)
-    g.set_tuning("ray_hdr", hdr)
-    _check_fwd_bwd(g, c, S)
+        g.set_tuning("records", records)
+        _check_fwd_bwd(g, c, S)
 
 
 def test_zero_async_overlap_keeps_results():
@@ -206,13 +188,3 @@ def test_small_batches_skip_the_ordering():
     assert_close(res[1][1][0], res[0][1][0], what="grad_sdf")
     assert_close(res[1][1][1], res[0][1][1], what="grad_rgb")
     assert np.array_equal(res[0][2], res[1][2])
-
-
-@pytest.mark.parametrize("march_keys", [0, 1])
-def test_march_written_sort_keys_match_oracle(march_keys):
-    """march_keys: the march writes the post-march sort keys itself (no k_ray_keys pass);
-    results must not depend on it."""
-    for c in (scene_case(), _mask_some(scene_case(), 0.15, 3)):
-        g = gpu_grid_from(c)
-        g.set_tuning("march_keys", march_keys)
-        _check_fwd_bwd(g, c, 64)

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from oracle import OracleGrid, RefGrid, ref_available
-from paper_2305_13220_b200.synthetic import SyntheticScene
+from fixtures import SyntheticScene
 
 H = 0.02  # voxel size of the known-answer grids
 LOCAL = (3, 3, 3)
