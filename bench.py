@@ -6,18 +6,24 @@ Workload (BASELINE.json configs[2], "cfg3"): ScanNet-scale synthetic room 11 x 1
 cameras, 1M rays per GPU per step (64 poses x 16384 random pixels), <= 64 samples per
 ray at step h/2, Laplace beta = 2h.  One step = render_forward (march + fused forward)
 + render_backward (fused adjoint + vector-atomic scatter) + active-block gradient
-reduction (NCCL all-reduce over NVLink for N > 1) + zeroing of the active gradients.
+reduction (N > 1) + zeroing of the active gradients.
 
 `--workload cfg5` (BASELINE.json configs[4]): the same grid, 8M rays per step in total split
 over the GPUs (strong scaling).
 
+`--impl reference`: the reference's CPU path on the host cores -- its own grid code and
+synthetic generator compiled verbatim (oracle/_ref) with the spec renderer on its API -- for
+the same workload, config and metric; rank 0 only.
+
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload cfg3|cfg5]
-Under torchrun (N > 1) every rank drives one GPU; rank 0 prints ONE JSON line.
+With --gpus N > 1 outside torchrun the script re-launches itself under torch.distributed.run
+(one rank per GPU); rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes
+import hashlib
 import json
 import os
 import statistics
@@ -30,24 +36,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from fixtures.workloads import (CFG1, CFG3, CFG4, CFG5, WORKLOADS, activation_frames,  # noqa: E402
+                                fill_in_chunks, make_scene, rays_for_rank)
+
 METRIC = "rays/s and samples/s fwd+bwd per GPU (1/2/4/8 B200); % HBM roofline vs CPU"
 # algorithmic bytes per VALID interpolated sample / per ray
 FWD_B_SAMPLE, FWD_B_RAY = 182.8, 80.0
 BWD_B_SAMPLE, BWD_B_RAY = 256.0, 28.0
 STEP_B_SAMPLE, STEP_B_RAY = FWD_B_SAMPLE + BWD_B_SAMPLE, FWD_B_RAY + BWD_B_RAY
-
-CFG3 = dict(room=(11.0, 11.0, 3.0), h=0.01, dilation=2, C=4, width=640, height=480,
-            n_objects=4, seed=1, fov=70.0, act_frames=64, ray_poses=64, rays_per_pose=16384,
-            max_samples=64, name="cfg3")
-# BASELINE.json configs[4]: the cfg3 grid, 8M rays per iteration (64 poses x 131072 px) split
-# over the ranks (strong scaling); `--workload cfg5`
-CFG5 = dict(CFG3, rays_per_pose=131072, strong=True, name="cfg5")
-WORKLOADS = {
-    "cfg3": ("cfg3: ScanNet-scale synthetic room 11x11x3 m, 1 cm voxels, 8^3 blocks, R=2 activation from 64 "
-             "ring-camera GT depth frames, 1M rays/GPU/step (64 poses x 16384 px), <=64 samples/ray, fwd+bwd"),
-    "cfg5": ("cfg5: the cfg3 grid (11x11x3 m, 1 cm voxels, R=2 from 64 GT depth frames), 8M rays/step in total "
-             "(64 poses x 131072 px) split contiguously over the GPUs, <=64 samples/ray, fwd+bwd"),
-}
+# SURVEY.md 8(d) "cfg4 bytes": activation 4 B per pixel read + per new block a 16 B slot, a 12 B
+# coordinate and the zero-initialised payload 512 (20 + 4 C) B; query 127 B per point
+ACT_B_PIXEL = 4.0
+QUERY_B_POINT = 8 * (4 + 4) + 22.8 + 24 + 16
 
 
 def log(*a):
@@ -61,6 +61,40 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def build_id() -> str:
+    """Hash of the product's kernel sources: ncu captures are tied to the build they profiled."""
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2305_13220_b200", "csrc")
+    for f in sorted(os.listdir(csrc)):
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(csrc, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def traffic_from_profiles(workload, rays_per_gpu, bid, path=None):
+    """Per-launch DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) and L2 hit
+    rates captured for this workload, per-GPU ray count AND this build; else {}."""
+    try:
+        with open(path or os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            entries = json.load(f)["captures"]
+    except Exception:
+        return {}
+    for e in entries:
+        if e.get("workload") == workload and e.get("rays_per_gpu") == rays_per_gpu and e.get("build_id") == bid:
+            return e
+    return {}
+
+
+def workload_config(cfg, blocks, rays, valid, world):
+    """The `config` object of the JSON line -- identical for both arms of the same workload."""
+    return {"workload": WORKLOADS[cfg["name"]], "blocks": int(blocks), "rays_per_gpu": int(rays),
+            "valid_samples_per_gpu": int(valid), "max_samples": cfg["max_samples"], "step_m": cfg["h"] / 2,
+            "beta_m": 2 * cfg["h"], "parallelism": f"rays sharded over {world} GPU(s), grid replicated",
+            "l2": f"no flush: inputs exceed L2 (payload + gradient planes {blocks * 512 * 32 / 1e9:.1f} GB "
+                  f"vs 126 MB L2)"}
 
 
 class ClockSampler:
@@ -142,84 +176,90 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------
-# inputs (host, identical for every arm)
-# ----------------------------------------------------------------------------------
-def make_scene(cfg):
-    from fixtures import SyntheticScene
-
-    r = cfg["room"]
-    return SyntheticScene(room_w=r[0], room_d=r[1], room_h=r[2], n_objects=cfg["n_objects"],
-                          width=cfg["width"], height=cfg["height"], n_frames=cfg["ray_poses"],
-                          fov_deg=cfg["fov"], label_channels=cfg["C"], seed=cfg["seed"])
-
-
-def activation_frames(scene, cfg):
-    cams = scene.cameras(cfg["act_frames"])
-    return cams, scene.depth(cams)
-
-
-def rays_for_rank(scene, cfg, rank, world):
-    """Global ray set = world x (poses x rays_per_pose) (weak scaling), or poses x rays_per_pose
-    whatever the world size (cfg5, strong scaling); rank r owns a contiguous shard."""
-    from fixtures import uniform_floats
-
-    poses, rpp = cfg["ray_poses"], cfg["rays_per_pose"]
-    if cfg.get("strong"):
-        if (poses * rpp) % world:
-            raise SystemExit(f"{poses * rpp} rays do not split evenly over {world} ranks")
-        o, d = scene.rays(poses, rpp, seed=0)
-        n = poses * rpp // world
-        u = uniform_floats(7 * n * world, 1).reshape(n * world, 7)[rank * n:(rank + 1) * n]
-        o, d = o[rank * n:(rank + 1) * n], d[rank * n:(rank + 1) * n]
-        return (np.ascontiguousarray(o), np.ascontiguousarray(d), np.ascontiguousarray(u[:, :3]),
-                np.ascontiguousarray(u[:, 3]), np.ascontiguousarray(u[:, 4:]))
-    o, d = scene.rays(poses * world, rpp, seed=0)
-    n = poses * rpp
-    o, d = o[rank * n:(rank + 1) * n], d[rank * n:(rank + 1) * n]
-    u = uniform_floats(7 * n * world, 1).reshape(n * world, 7)[rank * n:(rank + 1) * n]
-    return (np.ascontiguousarray(o), np.ascontiguousarray(d), np.ascontiguousarray(u[:, :3]),
-            np.ascontiguousarray(u[:, 3]), np.ascontiguousarray(u[:, 4:]))
-
-
-def fill_in_chunks(scene, cfg, coords, sink, chunk=8192):
-    """Synthetic payload (sdf clamped at mu = L*R, weight 1, rgb, one-hot logits)."""
-    h, R = cfg["h"], cfg["dilation"]
-    mu = 8 * h * R  # PAPER.md:502, mu = L * R
-    for f in range(0, len(coords), chunk):
-        c = coords[f:f + chunk]
-        p = scene.fill_payload(h, c, mu, cfg["C"])
-        sink(f, len(c), p)
-
-
-# ----------------------------------------------------------------------------------
 # CPU arms (oracle/, only here and in tests)
 # ----------------------------------------------------------------------------------
-def time_cpu_render(grid, o, d, cfg, dC, dD, dN, kind, target_s=12.0):
-    """fwd+bwd of a bounded ray sample on the host cores; returns (valid samples/s, info)."""
-    h = cfg["h"]
-    step, beta, S = h / 2, 2 * h, cfg["max_samples"]
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference CPU path on all host threads, rank 0 only.  Inputs come
+    from the reference's own SyntheticScene (synthetic.cpp, oracle/_ref); activation is its
+    allocate_for_frames (allocation.cpp:56-83, single thread as written); each step renders
+    the whole per-GPU ray set forward + backward with the spec renderer on its grid API
+    (march_ray -> gather_corners -> sdf_at / sdf_gradient_at / color_at, parallel_chunks over
+    rays, float atomics: SPEC.md:340-341).  No product code is loaded."""
+    if rank != 0:
+        return
+    import oracle
 
-    bufs = grid.grad_buffers() if kind == "port" else None
+    t_setup = time.perf_counter()
+    ref = oracle.ref_available()
+    scene = make_scene(cfg, reference=ref)  # fixture restatement only if _ref was not built
+    cams, depth = activation_frames(scene, cfg)
+    o, d, dC, dD, dN = rays_for_rank(scene, cfg, 0, world)
+    Grid = oracle.RefGrid if ref else oracle.OracleGrid
+    g = Grid(cfg["h"], 8, cfg["C"], capacity=1 << 22)
+    t0 = time.perf_counter()
+    g.allocate_frames(depth, cams, cfg["dilation"])
+    act_s = time.perf_counter() - t0
+    coords = g.coords()
+    fill_in_chunks(scene, cfg, coords, lambda f, n, p: g.set_payload(f, n, **p))
+    cores = os.cpu_count() or 1
+    Grid.set_threads(cores)
+    S, step_len, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
+    log(f"[reference] setup {time.perf_counter() - t_setup:.1f}s: {len(coords)} blocks "
+        f"(allocate_for_frames {act_s:.1f}s), {len(o)} rays, {cores} threads")
 
-    def run(n):
-        t0 = time.perf_counter()
-        if kind == "port":
-            f = grid.render_forward(o[:n], d[:n], step, S, beta)
-            grid.render_backward(o[:n], d[:n], step, S, beta, dC[:n], dD[:n], dN[:n], out=bufs)
+    def step():
+        f = g.render_forward(o, d, step_len, S, beta)
+        if ref:
+            g.render_backward(dC, dD, dN)
         else:
-            f = grid.render_forward(o[:n], d[:n], step, S, beta)
-            grid.render_backward(dC[:n], dD[:n], dN[:n])
-        return time.perf_counter() - t0, int(f["n_valid"].sum())
+            g.render_backward(o, d, step_len, S, beta, dC, dD, dN)
+        return f
 
-    n = 8192
-    dt, nv = run(n)
-    n = int(min(len(o), max(n, n * target_s / max(dt, 1e-3))))
-    dt, nv = run(n)
-    return nv / dt, n / dt, {"rays": n, "valid_samples": nv, "seconds": dt}
+    # setup, untimed: the reference renderer allocates its gradient shadow buffers
+    # (VoxelBlock::grad_sdf / grad_color, grid.hpp:69) on its first backward
+    f0 = g.render_forward(o[:1024], d[:1024], step_len, S, beta)
+    g.render_backward(dC[:1024], dD[:1024], dN[:1024]) if ref else None
+    del f0
+    for _ in range(args.warmup):
+        step()
+    times, nvalid = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        f = step()
+        times.append(time.perf_counter() - t0)
+        nvalid = int(f["n_valid"].sum())
+    t = sum(times) / len(times)
+    value = nvalid / t
+    kind = "reference" if ref else "port"
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic", "impl": "reference", "rays_per_s": len(o) / t,
+            "config": workload_config(cfg, len(coords), len(o), nvalid, world),
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
+                             "sample": f"the whole per-GPU step: {len(o)} {cfg['name']} rays fwd+bwd per step, "
+                                       f"{nvalid} valid samples"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
-def cpu_baseline_port(coords, payload_chunks, o, d, dC, dD, dN, cfg):
-    """The restated oracle (oracle/liboracle.so) on all host cores."""
+def parity_report(gpu, ref, what):
+    """|gpu - oracle| <= 1e-4 |oracle| + 1e-6 max|oracle| element-wise."""
+    g = np.asarray(gpu, np.float64).ravel()
+    r = np.asarray(ref, np.float64).ravel()
+    scale = float(np.abs(r).max()) if r.size else 0.0
+    err = np.abs(g - r)
+    bound = 1e-4 * np.abs(r) + 1e-6 * scale
+    rel = err / np.maximum(np.abs(r), 1e-6 * scale if scale > 0 else 1e-30)
+    return {"n": int(r.size), "outside": int((err > bound).sum()), "max_abs_err": float(err.max(initial=0.0)),
+            "max_err_over_bound": float((err / np.maximum(bound, 1e-300)).max(initial=0.0)),
+            "max_rel_err": float(rel.max(initial=0.0))}
+
+
+def cpu_leg_and_parity(grid, coords, payload_chunks, o, d, dC, dD, dN, cfg):
+    """The restated oracle (oracle/liboracle.so, fp64) on all host cores renders the SAME rays
+    on the SAME grid (same block order) forward + backward: timed as cpu_baseline, and compared
+    with the GPU's outputs, gradients and active set (the `parity` object)."""
     from oracle import OracleGrid
 
     og = OracleGrid(cfg["h"], 8, cfg["C"], capacity=max(len(coords), 1 << 21))
@@ -228,98 +268,38 @@ def cpu_baseline_port(coords, payload_chunks, o, d, dC, dD, dN, cfg):
         og.set_payload(f, n, **p)
     cores = os.cpu_count() or 1
     OracleGrid.set_threads(cores)
-    sps, rps, info = time_cpu_render(og, o, d, cfg, dC, dD, dN, "port")
-    return {"value": sps, "unit": "samples/s", "cores": cores, "kind": "port",
-            "rays_per_s": rps,
-            "sample": f"{info['rays']} {cfg.get('name', 'cfg3')} rays (first rays of the step), fwd+bwd, "
-                      f"{info['valid_samples']} valid samples in {info['seconds']:.2f} s"}
-
-
-def run_reference(args, cfg, rank, world):
-    """--impl reference: the reference CPU path (oracle/_ref = reference grid code compiled
-    verbatim + spec-restated renderer on its API), all host threads, rank 0 only."""
-    if rank != 0:
-        return
-    import oracle
-    from oracle import RefGrid
-
-    scene = make_scene(cfg)
-    cams, depth = activation_frames(scene, cfg)
-    o, d, dC, dD, dN = rays_for_rank(scene, cfg, 0, 1)
-    if oracle.ref_available():
-        kind = "reference"
-        g = RefGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22)
-        t0 = time.perf_counter()
-        g.allocate_frames(depth, cams, cfg["dilation"])  # allocation.cpp:56-83, single thread
-        log(f"[reference] allocate_for_frames: {g.block_count()} blocks in {time.perf_counter() - t0:.1f}s")
-        coords = g.coords()
-        fill_in_chunks(scene, cfg, coords, lambda f, n, p: g.set_payload(f, n, **p))
-        cores = os.cpu_count() or 1
-        RefGrid.set_threads(cores)
-        render = lambda n: (g.render_forward(o[:n], d[:n], cfg["h"] / 2, cfg["max_samples"], 2 * cfg["h"]),  # noqa: E731
-                            g.render_backward(dC[:n], dD[:n], dN[:n]))
-    else:
-        from oracle import OracleGrid
-
-        kind = "port"
-        g = OracleGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22)
-        g.allocate_frames(depth, cams, cfg["dilation"])
-        coords = g.coords()
-        fill_in_chunks(scene, cfg, coords, lambda f, n, p: g.set_payload(f, n, **p))
-        cores = os.cpu_count() or 1
-        OracleGrid.set_threads(cores)
-        render = lambda n: (g.render_forward(o[:n], d[:n], cfg["h"] / 2, cfg["max_samples"], 2 * cfg["h"]),  # noqa: E731
-                            g.render_backward(o[:n], d[:n], cfg["h"] / 2, cfg["max_samples"], 2 * cfg["h"],
-                                              dC[:n], dD[:n], dN[:n]))
-    # size one step's ray sample so a step takes ~3 s of host time (after a first call
-    # that allocates the reference's gradient shadow buffers)
-    render(1024)
+    S, step_len, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
     t0 = time.perf_counter()
-    f, _ = render(8192)
+    ref = og.render_forward(o, d, step_len, S, beta)
+    gs_o, gr_o, act_o = og.render_backward(o, d, step_len, S, beta, dC, dD, dN)
     dt = time.perf_counter() - t0
-    n = int(min(len(o), max(8192, 8192 * 3.0 / max(dt, 1e-3))))
-    for _ in range(args.warmup):
-        render(n)
-    times, nvalid = [], 0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        f, _ = render(n)
-        times.append(time.perf_counter() - t0)
-        nvalid = int(f["n_valid"].sum())
-    t = sum(times) / len(times)
-    value = nvalid / t
-    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic", "impl": "reference", "rays_per_s": n / t,
-            "config": {"workload": WORKLOADS[cfg["name"]] + "; bounded CPU ray sample per step",
-                       "blocks": int(len(coords)), "rays_per_step": n,
-                       "max_samples": cfg["max_samples"]},
-            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
-                             "sample": f"{n} {cfg['name']} rays per step (of {len(o)}), fwd+bwd, "
-                                       f"{nvalid} valid samples"},
-            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    OracleGrid.set_threads(1)
+    nvalid = int(ref["n_valid"].sum())
+    cpu = {"value": nvalid / dt, "unit": "samples/s", "cores": cores, "kind": "port", "rays_per_s": len(o) / dt,
+           "sample": f"the whole step: {len(o)} {cfg['name']} rays fwd+bwd, {nvalid} valid samples in {dt:.2f} s"}
+    # the GPU: one forward + backward of the same rays into zeroed gradient planes
+    grid.grad_zero()
+    out = grid.render_forward(o, d, step_len, S, beta)
+    grid.render_backward(dC, dD, dN)
+    gs, gr = grid.grads()
+    act = grid.active_mask()
+    par = {"rays": len(o), "tolerance": "|gpu - oracle| <= 1e-4 |oracle| + 1e-6 max|oracle| (SURVEY.md 8(c))",
+           "oracle": "oracle/liboracle.so (fp64 restatement, pinned to the compiled reference)",
+           "n_samples_equal": bool(np.array_equal(out["n_samples"], ref["n_samples"])),
+           "active_set_equal": bool(np.array_equal(act, act_o)), "active_blocks": int(act_o.sum())}
+    for k in ("rgb", "depth", "normal", "wsum"):
+        par[k] = parity_report(out[k], ref[k], k)
+    par["grad_sdf"] = parity_report(gs, gs_o, "grad_sdf")
+    par["grad_rgb"] = parity_report(gr, gr_o, "grad_rgb")
+    par["green"] = bool(par["n_samples_equal"] and par["active_set_equal"] and
+                        all(par[k]["outside"] == 0 for k in ("rgb", "depth", "normal", "wsum", "grad_sdf",
+                                                              "grad_rgb")))
+    return cpu, par
 
 
 # ----------------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------------
-def traffic_from_profiles(workload, rays_per_gpu):
-    """Per-launch DRAM bytes (ncu dram__bytes_read.sum + dram__bytes_write.sum) captured for
-    this workload at this per-GPU ray count, else {} (reported as null)."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        with open(p) as f:
-            entries = json.load(f)["captures"]
-    except Exception:
-        return {}
-    for e in entries:
-        if e.get("workload") == workload and e.get("rays_per_gpu") == rays_per_gpu:
-            return dict(e["bytes"], _l2_hit_pct=e.get("l2_hit_pct", {}))
-    return {}
-
-
 def _all_reduce(dist, t, op=None):
     """all_reduce that also works on a gloo group (CPU round trip)."""
     op = dist.ReduceOp.SUM if op is None else op
@@ -339,8 +319,6 @@ def run_ours(args, cfg, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-
-        from paper_2305_13220_b200.distributed import reduce_active_grads
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     # a real (non-legacy) stream shared by torch, NCCL ordering and the library
@@ -352,10 +330,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     cams, depth = activation_frames(scene, cfg)
     grid = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22, device=local_rank)
     grid.set_stream(stream)
-    # A/B hook for the performance knobs (results unaffected): SVR_TUNING="key=v,key=v"
+    # A/B hook for the result-neutral knobs: SVR_TUNING="key=v,key=v"
     for kv in filter(None, os.environ.get("SVR_TUNING", "").split(",")):
         k, v = kv.split("=")
         grid.set_tuning(k.strip(), int(v))
+    if args.lookup == "hash":
+        grid.set_lookup(1)
     rep = grid.allocate_for_frames(depth, cams, cfg["dilation"])
     coords = grid.coords()
     chunks = []
@@ -370,7 +350,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     o, d, dC, dD, dN = rays_for_rank(scene, cfg, rank, world)
     n_rays = len(o)
     log(f"[rank {rank}] setup {time.perf_counter() - t_setup:.1f}s: {len(coords)} blocks "
-        f"({rep.pixels_used} px), {n_rays} rays")
+        f"({rep.pixels_used} px), {n_rays} rays, lookup {'dense' if grid.info().lookup_mode == 2 else 'hash'}")
 
     S, step_len, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
     o_d = torch.from_numpy(o).to(dev)
@@ -382,6 +362,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "wsum": torch.empty((n_rays,), dtype=torch.float32, device=dev),
             "n_samples": None}
     grid.grad_zero()
+    reducer = make_reducer(args, grid, dev, dist, rank) if dist is not None else None
 
     ev = []
 
@@ -396,53 +377,12 @@ def run_ours(args, cfg, rank, world, local_rank):
         if e:
             e[2].record(stream)
             ev.append(e)
-        if dist is not None:
-            reducer["fn"]()  # K7 mask union + K8p peer-memory all-reduce (or K8 pack + NCCL)
+        if reducer is not None:
+            reducer["fn"]()  # active-block gradient all-reduce across the ranks
         grid.grad_zero_active()
 
-    # N > 1: the gradient reduction runs either as the fused peer-memory kernel over CUDA IPC
-    # mappings (K8p, distributed.PeerGradReducer) or as pack + NCCL all-reduce + unpack; both
-    # are timed over a few steps before the measurement and the faster one is used
-    reducer = {"fn": None, "used": None, "calib_ms": {}}
-    if dist is not None:
-        from paper_2305_13220_b200.distributed import PeerGradReducer
-
-        variants = {}
-        if dist.get_backend() == "nccl":
-            variants["nccl"] = lambda: reduce_active_grads(grid, dev)
-        if args.reduce in ("auto", "peer"):
-            try:
-                peer = PeerGradReducer(grid, dev)
-                variants["peer"] = peer.reduce
-            except Exception as e:  # pragma: no cover - no IPC / P2P on this system
-                log(f"[rank {rank}] peer reduction unavailable: {e}")
-        if args.reduce == "nccl":
-            variants.pop("peer", None)
-        for name, fn in variants.items():
-            reducer["fn"] = fn
-            for _ in range(2):
-                step(False)
-            torch.cuda.synchronize(dev)
-            dist.barrier()
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(stream)
-            for _ in range(3):
-                step(False)
-            c1.record(stream)
-            torch.cuda.synchronize(dev)
-            tt = torch.tensor([c0.elapsed_time(c1) / 3], dtype=torch.float64, device=dev)
-            _all_reduce(dist, tt, dist.ReduceOp.MAX)
-            reducer["calib_ms"][name] = float(tt.item())
-        best = min(reducer["calib_ms"], key=reducer["calib_ms"].get)
-        if args.reduce == "peer" and "peer" in variants:
-            best = "peer"
-        reducer["fn"], reducer["used"] = variants[best], best
-
-    # ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward, k_backward,
-    # k_active_count/scan/write, k_grad_zero_active (+ k_active_* / pack / unpack for N > 1);
-    # plus 2 CUB radix sorts (5 library kernels each) that only reorder rays
-    launches_per_step = 8 + (5 if world > 1 else 0)
-    library_launches_per_step = 10  # 2 CUB radix sorts of 24-bit keys: histogram + scan + 3 onesweep passes each
+    if reducer is not None:
+        calibrate_reducer(reducer, step, stream, dev, dist)
     for _ in range(max(args.warmup, 3)):
         step(False)
     torch.cuda.synchronize(dev)
@@ -516,7 +456,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     def step_host():
         grid.render_forward(o_h, d_h, step_len, S, beta, out=outs_h)
         grid.render_backward(dC_h, dD_h, dN_h)
-        if dist is not None:
+        if reducer is not None:
             reducer["fn"]()
         grid.grad_zero_active()
 
@@ -548,15 +488,17 @@ def run_ours(args, cfg, rank, world, local_rank):
     if rank != 0:
         return
     peak, peak_kind = peaks()
-    # dominant kernel: K6 backward (one launch) vs the forward call (K4 + K5)
+    bid = build_id()
+    # dominant kernel: K6 backward (one launch: k_backward_pipe); the forward call (ordering,
+    # k_march, k_forward) is reported beside it
     bwd_bytes = valid_per_step * BWD_B_SAMPLE + n_rays * BWD_B_RAY
     fwd_bytes = valid_per_step * FWD_B_SAMPLE + n_rays * FWD_B_RAY
     step_bytes = valid_per_step * STEP_B_SAMPLE + n_rays * STEP_B_RAY
-    traffic = traffic_from_profiles(cfg["name"], n_rays)
-    # the dominant single kernel is the backward (one launch: k_backward_pipe); the forward
-    # call is several launches (ordering, k_march, k_forward) and is reported beside it
+    cap = traffic_from_profiles(cfg["name"] + ("_hash" if args.lookup == "hash" else ""), n_rays, bid)
     dom, dom_ms, dom_bytes = "k_backward_pipe", bwd_ms, bwd_bytes
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    dram = cap.get("dram_bytes", {})
+    step_dram = sum(dram.get(k, 0) for k in ("k_march", "k_forward", "k_backward_pipe", "k_grad_zero_active"))
     line = {
         "metric": METRIC,
         "value": valid_total / (ms * 1e-3),
@@ -566,55 +508,109 @@ def run_ours(args, cfg, rank, world, local_rank):
         "dtype": "f32", "data": "synthetic",
         "rays_per_s": rays_total / (ms * 1e-3),
         "samples_marched_per_s": marched_total / (ms * 1e-3),
-        "config": {"workload": WORKLOADS[cfg["name"]],
-                   "blocks": int(info.block_count), "rays_per_gpu": n_rays,
-                   "valid_samples_per_gpu": valid_per_step, "max_samples": S,
-                   "step_m": step_len, "beta_m": beta, "lookup": "dense" if info.lookup_mode == 2 else "hash",
-                   "parallelism": f"rays sharded over {world} GPU(s), grid replicated",
-                   "grad_reduction": ({"used": reducer["used"], "calibration_ms_per_step": reducer["calib_ms"]}
-                                      if world > 1 else None),
-                   "l2": f"no flush: inputs exceed L2 (payload+grad planes "
-                         f"{info.block_count * 512 * 32 / 1e9:.1f} GB vs 126 MB L2)"},
+        "config": workload_config(cfg, info.block_count, n_rays, valid_per_step, world),
+        "build": {"id": bid, "lookup": "dense" if info.lookup_mode == 2 else "hash",
+                  "grad_reduction": ({"used": reducer["used"], "calibration_ms_per_step": reducer["calib_ms"]}
+                                     if reducer is not None else None)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
-                     "traffic": traffic.get(dom) if traffic else None,
+                     "traffic": dram.get(dom),
+                     "traffic_capture": cap.get("file"),
                      "bytes_model": "SURVEY.md 8(d): fwd 182.8 B/valid sample + 80 B/ray; "
                                     "bwd 256 B/valid sample + 28 B/ray",
                      # measured DRAM traffic of the same kernel over its duration: the byte model
                      # charges every corner read-modify-write to HBM, L2 serves most of them, so
                      # frac (model) can exceed 1 while the DRAM itself runs at dram_frac
-                     "dram_achieved": (traffic[dom] / (dom_ms * 1e-3) / 1e9) if traffic.get(dom) else None,
-                     "dram_frac": (traffic[dom] / (dom_ms * 1e-3) / 1e9 / peak) if traffic.get(dom) else None,
-                     "l2_hit_pct": traffic.get("_l2_hit_pct", {}).get(dom) if traffic else None,
+                     "dram_achieved": (dram[dom] / (dom_ms * 1e-3) / 1e9) if dram.get(dom) else None,
+                     "dram_frac": (dram[dom] / (dom_ms * 1e-3) / 1e9 / peak) if dram.get(dom) else None,
+                     "l2_hit_pct": cap.get("l2_hit_pct", {}).get(dom),
                      "kernel_ms": dom_ms, "fwd_call_ms": fwd_ms, "bwd_ms": bwd_ms,
                      "fwd_call_frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / peak,
-                     "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
+                     "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                     # whole-step measured DRAM bytes (ncu, this build) over the device step time
+                     "step_dram_frac": (step_dram / (ms * 1e-3) / 1e9 / peak) if step_dram else None},
         "e2e": {"value": valid_total / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                 "path": "SparseDenseGrid.render_forward/backward via C-ABI with pinned host buffers, "
                         "host_async (copies of step i+1 overlap kernels of step i)"},
-        "gpu_launches": launches_per_step * args.steps,
-        "library_launches": {"cub_radix_sort": library_launches_per_step * args.steps},
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "library_launches": {"cub_radix_sort": LIBRARY_LAUNCHES_PER_STEP * args.steps},
         "clocks": clk,
     }
-    del grid
-    torch.cuda.empty_cache()
-    if world == 1 and not args.no_extra and cfg["name"] == "cfg3":
-        try:
-            line["extra_configs"] = {"cfg1_reference_case": bench_cfg1(dev, stream, cpu=not args.no_cpu_baseline),
-                                     "cfg2_image_forward": bench_cfg2(dev, stream),
-                                     "cfg4_activation_and_query": bench_cfg4(dev, stream),
-                                     "cfg3_fusion_and_denoise": bench_fusion(dev, stream,
-                                                                             cpu=not args.no_cpu_baseline),
-                                     "cfg3_refine_step": bench_refine(dev, stream)}
-        except Exception as e:  # pragma: no cover
-            line["extra_configs"] = {"error": str(e)}
     if world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_port(coords, lambda: chunks, o, d, dC, dD, dN, cfg)
+            line["cpu_baseline"], line["parity"] = cpu_leg_and_parity(grid, coords, lambda: chunks, o, d, dC, dD,
+                                                                      dN, cfg)
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+    del grid, chunks
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_extra and cfg["name"] == "cfg3":
+        extra = {}
+        for name, fn in (("cfg1_reference_case", lambda: bench_cfg1(dev, stream, cpu=not args.no_cpu_baseline)),
+                         ("cfg2_image_forward", lambda: bench_cfg2(dev, stream, cpu=not args.no_cpu_baseline)),
+                         ("cfg3_hash_lookup", lambda: bench_cfg3_hash(args, dev, stream)),
+                         ("cfg4_activation_and_query", lambda: bench_cfg4(dev, stream, cpu=not args.no_cpu_baseline)),
+                         ("cfg3_fusion_and_denoise", lambda: bench_fusion(dev, stream, cpu=not args.no_cpu_baseline)),
+                         ("cfg3_refine_step", lambda: bench_refine(dev, stream))):
+            try:
+                extra[name] = fn()
+            except Exception as e:  # pragma: no cover
+                extra[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.empty_cache()
+        line["extra_configs"] = extra
     print(json.dumps(line), flush=True)
+
+
+# ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward, k_backward_pipe,
+# k_active_count / scan / write + k_grad_zero_active (+ the reduction's kernels for N > 1);
+# plus 2 CUB radix sorts that only reorder rays
+LAUNCHES_PER_STEP = 8
+LIBRARY_LAUNCHES_PER_STEP = 10  # 2 CUB radix sorts of 24-bit keys: histogram + scan + 3 onesweep passes each
+
+
+def make_reducer(args, grid, dev, dist, rank):
+    from paper_2305_13220_b200.distributed import PeerGradReducer, reduce_active_grads
+
+    variants = {}
+    if dist.get_backend() == "nccl" or args.reduce == "nccl":
+        variants["nccl"] = lambda: reduce_active_grads(grid, dev)
+    if args.reduce in ("auto", "peer") and dist.get_backend() == "nccl":
+        try:
+            variants["peer"] = PeerGradReducer(grid, dev).reduce
+        except Exception as e:  # pragma: no cover - no IPC / P2P on this system
+            log(f"[rank {rank}] peer reduction unavailable: {e}")
+    if not variants:  # gloo test hook: host-side collectives
+        variants["host"] = lambda: reduce_active_grads(grid, dev)
+    if args.reduce == "nccl":
+        variants.pop("peer", None)
+    return {"variants": variants, "fn": next(iter(variants.values())), "used": next(iter(variants)),
+            "calib_ms": {}, "force": args.reduce}
+
+
+def calibrate_reducer(reducer, step, stream, dev, dist):
+    """Time every available reduction over a few steps and keep the fastest (max over ranks)."""
+    import torch
+
+    for name, fn in reducer["variants"].items():
+        reducer["fn"] = fn
+        for _ in range(2):
+            step(False)
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(3):
+            step(False)
+        c1.record(stream)
+        torch.cuda.synchronize(dev)
+        tt = torch.tensor([c0.elapsed_time(c1) / 3], dtype=torch.float64, device=dev)
+        _all_reduce(dist, tt, dist.ReduceOp.MAX)
+        reducer["calib_ms"][name] = float(tt.item())
+    best = min(reducer["calib_ms"], key=reducer["calib_ms"].get)
+    if reducer["force"] in reducer["variants"]:
+        best = reducer["force"]
+    reducer["fn"], reducer["used"] = reducer["variants"][best], best
 
 
 def _events_ms(stream, fn, reps):
@@ -632,6 +628,18 @@ def _events_ms(stream, fn, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def _cpu_ref_grid(cfg, coords, chunks):
+    """The reference grid code (oracle/_ref) holding the same blocks + payload (else the port)."""
+    import oracle
+
+    Grid = oracle.RefGrid if oracle.ref_available() else oracle.OracleGrid
+    rg = Grid(cfg["h"], 8, cfg["C"], capacity=max(len(coords), 1 << 21))
+    rg.allocate_blocks(coords)
+    for f, nb, p in chunks:
+        rg.set_payload(f, nb, **p)
+    return Grid, rg, "reference" if Grid is oracle.RefGrid else "port"
+
+
 def bench_cfg1(dev, stream, cpu=True):
     """configs[0] (the reference's CPU-runnable case): 5x5x3 m room, 2 cm voxels (R=2 from 24
     ring frames), 4096 rays from the 24 ring poses, fwd+bwd.  GPU: device time per step
@@ -642,7 +650,7 @@ def bench_cfg1(dev, stream, cpu=True):
     from paper_2305_13220_b200 import SparseDenseGrid
     from fixtures import uniform_floats
 
-    cfg = dict(CFG3, room=(5.0, 5.0, 3.0), h=0.02, act_frames=24, ray_poses=24)
+    cfg = CFG1
     scene = make_scene(cfg)
     cams, depth = activation_frames(scene, cfg)
     g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
@@ -683,54 +691,48 @@ def bench_cfg1(dev, stream, cpu=True):
     except Exception as e:  # pragma: no cover
         out["cuda_graph"] = {"error": str(e)[:200]}
     if cpu:
-        import oracle
-
-        Grid = oracle.RefGrid if oracle.ref_available() else oracle.OracleGrid
-        rg = Grid(cfg["h"], 8, cfg["C"], capacity=1 << 21)
-        rg.allocate_blocks(coords)
-        for f, nb, p in chunks:
-            rg.set_payload(f, nb, **p)
+        Grid, rg, kind = _cpu_ref_grid(cfg, coords, chunks)
         res = {}
         for cores in (os.cpu_count() or 1, 1):
             Grid.set_threads(cores)
             best = None
             for _ in range(3):
                 t0 = time.perf_counter()
-                if Grid is oracle.RefGrid:
-                    f = rg.render_forward(o, d, step, S, beta)
+                f = rg.render_forward(o, d, step, S, beta)
+                if kind == "reference":
                     rg.render_backward(dC, dD, dN)
                 else:
-                    f = rg.render_forward(o, d, step, S, beta)
                     rg.render_backward(o, d, step, S, beta, dC, dD, dN)
                 dt = time.perf_counter() - t0
                 best = dt if best is None else min(best, dt)
             res[cores] = (int(f["n_valid"].sum()) / best, best)
         Grid.set_threads(1)
         allc = os.cpu_count() or 1
-        out["cpu_baseline"] = {"value": res[allc][0], "unit": "samples/s", "cores": allc,
-                               "kind": "reference" if Grid is oracle.RefGrid else "port",
+        out["cpu_baseline"] = {"value": res[allc][0], "unit": "samples/s", "cores": allc, "kind": kind,
                                "ms_per_step": res[allc][1] * 1e3,
                                "single_core": {"value": res[1][0], "ms_per_step": res[1][1] * 1e3},
                                "sample": "the whole cfg1 step (4096 rays fwd+bwd), best of 3"}
     del g
-    torch.cuda.empty_cache()
     return out
 
 
-def bench_cfg2(dev, stream):
+def bench_cfg2(dev, stream, cpu=True):
     """configs[1]: 5x5x3 m room, 2 cm voxels (R=2 from 24 ring frames), one full 640x480
-    image from camera_for_frame(0), forward only (color/depth/normal)."""
+    image from camera_for_frame(0), forward only (color/depth/normal).  CPU: the reference grid
+    code + spec renderer (oracle/_ref) on the same image, all host cores and 1 core."""
     import torch
 
     from paper_2305_13220_b200 import SparseDenseGrid
 
-    cfg = dict(CFG3, room=(5.0, 5.0, 3.0), h=0.02, act_frames=24, ray_poses=24)
+    cfg = CFG1
     scene = make_scene(cfg)
     cams, depth = activation_frames(scene, cfg)
     g = SparseDenseGrid(cfg["h"], 8, cfg["C"], device=dev.index)
     g.set_stream(stream)
     g.allocate_for_frames(depth, cams, cfg["dilation"])
-    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    coords = g.coords()
+    chunks = []
+    fill_in_chunks(scene, cfg, coords, lambda f, n, p: (g.set_payload(f, n, **p), chunks.append((f, n, p))))
     o, d = scene.image_rays(0)
     od, dd = torch.from_numpy(o).to(dev), torch.from_numpy(d).to(dev)
     n = len(o)
@@ -738,22 +740,105 @@ def bench_cfg2(dev, stream):
             for k, s in (("rgb", (n, 3)), ("depth", (n,)), ("normal", (n, 3)), ("wsum", (n,)))}
     outs["n_samples"] = None
     g.set_tuning("records", 0)  # inference: no backward context needed
-    g.set_tuning("ray_sort", 0)  # a full image in raster order is coherent already: 0.56 vs 0.71 ms sorted
+    g.set_tuning("ray_sort", 0)  # a full image in raster order is coherent already
     ms = _events_ms(stream, lambda: g.render_forward(od, dd, cfg["h"] / 2, 64, 2 * cfg["h"], out=outs), 20)
     st = g.render_stats()
-    return {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),
-            "ms_per_image": ms, "rays_per_s": n / (ms * 1e-3),
-            "samples_per_s": st.valid_samples / (ms * 1e-3)}
+    peak, _ = peaks()
+    fwd_bytes = st.valid_samples * FWD_B_SAMPLE + n * FWD_B_RAY
+    out = {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),
+           "ms_per_image": ms, "rays_per_s": n / (ms * 1e-3),
+           "samples_per_s": st.valid_samples / (ms * 1e-3),
+           "roofline": {"bound": "hbm", "achieved": fwd_bytes / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": fwd_bytes / (ms * 1e-3) / 1e9 / peak,
+                        "bytes_model": "SURVEY.md 8(d) forward-only: 182.8 B/valid sample + 80 B/ray"}}
+    if cpu:
+        Grid, rg, kind = _cpu_ref_grid(cfg, coords, chunks)
+        res = {}
+        for cores in (os.cpu_count() or 1, 1):
+            Grid.set_threads(cores)
+            t0 = time.perf_counter()
+            f = rg.render_forward(o, d, cfg["h"] / 2, 64, 2 * cfg["h"])
+            dt = time.perf_counter() - t0
+            res[cores] = (n / dt, int(f["n_valid"].sum()) / dt, dt)
+        Grid.set_threads(1)
+        allc = os.cpu_count() or 1
+        out["cpu_baseline"] = {"value": res[allc][0], "unit": "rays/s", "cores": allc, "kind": kind,
+                               "samples_per_s": res[allc][1], "ms_per_image": res[allc][2] * 1e3,
+                               "single_core": {"value": res[1][0], "unit": "rays/s", "ms_per_image": res[1][2] * 1e3},
+                               "sample": "the whole 640x480 image, forward only"}
+    del g
+    return out
 
 
-def bench_cfg4(dev, stream, n_frames=300, k=256):
-    """configs[3]: block activation + hash insert from 300 GT depth frames (640x480) into an
-    empty 1 cm grid (R=2), then a k^3 query_sdf_with_gradient sweep over the bounds."""
+def bench_cfg3_hash(args, dev, stream, steps=10):
+    """The headline cfg3 step with the hash table as the block lookup (SVR_LOOKUP_HASH) instead
+    of the dense AABB index: same rays, same grid, every march / forward block lookup and the
+    neighbour table go through the open-addressing table (K1)."""
     import torch
 
     from paper_2305_13220_b200 import SparseDenseGrid
 
-    cfg = dict(CFG3, ray_poses=n_frames)
+    cfg = CFG3
+    scene = make_scene(cfg)
+    cams, depth = activation_frames(scene, cfg)
+    g = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22, device=dev.index)
+    g.set_stream(stream)
+    g.set_lookup(1)
+    g.allocate_for_frames(depth, cams, cfg["dilation"])
+    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+    o, d, dC, dD, dN = (torch.from_numpy(a).to(dev) for a in rays_for_rank(scene, cfg, 0, 1))
+    S, step_len, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
+    g.grad_zero()
+    ev = []
+
+    def one():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        g.render_forward(o, d, step_len, S, beta, out={"n_samples": None})
+        e[1].record(stream)
+        g.render_backward(dC, dD, dN)
+        e[2].record(stream)
+        g.grad_zero_active()
+        ev.append(e)
+
+    ms = _events_ms(stream, one, steps)
+    g.join()
+    torch.cuda.synchronize()
+    ev = ev[2:]
+    st = g.render_stats()
+    info = g.info()
+    peak, _ = peaks()
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    bwd_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    bwd_bytes = st.valid_samples * BWD_B_SAMPLE + len(o) * BWD_B_RAY
+    step_bytes = st.valid_samples * STEP_B_SAMPLE + len(o) * STEP_B_RAY
+    out = {"lookup": "hash" if info.lookup_mode == 1 else "dense", "hash_slots": int(info.hash_slots),
+           "blocks": int(info.block_count), "rays": len(o), "valid_samples": int(st.valid_samples),
+           "ms_per_step": ms, "samples_per_s": st.valid_samples / (ms * 1e-3), "fwd_call_ms": fwd_ms,
+           "bwd_ms": bwd_ms,
+           "roofline": {"bound": "hbm", "kernel": "k_backward_pipe", "peak": peak, "unit": "GB/s",
+                        "achieved": bwd_bytes / (bwd_ms * 1e-3) / 1e9,
+                        "frac": bwd_bytes / (bwd_ms * 1e-3) / 1e9 / peak,
+                        "step_frac": step_bytes / (ms * 1e-3) / 1e9 / peak}}
+    cap = traffic_from_profiles("cfg3_hash", len(o), build_id())
+    if cap:
+        out["roofline"]["ncu"] = {"file": cap.get("file"), "dram_bytes": cap.get("dram_bytes"),
+                                  "l2_hit_pct": cap.get("l2_hit_pct")}
+    del g
+    return out
+
+
+def bench_cfg4(dev, stream, n_frames=300, k=256, cpu=True):
+    """configs[3]: block activation + hash insert from 300 GT depth frames (640x480) into an
+    empty 1 cm grid (R=2), then a k^3 query_sdf_with_gradient sweep over the bounds.  CPU: the
+    reference's allocate_for_frames (allocation.cpp:56-83, single thread as written) on the
+    same 300 frames -- its coordinate set is also compared with the GPU's (`parity`) -- and its
+    query_sdf_with_gradient (grid.cpp:250-261) on a bounded point sample."""
+    import torch
+
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    cfg = CFG4
     scene = make_scene(cfg)
     cams = scene.cameras(n_frames)
     depth = scene.depth(cams)
@@ -763,12 +848,17 @@ def bench_cfg4(dev, stream, n_frames=300, k=256):
         g = SparseDenseGrid(cfg["h"], 8, cfg["C"], capacity=1 << 22, device=dev.index)
         g.set_stream(stream)
         torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
+        e0.record(stream)
         rep = g.allocate_for_frames(depth_d, cams, cfg["dilation"])
+        e1.record(stream)
         torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-    act_s = min(times)
-    fill_in_chunks(scene, cfg, g.coords(), lambda f, n, p: g.set_payload(f, n, **p))
+        times.append((time.perf_counter() - t0, e0.elapsed_time(e1) * 1e-3))
+    act_s = min(t[0] for t in times)
+    act_dev_s = min(t[1] for t in times)
+    coords = g.coords()
+    fill_in_chunks(scene, cfg, coords, lambda f, n, p: g.set_payload(f, n, **p))
     info = g.info()
     L = cfg["h"] * 8
     lo = np.array(info.bounds_lo) * L
@@ -783,11 +873,55 @@ def bench_cfg4(dev, stream, n_frames=300, k=256):
 
     ms = _events_ms(stream, lambda: check(g._lib.svr_query(g._h, x.data_ptr(), len(pts), sdf.data_ptr(),
                                                            grad.data_ptr(), None, None, valid.data_ptr())), 5)
-    return {"frames": n_frames, "pixels": int(rep.pixels_used), "blocks": int(rep.blocks_added),
-            "activation_ms": act_s * 1e3, "pixels_per_s": rep.pixels_used / act_s,
-            "blocks_per_s": rep.blocks_added / act_s, "query_points": len(pts),
-            "query_valid": int(valid.sum().item()), "query_ms": ms,
-            "query_points_per_s": len(pts) / (ms * 1e-3)}
+    peak, _ = peaks()
+    C = cfg["C"]
+    act_bytes_all = depth.size * ACT_B_PIXEL + rep.blocks_added * (16 + 12 + 512 * (20 + 4 * C))
+    q_bytes = len(pts) * QUERY_B_POINT
+    out = {"frames": n_frames, "pixels": int(depth.size), "pixels_used": int(rep.pixels_used),
+           "blocks": int(rep.blocks_added), "activation_ms": act_s * 1e3, "activation_device_ms": act_dev_s * 1e3,
+           "pixels_per_s": depth.size / act_s, "blocks_per_s": rep.blocks_added / act_s,
+           "query_points": len(pts), "query_valid": int(valid.sum().item()), "query_ms": ms,
+           "query_points_per_s": len(pts) / (ms * 1e-3),
+           "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                        "bytes_model": "SURVEY.md 8(d) cfg4: 4 B/pixel + per new block 16 + 12 + 512 (20 + 4C) B; "
+                                       "query 127 B/point",
+                        "activation_achieved": act_bytes_all / act_s / 1e9,
+                        "activation_frac": act_bytes_all / act_s / 1e9 / peak,
+                        "query_achieved": q_bytes / (ms * 1e-3) / 1e9,
+                        "query_frac": q_bytes / (ms * 1e-3) / 1e9 / peak}}
+    if cpu:
+        import oracle
+
+        Grid = oracle.RefGrid if oracle.ref_available() else oracle.OracleGrid
+        kind = "reference" if Grid is oracle.RefGrid else "port"
+        rg = Grid(cfg["h"], 8, C, capacity=1 << 22)
+        Grid.set_threads(1)
+        t0 = time.perf_counter()
+        rrep = rg.allocate_frames(depth, cams, cfg["dilation"])
+        dt = time.perf_counter() - t0
+        rc = rg.coords()
+        m21 = 0x1FFFFF
+        key = lambda c: np.sort(((c[:, 0].astype(np.int64) & m21) << 42) | ((c[:, 1].astype(np.int64) & m21) << 21)  # noqa: E731
+                                | (c[:, 2].astype(np.int64) & m21))
+        out["parity"] = {"coordinate_set_equal": bool(len(rc) == len(coords) and np.array_equal(key(rc), key(coords))),
+                         "report_equal": bool((rrep.blocks_added, rrep.blocks_requested, rrep.pixels_used) ==
+                                              (rep.blocks_added, rep.blocks_requested, rep.pixels_used)),
+                         "blocks": int(len(rc)), "oracle": f"{kind} allocate_for_frames on the same 300 frames"}
+        out["cpu_baseline"] = {"value": depth.size / dt, "unit": "pixels/s", "cores": 1, "kind": kind,
+                               "blocks_per_s": rrep.blocks_added / dt, "activation_ms": dt * 1e3,
+                               "sample": "allocate_for_frames over all 300 frames (single thread, as written)"}
+        # query sweep on a bounded sample (the reference query is a serial loop)
+        fill_in_chunks(scene, cfg, rc, lambda f, n, p: rg.set_payload(f, n, **p))
+        sub = pts[:: max(1, len(pts) // (1 << 20))]
+        t0 = time.perf_counter()
+        q = rg.query(sub)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline_query"] = {"value": len(sub) / dt, "unit": "points/s", "cores": 1, "kind": kind,
+                                     "valid": int(q["valid"].sum()),
+                                     "sample": f"every {max(1, len(pts) // (1 << 20))}th point of the sweep "
+                                               f"({len(sub)} points) through query_sdf_with_gradient"}
+    del g
+    return out
 
 
 def bench_fusion(dev, stream, cpu=True):
@@ -923,21 +1057,37 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2 / cfg4 side measurements")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU timing / parity legs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg1/2/4, hash, fusion and refine rows")
     ap.add_argument("--reduce", default="auto", choices=["auto", "peer", "nccl"],
                     help="N > 1 gradient reduction: fused peer-memory kernel, NCCL, or the faster of both")
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS),
                     help="cfg3: 1M rays per GPU (weak scaling, default); cfg5: 8M rays split over the GPUs")
+    ap.add_argument("--lookup", default="auto", choices=["auto", "hash"],
+                    help="block lookup: dense AABB index when it fits (auto) or the hash table")
     ap.add_argument("--rays-per-pose", type=int, default=None)
-    ap.add_argument("--act-frames", type=int, default=CFG3["act_frames"])
+    ap.add_argument("--dry-run", action="store_true", help="print the resolved rank / world and exit")
     args = ap.parse_args()
     base = CFG5 if args.workload == "cfg5" else CFG3
-    cfg = dict(base, name=args.workload, act_frames=args.act_frames,
-               rays_per_pose=args.rays_per_pose or base["rays_per_pose"])
+    cfg = dict(base, rays_per_pose=args.rays_per_pose or base["rays_per_pose"])
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch under torch.distributed.run with --gpus ranks
+        import socket
+
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: one rank per GPU expected")
+    if args.dry_run:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local_rank, "impl": args.impl}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return

@@ -541,9 +541,7 @@ class RefScene:
             raise OracleError(st, self.lib().svrr_last_error().decode())
 
     def camera_for_frame(self, frame: int):
-        from paper_2305_13220_b200._lib import Camera  # the svr_camera layout (a plain struct)
-
-        c = Camera()
+        c = _Cam()  # the svr_camera layout; the product package is never imported here
         self._check(self.lib().svrr_scene_camera(self._h, frame, ctypes.addressof(c)))
         return c
 
@@ -554,7 +552,7 @@ class RefScene:
     def frames(self, cams, threads=0, label_channels=None, normals=False, what=("depth", "rgb", "sem")):
         C = self.spec.label_channels if label_channels is None else label_channels
         F, H, W = len(cams), self.spec.height, self.spec.width
-        arr = (type(cams[0]) * F)(*cams)
+        arr = (_Cam * F)(*[_Cam.from_any(c) for c in cams])
         out = {"depth": np.empty((F, H, W), np.float32) if "depth" in what else None,
                "rgb": np.empty((F, H, W, 3), np.float32) if "rgb" in what else None,
                "sem": np.empty((F, H, W, C), np.float32) if "sem" in what else None,

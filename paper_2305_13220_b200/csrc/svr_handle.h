@@ -202,6 +202,7 @@ struct svr_grid {
     uint64_t sort_min_rays = 32768;  // smaller batches are rendered in caller order
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
+    int bwd_scatter = 0;      // A/B: 0 parity-keyed warp hand-off, 1 cell-keyed
     int num_sms = 148;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;

@@ -332,13 +332,15 @@ struct SampleVal {
     float fx, fy, fz;
     float s, gx, gy, gz, r, gc, b;
     uint32_t smask;
-    uint32_t e0;  // block entry of the base voxel (kInvalid: invalid sample)
+    uint32_t bpar;  // parity of the base voxel: (bx & 1) | (by & 1) << 1 | (bz & 1) << 2
+    uint32_t e0;    // block entry of the base voxel (kInvalid: invalid sample)
 };
 
 __device__ __forceinline__ void zero_sample(SampleVal& v) {
     v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
     v.fx = v.fy = v.fz = 0.f;
     v.smask = 0;
+    v.bpar = 0;
     v.e0 = kInvalid;
 }
 
@@ -357,6 +359,7 @@ __device__ __forceinline__ void cell_geom(const GridView& g, const double o[3], 
     v.fx = fr[0], v.fy = fr[1], v.fz = fr[2];
     const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
     v.smask = (lx == 7 ? 1u : 0u) | (ly == 7 ? 2u : 0u) | (lz == 7 ? 4u : 0u);
+    v.bpar = (lx & 1u) | ((ly & 1u) << 1) | ((lz & 1u) << 2);
 }
 
 // Corner c of the cell lies in block (base + bits(c)) >> 3; only axes with local
@@ -746,6 +749,79 @@ __device__ __forceinline__ void scatter_pair_agg(float4* grad, const SampleVal& 
     scatter_corner_agg<7>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
 }
 
+// Parity-ordered scatter.  Every voxel of a cell has a distinct coordinate parity
+// p = (vx & 1) | (vy & 1) << 1 | (vz & 1) << 2, and a voxel shared by two cells has the same
+// parity in both -- so "the parity-p corner" is a label that persists as the ray moves from cell
+// to cell, whereas the corner index c = p ^ parity(base) flips on every face crossing.  Along a
+// ray the samples touching one voxel are consecutive (the 2x2x2 cells around it form a convex
+// box), so keying the warp hand-off by the parity-p voxel address merges the corners two
+// face-adjacent cells share, not only identical cells.  to_parity_order permutes the gidx
+// array (XOR butterfly on the base parity) and make_coef_par swaps the 1-D weight factors /
+// derivative signs of the odd axes, so corner_grad<p> yields the parity-p corner's gradient.
+__device__ __forceinline__ void to_parity_order(SampleVal& v) {
+    uint32_t* g = v.gidx;
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1) {
+        const bool sw = (v.bpar & bit) != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (!(i & bit)) {
+                const uint32_t a = g[i], b = g[i | bit];
+                g[i] = sw ? b : a;
+                g[i | bit] = sw ? a : b;
+            }
+    }
+}
+__device__ __forceinline__ CornerCoef make_coef_par(const SampleVal& v, float ds, float wk, const float dC[3],
+                                                   const float dN[3], float ih) {
+    CornerCoef k;
+    const bool bx = v.bpar & 1u, by = v.bpar & 2u, bz = v.bpar & 4u;
+    k.x1 = bx ? 1.f - v.fx : v.fx, k.x0 = bx ? v.fx : 1.f - v.fx;
+    k.y1 = by ? 1.f - v.fy : v.fy, k.y0 = by ? v.fy : 1.f - v.fy;
+    k.z1 = bz ? 1.f - v.fz : v.fz, k.z0 = bz ? v.fz : 1.f - v.fz;
+    k.ds = ds;
+    k.wn0 = (bx ? -wk : wk) * dN[0] * ih, k.wn1 = (by ? -wk : wk) * dN[1] * ih, k.wn2 = (bz ? -wk : wk) * dN[2] * ih;
+    k.wc0 = wk * dC[0], k.wc1 = wk * dC[1], k.wc2 = wk * dC[2];
+    return k;
+}
+template <int p>
+__device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                               const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
+                                               int lane) {
+    const uint32_t a0k = ok0 ? v0.gidx[p] : kInvalid, a1k = ok1 ? v1.gidx[p] : kInvalid;
+    const float4 a0 = ok0 ? corner_grad<p>(k0) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 a1 = ok1 ? corner_grad<p>(k1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool two = ok0 && ok1 && a0k != a1k;
+    const uint32_t first = ok0 ? a0k : a1k, last = ok1 ? a1k : a0k;
+    const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
+    const bool give = lane > 0 && first != kInvalid && first == prev_last;
+    const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
+    const float4 F = two ? a0 : f4add(a0, a1);
+    const float4 in = shfl_down4(F);  // lane l+1's first run (used only when recv)
+    if (two) {
+        if (!give) atomicAdd(grad + a0k, a0);
+        atomicAdd(grad + a1k, recv ? f4add(a1, in) : a1);
+    } else if (first != kInvalid) {
+        if (give) {
+            if (recv) atomicAdd(grad + first, in);
+        } else {
+            atomicAdd(grad + first, recv ? f4add(F, in) : F);
+        }
+    }
+}
+__device__ __forceinline__ void scatter_pair_par(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                                 const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
+                                                 int lane) {
+    scatter_parity<0>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<1>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<2>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<3>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<4>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<5>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<6>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_parity<7>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+}
+
 // ---------------------------------------------------------------------------
 // K6: backward.  Chunks of 64 samples are visited back to front; within a chunk the
 // suffix S_k = sum_{m>k} w_m v_m comes from a warp suffix scan (no cancellation-prone
@@ -827,13 +903,15 @@ __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* _
         float sexc = __shfl_down_sync(kFull, sinc, 1);
         if (lane == 31) sexc = 0.f;
         const float S1 = S_after + sexc, S0 = S1 + u1;
-        const CornerCoef k0 = make_coef(v0, ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f,
-                                        w0, dC, dN, ih);
-        const CornerCoef k1 = make_coef(v1, ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f,
-                                        w1, dC, dN, ih);
+        const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
+        const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
         if (ok0) mark_blocks(g, v0);
         if (ok1) mark_blocks(g, v1);
-        scatter_pair_agg(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
+        to_parity_order(v0);
+        to_parity_order(v1);
+        const CornerCoef k0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
+        const CornerCoef k1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
+        scatter_pair_par(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
         S_after += __shfl_sync(kFull, sinc, 0);
     }
 }
@@ -900,6 +978,7 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+template <bool kPar>
 __global__ void __launch_bounds__(kPipeWarps * 32, 3)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
@@ -1005,13 +1084,21 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 3)
             float sexc = __shfl_down_sync(kFull, sinc, 1);
             if (lane == 31) sexc = 0.f;
             const float S1 = sexc, S0 = S1 + u1;
-            const CornerCoef c0 = make_coef(v0, ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f,
-                                            w0, dC, dN, ih);
-            const CornerCoef c1 = make_coef(v1, ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f,
-                                            w1, dC, dN, ih);
+            const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
+            const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
             if (ok0) mark_blocks(g, v0);
             if (ok1) mark_blocks(g, v1);
-            scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
+            if (kPar) {
+                to_parity_order(v0);
+                to_parity_order(v1);
+                const CornerCoef c0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
+                const CornerCoef c1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
+                scatter_pair_par(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
+            } else {
+                const CornerCoef c0 = make_coef(v0, ds0, w0, dC, dN, ih);
+                const CornerCoef c1 = make_coef(v1, ds1, w1, dC, dN, ih);
+                scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
+            }
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
         st = (st + 1) % kStages;
@@ -1072,7 +1159,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
                                  const uint32_t* order, const uint32_t* counts, const double* t,
                                  uint32_t S, double step, double beta, const float* d_rgb,
                                  const float* d_depth, const float* d_normal, const float4* rec,
-                                 cudaStream_t s, int num_sms) {
+                                 cudaStream_t s, int num_sms, int scatter) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
     const size_t smem = sizeof(PipeSlot) * kStages * kPipeWarps + 8 * kStages * kPipeWarps;
@@ -1083,13 +1170,16 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     const uint64_t warps_total = ctas * kPipeWarps;
     static bool attr_set = false;  // per process; the attribute is per function, not per device
     if (!attr_set) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(k_backward_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return false;
+        for (auto fn : {k_backward_pipe<true>, k_backward_pipe<false>}) {
+            const cudaError_t e =
+                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return false;
+        }
         attr_set = true;
     }
-    k_backward_pipe<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(
-        g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total);
+    auto kern = scatter == 1 ? k_backward_pipe<false> : k_backward_pipe<true>;
+    kern<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb,
+                                                                    d_depth, d_normal, rec, warps_total);
     return true;
 }
 

@@ -22,7 +22,7 @@ RTOL, ATOL_FRAC = 1e-4, 1e-6
 def cfg3():
     import torch
 
-    import bench
+    import fixtures.workloads as bench
     from paper_2305_13220_b200 import SparseDenseGrid
 
     cfg = dict(bench.CFG3)
