@@ -67,7 +67,7 @@ void backward_kernels(svr_grid* g, const float* a, const float* b, const float* 
         svr_internal::launch_render_backward_pipe(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                                   g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,
                                                   g->ctx_step, g->ctx_beta, a, b, c, g->rec.as<float4>(),
-                                                  g->stream, g->num_sms, g->bwd_scatter);
+                                                  g->stream, g->num_sms);
     if (!piped)
         svr_internal::launch_render_backward(g->view(), g->ctx_o, g->ctx_d, n, g->ctx_order,
                                              g->counts.as<uint32_t>(), g->tbuf.as<double>(), g->ctx_S,

@@ -75,6 +75,8 @@ struct GridView {
                             // allocated block per AABB cell; 0 = allocated
     float4* grad;
     uint8_t* active;
+    uint8_t* touch;         // [A][8]: a valid sample with base block b and face-crossing mask k
+                            // was scattered (k_backward*); k_touch_expand folds it into active
     int32_t lo[3], hi[3];   // block AABB (grid.hpp:222)
     int32_t dim[3];         // hi - lo + 1
     int use_dense;

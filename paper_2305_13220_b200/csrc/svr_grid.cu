@@ -141,8 +141,6 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->use_records = value != 0;
         } else if (k == "bwd_pipe") {
             g->bwd_pipe = value != 0;
-        } else if (k == "bwd_scatter") {
-            g->bwd_scatter = static_cast<int>(value);
         } else if (k == "march_jump") {
             g->use_jump = value != 0;
         } else if (k == "zero_async") {

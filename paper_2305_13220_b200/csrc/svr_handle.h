@@ -180,6 +180,7 @@ struct svr_grid {
     uint32_t* meta = nullptr;
     float4* grad = nullptr;
     uint8_t* active = nullptr;
+    uint8_t* touch = nullptr;  // [A][8] backward touch flags (GridView::touch), all zero between calls
 
     int lookup_pref = SVR_LOOKUP_AUTO;
     bool dense_dirty = true;
@@ -202,7 +203,6 @@ struct svr_grid {
     uint64_t sort_min_rays = 32768;  // smaller batches are rendered in caller order
     bool use_records = true;  // forward leaves 32 B/sample records; backward skips the re-gather
     bool bwd_pipe = true;     // persistent backward streaming records with cp.async.bulk
-    int bwd_scatter = 0;      // A/B: 0 parity-keyed warp hand-off, 1 cell-keyed
     int num_sms = 148;
     const double* ctx_o = nullptr;
     const double* ctx_d = nullptr;
@@ -291,7 +291,7 @@ struct svr_grid {
         for (void* p : {static_cast<void*>(slots), static_cast<void*>(coords4), static_cast<void*>(pay),
                         static_cast<void*>(weight), static_cast<void*>(logits), static_cast<void*>(vmask),
                         static_cast<void*>(meta), static_cast<void*>(grad), static_cast<void*>(active),
-                        sort_tmp_p})
+                        static_cast<void*>(touch), sort_tmp_p})
             if (p) cudaFree(p);
         if (own_stream && stream) cudaStreamDestroy(stream);
         if (prev >= 0) cudaSetDevice(prev);
@@ -311,6 +311,7 @@ struct svr_grid {
         v.bdist = (use_dense && use_jump) ? bdist.as<uint8_t>() : nullptr;
         v.grad = grad;
         v.active = active;
+        v.touch = touch;
         for (int a = 0; a < 3; ++a) {
             v.lo[a] = lo[a];
             v.hi[a] = hi[a];
@@ -351,6 +352,7 @@ struct svr_grid {
         grow(meta, 1);
         grow(grad, kVox);
         grow(active, 1);
+        grow(touch, 8);
         cap_blocks = nc;
     }
 
@@ -364,6 +366,7 @@ struct svr_grid {
         SVR_CK(cudaMemsetAsync(meta + first, 0, count * sizeof(uint32_t), stream));
         SVR_CK(cudaMemsetAsync(grad + first * kVox, 0, count * kVox * sizeof(float4), stream));
         SVR_CK(cudaMemsetAsync(active + first, 0, count, stream));
+        SVR_CK(cudaMemsetAsync(touch + first * 8, 0, count * 8, stream));
     }
 
     // Host mirror + AABB after blocks [first, first+count) got coords (grid.cpp:96-106).

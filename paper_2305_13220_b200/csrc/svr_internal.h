@@ -42,7 +42,7 @@ bool launch_render_backward_pipe(const svr_dev::GridView& g, const double* o, co
                                  uint64_t n, const uint32_t* order, const uint32_t* counts,
                                  const double* t, uint32_t S, double step, double beta,
                                  const float* d_rgb, const float* d_depth, const float* d_normal,
-                                 const float4* rec, cudaStream_t s, int num_sms, int scatter = 0);
+                                 const float4* rec, cudaStream_t s, int num_sms);
 // Sort rays for locality; *sorted_ids points into ids or ids_alt.  post_march: keys / ids
 // were written by the march (Morton code of each ray's first-sample block); otherwise the
 // keys are computed here from the origin hash + octahedral-direction Morton code.

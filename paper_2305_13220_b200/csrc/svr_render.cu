@@ -685,68 +685,30 @@ __device__ __forceinline__ float4 corner_grad(const CornerCoef& k) {
     return make_float4(gs, w * k.wc0, w * k.wc1, w * k.wc2);
 }
 
-__device__ __forceinline__ void mark_block(const GridView& g, uint32_t blk) {
-    if (!g.active[blk]) g.active[blk] = 1;
+// Active-block marking through the touch table: a valid sample with base block b and
+// face-crossing mask k (corners in the blocks b + bits(c), c a subset of k) sets
+// touch[8 b + k] with a plain byte store -- no load, so the warp never waits on it -- once
+// per run of equal (b, k) along the ray (a lane's pair, and the previous lane's last sample).
+// k_touch_expand then marks the blocks of every flagged (b, k) and clears the table.
+__device__ __forceinline__ uint32_t touch_key(const SampleVal& v) {
+    return ((v.e0 & ~kFullBit) << 3) | v.smask;
 }
-__device__ __forceinline__ void mark_blocks(const GridView& g, const SampleVal& v) {
-    mark_block(g, v.gidx[0] >> 9);
-    if (v.smask) {  // corners in neighbour blocks: every other corner slot may differ
-#pragma unroll
-        for (int c = 1; c < 8; ++c)
-            if (c & v.smask) mark_block(g, v.gidx[c] >> 9);
-    }
+__device__ __forceinline__ void touch_pair(const GridView& g, const SampleVal& v0, const SampleVal& v1, bool ok0,
+                                           bool ok1, int lane) {
+    const uint32_t k0 = ok0 ? touch_key(v0) : kInvalid, k1 = ok1 ? touch_key(v1) : kInvalid;
+    const uint32_t last = ok1 ? k1 : k0;
+    uint32_t prev = __shfl_up_sync(kFull, last, 1);
+    if (lane == 0) prev = kInvalid;
+    if (ok0 && k0 != prev) g.touch[k0] = 1;
+    if (ok1 && k1 != (ok0 ? k0 : prev)) g.touch[k1] = 1;
 }
 
-// Warp-aggregated scatter of one lane's sample pair.  Along a ray consecutive samples share a
-// cell ~40 % of the time, so beyond merging a lane's own two samples, the first cell run of
-// lane l is handed to lane l-1 when it continues lane l-1's last run (one shuffle-down per
-// component); lane l-1 folds it into its last run's atomics.  Every contribution is still
-// issued exactly once: a lane that handed its only run away issues just what it received.
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 __device__ __forceinline__ float4 shfl_down4(float4 v) {
     return make_float4(__shfl_down_sync(kFull, v.x, 1), __shfl_down_sync(kFull, v.y, 1),
                        __shfl_down_sync(kFull, v.z, 1), __shfl_down_sync(kFull, v.w, 1));
-}
-template <int c>
-__device__ __forceinline__ void scatter_corner_agg(float4* grad, const SampleVal& v0, const SampleVal& v1,
-                                                   const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
-                                                   bool two, bool give, bool recv) {
-    const float4 a0 = ok0 ? corner_grad<c>(k0) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 a1 = ok1 ? corner_grad<c>(k1) : make_float4(0.f, 0.f, 0.f, 0.f);
-    // first run F (address fa) and last run L (address v1.gidx[c]); one run when !two
-    const float4 F = two ? a0 : f4add(a0, a1);
-    const float4 in = shfl_down4(F);  // lane l+1's first run (used only when recv)
-    const uint32_t fa = ok0 ? v0.gidx[c] : v1.gidx[c];
-    if (two) {
-        if (!give) atomicAdd(grad + fa, a0);
-        atomicAdd(grad + v1.gidx[c], recv ? f4add(a1, in) : a1);
-    } else if (ok0 || ok1) {
-        if (give) {
-            if (recv) atomicAdd(grad + fa, in);
-        } else {
-            atomicAdd(grad + fa, recv ? f4add(F, in) : F);
-        }
-    }
-}
-__device__ __forceinline__ void scatter_pair_agg(float4* grad, const SampleVal& v0, const SampleVal& v1,
-                                                 const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
-                                                 int lane) {
-    const uint32_t first = ok0 ? v0.gidx[0] : (ok1 ? v1.gidx[0] : kInvalid);
-    const uint32_t last = ok1 ? v1.gidx[0] : first;
-    const bool two = ok0 && ok1 && v0.gidx[0] != v1.gidx[0];
-    const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
-    const bool give = lane > 0 && first != kInvalid && first == prev_last;
-    const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
-    scatter_corner_agg<0>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<1>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<2>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<3>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<4>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<5>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<6>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
-    scatter_corner_agg<7>(grad, v0, v1, k0, k1, ok0, ok1, two, give, recv);
 }
 
 // Parity-ordered scatter.  Every voxel of a cell has a distinct coordinate parity
@@ -784,13 +746,29 @@ __device__ __forceinline__ CornerCoef make_coef_par(const SampleVal& v, float ds
     k.wc0 = wk * dC[0], k.wc1 = wk * dC[1], k.wc2 = wk * dC[2];
     return k;
 }
+// red.global.add.v4.f32 under a predicate: the scatter has no divergent branches.
+__device__ __forceinline__ void red_v4_if(float4* addr, float4 v, bool p) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n}" ::"l"(addr),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<uint32_t>(p))
+        : "memory");
+}
+__device__ __forceinline__ float4 f4sel(bool c, float4 a, float4 b) {
+    return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
+}
+// Parity-p corner of the lane's two samples.  Runs: F (first, address `first`) and the last
+// run (address `last`; the same run when !two).  A lane whose first run continues the
+// previous lane's last run gives F away (`give`); the previous lane adds it (`recv`) to the
+// atomic of its last run.  Every contribution is issued exactly once, by at most two
+// predicated reductions per lane.
 template <int p>
 __device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0, const SampleVal& v1,
                                                const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
                                                int lane) {
     const uint32_t a0k = ok0 ? v0.gidx[p] : kInvalid, a1k = ok1 ? v1.gidx[p] : kInvalid;
-    const float4 a0 = ok0 ? corner_grad<p>(k0) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 a1 = ok1 ? corner_grad<p>(k1) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 a0 = ok0 ? corner_grad<p>(k0) : z;
+    const float4 a1 = ok1 ? corner_grad<p>(k1) : z;
     const bool two = ok0 && ok1 && a0k != a1k;
     const uint32_t first = ok0 ? a0k : a1k, last = ok1 ? a1k : a0k;
     const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
@@ -798,16 +776,9 @@ __device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0
     const bool recv = __shfl_down_sync(kFull, give ? 1u : 0u, 1) != 0u && lane < 31;
     const float4 F = two ? a0 : f4add(a0, a1);
     const float4 in = shfl_down4(F);  // lane l+1's first run (used only when recv)
-    if (two) {
-        if (!give) atomicAdd(grad + a0k, a0);
-        atomicAdd(grad + a1k, recv ? f4add(a1, in) : a1);
-    } else if (first != kInvalid) {
-        if (give) {
-            if (recv) atomicAdd(grad + first, in);
-        } else {
-            atomicAdd(grad + first, recv ? f4add(F, in) : F);
-        }
-    }
+    red_v4_if(grad + a0k, a0, two && !give);
+    const float4 own = two ? a1 : (give ? z : F);
+    red_v4_if(grad + last, recv ? f4add(own, in) : own, last != kInvalid && (two || !give || recv));
 }
 __device__ __forceinline__ void scatter_pair_par(float4* grad, const SampleVal& v0, const SampleVal& v1,
                                                  const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
@@ -905,8 +876,7 @@ __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* _
         const float S1 = S_after + sexc, S0 = S1 + u1;
         const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
         const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
-        if (ok0) mark_blocks(g, v0);
-        if (ok1) mark_blocks(g, v1);
+        touch_pair(g, v0, v1, ok0, ok1, lane);
         to_parity_order(v0);
         to_parity_order(v1);
         const CornerCoef k0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
@@ -978,7 +948,6 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <bool kPar>
 __global__ void __launch_bounds__(kPipeWarps * 32, 3)
     k_backward_pipe(GridView g, const double* __restrict__ O, const double* __restrict__ D, uint64_t n,
                     const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts,
@@ -1086,23 +1055,43 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 3)
             const float S1 = sexc, S0 = S1 + u1;
             const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
             const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
-            if (ok0) mark_blocks(g, v0);
-            if (ok1) mark_blocks(g, v1);
-            if (kPar) {
-                to_parity_order(v0);
-                to_parity_order(v1);
-                const CornerCoef c0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
-                const CornerCoef c1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
-                scatter_pair_par(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
-            } else {
-                const CornerCoef c0 = make_coef(v0, ds0, w0, dC, dN, ih);
-                const CornerCoef c1 = make_coef(v1, ds1, w1, dC, dN, ih);
-                scatter_pair_agg(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
-            }
+            touch_pair(g, v0, v1, ok0, ok1, lane);
+            to_parity_order(v0);
+            to_parity_order(v1);
+            const CornerCoef c0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
+            const CornerCoef c1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
+            scatter_pair_par(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
         }
         __syncwarp();  // every lane is done reading slot st before it is refilled
         st = (st + 1) % kStages;
     }
+}
+
+// Fold the backward's touch table into the active flags: (b, k) flagged -> blocks
+// b + bits(c) for every c subset of k (the neighbour table), then clear the entry.
+__global__ void __launch_bounds__(256) k_touch_expand(GridView g) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= g.n_blocks) return;
+    uint2* t = reinterpret_cast<uint2*>(g.touch) + b;
+    const uint2 v = *t;
+    if (!(v.x | v.y)) return;
+    uint32_t need = 0;  // bit c: the block of corner offset c is touched
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t byte = ((k < 4 ? v.x : v.y) >> (8 * (k & 3))) & 0xFFu;
+        if (byte)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (!(c & ~k)) need |= 1u << c;
+    }
+    g.active[b] = 1;
+#pragma unroll
+    for (int c = 1; c < 8; ++c)
+        if (need & (1u << c)) {
+            const uint32_t e = g.nbr[static_cast<size_t>(b) * 8 + c];
+            if (e != kInvalid) g.active[e & ~kFullBit] = 1;
+        }
+    *t = make_uint2(0u, 0u);
 }
 
 }  // namespace
@@ -1153,13 +1142,14 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
     else
         k_backward<false><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal,
                                                rec);
+    k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
 }
 
 bool launch_render_backward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
                                  const uint32_t* order, const uint32_t* counts, const double* t,
                                  uint32_t S, double step, double beta, const float* d_rgb,
                                  const float* d_depth, const float* d_normal, const float4* rec,
-                                 cudaStream_t s, int num_sms, int scatter) {
+                                 cudaStream_t s, int num_sms) {
     if (!n) return true;
     if (!rec || S > 64 || (S & 1)) return false;
     const size_t smem = sizeof(PipeSlot) * kStages * kPipeWarps + 8 * kStages * kPipeWarps;
@@ -1170,16 +1160,14 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     const uint64_t warps_total = ctas * kPipeWarps;
     static bool attr_set = false;  // per process; the attribute is per function, not per device
     if (!attr_set) {
-        for (auto fn : {k_backward_pipe<true>, k_backward_pipe<false>}) {
-            const cudaError_t e =
-                cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            if (e != cudaSuccess) return false;
-        }
+        const cudaError_t e = cudaFuncSetAttribute(k_backward_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
+        if (e != cudaSuccess) return false;
         attr_set = true;
     }
-    auto kern = scatter == 1 ? k_backward_pipe<false> : k_backward_pipe<true>;
-    kern<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb,
-                                                                    d_depth, d_normal, rec, warps_total);
+    k_backward_pipe<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(
+        g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total);
+    k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
     return true;
 }
 

@@ -71,5 +71,5 @@ def test_two_rank_line_on_one_gpu(workload, rpp):
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["grad_reduction"]["used"] in ("peer", "nccl")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["build"]["grad_reduction"]["used"] in ("peer", "nccl")
     assert d["scaling"] == ("strong" if workload == "cfg5" else "weak")
