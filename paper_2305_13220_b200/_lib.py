@@ -11,7 +11,10 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int32, c_uint8, c_uint32, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsvr_b200.so")
+# SVR_LIB_VARIANT=name loads libsvr_b200.<name>.so instead (side-by-side A/B builds of the
+# same sources made by profiles/ab_build.sh; never set by the tests, smoke() or bench runs)
+_VARIANT = os.environ.get("SVR_LIB_VARIANT", "")
+LIB_PATH = os.path.join(HERE, f"libsvr_b200.{_VARIANT}.so" if _VARIANT else "libsvr_b200.so")
 
 SVR_OK = 0
 SVR_ERR_CONFIG = 2

@@ -364,8 +364,7 @@ __device__ __forceinline__ void cell_geom(const GridView& g, const double o[3], 
 
 // Corner c of the cell lies in block (base + bits(c)) >> 3; only axes with local
 // coordinate 7 cross a face (smask), and those corners take their block entry from the
-// per-block neighbour table.  kCheck: verify presence + validity (weight > 0).
-template <bool kCheck>
+// per-block neighbour table; verifies presence + validity (weight > 0).
 __device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3], uint32_t e0,
                                              SampleVal& v) {
     const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
@@ -379,11 +378,11 @@ __device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3
         const uint32_t k = static_cast<uint32_t>(c) & v.smask;
         uint32_t ec = e0;
         if (k && ok) ec = __ldg(g.nbr + static_cast<size_t>(blk0) * 8 + k);
-        if (kCheck) ok = ok && ec != kInvalid;
+        ok = ok && ec != kInvalid;
         full &= ec;
         v.gidx[c] = (ec & ~kFullBit) * kVox + (X[c & 1] + Y[(c >> 1) & 1] + Z[c >> 2]);
     }
-    if (kCheck && ok && !(full & kFullBit)) {  // some corner block is partially observed
+    if (ok && !(full & kFullBit)) {  // some corner block is partially observed
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             const uint32_t gi = v.gidx[c];
@@ -393,13 +392,34 @@ __device__ __forceinline__ bool corner_addrs(const GridView& g, const int base[3
     return ok;
 }
 
+// Parity-ordered corner addresses (the backward's scatter order, see scatter_pair_par):
+// gidx[p] = the cell corner whose voxel coordinates have parities p = (px, py, pz).  On axis a
+// that voxel is the base voxel when p_a equals the base parity, else base + 1; it lies in the
+// next block exactly when the base is at local 7 and p_a is even (the base is odd there), so
+// the neighbour-table slot of parity p is smask & ~p.
+__device__ __forceinline__ void corner_addrs_par(const GridView& g, const int base[3], uint32_t e0, SampleVal& v) {
+    const uint32_t lx = base[0] & 7, ly = base[1] & 7, lz = base[2] & 7;
+    const uint32_t blk0 = e0 & ~kFullBit;
+    // local offset of the parity-q voxel per axis (upper = base + 1 wraps to 0 across a face)
+    const uint32_t X[2] = {(lx + (lx & 1u)) & 7u, (lx + (~lx & 1u)) & 7u};
+    const uint32_t Y[2] = {((ly + (ly & 1u)) & 7u) * 8u, ((ly + (~ly & 1u)) & 7u) * 8u};
+    const uint32_t Z[2] = {((lz + (lz & 1u)) & 7u) * 64u, ((lz + (~lz & 1u)) & 7u) * 64u};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t k = v.smask & (~static_cast<uint32_t>(q) & 7u);
+        const uint32_t ec = k ? __ldg(g.nbr + static_cast<size_t>(blk0) * 8 + k) : e0;
+        v.gidx[q] = (ec & ~kFullBit) * kVox + (X[q & 1] + Y[(q >> 1) & 1] + Z[q >> 2]);
+    }
+    v.bpar = (lx & 1u) | ((ly & 1u) << 1) | ((lz & 1u) << 2);
+}
+
 // Full gather + trilinear interpolation of sdf, grad(sdf) and rgb (fp32 payload math).
 __device__ __forceinline__ bool eval_sample(const GridView& g, const double o[3], const double d[3],
                                             double t, SampleVal& v) {
     int base[3];
     cell_geom(g, o, d, t, base, v);
     const uint32_t e0 = lookup_block(g, base[0] >> 3, base[1] >> 3, base[2] >> 3);
-    const bool ok = corner_addrs<true>(g, base, e0, v);
+    const bool ok = corner_addrs(g, base, e0, v);
     if (!ok) {
         v.s = v.gx = v.gy = v.gz = v.r = v.gc = v.b = 0.f;
         v.e0 = kInvalid;
@@ -465,7 +485,7 @@ __device__ __forceinline__ bool eval_from_record(const GridView& g, const double
     }
     int base[3];
     cell_geom(g, o, d, t, base, v);
-    corner_addrs<false>(g, base, e0, v);
+    corner_addrs_par(g, base, e0, v);
     v.e0 = e0;
     v.s = a.x, v.r = a.y, v.gc = a.z, v.b = a.w;
     v.gx = b.x, v.gy = b.y, v.gz = b.z;
@@ -667,15 +687,6 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
 struct CornerCoef {
     float x0, x1, y0, y1, z0, z1, ds, wn0, wn1, wn2, wc0, wc1, wc2;
 };
-__device__ __forceinline__ CornerCoef make_coef(const SampleVal& v, float ds, float wk,
-                                                const float dC[3], const float dN[3], float ih) {
-    CornerCoef k;
-    k.x1 = v.fx, k.x0 = 1.f - v.fx, k.y1 = v.fy, k.y0 = 1.f - v.fy, k.z1 = v.fz, k.z0 = 1.f - v.fz;
-    k.ds = ds;
-    k.wn0 = wk * dN[0] * ih, k.wn1 = wk * dN[1] * ih, k.wn2 = wk * dN[2] * ih;
-    k.wc0 = wk * dC[0], k.wc1 = wk * dC[1], k.wc2 = wk * dC[2];
-    return k;
-}
 template <int c>
 __device__ __forceinline__ float4 corner_grad(const CornerCoef& k) {
     const float wx = (c & 1) ? k.x1 : k.x0, wy = (c & 2) ? k.y1 : k.y0, wz = (c & 4) ? k.z1 : k.z0;
@@ -753,9 +764,7 @@ __device__ __forceinline__ void red_v4_if(float4* addr, float4 v, bool p) {
         "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<uint32_t>(p))
         : "memory");
 }
-__device__ __forceinline__ float4 f4sel(bool c, float4 a, float4 b) {
-    return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
-}
+
 // Parity-p corner of the lane's two samples.  Runs: F (first, address `first`) and the last
 // run (address `last`; the same run when !two).  A lane whose first run continues the
 // previous lane's last run gives F away (`give`); the previous lane adds it (`recv`) to the
@@ -877,8 +886,10 @@ __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* _
         const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
         const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
         touch_pair(g, v0, v1, ok0, ok1, lane);
-        to_parity_order(v0);
-        to_parity_order(v1);
+        if (!kRec) {  // records give the parity order directly
+            to_parity_order(v0);
+            to_parity_order(v1);
+        }
         const CornerCoef k0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
         const CornerCoef k1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
         scatter_pair_par(g.grad, v0, v1, k0, k1, ok0, ok1, lane);
@@ -1056,8 +1067,6 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 3)
             const float ds0 = ok0 ? p.d0 * density_ds(v0.s, sg0, ib) * (Tn0 * vv0 - S0) : 0.f;
             const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
             touch_pair(g, v0, v1, ok0, ok1, lane);
-            to_parity_order(v0);
-            to_parity_order(v1);
             const CornerCoef c0 = make_coef_par(v0, ds0, w0, dC, dN, ih);
             const CornerCoef c1 = make_coef_par(v1, ds1, w1, dC, dN, ih);
             scatter_pair_par(g.grad, v0, v1, c0, c1, ok0, ok1, lane);
