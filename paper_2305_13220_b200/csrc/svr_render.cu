@@ -866,10 +866,13 @@ __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* _
         const float incl = warp_incl_scan(tau0 + tau1, lane);
         float excl = __shfl_up_sync(kFull, incl, 1);
         if (lane == 0) excl = 0.f;
-        const float P0 = tau_base + excl, P1 = P0 + tau0;
-        const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
-        const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
-        const float Tn0 = expf(-P1), Tn1 = expf(-(P1 + tau1));
+        const float P0 = tau_base + excl;
+        // T_k = exp(-P_k); T_(k+1) = T_k e^(-tau_k) = T_k + T_k m_k with m_k = expm1(-tau_k),
+        // w_k = -T_k m_k (one exp per lane; an invalid sample has tau = 0, m = 0)
+        const float T0 = expf(-P0), m0 = expm1f(-tau0), m1 = expm1f(-tau1);
+        const float Tn0 = fmaf(T0, m0, T0), Tn1 = fmaf(Tn0, m1, Tn0);
+        const float w0 = ok0 ? -T0 * m0 : 0.f;
+        const float w1 = ok1 ? -Tn0 * m1 : 0.f;
         const float vv0 = ok0 ? dC[0] * v0.r + dC[1] * v0.gc + dC[2] * v0.b +
                                     dD * static_cast<float>(p.t0) + dN[0] * v0.gx + dN[1] * v0.gy +
                                     dN[2] * v0.gz
@@ -1049,10 +1052,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32, 3)
             const float incl = warp_incl_scan(tau0 + tau1, lane);
             float excl = __shfl_up_sync(kFull, incl, 1);
             if (lane == 0) excl = 0.f;
-            const float P0 = excl, P1 = P0 + tau0;
-            const float w0 = ok0 ? expf(-P0) * -expm1f(-tau0) : 0.f;
-            const float w1 = ok1 ? expf(-P1) * -expm1f(-tau1) : 0.f;
-            const float Tn0 = expf(-P1), Tn1 = expf(-(P1 + tau1));
+            const float P0 = excl;
+            // T_k = exp(-P_k); T_(k+1) = T_k e^(-tau_k) = T_k + T_k m_k with m_k = expm1(-tau_k),
+            // w_k = -T_k m_k (one exp per lane; an invalid sample has tau = 0, m = 0)
+            const float T0 = expf(-P0), m0 = expm1f(-tau0), m1 = expm1f(-tau1);
+            const float Tn0 = fmaf(T0, m0, T0), Tn1 = fmaf(Tn0, m1, Tn0);
+            const float w0 = ok0 ? -T0 * m0 : 0.f;
+            const float w1 = ok1 ? -Tn0 * m1 : 0.f;
             const float vv0 = ok0 ? dC[0] * v0.r + dC[1] * v0.gc + dC[2] * v0.b + dD * static_cast<float>(p.t0) +
                                         dN[0] * v0.gx + dN[1] * v0.gy + dN[2] * v0.gz
                                   : 0.f;
