@@ -563,9 +563,9 @@ def run_ours(args, cfg, rank, world, local_rank):
 
 
 # ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward, k_backward_pipe,
-# k_active_count / scan / write + k_grad_zero_active (+ the reduction's kernels for N > 1);
-# plus 2 CUB radix sorts that only reorder rays
-LAUNCHES_PER_STEP = 8
+# k_touch_expand, k_active_count / scan / write + k_grad_zero_active (+ the reduction's kernels
+# for N > 1); plus 2 CUB radix sorts that only reorder rays
+LAUNCHES_PER_STEP = 9
 LIBRARY_LAUNCHES_PER_STEP = 10  # 2 CUB radix sorts of 24-bit keys: histogram + scan + 3 onesweep passes each
 
 
@@ -575,7 +575,7 @@ def make_reducer(args, grid, dev, dist, rank):
     variants = {}
     if dist.get_backend() == "nccl" or args.reduce == "nccl":
         variants["nccl"] = lambda: reduce_active_grads(grid, dev)
-    if args.reduce in ("auto", "peer") and dist.get_backend() == "nccl":
+    if args.reduce in ("auto", "peer"):  # sync-free peer group (CUDA IPC; gloo host barriers)
         try:
             variants["peer"] = PeerGradReducer(grid, dev).reduce
         except Exception as e:  # pragma: no cover - no IPC / P2P on this system

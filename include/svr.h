@@ -194,7 +194,9 @@ int svr_render_get_stats(svr_grid* g, svr_render_stats* out);
 int svr_grad_zero(svr_grid* g);
 int svr_grad_get(svr_grid* g, float* g_sdf, float* g_rgb);
 /* Active blocks (touched by a valid sample since the last grad_zero):
- * mask[A] (0/1, optional) and/or the ascending index list + count. */
+ * mask[A] (0/1, optional) and/or the ascending index list + count.  When every requested
+ * output is device memory the call is stream-ordered with no host synchronisation (list then
+ * receives A slots, entries past *count unspecified); a host count or list synchronises. */
 int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* count);
 /* Multi-GPU plumbing (device pointers): mark blocks from a union mask, then pack /
  * unpack the gradients of `blocks[n]` as [n][512][4] floats (g_sdf, g_r, g_g, g_b). */
@@ -243,6 +245,54 @@ int svr_ipc_open(const void* handle, int32_t device, void** ptr_out);
 int svr_ipc_close(void* ptr);
 int svr_grad_peer_allreduce(svr_grid* g, void* const* peer_planes, uint32_t world, uint32_t rank,
                             const uint32_t* rows, uint64_t n_rows);
+
+/* ---- the whole reduction without host synchronisation ----
+ * svr_reduce_grads: one process driving one handle per device (the replicas of one grid):
+ * afterwards every handle holds the summed gradients of all handles in its active blocks
+ * and the union active set.  Every step is stream-ordered on the handles' streams (cross-
+ * device event waits, no host synchronisation) when the devices reach each other's memory
+ * (NVLink / NVSwitch peer access, or handles sharing a device): union of the u8 flags by peer
+ * reads, ascending compaction, each handle sums its 1/n slice of the rows over the n planes in
+ * handle order and stores the sum into all n planes.  Otherwise (or mode SVR_REDUCE_NCCL) it
+ * uses NCCL, loaded at run time: ncclCommInitAll over the handles' devices (one handle per
+ * device), grouped ncclAllReduce(MAX) of the flags, pack -> grouped ncclAllReduce(SUM) ->
+ * unpack; that path reads the union count on the host once.  Replaces the reference's
+ * per-worker accumulation (proj/src/core/parallel.cpp:35-63). */
+#define SVR_REDUCE_AUTO 0
+#define SVR_REDUCE_PEER 1
+#define SVR_REDUCE_NCCL 2
+int svr_reduce_grads(svr_grid* const* grids, uint32_t n);
+int svr_reduce_grads_ex(svr_grid* const* grids, uint32_t n, int32_t mode);
+
+/* Multi-process form (one rank per GPU, e.g. torchrun): every rank exports its handle's
+ * gradient plane, active flags and two interprocess events (svr_peer_export_get), the
+ * exports are exchanged by any host channel, and svr_peer_group_open maps the others'.  One
+ * reduction is three phases per rank, each stream-ordered:
+ *   SVR_REDUCE_PUBLISH  record "backward done"
+ *   SVR_REDUCE_SUM      wait every rank's "done"; union, compaction, own slice of the sum
+ *                       over all planes; record "reduced"
+ *   SVR_REDUCE_ADOPT    wait every rank's "reduced"; adopt the union active set
+ * The caller runs a host-side barrier between consecutive phases (every rank must have
+ * recorded an event before any rank waits on it) -- a CPU rendezvous, not a device
+ * synchronisation.  A group is valid while the grid does not grow. */
+#define SVR_REDUCE_PUBLISH 0
+#define SVR_REDUCE_SUM 1
+#define SVR_REDUCE_ADOPT 2
+typedef struct svr_peer_export {
+    uint8_t grad[64];        /* cudaIpcMemHandle_t of the gradient plane */
+    uint8_t active[64];      /* cudaIpcMemHandle_t of the u8 active flags */
+    uint8_t ev_done[64];     /* cudaIpcEventHandle_t, phase PUBLISH */
+    uint8_t ev_reduced[64];  /* cudaIpcEventHandle_t, phase SUM */
+    uint64_t n_blocks;
+    int32_t device;
+    int32_t reserved;
+} svr_peer_export;
+typedef struct svr_peer_group svr_peer_group;
+int svr_peer_export_get(svr_grid* g, svr_peer_export* out);
+int svr_peer_group_open(svr_grid* g, const svr_peer_export* all, uint32_t world, uint32_t rank,
+                        svr_peer_group** out);
+int svr_peer_reduce_phase(svr_peer_group* pg, int32_t phase);
+int svr_peer_group_close(svr_peer_group* pg);
 
 /* ---- fusion + de-noising (SPEC.md:207-233 module "fusion", PAPER Eq. 9-11, sec. 3.4.3) ----
  * The reference declares the state (VoxelBlock::sum_*, grid.hpp:59-68) but ships no code;

@@ -270,4 +270,14 @@ inline void export_ply(SparseDenseGrid& grid, const std::string& path) {
     check(svr_mesh_save_ply(grid.handle(), path.c_str()));
 }
 
+// Multi-GPU: sum the active-block gradients of the replicas (one per device) into every
+// replica -- the cross-GPU form of the reference's per-worker accumulation
+// (parallel.cpp:35-63).  Stream-ordered, no host synchronisation, when the
+// devices reach each other's memory; NCCL otherwise (svr.h svr_reduce_grads_ex).
+inline void reduce_grads(const std::vector<SparseDenseGrid*>& replicas, int mode = SVR_REDUCE_AUTO) {
+    std::vector<svr_grid*> hs;
+    for (SparseDenseGrid* g : replicas) hs.push_back(g->handle());
+    check(svr_reduce_grads_ex(hs.data(), static_cast<std::uint32_t>(hs.size()), mode));
+}
+
 }  // namespace svr::b200

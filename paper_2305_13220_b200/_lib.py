@@ -101,6 +101,17 @@ class RefineConfig(ctypes.Structure):
                 ("mu", c_double)]
 
 
+class PeerExport(ctypes.Structure):
+    """svr_peer_export: IPC handles of one rank's gradient plane, active flags and phase events."""
+
+    _fields_ = [("grad", ctypes.c_uint8 * 64), ("active", ctypes.c_uint8 * 64), ("ev_done", ctypes.c_uint8 * 64),
+                ("ev_reduced", ctypes.c_uint8 * 64), ("n_blocks", c_uint64), ("device", c_int32),
+                ("reserved", c_int32)]
+
+
+SVR_REDUCE_AUTO, SVR_REDUCE_PEER, SVR_REDUCE_NCCL = 0, 1, 2
+SVR_REDUCE_PUBLISH, SVR_REDUCE_SUM, SVR_REDUCE_ADOPT = 0, 1, 2
+
 P = c_void_p  # every array argument: host or device address
 _I = c_int32
 
@@ -152,6 +163,12 @@ _PROTOS = {
     "svr_ipc_open": (_I, [P, c_int32, POINTER(c_void_p)]),
     "svr_ipc_close": (_I, [c_void_p]),
     "svr_grad_peer_allreduce": (_I, [c_void_p, P, c_uint32, c_uint32, P, c_uint64]),
+    "svr_reduce_grads": (_I, [P, c_uint32]),
+    "svr_reduce_grads_ex": (_I, [P, c_uint32, c_int32]),
+    "svr_peer_export_get": (_I, [c_void_p, POINTER(PeerExport)]),
+    "svr_peer_group_open": (_I, [c_void_p, P, c_uint32, c_uint32, POINTER(c_void_p)]),
+    "svr_peer_reduce_phase": (_I, [c_void_p, c_int32]),
+    "svr_peer_group_close": (_I, [c_void_p]),
     "svr_render_losses": (_I, [c_void_p, c_uint64, P, P, P, P, P, P, P, P, P, c_uint32, c_double, c_double,
                                P, P, P, POINTER(LossStats)]),
     "svr_sample_frame_rays": (_I, [c_void_p, P, c_uint32, P, P, P, c_uint32, c_uint32, c_uint64, P, P, P, P, P, P,

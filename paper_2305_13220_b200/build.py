@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["svr_render.cu", "svr_activate.cu", "svr_grads.cu", "svr_regularize.cu",
            "svr_fusion.cu", "svr_mesh.cu", "svr_losses.cu", "svr_refine.cu", "svr_grid.cu", "svr_api_render.cu",
-           "svr_api_more.cu", "svr_refine_host.cu"]
+           "svr_api_more.cu", "svr_refine_host.cu", "svr_reduce.cu"]
 OUT = os.path.join(HERE, "libsvr_b200.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -291,6 +291,15 @@ int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* coun
             auto* dcount = g->active_count.as<unsigned long long>();
             svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
             SVR_LAUNCHED();
+            if ((!count || is_device_ptr(count)) && (!list || is_device_ptr(list))) {
+                // device outputs: stream-ordered, no host read of the count (the list gets
+                // all nb slots; entries past *count are unspecified)
+                if (count) SVR_CK(cudaMemcpyAsync(count, dcount, 8, cudaMemcpyDeviceToDevice, g->stream));
+                if (list && nb)
+                    SVR_CK(cudaMemcpyAsync(list, g->active_list.p, 4ull * nb, cudaMemcpyDeviceToDevice, g->stream));
+                st.finish();
+                return;
+            }
             unsigned long long c = 0;
             SVR_CK(cudaMemcpyAsync(&c, dcount, 8, cudaMemcpyDeviceToHost, g->stream));
             SVR_CK(cudaStreamSynchronize(g->stream));

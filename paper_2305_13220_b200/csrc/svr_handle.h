@@ -212,6 +212,10 @@ struct svr_grid {
     bool ctx_valid = false;
 
     DevBuf active_list, active_count;  // count: u64 + per-CTA scratch
+    // multi-GPU reduction (svr_reduce.cu): union flags, its ascending list + device count,
+    // the NCCL fallback's pack buffer, and the two interprocess-capable phase events
+    DevBuf red_union, red_list, red_count, red_pack;
+    cudaEvent_t red_done = nullptr, red_reduced = nullptr;
     DevBuf rms;                        // RMSProp state float4 [rms_blocks][512]
     uint64_t rms_blocks = 0;
     // fusion session: 32.32 fixed-point sums [fuse_blocks][4 + C][512] + counts [.][512]
@@ -280,6 +284,8 @@ struct svr_grid {
             cudaEventDestroy(side_join);
             cudaStreamDestroy(side);
         }
+        for (cudaEvent_t e : {red_done, red_reduced})
+            if (e) cudaEventDestroy(e);
         if (h2d) {
             cudaStreamSynchronize(h2d);
             cudaStreamSynchronize(d2h);

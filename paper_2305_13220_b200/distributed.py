@@ -10,7 +10,9 @@ voxel gradients must be summed.  Only blocks touched by some rank carry gradient
 
 ``reduce_active_grads`` drives steps 1-4 for a ``SparseDenseGrid`` whose kernels run on
 torch's current stream (grid.set_stream), so NCCL and the pack/unpack kernels are
-stream-ordered.  The collective sequence itself is ``allreduce_active`` and is backend
+stream-ordered; it reads the active count on the host.  ``PeerGradReducer`` (one process per
+GPU) and ``reduce_grads`` (one process, one handle per GPU) do the whole reduction on the
+devices with no host synchronisation (csrc/svr_reduce.cu).  The collective sequence itself is ``allreduce_active`` and is backend
 agnostic, which lets tests exercise it with gloo on CPU tensors.
 """
 from __future__ import annotations
@@ -84,17 +86,22 @@ class _GridStore:
 
 
 class PeerGradReducer:
-    """The fused alternative to steps 2-4 (K8p): every rank maps the other ranks' gradient
-    planes (CUDA IPC over NVLink), and after a barrier each rank reduces its 1/world slice of
-    the common active list straight in peer memory -- sum in rank order, store to every
-    plane -- so there is no pack buffer, no unpack and no NCCL ring for the 2.4 GB payload.
-    Only the u8 mask union still goes through the process group.  Construct after the grid
-    has all its blocks (the planes must not be reallocated while mapped)."""
+    """The fused alternative to steps 1-4 (K8r, csrc/svr_reduce.cu), free of device
+    synchronisation: every rank exports its gradient plane, active flags and two
+    interprocess events (CUDA IPC), maps the other ranks', and one reduction is three
+    stream-ordered phases on the grid's own stream -- publish (record "done"), sum (wait every
+    rank's "done", union of the flags by peer reads, ascending compaction, this rank's 1/world
+    slice of the rows summed over all planes in rank order and stored into every plane, record
+    "reduced"), adopt (wait every rank's "reduced", take the union active set).  Between the
+    phases the ranks meet at a host barrier on a gloo group, so every rank has recorded an
+    event before another waits on it; no phase synchronises a device or reads a count on the
+    host, so the host keeps queueing work ahead of the GPU.  Construct after the grid has all
+    its blocks (the mapped planes must not be reallocated)."""
 
     def __init__(self, grid, device, group=None):
         import ctypes
 
-        from ._lib import check
+        from ._lib import PeerExport, check
 
         self.grid, self.device, self.group = grid, torch.device(device), group
         self.world = dist.get_world_size(group)
@@ -102,53 +109,46 @@ class PeerGradReducer:
         if self.world > 8:
             raise ValueError("PeerGradReducer: at most 8 ranks")
         lib = grid._lib
-        h = (ctypes.c_uint8 * 64)()
-        nbytes = ctypes.c_uint64()
-        check(lib.svr_grad_ipc_handle(grid._h, ctypes.addressof(h), ctypes.byref(nbytes)))
-        allh = [None] * self.world
-        dist.all_gather_object(allh, (bytes(h), nbytes.value), group=group)
-        self.ptrs = (ctypes.c_void_p * self.world)()
-        self.opened = []
-        dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
-        for q, (hb, _) in enumerate(allh):
-            if q == self.rank:
-                continue
-            p = ctypes.c_void_p()
-            buf = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
-            check(lib.svr_ipc_open(ctypes.addressof(buf), dev, ctypes.byref(p)))
-            self.ptrs[q] = p.value
-            self.opened.append(p)
-        self._gloo = dist.get_backend(group) == "gloo"
+        ex = PeerExport()
+        check(lib.svr_peer_export_get(grid._h, ctypes.byref(ex)))
+        allx = [None] * self.world
+        dist.all_gather_object(allx, bytes(ex), group=group)
+        self._exports = (PeerExport * self.world)()
+        for q, raw in enumerate(allx):
+            ctypes.memmove(ctypes.addressof(self._exports[q]), raw, ctypes.sizeof(PeerExport))
+        # host rendezvous between the phases: a CPU-only (gloo) barrier
+        self._host = group if dist.get_backend(group) == "gloo" else dist.new_group(backend="gloo")
+        self._pg = ctypes.c_void_p()
+        check(lib.svr_peer_group_open(grid._h, ctypes.addressof(self._exports), self.world, self.rank,
+                                      ctypes.byref(self._pg)))
 
-    def reduce(self) -> torch.Tensor:
-        import ctypes
+    def reduce(self) -> None:
+        from ._lib import SVR_REDUCE_ADOPT, SVR_REDUCE_PUBLISH, SVR_REDUCE_SUM, check
 
-        from ._lib import check
-
-        store = _GridStore(self.grid, self.device)
-        mask = store.mask_tensor()
-        self.grid.synchronize()  # the mask (and the backward) are complete whatever stream reads them
-        if self._gloo:
-            m = mask.cpu()
-            dist.all_reduce(m, op=dist.ReduceOp.MAX, group=self.group)
-            mask = m.to(self.device)
-        else:
-            dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=self.group)
-        store.set_mask(mask)
-        blocks = store.active_list()
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)  # every rank's backward is in its plane
-        if blocks.numel():
-            check(self.grid._lib.svr_grad_peer_allreduce(self.grid._h, ctypes.addressof(self.ptrs), self.world, self.rank,
-                                                         blocks.data_ptr(), blocks.numel()))
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)  # every slice is summed into every plane
-        return blocks
+        lib = self.grid._lib
+        check(lib.svr_peer_reduce_phase(self._pg, SVR_REDUCE_PUBLISH))
+        dist.barrier(group=self._host)  # every rank recorded "done"
+        check(lib.svr_peer_reduce_phase(self._pg, SVR_REDUCE_SUM))
+        dist.barrier(group=self._host)  # every rank recorded "reduced"
+        check(lib.svr_peer_reduce_phase(self._pg, SVR_REDUCE_ADOPT))
 
     def close(self):
-        for p in self.opened:
-            self.grid._lib.svr_ipc_close(p)
-        self.opened = []
+        if self._pg:
+            self.grid._lib.svr_peer_group_close(self._pg)
+            self._pg = None
+
+
+def reduce_grads(grids, mode: str = "auto") -> None:
+    """Single process, one SparseDenseGrid replica per device: sum the active-block gradients
+    of all handles into every handle (svr_reduce_grads_ex; stream-ordered across the devices
+    with peer access, NCCL otherwise or when mode == "nccl")."""
+    import ctypes
+
+    from ._lib import SVR_REDUCE_AUTO, SVR_REDUCE_NCCL, SVR_REDUCE_PEER, check
+
+    m = {"auto": SVR_REDUCE_AUTO, "peer": SVR_REDUCE_PEER, "nccl": SVR_REDUCE_NCCL}[mode]
+    hs = (ctypes.c_void_p * len(grids))(*[g._h for g in grids])
+    check(grids[0]._lib.svr_reduce_grads_ex(ctypes.addressof(hs), len(grids), m))
 
 
 def reduce_active_grads(grid, device, group=None) -> torch.Tensor:

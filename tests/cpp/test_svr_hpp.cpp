@@ -142,6 +142,23 @@ int main() {
         g.zero_grad();
         g.render_backward(dC, &dD, dN);
         CHECK(g.active_blocks().size() == 1);
+        // two replicas, each rendering the same ray: reduce_grads sums them into both
+        SparseDenseGrid g2(0.02, 8, 1);
+        allocate_for_points(g2, p, 1, 0);
+        fill_all(g2, [](double, double, double) { return -1.0f; });
+        g2.render_forward(o, d, 1, 0.01, 64, 1e-4, RenderOutputs{rgb, &depth, normal, &wsum, &ns});
+        g2.zero_grad();
+        g2.render_backward(dC, &dD, dN);
+        std::vector<float> s1(512), r1(1536), s2(512), r2(1536);
+        g.grads(s1.data(), r1.data());
+        reduce_grads({&g, &g2}, SVR_REDUCE_PEER);
+        g.grads(s2.data(), r2.data());
+        bool doubled = true, nonzero = false;
+        for (int i = 0; i < 1536; ++i) doubled &= r2[i] == 2.0f * r1[i], nonzero |= r1[i] != 0.0f;
+        CHECK(doubled && nonzero);
+        g2.grads(s1.data(), r1.data());
+        CHECK(s1 == s2 && r1 == r2);
+        CHECK(g2.active_blocks().size() == 1);
     }
     {  // SDGV round trip (test_grid.cpp:373)
         SparseDenseGrid g(0.0175, 8, 3);

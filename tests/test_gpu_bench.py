@@ -65,11 +65,11 @@ def test_two_rank_line_on_one_gpu(workload, rpp):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                         "--gpus", "2", "--workload", workload, "--rays-per-pose", str(rpp), "--steps", "3",
-                        "--warmup", "3", "--no-extra", "--no-cpu-baseline"],
+                        "--warmup", "3", "--no-extra", "--no-cpu-baseline", "--reduce", "peer"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["build"]["grad_reduction"]["used"] in ("peer", "nccl")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["build"]["grad_reduction"]["used"] == "peer"
     assert d["scaling"] == ("strong" if workload == "cfg5" else "weak")

@@ -1,8 +1,10 @@
-"""GPU: the peer-memory active-block all-reduce (K8p).  (1) Emulated ranks: W gradient
-planes on one GPU, one kernel launch per rank slice -- every plane ends with the rank-order
-sum.  (2) Real CUDA IPC plumbing: 2 processes on the one GPU (gloo for the host barriers),
-each mapping the other's plane; the kernels never wait on each other (host barriers between
-launches), so this is safe on a single device."""
+"""GPU: the peer-memory active-block all-reduce.  (1) Emulated ranks: W gradient planes on
+one GPU, one kernel launch per rank slice -- every plane ends with the rank-order sum.
+(2) The sync-free group (K8r, PeerGradReducer): 2 processes on the one GPU with CUDA IPC
+planes, flags and interprocess events, gloo host barriers between the phases; the kernels
+only wait on events recorded before the wait (no kernel spins on another), so this is safe
+on a single device.  (3) svr_reduce_grads: one process, several handles on the one GPU
+(peer path) and the NCCL path on one device."""
 import ctypes
 import os
 import socket
@@ -90,9 +92,11 @@ def _worker(rank, world, port, out_dir):
     g.allocate_blocks(COORDS)
     _load(g, *_rank_grads(rank, len(COORDS)))
     red = PeerGradReducer(g, "cuda:0")
-    blocks = red.reduce()
+    red.reduce()  # stream-ordered, no device synchronisation inside
     np.save(os.path.join(out_dir, f"r{rank}.npy"), _plane(g))
-    np.save(os.path.join(out_dir, f"b{rank}.npy"), blocks.cpu().numpy())
+    np.save(os.path.join(out_dir, f"b{rank}.npy"), np.flatnonzero(g.active_mask()))
+    red.reduce()  # a second step on the same group (events re-recorded): sums again
+    np.save(os.path.join(out_dir, f"s{rank}.npy"), _plane(g))
     red.close()
     dist.barrier()
     dist.destroy_process_group()
@@ -113,3 +117,75 @@ def test_peer_allreduce_ipc_two_processes_one_gpu(tmp_path):
         assert np.array_equal(got[union], tot[union]), r
         assert not got[~union].any()
         assert np.array_equal(np.load(tmp_path / f"b{r}.npy"), np.flatnonzero(union))
+        # second reduction: every plane held the sum, so the new sum is world x that
+        assert np.array_equal(np.load(tmp_path / f"s{r}.npy")[union], world * tot[union]), r
+
+
+def _render_case(lookup=None):
+    from common import scene_case
+
+    return scene_case()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_reduce_grads_single_process_handles(n):
+    """n replicas, each rendering its contiguous ray shard, summed by svr_reduce_grads (peer
+    path, stream-ordered across the handles' own streams): every replica ends with the
+    full-batch gradients and the full-batch active set."""
+    from common import assert_close, gpu_grid_from, scene_case
+
+    from paper_2305_13220_b200.distributed import reduce_grads
+
+    case = scene_case()
+    R = len(case["o"])
+    full = gpu_grid_from(case)
+    full.grad_zero()
+    full.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    full.render_backward(case["dC"], case["dD"], case["dN"])
+    gs_ref, gr_ref = full.grads()
+    act_ref = full.active_mask()
+    grids = []
+    for i in range(n):
+        a, b = R * i // n, R * (i + 1) // n
+        g = gpu_grid_from(case)
+        g.grad_zero()
+        g.render_forward(case["o"][a:b], case["d"][a:b], case["step"], 64, case["beta"])
+        g.render_backward(case["dC"][a:b], case["dD"][a:b], case["dN"][a:b])
+        grids.append(g)
+    reduce_grads(grids, "peer")
+    planes = []
+    for g in grids:
+        gs, gr = g.grads()
+        assert_close(gs, gs_ref, what="grad_sdf")
+        assert_close(gr, gr_ref, what="grad_rgb")
+        assert np.array_equal(g.active_mask(), act_ref)
+        planes.append((gs, gr))
+    for gs, gr in planes[1:]:  # rank-order sums: bitwise identical replicas
+        assert np.array_equal(gs, planes[0][0]) and np.array_equal(gr, planes[0][1])
+
+
+def test_reduce_grads_nccl_one_device():
+    """The NCCL path (dlopen'ed libnccl, ncclCommInitAll, grouped all-reduces, pack/unpack)
+    on the one device: a one-rank sum leaves the gradients and the active set unchanged;
+    two handles on one device are refused (NCCL needs one per device)."""
+    from common import gpu_grid_from, scene_case
+
+    from paper_2305_13220_b200._lib import ConfigError
+    from paper_2305_13220_b200.distributed import reduce_grads
+
+    import torch  # noqa: F401  (the process's NCCL is torch's, as in the bench)
+
+    case = scene_case()
+    g = gpu_grid_from(case)
+    g.grad_zero()
+    g.render_forward(case["o"], case["d"], case["step"], 64, case["beta"])
+    g.render_backward(case["dC"], case["dD"], case["dN"])
+    gs, gr = g.grads()
+    act = g.active_mask()
+    reduce_grads([g], "nccl")
+    gs2, gr2 = g.grads()
+    assert np.array_equal(gs2, gs) and np.array_equal(gr2, gr)
+    assert np.array_equal(g.active_mask(), act)
+    g2 = gpu_grid_from(case)
+    with pytest.raises(ConfigError):
+        reduce_grads([g, g2], "nccl")
