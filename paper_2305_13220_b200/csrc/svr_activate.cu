@@ -284,16 +284,18 @@ void launch_sort_keys(unsigned long long* keys, uint64_t n, void** tmp, size_t* 
     if (n < 2) return;
     // sort in place through a double buffer placed after the keys in tmp
     size_t need = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, need, keys, keys, static_cast<int>(n), 0, 63, s);
+    SVR_LCK(cub::DeviceRadixSort::SortKeys(nullptr, need, keys, keys, static_cast<int>(n), 0, 63, s));
     const size_t total = need + n * sizeof(unsigned long long) + 256;
     if (*tmp_bytes < total) {
         if (*tmp) cudaFree(*tmp);
-        cudaMalloc(tmp, total);
+        *tmp = nullptr;
+        *tmp_bytes = 0;
+        SVR_LCK(cudaMalloc(tmp, total));
         *tmp_bytes = total;
     }
     auto* alt = reinterpret_cast<unsigned long long*>(static_cast<char*>(*tmp) + ((need + 255) / 256) * 256);
-    cudaMemcpyAsync(alt, keys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s);
-    cub::DeviceRadixSort::SortKeys(*tmp, need, alt, keys, static_cast<int>(n), 0, 63, s);
+    SVR_LCK(cudaMemcpyAsync(alt, keys, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    SVR_LCK(cub::DeviceRadixSort::SortKeys(*tmp, need, alt, keys, static_cast<int>(n), 0, 63, s));
 }
 
 void launch_hash_insert(HashSlot* slots, unsigned long long mask, const unsigned long long* keys,

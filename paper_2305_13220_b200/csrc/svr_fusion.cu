@@ -459,7 +459,7 @@ void launch_denoise(const GridView& g, const int32_t* coords4, float4* pay_out, 
     for (int i = 0; i <= 2 * radius; ++i) a.gw[i] = gw[i];
     const size_t smem = denoise_smem_bytes(radius);
 #define SVR_DN(R)                                                                                       \
-    cudaFuncSetAttribute(k_denoise<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)); \
+    SVR_LCK(cudaFuncSetAttribute(k_denoise<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
     k_denoise<R><<<g.n_blocks, kDnThreads, smem, s>>>(a)
     switch (radius) {
         case 0: SVR_DN(0); break;

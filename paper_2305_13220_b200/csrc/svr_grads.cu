@@ -279,7 +279,7 @@ void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, nullptr, tmp, dim[0], dim[1], dim[2], 0);
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, tmp, out, dim[0], dim[1], dim[2], 1);
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, out, tmp, dim[0], dim[1], dim[2], 2);
-    cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToDevice, s);
+    SVR_LCK(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToDevice, s));
 }
 
 void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank, const uint32_t* rows,
@@ -290,7 +290,8 @@ void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank,
     const uint64_t first = n_rows * rank / world, last = n_rows * (rank + 1) / world;
     if (last <= first) return;
     const uint64_t count = last - first;
-    const unsigned grid = static_cast<unsigned>(count < 148u * 8u ? count : 148u * 8u);
+    const uint64_t cap = sm_count() * 8ull;
+    const unsigned grid = static_cast<unsigned>(count < cap ? count : cap);
     k_peer_allreduce<<<grid, 512, 0, s>>>(pl, world, rows, first, count);
 }
 
@@ -312,7 +313,7 @@ void launch_active_list(const uint8_t* active, uint32_t n, uint32_t* list,
     const uint32_t nctas = (n + 1023) / 1024;
     uint32_t* per_cta = reinterpret_cast<uint32_t*>(count + 1);
     if (nctas == 0) {
-        cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+        SVR_LCK(cudaMemsetAsync(count, 0, sizeof(unsigned long long), s));
         return;
     }
     k_active_count<<<nctas, 1024, 0, s>>>(active, n, per_cta);
@@ -341,7 +342,7 @@ void launch_grad_zero_active(float4* grad, uint8_t* active, const uint32_t* list
                              const unsigned long long* count, uint32_t n_max, cudaStream_t s,
                              unsigned ctas_per_sm) {
     if (!n_max) return;
-    const unsigned cap = 148u * ctas_per_sm;
+    const unsigned cap = sm_count() * ctas_per_sm;
     const unsigned grid = n_max < cap ? n_max : cap;
     k_grad_zero_active<<<grid, 128, 0, s>>>(grad, active, list, count);
 }

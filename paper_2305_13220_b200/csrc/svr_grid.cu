@@ -12,6 +12,17 @@ using namespace svr_host;
 namespace svr_internal {
 thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+unsigned sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    SVR_LCK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) SVR_LCK(cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev));
+    return static_cast<unsigned>(cache[dev]);
+}
+void throw_cuda(cudaError_t e, const char* what) {
+    throw svr_host::Fail{SVR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
 }  // namespace svr_internal
 
 namespace {

@@ -13,6 +13,17 @@
 namespace svr_internal {
 
 void set_error(const std::string& msg);
+// Launchers report CUDA runtime failures by throwing the ABI's status exception
+// (SVR_ERR_CUDA, caught by the entry point's guarded() wrapper); defined in svr_grid.cu.
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what);
+// SM count of the current device (cached per device): persistent / grid-stride grids are
+// sized in multiples of it.  Defined in svr_grid.cu.
+unsigned sm_count();
+#define SVR_LCK(expr)                                                            \
+    do {                                                                         \
+        const cudaError_t e_ = (expr);                                           \
+        if (e_ != cudaSuccess) ::svr_internal::throw_cuda(e_, #expr);            \
+    } while (0)
 
 struct Status {
     int code;

@@ -145,7 +145,7 @@ void launch_render_losses(uint64_t n, const float* rgb, const float* depth, cons
                           const float* wsum, const float* tgt, const float* pdepth, const float* pnormal,
                           const uint32_t* cam_idx, const svr_camera* cams, double lambda_d, double lambda_n,
                           float* d_rgb, float* d_depth, float* d_normal, double* acc, cudaStream_t s) {
-    cudaMemsetAsync(acc, 0, 16 * sizeof(double), s);
+    SVR_LCK(cudaMemsetAsync(acc, 0, 16 * sizeof(double), s));
     if (!n) return;
     LossArgs a{n, rgb, depth, normal, wsum, tgt, pdepth, pnormal, cam_idx, cams, lambda_d, lambda_n,
                d_rgb, d_depth, d_normal, acc};

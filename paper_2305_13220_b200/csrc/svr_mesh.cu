@@ -413,9 +413,9 @@ void run_marching_cubes(const GridView& g, const int32_t* coords4, const uint32_
     uint32_t* boff = sc.as<uint32_t>(A);
     k_mc_count<<<A, 512, 0, s>>>(m, btris);
     size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, btris, boff, static_cast<int>(A), s);
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, btris, boff, static_cast<int>(A), s), "scan / sort");
     void* tmp = sc.get(tb);
-    cub::DeviceScan::ExclusiveSum(tmp, tb, btris, boff, static_cast<int>(A), s);
+    ck(cub::DeviceScan::ExclusiveSum(tmp, tb, btris, boff, static_cast<int>(A), s), "scan / sort");
     uint32_t h2[2];
     ck(cudaMemcpyAsync(&h2[0], boff + A - 1, 4, cudaMemcpyDeviceToHost, s), "count");
     ck(cudaMemcpyAsync(&h2[1], btris + A - 1, 4, cudaMemcpyDeviceToHost, s), "count");
@@ -434,21 +434,21 @@ void run_marching_cubes(const GridView& g, const int32_t* coords4, const uint32_
     cub::DoubleBuffer<unsigned long long> kb(keys, keys2);
     cub::DoubleBuffer<uint32_t> vb(slots, slots2);
     tb = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, static_cast<int>(N), 0, 64, s);
+    ck(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, static_cast<int>(N), 0, 64, s), "scan / sort");
     tmp = sc.get(tb);
-    cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, static_cast<int>(N), 0, 64, s);
+    ck(cub::DeviceRadixSort::SortPairs(tmp, tb, kb, vb, static_cast<int>(N), 0, 64, s), "scan / sort");
     auto* first = sc.as<uint32_t>(N);
     auto* headpos = sc.as<uint32_t>(N);
     auto* headmax = sc.as<uint32_t>(N);
     auto* vid = sc.as<uint32_t>(N);
     k_mc_heads<<<grid_for(N, 256), 256, 0, s>>>(kb.Current(), vb.Current(), N, first, headpos);
     tb = 0;
-    cub::DeviceScan::InclusiveScan(nullptr, tb, headpos, headmax, cub::Max(), static_cast<int>(N), s);
+    ck(cub::DeviceScan::InclusiveScan(nullptr, tb, headpos, headmax, cub::Max(), static_cast<int>(N), s), "scan / sort");
     size_t tb2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb2, first, vid, static_cast<int>(N), s);
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tb2, first, vid, static_cast<int>(N), s), "scan / sort");
     tmp = sc.get(std::max(tb, tb2));
-    cub::DeviceScan::InclusiveScan(tmp, tb, headpos, headmax, cub::Max(), static_cast<int>(N), s);
-    cub::DeviceScan::ExclusiveSum(tmp, tb2, first, vid, static_cast<int>(N), s);
+    ck(cub::DeviceScan::InclusiveScan(tmp, tb, headpos, headmax, cub::Max(), static_cast<int>(N), s), "scan / sort");
+    ck(cub::DeviceScan::ExclusiveSum(tmp, tb2, first, vid, static_cast<int>(N), s), "scan / sort");
     uint32_t hv[2];
     ck(cudaMemcpyAsync(&hv[0], vid + N - 1, 4, cudaMemcpyDeviceToHost, s), "count");
     ck(cudaMemcpyAsync(&hv[1], first + N - 1, 4, cudaMemcpyDeviceToHost, s), "count");
@@ -461,9 +461,9 @@ void run_marching_cubes(const GridView& g, const int32_t* coords4, const uint32_
     auto* toff = sc.as<uint32_t>(T);
     k_mc_keep<<<grid_for(T, 256), 256, 0, s>>>(tri_idx, out.v, T, keep);
     tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, keep, toff, static_cast<int>(T), s);
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, tb, keep, toff, static_cast<int>(T), s), "scan / sort");
     tmp = sc.get(tb);
-    cub::DeviceScan::ExclusiveSum(tmp, tb, keep, toff, static_cast<int>(T), s);
+    ck(cub::DeviceScan::ExclusiveSum(tmp, tb, keep, toff, static_cast<int>(T), s), "scan / sort");
     k_mc_compact<<<grid_for(T, 256), 256, 0, s>>>(tri_idx, keep, toff, T, out.t);
     k_mc_attrs<<<grid_for(nv, 256), 256, 0, s>>>(g, out.v, nv, out.n, out.c, out.l);
     ck(cudaMemcpyAsync(&hv[0], toff + T - 1, 4, cudaMemcpyDeviceToHost, s), "count");

@@ -138,12 +138,12 @@ uint64_t band_points(const double* o, const double* d, const uint32_t* counts, c
     uint32_t* off = scratch + n;
     k_band_count<<<grid, 256, 0, s>>>(counts, rec, n, S, band, cnt);
     size_t bytes = tmp_bytes;
-    cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, off, static_cast<int>(n), s);
+    SVR_LCK(cub::DeviceScan::ExclusiveSum(tmp, bytes, cnt, off, static_cast<int>(n), s));
     uint32_t h[2];
-    cudaMemcpyAsync(&h[0], off + n - 1, 4, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(&h[1], cnt + n - 1, 4, cudaMemcpyDeviceToHost, s);
+    SVR_LCK(cudaMemcpyAsync(&h[0], off + n - 1, 4, cudaMemcpyDeviceToHost, s));
+    SVR_LCK(cudaMemcpyAsync(&h[1], cnt + n - 1, 4, cudaMemcpyDeviceToHost, s));
     if (pts) k_band_write<<<grid, 256, 0, s>>>(o, d, counts, t, rec, n, S, band, off, cap, pts);
-    cudaStreamSynchronize(s);
+    SVR_LCK(cudaStreamSynchronize(s));
     return static_cast<uint64_t>(h[0]) + h[1];
 }
 

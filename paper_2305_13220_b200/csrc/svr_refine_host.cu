@@ -126,7 +126,7 @@ int svr_refiner_destroy(svr_refiner* r) {
     return guarded([&] {
         if (!r) return;
         GridGuard dg(r->g);
-        cudaStreamSynchronize(r->g->stream);
+        SVR_CK(cudaStreamSynchronize(r->g->stream));
         delete r;
     });
 }

@@ -168,7 +168,8 @@ void launch_rmsprop(float4* pay, float4* grad, float4* rms, uint8_t* active, con
                     const unsigned long long* count, uint32_t n_max, float lr, float alpha, float eps,
                     cudaStream_t s) {
     if (!n_max) return;
-    const unsigned grid = n_max < 148u * 16u ? n_max : 148u * 16u;
+    const unsigned cap = sm_count() * 16u;
+    const unsigned grid = n_max < cap ? n_max : cap;
     k_rmsprop<<<grid, 128, 0, s>>>(pay, grad, rms, active, list, count, lr, alpha, eps);
 }
 

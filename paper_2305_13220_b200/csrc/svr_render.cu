@@ -1175,9 +1175,8 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     const uint64_t warps_total = ctas * kPipeWarps;
     static bool attr_set = false;  // per process; the attribute is per function, not per device
     if (!attr_set) {
-        const cudaError_t e = cudaFuncSetAttribute(k_backward_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(smem));
-        if (e != cudaSuccess) return false;
+        SVR_LCK(cudaFuncSetAttribute(k_backward_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
         attr_set = true;
     }
     k_backward_pipe<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(
@@ -1203,14 +1202,14 @@ void launch_ray_order(const double* o, const double* d, uint64_t n, const GridVi
     }
     cub::DoubleBuffer<uint32_t> kb(keys, keys_alt), vb(ids, ids_alt);
     size_t bytes = tmp_bytes;
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, end_bit, s);
+    SVR_LCK(cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, static_cast<int>(n), 0, end_bit, s));
     *sorted_ids = vb.Current();
 }
 
 size_t ray_order_tmp_bytes(uint64_t n) {
     size_t bytes = 0;
     cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int>(n), 0, 32);
+    SVR_LCK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, static_cast<int>(n), 0, 32));
     return bytes;
 }
 
