@@ -120,6 +120,32 @@ __global__ void __launch_bounds__(512) k_peer_allreduce(PeerPlanes pl, uint32_t 
     }
 }
 
+// AABB extension over new blocks (grid.cpp:96-106): warp min / max, one atomic per warp.
+__global__ void k_bounds(const int4* __restrict__ c, uint64_t n, int32_t* b) {
+    int32_t lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int4 v = c[i];
+        lo[0] = min(lo[0], v.x), lo[1] = min(lo[1], v.y), lo[2] = min(lo[2], v.z);
+        hi[0] = max(hi[0], v.x), hi[1] = max(hi[1], v.y), hi[2] = max(hi[2], v.z);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            lo[a] = min(lo[a], __shfl_xor_sync(0xFFFFFFFFu, lo[a], off));
+            hi[a] = max(hi[a], __shfl_xor_sync(0xFFFFFFFFu, hi[a], off));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(b + a, lo[a]);
+            atomicMax(b + 3 + a, hi[a]);
+        }
+    }
+}
+
 // Per-block table of the 8 blocks a trilinear cell can touch: entry k = lookup of
 // coord + (k & 1, (k >> 1) & 1, k >> 2) (k = 0 is the block itself), with the all-valid bit.
 __global__ void k_nbr_build(GridView g, const int4* __restrict__ coords, uint32_t n, uint32_t* nbr) {
@@ -293,6 +319,12 @@ void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank,
     const uint64_t cap = sm_count() * 8ull;
     const unsigned grid = static_cast<unsigned>(count < cap ? count : cap);
     k_peer_allreduce<<<grid, 512, 0, s>>>(pl, world, rows, first, count);
+}
+
+void launch_bounds(const int32_t* coords4, uint64_t n, int32_t* b, cudaStream_t s) {
+    if (!n) return;
+    const uint64_t want = (n + 255) / 256, cap = sm_count() * 4ull;
+    k_bounds<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), n, b);
 }
 
 void launch_nbr_build(const GridView& g, const int32_t* coords4, uint32_t n, uint32_t* nbr,

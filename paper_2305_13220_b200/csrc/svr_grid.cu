@@ -4,6 +4,9 @@
 // the dense AABB lookup index lazily.  There is no CPU compute fallback: every
 // numerical result comes from the sm_100a kernels in svr_render.cu / svr_activate.cu /
 // svr_grads.cu, and a missing or failing device surfaces as SVR_ERR_CUDA.
+#include <map>
+#include <mutex>
+
 #include "svr_handle.h"
 
 using namespace svr_dev;
@@ -12,6 +15,52 @@ using namespace svr_host;
 namespace svr_internal {
 thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace svr_internal
+
+namespace svr_host {
+namespace {
+std::mutex g_cache_mu;
+std::map<int, std::multimap<size_t, void*>> g_cache;  // device -> (true size, block)
+}  // namespace
+
+void* dev_alloc(size_t bytes, size_t* got) {
+    bytes = std::max<size_t>(bytes, 256);
+    int dev = 0;
+    SVR_CK(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto& m = g_cache[dev];
+        auto it = m.lower_bound(bytes);  // smallest cached block that fits, if not much larger
+        if (it != m.end() && it->first <= bytes + bytes / 8 + (2u << 20)) {
+            void* p = it->second;
+            *got = it->first;
+            m.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {  // give the cached blocks of this device back, retry
+        cudaGetLastError();
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        cudaDeviceSynchronize();
+        for (auto& kv : g_cache[dev]) cudaFree(kv.second);
+        g_cache[dev].clear();
+        e = cudaMalloc(&p, bytes);
+    }
+    SVR_CK(e);
+    *got = bytes;
+    return p;
+}
+
+void dev_release(void* p, size_t bytes, int device) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[device].emplace(bytes, p);
+}
+}  // namespace svr_host
+
+namespace svr_internal {
 unsigned sm_count() {
     static int cache[64] = {0};
     int dev = 0;
@@ -58,7 +107,8 @@ svr_grid* make_grid(double h, int32_t B, int32_t C, uint64_t capacity, int32_t d
         SVR_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     g->nslots = next_pow2(std::max<uint64_t>(2 * g->capacity, 1024));
-    SVR_CK(cudaMalloc(&g->slots, g->nslots * sizeof(HashSlot)));
+    size_t got = 0;
+    g->slots = static_cast<HashSlot*>(dev_alloc(g->nslots * sizeof(HashSlot), &got));
     SVR_CK(cudaMemsetAsync(g->slots, 0xFF, g->nslots * sizeof(HashSlot), g->stream));
     SVR_CK(cudaStreamSynchronize(g->stream));
     return g.release();
@@ -329,9 +379,11 @@ int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* c
             unsigned long long* counters = ks.list + cap;
             SVR_CK(cudaMemsetAsync(counters, 0, 24, g->stream));
             svr_internal::launch_keyset_clear(ks, g->stream);
+            g->scratch_e.ensure(static_cast<size_t>(n_frames) * (W + H) * sizeof(double));
             svr_internal::launch_depth_to_keys(dd, dc, n_frames, W, H, ds, sf_rows, sf_cols, g->L, ks,
                                                counters, counters + 1,
-                                               reinterpret_cast<uint32_t*>(counters + 2), g->stream);
+                                               reinterpret_cast<uint32_t*>(counters + 2),
+                                               g->scratch_e.as<double>(), g->stream);
             SVR_LAUNCHED();
             SVR_CK(cudaMemcpyAsync(hc, counters, 24, cudaMemcpyDeviceToHost, g->stream));
             SVR_CK(cudaStreamSynchronize(g->stream));
@@ -343,10 +395,9 @@ int svr_grid_activate_depth(svr_grid* g, const float* depth, const svr_camera* c
             throw Fail{SVR_ERR_CONFIG, "allocate: block coordinate outside +-2^20"};
         rep.pixels_used = hc[1];
         // keep the base list alive while commit reuses scratch_a? copy it out first
-        DevBuf base;
-        base.ensure(std::max<uint64_t>(hc[0], 1) * 8);
-        SVR_CK(cudaMemcpyAsync(base.p, ks.list, hc[0] * 8, cudaMemcpyDeviceToDevice, g->stream));
-        g->commit(base.as<unsigned long long>(), hc[0], dilation, rep);
+        g->scratch_d.ensure(std::max<uint64_t>(hc[0], 1) * 8);
+        SVR_CK(cudaMemcpyAsync(g->scratch_d.p, ks.list, hc[0] * 8, cudaMemcpyDeviceToDevice, g->stream));
+        g->commit(g->scratch_d.as<unsigned long long>(), hc[0], dilation, rep);
         SVR_CK(cudaStreamSynchronize(g->stream));
     });
     if (report) *report = rep;
@@ -367,12 +418,13 @@ int svr_grid_find(svr_grid* g, const int32_t* coords, uint64_t n, uint32_t* idx_
 
 int svr_grid_coords(svr_grid* g, int32_t* out) {
     return guarded([&] {
-        if (g->coords.empty()) return;
+        if (!g->n()) return;
+        GridGuard dg(g);
+        const std::vector<int32_t>& hc = g->host_coords();
         if (is_device_ptr(out)) {
-            GridGuard dg(g);
-            SVR_CK(cudaMemcpy(out, g->coords.data(), g->coords.size() * 4, cudaMemcpyHostToDevice));
+            SVR_CK(cudaMemcpy(out, hc.data(), hc.size() * 4, cudaMemcpyHostToDevice));
         } else {
-            std::memcpy(out, g->coords.data(), g->coords.size() * 4);
+            std::memcpy(out, hc.data(), hc.size() * 4);
         }
     });
 }
@@ -472,6 +524,11 @@ int svr_grid_save_sdgv(svr_grid* g, const char* path) {
         os.write(reinterpret_cast<const char*>(&nb), 8);
         os.write(reinterpret_cast<const char*>(&C), 4);
         const uint32_t chunk = 4096;
+        const std::vector<int32_t>* hc = nullptr;
+        {
+            GridGuard dg(g);
+            hc = &g->host_coords();
+        }
         std::vector<float> sdf, w, rgb, lg;
         for (uint64_t f = 0; f < nb; f += chunk) {
             const uint32_t m = static_cast<uint32_t>(std::min<uint64_t>(chunk, nb - f));
@@ -483,7 +540,7 @@ int svr_grid_save_sdgv(svr_grid* g, const char* path) {
                                                 rgb.data(), lg.data());
             if (st) throw Fail{st, svr_internal::g_err};
             for (uint32_t i = 0; i < m; ++i) {
-                os.write(reinterpret_cast<const char*>(&g->coords[3 * (f + i)]), 12);
+                os.write(reinterpret_cast<const char*>(&(*hc)[3 * (f + i)]), 12);
                 os.write(reinterpret_cast<const char*>(&sdf[static_cast<size_t>(i) * kVox]), kVox * 4);
                 os.write(reinterpret_cast<const char*>(&w[static_cast<size_t>(i) * kVox]), kVox * 4);
                 os.write(reinterpret_cast<const char*>(&rgb[static_cast<size_t>(i) * kVox * 3]), kVox * 12);

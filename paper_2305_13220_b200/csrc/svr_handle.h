@@ -75,25 +75,39 @@ struct DeviceGuard {
     }
 };
 
-// Grow-only device buffer.
+// Process-wide cache of device allocations (svr_grid.cu): blocks a handle gives back -- when
+// it is destroyed or a buffer grows -- are kept mapped and handed to later requests of a
+// similar size on the same device, instead of being returned with cudaFree and re-mapped by
+// cudaMalloc (which costs ~0.3-1 ms per GB).  dev_alloc returns the block's true size;
+// dev_release requires that no queued work still uses the block.  On cudaMalloc failure the
+// device's cached blocks are freed and the allocation retried.
+void* dev_alloc(size_t bytes, size_t* got);
+void dev_release(void* p, size_t bytes, int device);
+
+// Grow-only device buffer (on the caching allocator).
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    int dev = -1;
     void ensure(size_t need) {
         if (need <= bytes) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-        SVR_CK(cudaMalloc(&p, need));
-        bytes = need;
+        release();
+        SVR_CK(cudaGetDevice(&dev));
+        p = dev_alloc(need, &bytes);
     }
     template <typename T>
     T* as() const {
         return static_cast<T*>(p);
     }
-    ~DevBuf() {
-        if (p) cudaFree(p);
+    // as cudaFree did implicitly: the device is idle before the block is handed back
+    void release() {
+        if (!p) return;
+        cudaDeviceSynchronize();
+        dev_release(p, bytes, dev);
+        p = nullptr;
+        bytes = 0;
     }
+    ~DevBuf() { release(); }
 };
 
 // Host <-> device staging for one API call.  Device pointers pass through; host
@@ -165,7 +179,12 @@ struct svr_grid {
     double h = 0, inv_h = 0, L = 0;
     int32_t C = 1;
     uint64_t capacity = 0;
-    std::vector<int32_t> coords;  // host mirror, 3 per block
+    uint64_t nblk = 0;             // allocated blocks
+    std::vector<int32_t> coords;   // host mirror, 3 per block: blocks [0, coords_synced) pulled
+    uint64_t coords_synced = 0;
+    void* pin = nullptr;           // pinned staging (host_coords, bounds)
+    size_t pin_bytes = 0;
+    DevBuf bounds_dev;
     int32_t lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
 
     HashSlot* slots = nullptr;
@@ -267,11 +286,35 @@ struct svr_grid {
     }
     uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
-    DevBuf scratch_a, scratch_b, scratch_c, sort_tmp;
-    void* sort_tmp_p = nullptr;
-    size_t sort_tmp_bytes = 0;
+    DevBuf scratch_a, scratch_b, scratch_c, scratch_d, scratch_e, sort_tmp;
 
-    uint64_t n() const { return coords.size() / 3; }
+    uint64_t n() const { return nblk; }
+    // host mirror of the block coordinates (x, y, z per block), pulled from coords4 lazily
+    const std::vector<int32_t>& host_coords() {
+        if (coords_synced < nblk) {
+            const uint64_t cnt = nblk - coords_synced;
+            int32_t* st = static_cast<int32_t*>(pinned(cnt * 16));
+            SVR_CK(cudaMemcpyAsync(st, coords4 + coords_synced * 4, cnt * 16, cudaMemcpyDeviceToHost, stream));
+            SVR_CK(cudaStreamSynchronize(stream));
+            coords.resize(3 * nblk);
+            int32_t* dst = coords.data() + 3 * coords_synced;
+            for (uint64_t i = 0; i < cnt; ++i)
+                dst[3 * i] = st[4 * i], dst[3 * i + 1] = st[4 * i + 1], dst[3 * i + 2] = st[4 * i + 2];
+            coords_synced = nblk;
+        }
+        return coords;
+    }
+    // grow-only pinned host staging buffer
+    void* pinned(size_t bytes) {
+        if (bytes > pin_bytes) {
+            if (pin) cudaFreeHost(pin);
+            pin = nullptr;
+            pin_bytes = 0;
+            SVR_CK(cudaMallocHost(&pin, bytes));
+            pin_bytes = bytes;
+        }
+        return pin;
+    }
 
     ~svr_grid() {
         int prev = -1;
@@ -294,11 +337,15 @@ struct svr_grid {
             cudaStreamDestroy(h2d);
             cudaStreamDestroy(d2h);
         }
-        for (void* p : {static_cast<void*>(slots), static_cast<void*>(coords4), static_cast<void*>(pay),
-                        static_cast<void*>(weight), static_cast<void*>(logits), static_cast<void*>(vmask),
-                        static_cast<void*>(meta), static_cast<void*>(grad), static_cast<void*>(active),
-                        static_cast<void*>(touch), sort_tmp_p})
-            if (p) cudaFree(p);
+        if (slots) dev_release(slots, nslots * sizeof(HashSlot), device);
+        const uint64_t cb = cap_blocks;
+        const std::pair<void*, size_t> blocks[] = {
+            {coords4, cb * 16}, {pay, cb * kVox * sizeof(float4)}, {weight, cb * kVox * 4},
+            {logits, cb * kVox * 4 * static_cast<size_t>(C)}, {vmask, cb * 64}, {meta, cb * 4},
+            {grad, cb * kVox * sizeof(float4)}, {active, cb}, {touch, cb * 8}};
+        for (const auto& b : blocks)
+            if (b.first) dev_release(b.first, b.second, device);
+        if (pin) cudaFreeHost(pin);
         if (own_stream && stream) cudaStreamDestroy(stream);
         if (prev >= 0) cudaSetDevice(prev);
     }
@@ -338,15 +385,19 @@ struct svr_grid {
         uint64_t nc = std::max<uint64_t>(need, std::min<uint64_t>(capacity, cap_blocks * 2));
         nc = std::max<uint64_t>(nc, 64);
         nc = std::min<uint64_t>(std::max(nc, need), std::max<uint64_t>(capacity, need));
+        if (cap_blocks) {  // the old arrays go back to the cache: no queued work may use them
+            SVR_CK(cudaStreamSynchronize(stream));
+            if (side) SVR_CK(cudaStreamSynchronize(side));
+        }
         auto grow = [&](auto*& ptr, size_t per_block) {
             using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
-            T* np = nullptr;
-            SVR_CK(cudaMalloc(&np, nc * per_block * sizeof(T)));
+            size_t got = 0;
+            T* np = static_cast<T*>(dev_alloc(nc * per_block * sizeof(T), &got));
             if (ptr) {
                 SVR_CK(cudaMemcpyAsync(np, ptr, cap_blocks * per_block * sizeof(T),
                                        cudaMemcpyDeviceToDevice, stream));
                 SVR_CK(cudaStreamSynchronize(stream));
-                cudaFree(ptr);
+                dev_release(ptr, cap_blocks * per_block * sizeof(T), device);
             }
             ptr = np;
         };
@@ -375,21 +426,23 @@ struct svr_grid {
         SVR_CK(cudaMemsetAsync(touch + first * 8, 0, count * 8, stream));
     }
 
-    // Host mirror + AABB after blocks [first, first+count) got coords (grid.cpp:96-106).
-    void pull_coords(uint64_t first, uint64_t count) {
-        std::vector<int32_t> c4(count * 4);
-        SVR_CK(cudaMemcpyAsync(c4.data(), coords4 + first * 4, count * 16, cudaMemcpyDeviceToHost, stream));
+    // Blocks [first, first+count) got their coords in coords4: count them and extend the
+    // AABB (grid.cpp:96-106) with a device min/max reduction (24 bytes read back); the host
+    // coordinate mirror is pulled only when asked for (host_coords).
+    void grew(uint64_t first, uint64_t count) {
+        if (!count) return;
+        int32_t* b = static_cast<int32_t*>(pinned(64));
+        const int32_t init[6] = {first ? lo[0] : INT32_MAX, first ? lo[1] : INT32_MAX, first ? lo[2] : INT32_MAX,
+                                 first ? hi[0] : INT32_MIN, first ? hi[1] : INT32_MIN, first ? hi[2] : INT32_MIN};
+        std::memcpy(b, init, sizeof(init));
+        bounds_dev.ensure(32);
+        SVR_CK(cudaMemcpyAsync(bounds_dev.p, b, 24, cudaMemcpyHostToDevice, stream));
+        svr_internal::launch_bounds(coords4 + first * 4, count, bounds_dev.as<int32_t>(), stream);
+        SVR_LAUNCHED();
+        SVR_CK(cudaMemcpyAsync(b, bounds_dev.p, 24, cudaMemcpyDeviceToHost, stream));
         SVR_CK(cudaStreamSynchronize(stream));
-        for (uint64_t i = 0; i < count; ++i) push_coord(c4[4 * i], c4[4 * i + 1], c4[4 * i + 2]);
-    }
-    void push_coord(int32_t x, int32_t y, int32_t z) {
-        if (coords.empty()) {
-            lo[0] = hi[0] = x, lo[1] = hi[1] = y, lo[2] = hi[2] = z;
-        } else {
-            lo[0] = std::min(lo[0], x), lo[1] = std::min(lo[1], y), lo[2] = std::min(lo[2], z);
-            hi[0] = std::max(hi[0], x), hi[1] = std::max(hi[1], y), hi[2] = std::max(hi[2], z);
-        }
-        coords.push_back(x), coords.push_back(y), coords.push_back(z);
+        for (int a = 0; a < 3; ++a) lo[a] = b[a], hi[a] = b[3 + a];
+        nblk = first + count;
         dense_dirty = true;
     }
 
@@ -437,7 +490,7 @@ struct svr_grid {
         svr_internal::launch_hash_insert(slots, nslots - 1, d_keys, count, static_cast<uint32_t>(first),
                                          coords4, stream);
         SVR_LAUNCHED();
-        pull_coords(first, count);
+        grew(first, count);
     }
 
     // commit (allocation.cpp:19-43) on a device list of unique base keys.
@@ -473,7 +526,10 @@ struct svr_grid {
         unsigned long long nfresh = 0;
         SVR_CK(cudaMemcpyAsync(&nfresh, nfresh_d, 8, cudaMemcpyDeviceToHost, stream));
         SVR_CK(cudaStreamSynchronize(stream));
-        svr_internal::launch_sort_keys(fresh, nfresh, &sort_tmp_p, &sort_tmp_bytes, stream);
+        if (nfresh > 1) {
+            sort_tmp.ensure(svr_internal::sort_keys_tmp_bytes(nfresh));
+            svr_internal::launch_sort_keys(fresh, nfresh, sort_tmp.p, stream);
+        }
         SVR_LAUNCHED();
         const uint64_t room = capacity > n() ? capacity - n() : 0;
         const uint64_t take = std::min<uint64_t>(nfresh, room);

@@ -19,6 +19,8 @@ void set_error(const std::string& msg);
 // SM count of the current device (cached per device): persistent / grid-stride grids are
 // sized in multiples of it.  Defined in svr_grid.cu.
 unsigned sm_count();
+// AABB of blocks coords4[0, n) folded into b[6] = {lo xyz, hi xyz} (svr_grads.cu)
+void launch_bounds(const int32_t* coords4, uint64_t n, int32_t* b, cudaStream_t s);
 #define SVR_LCK(expr)                                                            \
     do {                                                                         \
         const cudaError_t e_ = (expr);                                           \
@@ -77,12 +79,13 @@ void launch_points_to_keys(const double* xyz, uint64_t n, double L, KeySet ks,
 void launch_depth_to_keys(const float* depth, const svr_camera* cams, uint32_t n_frames,
                           int32_t W, int32_t H, const double* scales, int32_t rows, int32_t cols,
                           double L, KeySet ks, unsigned long long* count,
-                          unsigned long long* pixels, uint32_t* flags, cudaStream_t s);
+                          unsigned long long* pixels, uint32_t* flags, double* tab, cudaStream_t s);
 void launch_dilate(const unsigned long long* base, uint64_t nbase, int32_t R, KeySet ks,
                    unsigned long long* count, uint32_t* flags, cudaStream_t s);
 void launch_filter_fresh(const svr_dev::GridView& g, const unsigned long long* keys, uint64_t n,
                          unsigned long long* fresh, unsigned long long* nfresh, cudaStream_t s);
-void launch_sort_keys(unsigned long long* keys, uint64_t n, void** tmp, size_t* tmp_bytes,
+size_t sort_keys_tmp_bytes(uint64_t n);
+void launch_sort_keys(unsigned long long* keys, uint64_t n, void* tmp,
                       cudaStream_t s);
 void launch_hash_insert(svr_dev::HashSlot* slots, unsigned long long mask,
                         const unsigned long long* keys, uint64_t n, uint32_t first_index,

@@ -1157,7 +1157,7 @@ void launch_render_backward(const GridView& g, const double* o, const double* d,
     else
         k_backward<false><<<grid, 256, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal,
                                                rec);
-    k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
+    if (g.n_blocks) k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
 }
 
 bool launch_render_backward_pipe(const GridView& g, const double* o, const double* d, uint64_t n,
@@ -1181,7 +1181,7 @@ bool launch_render_backward_pipe(const GridView& g, const double* o, const doubl
     }
     k_backward_pipe<<<static_cast<unsigned>(ctas), kPipeWarps * 32, smem, s>>>(
         g, o, d, n, order, counts, t, S, step, ib, d_rgb, d_depth, d_normal, rec, warps_total);
-    k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
+    if (g.n_blocks) k_touch_expand<<<grid_for(g.n_blocks, 256), 256, 0, s>>>(g);
     return true;
 }
 

@@ -112,8 +112,8 @@ def test_render_golden():
     g.render_backward(z["dC"], z["dD"], z["dN"])
     gs, gr = g.grads()
     idx = g.find(z["grad_blocks"])
-    assert_close(gs[idx], z["grad_sdf"], rtol=2e-4, what="grad_sdf")
-    assert_close(gr[idx], z["grad_rgb"], rtol=2e-4, what="grad_rgb")
+    assert_close(gs[idx], z["grad_sdf"], what="grad_sdf")
+    assert_close(gr[idx], z["grad_rgb"], what="grad_rgb")
 
 
 def test_sdgv_reference_file_roundtrip(tmp_path):

@@ -37,12 +37,21 @@ def test_backward_step_chain_matches_oracle():
     args = (case["o"], case["d"], case["step"], 64, case["beta"])
     oout = og.render_forward(*args)
     ograds, _ = oracle_losses(oout, tgt, pd, pn, cam_idx, cams)
-    # the L1 sign terms flip where |C - C*| ~ fp32 rounding: compare rays whose upstream agrees
+    # the L1 sign terms flip where |C - C*| ~ fp32 rounding: those rays (< 1 %) carry an
+    # upstream gradient that legitimately differs, so both chains drop them, and the rest is
+    # held to the renderer's own tolerance (1e-4 |ref| + 1e-6 max|ref|)
     same = np.all(np.sign(ograds["d_rgb"]) == np.sign(grads["d_rgb"]), axis=1)
     assert same.mean() > 0.99
-    ogs, ogr, act = og.render_backward(*args, ograds["d_rgb"], ograds["d_depth"], ograds["d_normal"])
-    assert_close(gs, ogs, rtol=1e-3, atol_frac=1e-4, what="grad_sdf")
-    assert_close(gr, ogr, rtol=1e-3, atol_frac=1e-4, what="grad_rgb")
+    keep = same.astype(np.float32)
+    up = {k: np.ascontiguousarray((grads[k].T * keep).T if grads[k].ndim == 2 else grads[k] * keep)
+          for k in ("d_rgb", "d_depth", "d_normal")}
+    oup = {k: (ograds[k].T * keep).T if ograds[k].ndim == 2 else ograds[k] * keep for k in up}
+    g.grad_zero()
+    g.render_backward(up["d_rgb"], up["d_depth"], up["d_normal"])
+    gs, gr = g.grads()
+    ogs, ogr, act = og.render_backward(*args, oup["d_rgb"], oup["d_depth"], oup["d_normal"])
+    assert_close(gs, ogs, what="grad_sdf")
+    assert_close(gr, ogr, what="grad_rgb")
     assert np.array_equal(g.active_mask(), act)
 
 
