@@ -14,6 +14,6 @@ timeout 900 python bench.py > $O/$TAG.bench.json 2> $O/$TAG.bench.err; rc=$?; ec
 [ $rc = 0 ] || { tail -30 $O/$TAG.bench.err; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file $O/$TAG.launches.csv \
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extra > $O/$TAG.ncu1.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_forward_multi|k_backward_pipe|k_march' \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_forward|k_backward_pipe|k_march' \
   --launch-skip 6 -c 3 -o $O/$TAG.full -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extra > $O/$TAG.ncu2.log 2>&1; echo "ncu full rc=$?"
 ls -la $O | tail -20
