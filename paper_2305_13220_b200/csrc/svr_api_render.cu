@@ -55,9 +55,16 @@ void forward_kernels(svr_grid* g, const double* dO, const double* dD, uint64_t n
     g->ctx_rec = g->use_records;
     if (g->ctx_rec) g->rec.ensure(n * max_samples * 32);
     float4* recp = g->ctx_rec ? g->rec.as<float4>() : nullptr;
+    // a pending svr_grad_zero_active rides along when each warp gets at most 8 row chunks
+    // (512 B stores); otherwise it runs as its own kernel first
+    const bool fuse_zero = g->zero_pending && n && g->n() * (kVox / 32) <= 8 * n;
+    if (g->zero_pending && !fuse_zero) g->flush_zero();
+    g->zero_pending = false;
     svr_internal::launch_render_forward(v, dO, dD, n, g->ctx_order, g->counts.as<uint32_t>(), g->tbuf.as<double>(),
                                         max_samples, step, beta, a, b, c, e, g->nvalid.as<unsigned long long>(),
-                                        recp, g->stream);
+                                        recp, g->stream, fuse_zero ? g->grad : nullptr, fuse_zero ? g->active : nullptr,
+                                        fuse_zero ? g->active_list.as<uint32_t>() : nullptr,
+                                        fuse_zero ? g->active_count.as<unsigned long long>() : nullptr);
 }
 
 void backward_kernels(svr_grid* g, const float* a, const float* b, const float* c) {
@@ -84,7 +91,7 @@ int svr_render_forward(svr_grid* g, const double* o, const double* d, uint64_t n
         if (!(step > 0.0)) throw Fail{SVR_ERR_CONFIG, "render: step must be positive"};
         if (max_samples < 1 || max_samples > 2048)
             throw Fail{SVR_ERR_CONFIG, "render: max_samples must be in [1, 2048]"};
-        DeviceGuard dg(g->device);  // no join: march + forward overlap a pending zero_async
+        DeviceGuard dg(g->device);  // no flush: the forward kernel fuses a pending zeroing
         g->ensure_lookup();
         g->ctx_valid = false;
         g->ctx_aslot = -1;
@@ -361,22 +368,9 @@ int svr_grad_zero_active(svr_grid* g) {
         g->active_count.ensure(8 + 4 * ((nb + 1023) / 1024 + 2));
         auto* dcount = g->active_count.as<unsigned long long>();
         svr_internal::launch_active_list(g->active, nb, g->active_list.as<uint32_t>(), dcount, g->stream);
-        cudaStream_t zs = g->stream;
-        if (g->zero_async) {  // overlaps the next render_forward; joined by the next other call
-            g->ensure_side();
-            SVR_CK(cudaEventRecord(g->side_fork, g->stream));
-            SVR_CK(cudaStreamWaitEvent(g->side, g->side_fork, 0));
-            zs = g->side;
-        }
-        // side stream: a few CTAs per SM at the lowest priority, so the next forward's CTAs
-        // keep the SMs and the zeroing fills their idle store bandwidth
-        svr_internal::launch_grad_zero_active(g->grad, g->active, g->active_list.as<uint32_t>(), dcount,
-                                              nb, zs, g->zero_async ? static_cast<unsigned>(g->zero_async) : 16u);
         SVR_LAUNCHED();
-        if (g->zero_async) {
-            SVR_CK(cudaEventRecord(g->side_join, g->side));
-            g->side_pending = true;
-        }
+        g->zero_pending = true;  // the next render_forward stores the zeros (zero_fused), or
+        if (!g->zero_fused) g->flush_zero();  // now, in order
     });
 }
 

@@ -204,10 +204,9 @@ int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value) {
             g->bwd_pipe = value != 0;
         } else if (k == "march_jump") {
             g->use_jump = value != 0;
-        } else if (k == "zero_async") {
-            g->join_side();
-            if (value < 0 || value > 16) throw Fail{SVR_ERR_CONFIG, "tuning: zero_async is 0..16"};
-            g->zero_async = static_cast<int>(value);
+        } else if (k == "zero_fused") {
+            GridGuard dg(g);
+            g->zero_fused = value != 0;
         } else if (k == "host_async") {
             SVR_CK(cudaStreamSynchronize(g->stream));
             if (g->h2d) {

@@ -264,25 +264,20 @@ struct svr_grid {
             for (cudaEvent_t* e : {&a.in_ev, &a.up_ev, &a.fwd_ev, &a.out_ev, &a.free_ev})
                 SVR_CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    // "zero_async": svr_grad_zero_active runs its zeroing kernel on a side stream, so it
-    // overlaps the next render_forward (march + forward never touch the gradient planes or
-    // the active flags); every other entry point joins the side stream first (GridGuard).
-    int zero_async = 8;  // 0: in order on the handle's stream; n > 0: side stream, n CTAs per SM
-    cudaStream_t side = nullptr;
-    cudaEvent_t side_fork = nullptr, side_join = nullptr;
-    bool side_pending = false;
-    void ensure_side() {
-        if (side) return;
-        int lo = 0, hi = 0;
-        SVR_CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // lo = numerically largest = lowest
-        SVR_CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
-        SVR_CK(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
-        SVR_CK(cudaEventCreateWithFlags(&side_join, cudaEventDisableTiming));
-    }
-    void join_side() {
-        if (!side_pending) return;
-        SVR_CK(cudaStreamWaitEvent(stream, side_join, 0));
-        side_pending = false;
+    // Deferred zeroing ("zero_fused", default on): svr_grad_zero_active only compacts the
+    // active list (device count) and leaves the zeroing pending; the next render_forward's
+    // K5 warps store the zeros next to their ray work (the forward is latency bound, its DRAM
+    // has room for the 1 GB of stores), and every other entry point runs the pending zeroing
+    // kernel first (GridGuard).  Off: the zeroing kernel runs in order at once.
+    bool zero_fused = true;
+    bool zero_pending = false;
+    void flush_zero() {
+        if (!zero_pending) return;
+        zero_pending = false;
+        svr_internal::launch_grad_zero_active(grad, active, active_list.as<uint32_t>(),
+                                              active_count.as<unsigned long long>(), static_cast<uint32_t>(n()),
+                                              stream, 16u);
+        SVR_LAUNCHED();
     }
     uint64_t spare_cap = 0;          // cap_blocks the spare pair was sized for
     DevBuf fuse_sum, fuse_cnt;
@@ -321,12 +316,6 @@ struct svr_grid {
         cudaGetDevice(&prev);
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        if (side) {
-            cudaStreamSynchronize(side);
-            cudaEventDestroy(side_fork);
-            cudaEventDestroy(side_join);
-            cudaStreamDestroy(side);
-        }
         for (cudaEvent_t e : {red_done, red_reduced})
             if (e) cudaEventDestroy(e);
         if (h2d) {
@@ -385,10 +374,7 @@ struct svr_grid {
         uint64_t nc = std::max<uint64_t>(need, std::min<uint64_t>(capacity, cap_blocks * 2));
         nc = std::max<uint64_t>(nc, 64);
         nc = std::min<uint64_t>(std::max(nc, need), std::max<uint64_t>(capacity, need));
-        if (cap_blocks) {  // the old arrays go back to the cache: no queued work may use them
-            SVR_CK(cudaStreamSynchronize(stream));
-            if (side) SVR_CK(cudaStreamSynchronize(side));
-        }
+        if (cap_blocks) SVR_CK(cudaStreamSynchronize(stream));  // the old arrays go back to the cache
         auto grow = [&](auto*& ptr, size_t per_block) {
             using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
             size_t got = 0;
@@ -548,9 +534,9 @@ struct svr_grid {
 };
 
 namespace svr_host {
-// Entry-point guard: the handle's device, and the handle's stream joined with any pending
-// side-stream work (zero_async) -- every entry point except render_forward uses it.
+// Entry-point guard: the handle's device, and any pending deferred zeroing run in order on the
+// handle's stream -- every entry point except render_forward (which fuses it) uses it.
 struct GridGuard : DeviceGuard {
-    explicit GridGuard(svr_grid* g) : DeviceGuard(g->device) { g->join_side(); }
+    explicit GridGuard(svr_grid* g) : DeviceGuard(g->device) { g->flush_zero(); }
 };
 }  // namespace svr_host

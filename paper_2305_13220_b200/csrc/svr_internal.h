@@ -43,7 +43,9 @@ void launch_render_forward(const svr_dev::GridView& g, const double* o, const do
                            uint64_t n, const uint32_t* order, const uint32_t* counts,
                            const double* t, uint32_t S, double step, double beta, float* rgb,
                            float* depth, float* normal, float* wsum,
-                           unsigned long long* valid_counter, float4* rec, cudaStream_t s);
+                           unsigned long long* valid_counter, float4* rec, cudaStream_t s,
+                           float4* zgrad = nullptr, uint8_t* zactive = nullptr, const uint32_t* zlist = nullptr,
+                           const unsigned long long* zcount = nullptr);
 // Non-pipelined backward (any max_samples; re-gathers the payload when rec == NULL).
 void launch_render_backward(const svr_dev::GridView& g, const double* o, const double* d,
                             uint64_t n, const uint32_t* order, const uint32_t* counts,

@@ -629,6 +629,13 @@ __global__ void __launch_bounds__(256) k_ray_keys_dir(const double* __restrict__
 // decision instead of a dependent load.  Leaves a 32 B record per sample for the backward.
 // ---------------------------------------------------------------------------
 constexpr int kFwdThreads = 32;
+// the gradient rows a pending svr_grad_zero_active leaves to the next forward
+struct ZeroRows {
+    float4* grad;
+    uint8_t* active;
+    const uint32_t* list;               // ascending active rows (nullptr: nothing pending)
+    const unsigned long long* count;    // device-side row count
+};
 __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const double* __restrict__ O,
                                                              const double* __restrict__ D, uint64_t n,
                                                              const uint32_t* __restrict__ order,
@@ -636,7 +643,8 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
                                                              const double* __restrict__ T, uint32_t S,
                                                              double step, float ib, float* rgb, float* depth,
                                                              float* normal, float* wsum,
-                                                             unsigned long long* valid_counter, float4* rec) {
+                                                             unsigned long long* valid_counter, float4* rec,
+                                                             ZeroRows z) {
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t w = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     if (w >= n) return;
@@ -680,6 +688,15 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
     }
     write_ray_outputs(warp_sum8(acc, lane), lane, r, rgb, depth, normal, wsum);
     if (lane == 0 && valid_counter && nvalid) atomicAdd(valid_counter, static_cast<unsigned long long>(nvalid));
+    if (z.list) {  // a pending svr_grad_zero_active: this warp's share of the active rows, 512 B a store
+        const unsigned long long chunks = *z.count * (kVox / 32);
+        for (unsigned long long j = w; j < chunks; j += n) {
+            const uint32_t row = z.list[j / (kVox / 32)];
+            const uint32_t part = static_cast<uint32_t>(j % (kVox / 32));
+            z.grad[static_cast<size_t>(row) * kVox + part * 32 + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (part == 0 && lane == 0) z.active[row] = 0;
+        }
+    }
 }
 
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
@@ -1136,11 +1153,13 @@ void launch_march(const GridView& g, const double* o, const double* d, uint64_t 
 void launch_render_forward(const GridView& g, const double* o, const double* d, uint64_t n,
                            const uint32_t* order, const uint32_t* counts, const double* t, uint32_t S,
                            double step, double beta, float* rgb, float* depth, float* normal,
-                           float* wsum, unsigned long long* valid_counter, float4* rec, cudaStream_t s) {
+                           float* wsum, unsigned long long* valid_counter, float4* rec, cudaStream_t s,
+                           float4* zgrad, uint8_t* zactive, const uint32_t* zlist, const unsigned long long* zcount) {
     if (!n) return;
     const float ib = static_cast<float>(1.0 / beta);
     k_forward<<<grid_for(n * 32, kFwdThreads), kFwdThreads, 0, s>>>(g, o, d, n, order, counts, t, S, step, ib, rgb,
-                                                                    depth, normal, wsum, valid_counter, rec);
+                                                                    depth, normal, wsum, valid_counter, rec,
+                                                                    ZeroRows{zgrad, zactive, zlist, zcount});
 }
 
 void launch_render_backward(const GridView& g, const double* o, const double* d, uint64_t n,
