@@ -701,15 +701,30 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
 
 // Gradient of corner c of one sample: (g_sdf, g_r, g_g, g_b) with
 //   g_sdf = w_c dL/ds + dw_c . (w_k dN),  g_rgb = w_c w_k dC.
+// The sdf term is evaluated factored, g_sdf = wz (wy (wx ds + sx wn_x) + sy wx wn_y) + sz wx wy
+// wn_z, so the corners sharing (x, y) share the x and xy partial products:
+// ax[i] = w_x(i) ds + s_x(i) wn_x, bx[i] = w_x(i) wn_y (i = the corner's x bit).
 struct CornerCoef {
-    float x0, x1, y0, y1, z0, z1, ds, wn0, wn1, wn2, wc0, wc1, wc2;
+    float x0, x1, y0, y1, z0, z1, ax0, ax1, bx0, bx1, wn2, wc0, wc1, wc2;
 };
+struct XYPart {
+    float bxy, wxy, cxy;
+};
+template <int q>  // the xy partials of corners q and q + 4 (q = x bit | y bit << 1)
+__device__ __forceinline__ XYPart xy_part(const CornerCoef& k) {
+    const float wx = (q & 1) ? k.x1 : k.x0, wy = (q & 2) ? k.y1 : k.y0;
+    const float ax = (q & 1) ? k.ax1 : k.ax0, bx = (q & 1) ? k.bx1 : k.bx0;
+    XYPart r;
+    r.bxy = fmaf(wy, ax, (q & 2) ? bx : -bx);
+    r.wxy = wx * wy;
+    r.cxy = r.wxy * k.wn2;
+    return r;
+}
 template <int c>
-__device__ __forceinline__ float4 corner_grad(const CornerCoef& k) {
-    const float wx = (c & 1) ? k.x1 : k.x0, wy = (c & 2) ? k.y1 : k.y0, wz = (c & 4) ? k.z1 : k.z0;
-    const float sx = (c & 1) ? 1.f : -1.f, sy = (c & 2) ? 1.f : -1.f, sz = (c & 4) ? 1.f : -1.f;
-    const float w = wx * wy * wz;
-    const float gs = w * k.ds + sx * (wy * wz) * k.wn0 + sy * (wx * wz) * k.wn1 + sz * (wx * wy) * k.wn2;
+__device__ __forceinline__ float4 corner_grad(const CornerCoef& k, const XYPart& xy) {
+    const float wz = (c & 4) ? k.z1 : k.z0;
+    const float gs = fmaf(wz, xy.bxy, (c & 4) ? xy.cxy : -xy.cxy);
+    const float w = xy.wxy * wz;
     return make_float4(gs, w * k.wc0, w * k.wc1, w * k.wc2);
 }
 
@@ -769,8 +784,10 @@ __device__ __forceinline__ CornerCoef make_coef_par(const SampleVal& v, float ds
     k.x1 = bx ? 1.f - v.fx : v.fx, k.x0 = bx ? v.fx : 1.f - v.fx;
     k.y1 = by ? 1.f - v.fy : v.fy, k.y0 = by ? v.fy : 1.f - v.fy;
     k.z1 = bz ? 1.f - v.fz : v.fz, k.z0 = bz ? v.fz : 1.f - v.fz;
-    k.ds = ds;
-    k.wn0 = (bx ? -wk : wk) * dN[0] * ih, k.wn1 = (by ? -wk : wk) * dN[1] * ih, k.wn2 = (bz ? -wk : wk) * dN[2] * ih;
+    const float wn0 = (bx ? -wk : wk) * dN[0] * ih, wn1 = (by ? -wk : wk) * dN[1] * ih;
+    k.wn2 = (bz ? -wk : wk) * dN[2] * ih;
+    k.ax0 = fmaf(k.x0, ds, -wn0), k.ax1 = fmaf(k.x1, ds, wn0);
+    k.bx0 = k.x0 * wn1, k.bx1 = k.x1 * wn1;
     k.wc0 = wk * dC[0], k.wc1 = wk * dC[1], k.wc2 = wk * dC[2];
     return k;
 }
@@ -789,12 +806,12 @@ __device__ __forceinline__ void red_v4_if(float4* addr, float4 v, bool p) {
 // predicated reductions per lane.
 template <int p>
 __device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0, const SampleVal& v1,
-                                               const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
-                                               int lane) {
+                                               const CornerCoef& k0, const CornerCoef& k1, const XYPart& x0,
+                                               const XYPart& x1, bool ok0, bool ok1, int lane) {
     const uint32_t a0k = ok0 ? v0.gidx[p] : kInvalid, a1k = ok1 ? v1.gidx[p] : kInvalid;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 a0 = ok0 ? corner_grad<p>(k0) : z;
-    const float4 a1 = ok1 ? corner_grad<p>(k1) : z;
+    const float4 a0 = ok0 ? corner_grad<p>(k0, x0) : z;
+    const float4 a1 = ok1 ? corner_grad<p>(k1, x1) : z;
     const bool two = ok0 && ok1 && a0k != a1k;
     const uint32_t first = ok0 ? a0k : a1k, last = ok1 ? a1k : a0k;
     const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
@@ -806,17 +823,20 @@ __device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0
     const float4 own = two ? a1 : (give ? z : F);
     red_v4_if(grad + last, recv ? f4add(own, in) : own, last != kInvalid && (two || !give || recv));
 }
+template <int q>
+__device__ __forceinline__ void scatter_xy(float4* grad, const SampleVal& v0, const SampleVal& v1,
+                                           const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1, int lane) {
+    const XYPart x0 = xy_part<q>(k0), x1 = xy_part<q>(k1);
+    scatter_parity<q>(grad, v0, v1, k0, k1, x0, x1, ok0, ok1, lane);
+    scatter_parity<q + 4>(grad, v0, v1, k0, k1, x0, x1, ok0, ok1, lane);
+}
 __device__ __forceinline__ void scatter_pair_par(float4* grad, const SampleVal& v0, const SampleVal& v1,
                                                  const CornerCoef& k0, const CornerCoef& k1, bool ok0, bool ok1,
                                                  int lane) {
-    scatter_parity<0>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<1>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<2>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<3>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<4>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<5>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<6>(grad, v0, v1, k0, k1, ok0, ok1, lane);
-    scatter_parity<7>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_xy<0>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_xy<1>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_xy<2>(grad, v0, v1, k0, k1, ok0, ok1, lane);
+    scatter_xy<3>(grad, v0, v1, k0, k1, ok0, ok1, lane);
 }
 
 // ---------------------------------------------------------------------------
