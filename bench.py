@@ -533,7 +533,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                 "path": "SparseDenseGrid.render_forward/backward via C-ABI with pinned host buffers, "
                         "host_async (copies of step i+1 overlap kernels of step i)"},
-        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps + 1,
         "library_launches": {"cub_radix_sort": LIBRARY_LAUNCHES_PER_STEP * args.steps},
         "clocks": clk,
     }
@@ -562,10 +562,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
-# ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward, k_backward_pipe,
-# k_touch_expand, k_active_count / scan / write + k_grad_zero_active (+ the reduction's kernels
-# for N > 1); plus 2 CUB radix sorts that only reorder rays
-LAUNCHES_PER_STEP = 9
+# ours per step: k_ray_keys_dir, k_march (+ post-march keys), k_forward (+ the previous step's
+# deferred zeroing), k_backward_pipe, k_touch_expand, k_active_count / scan / write (+ the
+# reduction's kernels for N > 1); the last step's zeroing runs as k_grad_zero_active at the end of
+# the timed region; plus 2 CUB radix sorts that only reorder rays
+LAUNCHES_PER_STEP = 8
 LIBRARY_LAUNCHES_PER_STEP = 10  # 2 CUB radix sorts of 24-bit keys: histogram + scan + 3 onesweep passes each
 
 

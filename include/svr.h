@@ -101,40 +101,32 @@ int svr_grid_destroy(svr_grid* g);
  * be complete in the order of this stream when a call is issued. */
 int svr_grid_set_stream(svr_grid* g, void* cuda_stream);
 int svr_grid_synchronize(svr_grid* g);
-/* Orders the handle's stream after the handle's internal side-stream work (a pending
- * zero_async zeroing) without blocking the host; every call but render_forward does this. */
+/* Orders the handle's stream after the handle's pending internal work (a deferred
+ * svr_grad_zero_active zeroing) without blocking the host; every call but render_forward
+ * does this. */
 int svr_grid_join(svr_grid* g);
 int svr_grid_get_info(svr_grid* g, svr_grid_info* out);
 int svr_grid_set_lookup(svr_grid* g, int32_t mode);
-/* Performance knobs (results are unaffected): "ray_sort" (bit 1: order the march by origin +
- * octahedral direction; bit 0: order forward/backward by the Morton code of each ray's
- * first-sample block; default 3 = both -- for random ray batches; a full image in raster
- * order is coherent already and renders faster with 0), "sort_min_rays" (default 32768:
- * smaller batches skip both orderings),
- * "fwd_min_blocks" / "bwd_min_blocks" (1-4, CTAs per SM the kernels are compiled for),
- * "records" (0/1: the forward leaves 32 B per sample so the backward skips the re-gather),
- * "sort_impl" (1 CUB radix sort -- default, 0 in-house bucketed counting sort), "fwd_pipe" /
- * "bwd_pipe" (0/1, persistent cp.async.bulk-pipelined kernels), "fwd_pipe_min_blocks",
- * "pipe_min_blocks", "fwd_split" (forward lane layout, default 3: one sample per lane per 32-sample
- * pass with the ray's o / d in shared memory, one-warp CTAs, 32 warps per SM, each lane's t
- * loaded one pass ahead; 2: the same without the t prefetch; 1: lane l owns samples l and
- * 32 + l; 0: samples 2l and 2l + 1), "ray_hdr" (0/1, default 0: with fwd_split 3 and sorted rays, a
- * k_ray_headers pass hands the forward {id, count} in sorted order -- measured neutral),
- * "march_keys" (0/1, default 1: the march writes each ray's post-march sort key from the first
- * sample it emits, instead of a separate key pass re-reading the t rows),
- * "bwd_hdr" (0/1, default 1: the pipelined backward streams each ray's origin, direction,
- * upstream gradients and sample count into its ring slot with cp.async, completed on the
- * slot's mbarrier, instead of loading them when the ray starts), "march_jump" (0/1, default 1: exact
- * empty-space jumps over the block-distance field), "warp_agg" (0/1, default 1: the backward scatter hands a lane's first
- * cell run to the previous lane when it continues that lane's last run, one atomic per run),
- * "fuse_batch" (frames per fusion launch, 0 = auto), "host_async" (0/1:
- * render_forward / render_backward given PINNED host arrays return without waiting; the
- * transfers run on two internal copy streams through double-buffered device slots so one
- * step's copies overlap the previous step's kernels; host outputs are valid, and host inputs
- * may be reused, only after svr_grid_synchronize), "zero_async" (0-16, default 8:
- * svr_grad_zero_active zeroes on an internal side stream so the zeroing overlaps the next
- * svr_render_forward; every other call on the handle -- render_backward first -- orders its
- * work after it, so results are unchanged; n > 0 = n CTAs per SM on a lowest-priority stream). */
+/* Performance knobs (results are unaffected; unknown keys -> SVR_ERR_CONFIG):
+ *   "ray_sort"      bit 1: order the march by origin + octahedral direction; bit 0: order
+ *                   forward / backward by the Morton code of each ray's first-sample block;
+ *                   default 3 = both (random ray batches; a full image in raster order is
+ *                   coherent already and renders faster with 0)
+ *   "sort_min_rays" default 32768: smaller batches skip both orderings
+ *   "records"       0/1, default 1: the forward leaves 32 B per sample so the backward skips
+ *                   the re-gather (0 for inference: no backward context)
+ *   "bwd_pipe"      0/1, default 1: the persistent cp.async.bulk-pipelined backward (needs
+ *                   records and max_samples <= 64)
+ *   "march_jump"    0/1, default 1: exact empty-space jumps over the block-distance field
+ *   "zero_fused"    0/1, default 1: svr_grad_zero_active defers the zeroing to the next
+ *                   render_forward's warps; every other call runs it first.  0: in order at
+ *                   once
+ *   "host_async"    0/1: render_forward / render_backward given PINNED host arrays return
+ *                   without waiting; the transfers run on two internal copy streams through
+ *                   double-buffered device slots so one step's copies overlap the previous
+ *                   step's kernels; host outputs are valid, and host inputs may be reused,
+ *                   only after svr_grid_synchronize
+ *   "fuse_batch"    frames per fusion launch, 0 = auto */
 int svr_grid_set_tuning(svr_grid* g, const char* key, int64_t value);
 
 /* save_grid / load_grid (grid_io.cpp:37-97): SDGV v1; load keeps index = record order. */
@@ -203,7 +195,10 @@ int svr_active_blocks(svr_grid* g, uint8_t* mask, uint32_t* list, uint64_t* coun
 int svr_active_set_mask(svr_grid* g, const uint8_t* mask);
 int svr_grad_pack(svr_grid* g, const uint32_t* blocks, uint64_t n, float* out);
 int svr_grad_unpack(svr_grid* g, const uint32_t* blocks, uint64_t n, const float* in);
-/* Zero the gradients of the active blocks only and clear the active mask. */
+/* Zero the gradients of the active blocks only and clear the active mask.  Stream-ordered;
+ * with "zero_fused" (default) the zeros are stored by the next svr_render_forward's kernel,
+ * and any other call on the handle (reads included) runs the pending zeroing first, so every
+ * observable result is as if it ran here. */
 int svr_grad_zero_active(svr_grid* g);
 
 /* --- the losses / update around the rendering path ---------- */
@@ -238,8 +233,8 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps);
 #define SVR_IPC_HANDLE_BYTES 64
 int svr_grad_ipc_handle(svr_grid* g, void* handle_out, uint64_t* plane_bytes);
 /* The gradient plane itself (float4 [capacity][512], device memory of the handle's GPU).
- * Work that reads it outside this API must follow svr_grid_synchronize (a pending
- * zero_async zeroing runs on the handle's side stream). */
+ * Work that reads it outside this API must follow svr_grid_join / svr_grid_synchronize (a
+ * deferred svr_grad_zero_active zeroing may still be pending). */
 int svr_grad_plane(svr_grid* g, void** ptr_out, uint64_t* plane_bytes);
 int svr_ipc_open(const void* handle, int32_t device, void** ptr_out);
 int svr_ipc_close(void* ptr);

@@ -128,7 +128,7 @@ class SparseDenseGrid:
         check(self._lib.svr_grid_synchronize(self._h))
 
     def join(self) -> None:
-        """Order the handle's stream after its side-stream work (no host wait)."""
+        """Order the handle's stream after its pending internal work (a deferred zeroing; no host wait)."""
         check(self._lib.svr_grid_join(self._h))
 
     def set_lookup(self, mode: int) -> None:

@@ -90,3 +90,30 @@ def test_invalid_render_arguments_are_config_errors(kw):
     a.update(kw)
     with pytest.raises(ConfigError):
         g.render_forward(c["o"][:8], c["d"][:8], a["step"], a["S"], a["beta"])
+
+
+def test_active_blocks_device_outputs_stay_stream_ordered():
+    """svr_active_blocks with device outputs (count and list) is stream-ordered, no host read of
+    the count: the device count and the first `count` list entries match the host form."""
+    import ctypes
+
+    import torch
+
+    from common import gpu_grid_from, scene_case
+
+    from paper_2305_13220_b200._lib import check
+
+    c = scene_case()
+    g = gpu_grid_from(c)
+    g.set_stream(torch.cuda.current_stream())
+    g.grad_zero()
+    g.render_forward(c["o"], c["d"], c["step"], 64, c["beta"])
+    g.render_backward(c["dC"], c["dD"], c["dN"])
+    A = g.block_count()
+    lst = torch.full((A,), -1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    check(g._lib.svr_active_blocks(g._h, None, lst.data_ptr(), cnt.data_ptr()))
+    torch.cuda.synchronize()
+    want = np.flatnonzero(g.active_mask())
+    n = int(cnt.item())
+    assert n == len(want) and np.array_equal(lst[:n].cpu().numpy(), want)
