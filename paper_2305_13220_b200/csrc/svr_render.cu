@@ -305,10 +305,21 @@ __global__ void __launch_bounds__(kMarchThreads, 6) k_march(GridView g, const do
         s_od[3 + a][threadIdx.x] = D[3 * r + a];
     }
     const StridedVec o{&s_od[0][threadIdx.x], kMarchThreads}, d{&s_od[3][threadIdx.x], kMarchThreads};
+    // t values leave in aligned pairs (one 16 B store per two samples: half the store
+    // instructions of this thread-per-ray kernel, whose stores never coalesce across lanes)
+    double t_even = 0.0;
+    const bool pairs = (S & 1u) == 0;
     const uint32_t cnt = march_dev(g, o, d, step, S, [&](uint32_t k, double t) {
-        tr[k] = t;
+        if (!pairs) {
+            tr[k] = t;
+        } else if (k & 1u) {
+            *reinterpret_cast<double2*>(tr + k - 1) = make_double2(t_even, t);
+        } else {
+            t_even = t;
+        }
         if (k == 0) t_first = t;
     });
+    if (pairs && (cnt & 1u)) tr[cnt - 1] = t_even;
     counts[r] = cnt;
     if (pkeys) {  // the post-march sort key without re-reading the t row
         pkeys[r] = first_sample_key(g, o, d, cnt, t_first);
