@@ -552,12 +552,17 @@ def run_ours(args, cfg, rank, world, local_rank):
                          ("cfg3_hash_lookup", lambda: bench_cfg3_hash(args, dev, stream)),
                          ("cfg4_activation_and_query", lambda: bench_cfg4(dev, stream, cpu=not args.no_cpu_baseline)),
                          ("cfg3_fusion_and_denoise", lambda: bench_fusion(dev, stream, cpu=not args.no_cpu_baseline)),
-                         ("cfg3_refine_step", lambda: bench_refine(dev, stream))):
+                         ("cfg3_refine_step", lambda: bench_refine(dev, stream, cpu=not args.no_cpu_baseline))):
             try:
                 extra[name] = fn()
             except Exception as e:  # pragma: no cover
                 extra[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
             torch.cuda.empty_cache()
+        if "cpu_baseline" in line and "error" not in extra.get("cfg3_hash_lookup", {"error": 1}):
+            # the reference renders through its own hash BlockMap whatever the GPU lookup mode
+            extra["cfg3_hash_lookup"]["cpu_baseline"] = dict(
+                line["cpu_baseline"], sample="the main line's CPU leg (the reference looks every block up in its "
+                                             "hash BlockMap; the dense index is a GPU-side choice)")
         line["extra_configs"] = extra
     print(json.dumps(line), flush=True)
 
@@ -679,8 +684,14 @@ def bench_cfg1(dev, stream, cpu=True):
 
     ms = _events_ms(stream, one, 50)
     st = g.render_stats()
+    peak, _ = peaks()
+    step_bytes = st.valid_samples * STEP_B_SAMPLE + n * STEP_B_RAY
     out = {"blocks": g.block_count(), "rays": n, "valid_samples": int(st.valid_samples),
-           "ms_per_step": ms, "samples_per_s": st.valid_samples / (ms * 1e-3)}
+           "ms_per_step": ms, "samples_per_s": st.valid_samples / (ms * 1e-3),
+           "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                        "bytes_model": "SURVEY.md 8(d): 438.8 B/valid sample + 108 B/ray (fwd + bwd)",
+                        "achieved": step_bytes / (ms * 1e-3) / 1e9, "frac": step_bytes / (ms * 1e-3) / 1e9 / peak,
+                        "note": "launch-bound at 4096 rays (10 kernels for 0.25 M samples)"}}
     # launch-bound at this size: the same step captured once into a CUDA graph and replayed
     try:
         graph = torch.cuda.CUDAGraph()
@@ -966,12 +977,28 @@ def bench_fusion(dev, stream, cpu=True):
     vox = A * 512
     # algorithmic bytes of one denoise: read + write payload float4 + logits, read validity
     den_bytes = vox * (16 + 4 * C) * 2 + A * 64
+    # fuse_all: the 32.32 fixed-point sums (4 + C channels) and counts read + written once per
+    # launch, the frames read (depth 4 + rgb 12 + semantics 4C per pixel), the finalize pass
+    # writing payload + weight + logits + validity
+    npx = depth.size
+    fuse_bytes = vox * ((4 + C) * 8 + 4) * 2 + npx * (4 + 12 + 4 * C) + vox * (16 + 4 + 4 * C) + A * 64
+    peak, _ = peaks()
     out = {"blocks": A, "frames": len(cams), "voxel_frame_pairs": vox * len(cams),
            "associations": int(r.in_view), "integrated": int(r.integrated), "rejected": int(r.rejected),
            "fuse_all_ms": fuse_ms, "voxel_frames_per_s": vox * len(cams) / (fuse_ms * 1e-3),
            "associations_per_s": r.in_view / (fuse_ms * 1e-3),
            "denoise_ms": den_ms, "denoise_voxels_per_s": vox / (den_ms * 1e-3),
            "denoise_GBps_algorithmic": den_bytes / (den_ms * 1e-3) / 1e9,
+           "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                        "bytes_model": "fuse_all: sums + counts read and written once, frames read once, finalize "
+                                       "writes payload / weight / logits / validity; denoise: payload + logits read "
+                                       "and written, validity read",
+                        "fuse_achieved": fuse_bytes / (fuse_ms * 1e-3) / 1e9,
+                        "fuse_frac": fuse_bytes / (fuse_ms * 1e-3) / 1e9 / peak,
+                        "denoise_achieved": den_bytes / (den_ms * 1e-3) / 1e9,
+                        "denoise_frac": den_bytes / (den_ms * 1e-3) / 1e9 / peak,
+                        "note": "k_fuse is FP64-issue bound (exact Camera::project per voxel-frame pair), "
+                                "k_denoise issue / barrier bound (fp64 separable passes)"},
            "marching_cubes_ms": mc_ms, "mesh_vertices": int(mc["nv"].value), "mesh_triangles": int(mc["nt"].value),
            "marching_cubes_cells_per_s": vox / (mc_ms * 1e-3),
            "launches": {"fuse_all": "memset x2 + k_fuse x ceil(64 / batch) + k_fuse_finalize",
@@ -1014,7 +1041,7 @@ def bench_fusion(dev, stream, cpu=True):
     return out
 
 
-def bench_refine(dev, stream, steps=20):
+def bench_refine(dev, stream, steps=20, cpu=True):
     """SURVEY.md 8(f) / SPEC.md:320-327: the full refinement step at the paper's batch (64 images
     x 1024 rays) on the cfg3 grid with device-resident 640x480 frames (rgb, depth prior,
     normal prior): sample batch -> forward -> losses -> backward -> Eikonal -> RMSProp."""
@@ -1046,11 +1073,55 @@ def bench_refine(dev, stream, steps=20):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     st = ref.step(0, 1, stats=True)
+    # the step's sizes for the byte model: re-render the last batch (forward + backward only)
+    S, step_m, beta = 256, cfg["h"] / 2, 2 * cfg["h"]
+    g.grad_zero()
+    g.render_forward(ref.o, ref.d, step_m, S, beta)
+    g.render_backward(ref.grads["d_rgb"], ref.grads["d_depth"], ref.grads["d_normal"])
+    valid = int(g.render_stats().valid_samples)
+    act = int(g.active_mask().sum())
+    g.grad_zero()
+    peak, _ = peaks()
+    step_bytes = valid * STEP_B_SAMPLE + ref.n * STEP_B_RAY + act * 512 * 96
     out = {"rays_per_step": ref.n, "max_samples": 256, "ms_per_step": ms, "rays_per_s": ref.n / (ms * 1e-3),
+           "valid_samples": valid, "active_blocks": act,
+           "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s",
+                        "bytes_model": "render 438.8 B/valid sample + 108 B/ray; RMSProp 96 B per active voxel "
+                                       "(gradient, rms state and payload float4 read + written)",
+                        "achieved": step_bytes / (ms * 1e-3) / 1e9, "frac": step_bytes / (ms * 1e-3) / 1e9 / peak},
            "loss": {k: st[k] for k in ("L_c", "L_d", "L_n", "L_eik", "total")},
            "launches_per_step": "k_sample_frame_rays, ray order x2 (+CUB), k_march, k_forward, k_loss_sums, "
                                 "k_loss_fit, k_loss_grad, k_backward (S > 64: non-pipelined), k_band_count (+CUB scan), k_band_write, "
                                 "k_sample_uniform, k_eik_stats, k_eik_scatter, k_active_*, k_rmsprop"}
+    if cpu:  # the oracle's fp64 step on the host cores over 1/16 of the same batch
+        from oracle import OracleGrid, render_losses as oracle_losses
+
+        A = g.block_count()
+        og = OracleGrid(cfg["h"], 8, cfg["C"], capacity=max(A, 1 << 21))
+        og.allocate_blocks(g.coords())
+        for f in range(0, A, 16384):
+            m = min(16384, A - f)
+            og.set_payload(f, m, **g.get_payload(f, m))
+        m = ref.n // 16
+        host = {k: v[:m].cpu().numpy() for k, v in (("o", ref.o), ("d", ref.d), ("tgt", ref.tgt), ("pd", ref.pd),
+                                                      ("pn", ref.pn), ("ci", ref.ci))}
+        npts = min(len(ref.pts), ref.cfg.uniform_points + ref.cfg.band_cap) // 16
+        pts = ref.pts[:npts].cpu().numpy()
+        cores = os.cpu_count() or 1
+        OracleGrid.set_threads(cores)
+        t0 = time.perf_counter()
+        o_out = og.render_forward(host["o"], host["d"], step_m, S, beta)
+        o_g, _ = oracle_losses(o_out, host["tgt"], host["pd"], host["pn"], host["ci"], cams)
+        gs, gr, active = og.render_backward(host["o"], host["d"], step_m, S, beta, o_g["d_rgb"], o_g["d_depth"],
+                                            o_g["d_normal"])
+        _, _, egs, eact = og.eikonal(pts, 1.0)
+        rms = np.zeros((A, 512, 4), np.float32)
+        og.rmsprop(gs + egs, gr, active | eact, 1e-3, 0.9, 1e-8, rms)
+        dt = time.perf_counter() - t0
+        OracleGrid.set_threads(1)
+        out["cpu_baseline"] = {"value": m / dt, "unit": "rays/s", "cores": cores, "kind": "port",
+                               "sample": f"{m} rays of the batch (1/16): forward + losses + backward + Eikonal on "
+                                         f"{npts} points + RMSProp, fp64 oracle ({dt:.2f} s)"}
     del ref, g
     torch.cuda.empty_cache()
     return out
