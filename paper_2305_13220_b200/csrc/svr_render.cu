@@ -667,7 +667,10 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
     const double* o = s_od[wib];
     const double* d = o + 3;
     const double* tr = T + static_cast<uint64_t>(r) * S;
-    double t_cur = static_cast<uint32_t>(lane) < cnt ? tr[lane] : 0.0;  // t of the upcoming pass
+    // t of the upcoming pass and of the sample after it (delta_k = t_{k+1} - t_k), both loaded
+    // one pass ahead (no shuffles: they share the L1 data path with the gathers)
+    double t_cur = static_cast<uint32_t>(lane) < cnt ? tr[lane] : 0.0;
+    double tn_cur = static_cast<uint32_t>(lane) + 1 < cnt ? tr[lane + 1] : 0.0;
     uint32_t nvalid = 0;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // C, D, N, W
     float tau_base = 0.f;
@@ -675,10 +678,9 @@ __global__ void __launch_bounds__(kFwdThreads, 32) k_forward(GridView g, const d
         const uint32_t k0 = base + lane;
         const bool in0 = k0 < cnt;
         const double t0 = in0 ? t_cur : 0.0;
+        const double tn0 = tn_cur;
         t_cur = k0 + 32 < cnt ? tr[k0 + 32] : 0.0;  // one pass ahead
-        double tn0 = __shfl_down_sync(kFull, t0, 1);
-        const double tl0 = __shfl_sync(kFull, t_cur, 0);
-        if (lane == 31) tn0 = tl0;
+        tn_cur = k0 + 33 < cnt ? tr[k0 + 33] : 0.0;
         const float d0 = (k0 + 1 < cnt) ? static_cast<float>(__dsub_rn(tn0, t0)) : static_cast<float>(step);
         SampleVal v0;
         const bool ok0 = eval_slot(g, o, d, in0, t0, v0);
