@@ -1,13 +1,17 @@
 // sm_100a kernels of the rendering hot path:
 //   K2 k_query     -- fp64 trilinear query, bit-exact with grid.cpp:112-261
 //   K4 k_march     -- ray-block DDA + fixed-step sampling, bit-exact with grid.cpp:263-353
-//   K5 k_forward   -- fused gather/interpolate/Laplace density/compositing, warp per ray
-//   K6 k_backward  -- compositing adjoint (warp suffix scan) + trilinear adjoint +
-//                     red.global.add.v4.f32 scatter into the float4 gradient planes
+//   K5 k_forward   -- fused gather/interpolate/Laplace density/compositing, warp per ray;
+//                     leaves the per-sample records; stores a pending zeroing's zeros
+//   K6p k_backward_pipe -- persistent warps streaming t + record rows (cp.async.bulk ring):
+//                     compositing adjoint (warp scans) + factored trilinear adjoint +
+//                     predicated red.global.add.v4.f32 scatter into the float4 gradient
+//                     planes; active blocks through the touch table (k_touch_expand)
+//   K6 k_backward  -- the same for max_samples > 64 / no records (64-sample chunks)
 // Discrete decisions (which block/cell, sample t) use fp64 with explicit _rn
 // intrinsics so nvcc cannot contract them into FMA (the reference's x86-64 Release
 // build has no FMA, proj/CMakeLists.txt:9-11).  Continuous interpolation and
-// compositing run in fp32 (tolerance in tests/test_gpu_render.py).
+// compositing run in fp32 (tolerance 1e-4 |ref| + 1e-6 max |ref|, tests/common.py).
 #include <cfloat>
 #include <cstdint>
 
@@ -856,8 +860,8 @@ __device__ __forceinline__ void scatter_pair_par(float4* grad, const SampleVal& 
 // K6: backward.  Chunks of 64 samples are visited back to front; within a chunk the
 // suffix S_k = sum_{m>k} w_m v_m comes from a warp suffix scan (no cancellation-prone
 // "total minus prefix").  dL/dtau_k = T_{k+1} v_k - S_k, dL/ds_k = delta_k sigma' dL/dtau_k.
-// Corner gradients are produced and issued one corner at a time (red.global.add.v4.f32);
-// a lane whose two samples share a cell sums them first.
+// The scatter is K6p's (scatter_pair_par: parity-keyed runs, predicated red.v4); without
+// records the corner addresses are permuted into parity order first.
 // ---------------------------------------------------------------------------
 template <bool kRec>
 __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* __restrict__ O,
