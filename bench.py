@@ -64,13 +64,19 @@ def peaks():
 
 
 def build_id() -> str:
-    """Hash of the product's kernel sources: ncu captures are tied to the build they profiled."""
+    """Hash of the product's kernel sources with comments and blank space removed: ncu captures
+    are tied to the code they profiled (a comment edit does not orphan them)."""
+    import re
+
     h = hashlib.sha256()
     csrc = os.path.join(ROOT, "paper_2305_13220_b200", "csrc")
     for f in sorted(os.listdir(csrc)):
         if f.endswith((".cu", ".cuh", ".h")):
-            with open(os.path.join(csrc, f), "rb") as fh:
-                h.update(f.encode() + fh.read())
+            with open(os.path.join(csrc, f), encoding="utf-8") as fh:
+                src = fh.read()
+            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+            src = re.sub(r"//[^\n]*", "", src)
+            h.update(f.encode() + " ".join(src.split()).encode())
     return h.hexdigest()[:16]
 
 
