@@ -73,6 +73,8 @@ struct GridView {
     const uint32_t* nbr;    // [A][8]: entry of block + (k&1, k>>1&1, k>>2), k = 0..7
     const uint8_t* bdist;   // dense mode: Chebyshev distance (blocks, capped) to the nearest
                             // allocated block per AABB cell; 0 = allocated
+    const uint8_t* sbdist;  // hash mode: the same over 8^3-block superblocks (superblock units)
+    int32_t sb_lo[3], sb_dim[3];
     float4* grad;
     uint8_t* active;
     uint8_t* touch;         // [A][8]: a valid sample with base block b and face-crossing mask k

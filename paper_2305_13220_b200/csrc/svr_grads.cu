@@ -71,6 +71,16 @@ __global__ void k_dense_build(const int4* __restrict__ coords, const uint32_t* _
     atomicOr(occ + (cell >> 5), 1u << (cell & 31));
 }
 
+// Superblock occupancy (hash mode): bit of superblock (coord >> 3) set for every block.
+__global__ void k_superblock_occ(const int4* __restrict__ coords, uint32_t n, int32_t lx, int32_t ly, int32_t lz,
+                                 int32_t dx, int32_t dy, uint32_t* occ) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    const size_t cell = (static_cast<size_t>((c.z >> 3) - lz) * dy + ((c.y >> 3) - ly)) * dx + ((c.x >> 3) - lx);
+    atomicOr(occ + (cell >> 5), 1u << (cell & 31));
+}
+
 // Chebyshev block-distance field over the dense AABB (for empty-space jumps in the march):
 // three separable windowed passes, out = min_k max(|k|, in[cell + k e_axis]), |k| <= cap;
 // pass 0 reads the occupancy bits (allocated = 0, empty = cap + 1).
@@ -296,6 +306,13 @@ void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n
     if (!n) return;
     k_dense_build<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), meta, n,
                                                   lo[0], lo[1], lo[2], dim[0], dim[1], dense, occ);
+}
+
+void launch_superblock_occ(const int32_t* coords4, uint32_t n, const int32_t* sb_lo, const int32_t* sb_dim,
+                           uint32_t* occ, cudaStream_t s) {
+    if (!n) return;
+    k_superblock_occ<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), n, sb_lo[0], sb_lo[1],
+                                                      sb_lo[2], sb_dim[0], sb_dim[1], occ);
 }
 
 void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t* tmp, cudaStream_t s) {

@@ -206,6 +206,9 @@ struct svr_grid {
     int use_dense = 0;
     int32_t dim[3] = {0, 0, 0};
     DevBuf dense, occ, nbr, bdist, bdist_tmp;
+    DevBuf sb_occ, sbdist, sbdist_tmp;  // hash mode: superblock occupancy + distance field
+    int use_sb = 0;
+    int32_t sb_lo[3] = {0, 0, 0}, sb_dim[3] = {0, 0, 0};
     bool use_jump = true;   // march: exact empty-space jumps over the block-distance field
 
     // render context
@@ -351,6 +354,8 @@ struct svr_grid {
         v.logits = logits;
         v.nbr = nbr.as<uint32_t>();
         v.bdist = (use_dense && use_jump) ? bdist.as<uint8_t>() : nullptr;
+        v.sbdist = (!use_dense && use_sb && use_jump) ? sbdist.as<uint8_t>() : nullptr;
+        for (int a = 0; a < 3; ++a) v.sb_lo[a] = sb_lo[a], v.sb_dim[a] = sb_dim[a];
         v.grad = grad;
         v.active = active;
         v.touch = touch;
@@ -460,6 +465,28 @@ struct svr_grid {
             svr_internal::launch_bdist(occ.as<uint32_t>(), dim, bdist.as<uint8_t>(), bdist_tmp.as<uint8_t>(), stream);
             SVR_LAUNCHED();
             use_dense = 1;
+        }
+        use_sb = 0;
+        if (!use_dense) {  // hash mode: superblock (8^3 blocks) occupancy + distance field
+            uint64_t sc = 1;
+            for (int a = 0; a < 3; ++a) {
+                sb_lo[a] = lo[a] >> 3;  // arithmetic shift = floor division
+                sb_dim[a] = (hi[a] >> 3) - sb_lo[a] + 1;
+                sc *= static_cast<uint64_t>(sb_dim[a]);
+            }
+            if (sc <= (1ull << 30)) {
+                sb_occ.ensure(((sc + 31) / 32) * 4);
+                SVR_CK(cudaMemsetAsync(sb_occ.p, 0, ((sc + 31) / 32) * 4, stream));
+                svr_internal::launch_superblock_occ(coords4, static_cast<uint32_t>(n()), sb_lo, sb_dim,
+                                                    sb_occ.as<uint32_t>(), stream);
+                SVR_LAUNCHED();
+                sbdist.ensure(sc);
+                sbdist_tmp.ensure(sc);
+                svr_internal::launch_bdist(sb_occ.as<uint32_t>(), sb_dim, sbdist.as<uint8_t>(),
+                                           sbdist_tmp.as<uint8_t>(), stream);
+                SVR_LAUNCHED();
+                use_sb = 1;
+            }
         }
         nbr.ensure(n() * 32);
         svr_internal::launch_nbr_build(view(), coords4, static_cast<uint32_t>(n()), nbr.as<uint32_t>(),

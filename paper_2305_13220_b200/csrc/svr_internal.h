@@ -106,6 +106,8 @@ void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n
                         const int32_t* lo, const int32_t* dim, uint32_t* dense, uint32_t* occ,
                         cudaStream_t s);
 void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t* tmp, cudaStream_t s);
+void launch_superblock_occ(const int32_t* coords4, uint32_t n, const int32_t* sb_lo, const int32_t* sb_dim,
+                           uint32_t* occ, cudaStream_t s);
 void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank, const uint32_t* rows,
                            uint64_t n_rows, cudaStream_t s);
 void launch_nbr_build(const svr_dev::GridView& g, const int32_t* coords4, uint32_t n, uint32_t* nbr,

@@ -187,10 +187,25 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const V& o, con
         if (g.bdist) {
             dist = __ldg(g.bdist + static_cast<uint32_t>(cell));
             alloc = dist == 0;
+        } else if (g.use_dense) {
+            alloc = ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0;
         } else {
-            alloc = g.use_dense
-                        ? ((__ldg(g.occ + (static_cast<uint32_t>(cell) >> 5)) >> (cell & 31)) & 1u) != 0
-                        : hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+            // hash mode: a superblock at Chebyshev distance dsb >= 1 from every occupied one has
+            // every block within 8 (dsb - 1) of this one empty -- no probe, and a jump when that
+            // radius allows (dist - 1 = 8 (dsb - 1)); otherwise the block's own hash probe
+            int dsb = 0;
+            if (g.sbdist) {
+                const uint32_t sx = static_cast<uint32_t>((b0 >> 3) - g.sb_lo[0]);
+                const uint32_t sy = static_cast<uint32_t>((b1 >> 3) - g.sb_lo[1]);
+                const uint32_t sz = static_cast<uint32_t>((b2 >> 3) - g.sb_lo[2]);
+                dsb = __ldg(g.sbdist + (static_cast<size_t>(sz) * g.sb_dim[1] + sy) * g.sb_dim[0] + sx);
+            }
+            if (dsb >= 1) {
+                alloc = false;
+                dist = 8 * (dsb - 1) + 1;
+            } else {
+                alloc = hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+            }
         }
         if (dist >= 3) {
             open = false;

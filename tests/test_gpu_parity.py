@@ -215,12 +215,13 @@ def test_march_bit_exact_random_rays_with_degenerate_directions(case, lookup):
     assert mask.sum() > 500_000
 
 
-@pytest.mark.parametrize("jump", [1, 0])
-def test_march_empty_space_jumps_bit_exact(jump):
+@pytest.mark.parametrize("jump,lookup", [(1, 2), (0, 2), (1, 1)])
+def test_march_empty_space_jumps_bit_exact(jump, lookup):
     """Sparse block clusters inside a 96^3-block AABB, so most of each ray's walk crosses
-    wide empty space where the dense-mode march jumps over the block-distance field: counts,
-    t and delta must equal the oracle's step-by-step walk bit for bit (random rays, rays
-    through exact block corners / along block edges, axis-parallel and diagonal rays)."""
+    wide empty space where the march jumps -- over the block-distance field (dense index) or
+    the 8^3-superblock distance field (hash mode): counts, t and delta must equal the oracle's
+    step-by-step walk bit for bit (random rays, rays through exact block corners / along block
+    edges, axis-parallel and diagonal rays)."""
     from paper_2305_13220_b200 import SparseDenseGrid
 
     h = 0.01
@@ -237,7 +238,7 @@ def test_march_empty_space_jumps_bit_exact(jump):
     g = SparseDenseGrid(h, 8, 1)
     g.allocate_blocks(coords)
     g.set_payload(0, A, weight=np.ones((A, 512), np.float32))
-    g.set_lookup(2)  # dense AABB index (the jump needs the distance field)
+    g.set_lookup(lookup)  # 2: dense AABB index + block distances; 1: hash + superblock distances
     g.set_tuning("march_jump", jump)
     n = 60_000
     o = rng.uniform(-0.5, 96 * L + 0.5, size=(n, 3))
