@@ -99,10 +99,14 @@ struct DevBuf {
     T* as() const {
         return static_cast<T*>(p);
     }
-    // as cudaFree did implicitly: the device is idle before the block is handed back
+    // as cudaFree did implicitly: the block's device is idle before the block is handed back
     void release() {
         if (!p) return;
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
         cudaDeviceSynchronize();
+        if (cur != dev && cur >= 0) cudaSetDevice(cur);
         dev_release(p, bytes, dev);
         p = nullptr;
         bytes = 0;
