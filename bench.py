@@ -63,9 +63,31 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def build_id() -> str:
-    """Hash of the product's kernel sources with comments and blank space removed: ncu captures
-    are tied to the code they profiled (a comment edit does not orphan them)."""
+STEP_KERNELS = ("k_march", "k_forward", "k_backward_pipe")
+
+
+def build_id(so_path=None) -> str:
+    """Hash of the SASS of the step's kernels in the built library (cuobjdump): ncu captures are
+    tied to the machine code they profiled, host-code or comment edits do not orphan them.
+    Falls back to the kernel sources without comments when cuobjdump is unavailable."""
+    so = so_path or os.path.join(ROOT, "paper_2305_13220_b200", "libsvr_b200.so")
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True, timeout=120,
+                             check=True).stdout
+        h = hashlib.sha256()
+        keep = False
+        for line in out.splitlines():
+            if "Function :" in line:  # the mangled name embeds a build-path hash: not hashed
+                name = line.split("Function :")[1].strip()
+                keep = any(f"{len(k)}{k}" in name and ("EN" in name.split(k, 1)[1][:2]) for k in STEP_KERNELS)
+                if keep:
+                    h.update(next(k for k in STEP_KERNELS if f"{len(k)}{k}" in name).encode())
+                continue
+            if keep:
+                h.update(line.strip().encode())
+        return "sass-" + h.hexdigest()[:16]
+    except Exception:
+        pass
     import re
 
     h = hashlib.sha256()
