@@ -29,10 +29,8 @@ void fuse_grow(svr_grid* g) {
             SVR_CK(cudaMemcpyAsync(c2.p, g->fuse_cnt.p, g->fuse_blocks * per_cnt, cudaMemcpyDeviceToDevice, g->stream));
         }
         SVR_CK(cudaStreamSynchronize(g->stream));
-        std::swap(g->fuse_sum.p, s2.p);
-        std::swap(g->fuse_sum.bytes, s2.bytes);
-        std::swap(g->fuse_cnt.p, c2.p);
-        std::swap(g->fuse_cnt.bytes, c2.bytes);
+        g->fuse_sum.swap(s2);
+        g->fuse_cnt.swap(c2);
     }
     const uint64_t f = g->fuse_blocks;
     SVR_CK(cudaMemsetAsync(static_cast<char*>(g->fuse_sum.p) + f * per_sum, 0, (nb - f) * per_sum, g->stream));

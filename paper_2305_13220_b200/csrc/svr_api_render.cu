@@ -424,8 +424,7 @@ int svr_rmsprop_step(svr_grid* g, float lr, float alpha, float eps) {
                 SVR_CK(cudaMemcpyAsync(fresh.p, g->rms.p, g->rms_blocks * kVox * sizeof(float4),
                                        cudaMemcpyDeviceToDevice, g->stream));
             SVR_CK(cudaStreamSynchronize(g->stream));
-            std::swap(g->rms.p, fresh.p);
-            std::swap(g->rms.bytes, fresh.bytes);
+            g->rms.swap(fresh);
             g->rms_blocks = nb;
         }
         g->active_list.ensure(nb * 4);

@@ -99,11 +99,17 @@ struct DevBuf {
     T* as() const {
         return static_cast<T*>(p);
     }
+    void swap(DevBuf& o) {
+        std::swap(p, o.p);
+        std::swap(bytes, o.bytes);
+        std::swap(dev, o.dev);
+    }
     // as cudaFree did implicitly: the block's device is idle before the block is handed back
     void release() {
         if (!p) return;
         int cur = -1;
         cudaGetDevice(&cur);
+        if (dev < 0) dev = cur;
         if (cur != dev) cudaSetDevice(dev);
         cudaDeviceSynchronize();
         if (cur != dev && cur >= 0) cudaSetDevice(cur);
