@@ -135,12 +135,20 @@ __global__ void __launch_bounds__(256) k_depth_to_keys(const float* __restrict__
         const double vy = t[W + y];
         const float* drow = depth + static_cast<size_t>(row) * W;
         const double* sf = scales ? scales + static_cast<size_t>(f) * rows * cols : nullptr;
-        for (int x0 = 0; x0 < W; x0 += 32) {
+        // four 32-pixel chunks per group: their depth loads are in flight together
+        for (int xg = 0; xg < W; xg += 128) {
+        float dq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dq[u] = xg + 32 * u + lane < W ? __ldg(drow + xg + 32 * u + lane) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int x0 = xg + 32 * u;
+            if (x0 >= W) break;  // warp-uniform
             const int x = x0 + lane;
             bool have = x < W;
             unsigned long long key = 0;
             if (have) {
-                const float dv = drow[x];
+                const float dv = dq[u];
                 have = dv > 0.0f;
                 double scale = 1.0;
                 if (have && sf) {
@@ -169,6 +177,7 @@ __global__ void __launch_bounds__(256) k_depth_to_keys(const float* __restrict__
             }
             used += have ? 1u : 0u;
             warp_insert(have, key, ks, count);
+        }
         }
     }
 #pragma unroll
