@@ -25,6 +25,7 @@ constexpr uint32_t kFullBit = 0x80000000u;
 constexpr unsigned long long kEmptyKey = ~0ull;
 constexpr int kRes = 8;        // block resolution
 constexpr int kVox = 512;      // voxels per block
+constexpr uint32_t kNoBrick = 0x80000000u;  // GridView::sbinfo: superblock without a brick
 constexpr uint64_t kMaxBlocks = 1ull << 23;  // 32-bit voxel addresses: block * 512 + local
 constexpr int32_t kCoordLim = 1 << 20;
 
@@ -75,6 +76,9 @@ struct GridView {
                             // allocated block per AABB cell; 0 = allocated
     const uint8_t* sbdist;  // hash mode: the same over 8^3-block superblocks (superblock units)
     int32_t sb_lo[3], sb_dim[3];
+    const uint32_t* sbinfo; // hash mode: per superblock, its brick (superblock distance <= 1) or
+                            // kNoBrick | superblock distance
+    const uint8_t* bricks;  // [brick][512] block distances (capped at 9) of those superblocks
     float4* grad;
     uint8_t* active;
     uint8_t* touch;         // [A][8]: a valid sample with base block b and face-crossing mask k

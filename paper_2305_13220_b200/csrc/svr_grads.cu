@@ -108,6 +108,69 @@ __global__ void k_bdist_pass(const uint32_t* __restrict__ occ, const uint8_t* __
     out[i] = static_cast<uint8_t>(best);
 }
 
+// Hash mode: block-distance bricks.  Every superblock at superblock distance <= 1 from an
+// occupied one owns a brick of 8^3 u8 block distances: the exact Chebyshev distance to the
+// nearest allocated block, capped at kBrickCap + 1.  A block of a superblock at distance >= 2
+// is at least 8 + 1 blocks from every allocated one, so reading brick-less superblocks as
+// kBrickCap + 1 = 9 keeps the three separable passes exact up to the cap.
+constexpr int kBrickCap = 8;
+__global__ void k_brick_assign(const uint8_t* __restrict__ sbdist, uint64_t n, uint32_t* info, uint32_t* brick_sb,
+                               uint32_t* counter) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t d = sbdist[i];
+    if (d <= 1) {
+        const uint32_t b = atomicAdd(counter, 1u);
+        info[i] = b;
+        brick_sb[b] = static_cast<uint32_t>(i);
+    } else {
+        info[i] = kNoBrick | d;
+    }
+}
+__global__ void k_brick_occ(const int4* __restrict__ coords, uint32_t n, int32_t lx, int32_t ly, int32_t lz,
+                            int32_t dx, int32_t dy, const uint32_t* __restrict__ info, uint8_t* bricks) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int4 c = coords[i];
+    const size_t sb = (static_cast<size_t>((c.z >> 3) - lz) * dy + ((c.y >> 3) - ly)) * dx + ((c.x >> 3) - lx);
+    bricks[static_cast<size_t>(info[sb]) * kVox + (c.x & 7) + 8 * ((c.y & 7) + 8 * (c.z & 7))] = 0;
+}
+// out = min_k max(|k|, in[cell + k e_axis]), |k| <= kBrickCap, across brick boundaries
+__global__ void k_brick_pass(const uint8_t* __restrict__ in, uint8_t* out, const uint32_t* __restrict__ info,
+                             const uint32_t* __restrict__ brick_sb, uint32_t n_bricks, int32_t dx, int32_t dy,
+                             int32_t dz, int axis) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<uint64_t>(n_bricks) * kVox) return;
+    const uint32_t local = static_cast<uint32_t>(i & (kVox - 1));
+    const uint32_t sb = brick_sb[i / kVox];
+    int32_t sc[3] = {static_cast<int32_t>(sb % dx), static_cast<int32_t>((sb / dx) % dy),
+                     static_cast<int32_t>(sb / (static_cast<uint32_t>(dx) * dy))};
+    const int32_t dims[3] = {dx, dy, dz};
+    int32_t lc[3] = {static_cast<int32_t>(local & 7), static_cast<int32_t>((local >> 3) & 7),
+                     static_cast<int32_t>(local >> 6)};
+    const int32_t pos = lc[axis];
+    int best = kBrickCap + 1;
+    for (int k = -kBrickCap; k <= kBrickCap; ++k) {
+        const int32_t q = pos + k;
+        const int32_t off = q < 0 ? -1 : (q > 7 ? 1 : 0);
+        int32_t nc[3] = {sc[0], sc[1], sc[2]};
+        nc[axis] += off;
+        int v = kBrickCap + 1;
+        if (nc[axis] >= 0 && nc[axis] < dims[axis]) {
+            const uint32_t inf = info[(static_cast<size_t>(nc[2]) * dy + nc[1]) * dx + nc[0]];
+            if (!(inf & kNoBrick)) {
+                int32_t l2[3] = {lc[0], lc[1], lc[2]};
+                l2[axis] = q & 7;
+                v = in[static_cast<size_t>(inf) * kVox + l2[0] + 8 * (l2[1] + 8 * l2[2])];
+            }
+        }
+        const int ak = k < 0 ? -k : k;
+        const int m = v > ak ? v : ak;
+        if (m < best) best = m;
+    }
+    out[i] = static_cast<uint8_t>(best);
+}
+
 // K8p: active-block gradient all-reduce directly over the ranks' gradient planes (peer memory:
 // NVLink P2P through CUDA IPC mappings).  Rank r owns the slice [r n / W, (r + 1) n / W) of
 // the ascending active list; for each of its rows every thread sums one float4 over the W
@@ -323,6 +386,32 @@ void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, tmp, out, dim[0], dim[1], dim[2], 1);
     k_bdist_pass<<<grid, 256, 0, s>>>(occ, out, tmp, dim[0], dim[1], dim[2], 2);
     SVR_LCK(cudaMemcpyAsync(out, tmp, n, cudaMemcpyDeviceToDevice, s));
+}
+
+uint32_t launch_brick_assign(const int32_t* sb_dim, const uint8_t* sbdist, uint32_t* info, uint32_t* brick_sb,
+                             uint32_t* counter, cudaStream_t s) {
+    const uint64_t sc = static_cast<uint64_t>(sb_dim[0]) * sb_dim[1] * sb_dim[2];
+    if (!sc) return 0;
+    SVR_LCK(cudaMemsetAsync(counter, 0, 4, s));
+    k_brick_assign<<<static_cast<unsigned>((sc + 255) / 256), 256, 0, s>>>(sbdist, sc, info, brick_sb, counter);
+    uint32_t nb = 0;
+    SVR_LCK(cudaMemcpyAsync(&nb, counter, 4, cudaMemcpyDeviceToHost, s));
+    SVR_LCK(cudaStreamSynchronize(s));
+    return nb;
+}
+
+void launch_brick_fill(const int32_t* coords4, uint32_t n, const int32_t* sb_lo, const int32_t* sb_dim,
+                       const uint32_t* info, const uint32_t* brick_sb, uint32_t n_bricks, uint8_t* bricks,
+                       uint8_t* tmp, cudaStream_t s) {
+    if (!n || !n_bricks) return;
+    const size_t bytes = static_cast<size_t>(n_bricks) * kVox;
+    SVR_LCK(cudaMemsetAsync(tmp, kBrickCap + 1, bytes, s));
+    k_brick_occ<<<(n + 255) / 256, 256, 0, s>>>(reinterpret_cast<const int4*>(coords4), n, sb_lo[0], sb_lo[1],
+                                                 sb_lo[2], sb_dim[0], sb_dim[1], info, tmp);
+    const unsigned grid = static_cast<unsigned>((bytes + 255) / 256);
+    k_brick_pass<<<grid, 256, 0, s>>>(tmp, bricks, info, brick_sb, n_bricks, sb_dim[0], sb_dim[1], sb_dim[2], 0);
+    k_brick_pass<<<grid, 256, 0, s>>>(bricks, tmp, info, brick_sb, n_bricks, sb_dim[0], sb_dim[1], sb_dim[2], 1);
+    k_brick_pass<<<grid, 256, 0, s>>>(tmp, bricks, info, brick_sb, n_bricks, sb_dim[0], sb_dim[1], sb_dim[2], 2);
 }
 
 void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank, const uint32_t* rows,

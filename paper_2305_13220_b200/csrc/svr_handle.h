@@ -217,7 +217,9 @@ struct svr_grid {
     int32_t dim[3] = {0, 0, 0};
     DevBuf dense, occ, nbr, bdist, bdist_tmp;
     DevBuf sb_occ, sbdist, sbdist_tmp;  // hash mode: superblock occupancy + distance field
+    DevBuf sb_info, brick_sb, brick_cnt, bricks, bricks_tmp;  // hash mode: block-distance bricks
     int use_sb = 0;
+    uint32_t n_bricks = 0;
     int32_t sb_lo[3] = {0, 0, 0}, sb_dim[3] = {0, 0, 0};
     bool use_jump = true;   // march: exact empty-space jumps over the block-distance field
 
@@ -365,6 +367,8 @@ struct svr_grid {
         v.nbr = nbr.as<uint32_t>();
         v.bdist = (use_dense && use_jump) ? bdist.as<uint8_t>() : nullptr;
         v.sbdist = (!use_dense && use_sb && use_jump) ? sbdist.as<uint8_t>() : nullptr;
+        v.sbinfo = (v.sbdist && n_bricks) ? sb_info.as<uint32_t>() : nullptr;
+        v.bricks = v.sbinfo ? bricks.as<uint8_t>() : nullptr;
         for (int a = 0; a < 3; ++a) v.sb_lo[a] = sb_lo[a], v.sb_dim[a] = sb_dim[a];
         v.grad = grad;
         v.active = active;
@@ -496,6 +500,22 @@ struct svr_grid {
                                            sbdist_tmp.as<uint8_t>(), stream);
                 SVR_LAUNCHED();
                 use_sb = 1;
+                n_bricks = 0;
+                if (sc <= (1ull << 26)) {  // block-distance bricks of the superblocks near blocks
+                    sb_info.ensure(sc * 4);
+                    brick_sb.ensure(sc * 4);
+                    brick_cnt.ensure(4);
+                    const uint32_t nb = svr_internal::launch_brick_assign(
+                        sb_dim, sbdist.as<uint8_t>(), sb_info.as<uint32_t>(), brick_sb.as<uint32_t>(),
+                        brick_cnt.as<uint32_t>(), stream);
+                    bricks.ensure(static_cast<size_t>(nb) * 512);
+                    bricks_tmp.ensure(static_cast<size_t>(nb) * 512);
+                    svr_internal::launch_brick_fill(coords4, static_cast<uint32_t>(n()), sb_lo, sb_dim,
+                                                    sb_info.as<uint32_t>(), brick_sb.as<uint32_t>(), nb,
+                                                    bricks.as<uint8_t>(), bricks_tmp.as<uint8_t>(), stream);
+                    SVR_LAUNCHED();
+                    n_bricks = nb;
+                }
             }
         }
         nbr.ensure(n() * 32);

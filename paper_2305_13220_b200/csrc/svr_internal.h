@@ -106,6 +106,13 @@ void launch_dense_build(const int32_t* coords4, const uint32_t* meta, uint32_t n
                         const int32_t* lo, const int32_t* dim, uint32_t* dense, uint32_t* occ,
                         cudaStream_t s);
 void launch_bdist(const uint32_t* occ, const int32_t* dim, uint8_t* out, uint8_t* tmp, cudaStream_t s);
+// hash mode block-distance bricks (svr_grads.cu): superblock info + brick count (synchronises),
+// then the bricks' occupancy and three separable distance passes
+uint32_t launch_brick_assign(const int32_t* sb_dim, const uint8_t* sbdist, uint32_t* info, uint32_t* brick_sb,
+                             uint32_t* counter, cudaStream_t s);
+void launch_brick_fill(const int32_t* coords4, uint32_t n, const int32_t* sb_lo, const int32_t* sb_dim,
+                       const uint32_t* info, const uint32_t* brick_sb, uint32_t n_bricks, uint8_t* bricks,
+                       uint8_t* tmp, cudaStream_t s);
 void launch_superblock_occ(const int32_t* coords4, uint32_t n, const int32_t* sb_lo, const int32_t* sb_dim,
                            uint32_t* occ, cudaStream_t s);
 void launch_peer_allreduce(float4* const* planes, uint32_t world, uint32_t rank, const uint32_t* rows,

@@ -194,17 +194,30 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const V& o, con
             // every block within 8 (dsb - 1) of this one empty -- no probe, and a jump when that
             // radius allows (dist - 1 = 8 (dsb - 1)); otherwise the block's own hash probe
             int dsb = 0;
-            if (g.sbdist) {
+            if (g.sbinfo) {  // bricks: the block's own distance near blocks, no probe at all
                 const uint32_t sx = static_cast<uint32_t>((b0 >> 3) - g.sb_lo[0]);
                 const uint32_t sy = static_cast<uint32_t>((b1 >> 3) - g.sb_lo[1]);
                 const uint32_t sz = static_cast<uint32_t>((b2 >> 3) - g.sb_lo[2]);
-                dsb = __ldg(g.sbdist + (static_cast<size_t>(sz) * g.sb_dim[1] + sy) * g.sb_dim[0] + sx);
-            }
-            if (dsb >= 1) {
-                alloc = false;
-                dist = 8 * (dsb - 1) + 1;
+                const uint32_t inf = __ldg(g.sbinfo + (static_cast<size_t>(sz) * g.sb_dim[1] + sy) * g.sb_dim[0] + sx);
+                if (inf & kNoBrick) {
+                    dist = 8 * (static_cast<int>(inf & 0xFFu) - 1) + 1;
+                } else {
+                    dist = __ldg(g.bricks + static_cast<size_t>(inf) * kVox + (b0 & 7) + 8 * ((b1 & 7) + 8 * (b2 & 7)));
+                }
+                alloc = dist == 0;
             } else {
-                alloc = hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+                if (g.sbdist) {
+                    const uint32_t sx = static_cast<uint32_t>((b0 >> 3) - g.sb_lo[0]);
+                    const uint32_t sy = static_cast<uint32_t>((b1 >> 3) - g.sb_lo[1]);
+                    const uint32_t sz = static_cast<uint32_t>((b2 >> 3) - g.sb_lo[2]);
+                    dsb = __ldg(g.sbdist + (static_cast<size_t>(sz) * g.sb_dim[1] + sy) * g.sb_dim[0] + sx);
+                }
+                if (dsb >= 1) {
+                    alloc = false;
+                    dist = 8 * (dsb - 1) + 1;
+                } else {
+                    alloc = hash_find(g, pack_key(b0, b1, b2)) != kInvalid;
+                }
             }
         }
         if (dist >= 3) {

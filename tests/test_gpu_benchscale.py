@@ -42,7 +42,8 @@ def cfg3():
         og.set_payload(f, n, **p)
 
     fill_in_chunks(scene, cfg, coords, sink)
-    o, d, dC, dD, dN = (a[:N_RAYS] for a in rays_for_rank(scene, cfg, 0, 1))
+    rays = rays_for_rank(scene, cfg, 0, 1)
+    o, d, dC, dD, dN = (a[:N_RAYS] for a in rays)
     S, step, beta = cfg["max_samples"], cfg["h"] / 2, 2 * cfg["h"]
     OracleGrid.set_threads(16)
     try:
@@ -52,7 +53,7 @@ def cfg3():
         OracleGrid.set_threads(1)
     del og
     assert 250_000 < len(coords) < 350_000
-    return {"g": g, "o": o, "d": d, "dC": dC, "dD": dD, "dN": dN, "S": S, "step": step, "beta": beta,
+    return {"g": g, "o_all": rays[0], "d_all": rays[1], "o": o, "d": d, "dC": dC, "dD": dD, "dN": dN, "S": S, "step": step, "beta": beta,
             "ref": ref, "gs": gs, "gr": gr, "act": act, "oracle_mod": oracle}
 
 
@@ -75,6 +76,28 @@ def test_bench_grid_ray_subset_matches_oracle(cfg3, lookup):
     assert_close(gs, c["gs"], what="grad_sdf")
     assert_close(gr, c["gr"], what="grad_rgb")
     g.set_lookup(0)
+
+
+def test_bench_rays_march_same_in_both_lookup_modes(cfg3):
+    """All 1,048,576 bench rays: the hash-mode march (superblock distances, block-distance
+    bricks near the blocks, hash probes nowhere) emits the same counts and t values, bit for
+    bit, as the dense-index march -- both are the reference's march_ray (grid.cpp:337-353),
+    which the 65,536-ray subset above checks against the oracle directly."""
+    c = cfg3
+    g = c["g"]
+    S, step = c["S"], c["step"]
+    try:
+        for a in range(0, len(c["o_all"]), 1 << 18):
+            o, d = c["o_all"][a:a + (1 << 18)], c["d_all"][a:a + (1 << 18)]
+            g.set_lookup(2)
+            md = g.march(o, d, step, S)
+            g.set_lookup(1)
+            mh = g.march(o, d, step, S)
+            assert np.array_equal(md["counts"], mh["counts"])
+            valid = np.arange(S)[None, :] < md["counts"][:, None]
+            assert np.array_equal(md["t"][valid].view(np.uint64), mh["t"][valid].view(np.uint64))
+    finally:
+        g.set_lookup(0)
 
 
 def test_cfg4_activation_matches_reference():
