@@ -511,19 +511,26 @@ __device__ __forceinline__ void store_record(float4* rec, const SampleVal& v) {
     rec[1] = make_float4(v.gx, v.gy, v.gz, __uint_as_float(v.e0));
 }
 
+// The backward's invalid sample: zeros, and no corner addresses (the scatter keys on them).
+__device__ __forceinline__ void zero_sample_bwd(SampleVal& v) {
+    zero_sample(v);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v.gidx[c] = kInvalid;
+}
+
 // `rec` may point to global memory (k_backward) or shared memory (k_backward_pipe):
 // generic loads only.
 __device__ __forceinline__ bool eval_from_record(const GridView& g, const double o[3],
                                                  const double d[3], bool in, double t,
                                                  const float4* rec, SampleVal& v) {
     if (!in) {
-        zero_sample(v);
+        zero_sample_bwd(v);
         return false;
     }
     const float4 a = rec[0], b = rec[1];
     const uint32_t e0 = __float_as_uint(b.w);
     if (e0 == kInvalid) {
-        zero_sample(v);
+        zero_sample_bwd(v);
         return false;
     }
     int base[3];
@@ -853,10 +860,12 @@ template <int p>
 __device__ __forceinline__ void scatter_parity(float4* grad, const SampleVal& v0, const SampleVal& v1,
                                                const CornerCoef& k0, const CornerCoef& k1, const XYPart& x0,
                                                const XYPart& x1, bool ok0, bool ok1, int lane) {
-    const uint32_t a0k = ok0 ? v0.gidx[p] : kInvalid, a1k = ok1 ? v1.gidx[p] : kInvalid;
+    const uint32_t a0k = v0.gidx[p], a1k = v1.gidx[p];  // kInvalid for an invalid sample
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 a0 = ok0 ? corner_grad<p>(k0, x0) : z;
-    const float4 a1 = ok1 ? corner_grad<p>(k1, x1) : z;
+    // an invalid sample's coefficients are zero (ds = w = 0, zeroed geometry), so its corner
+    // gradients are zero without a select
+    const float4 a0 = corner_grad<p>(k0, x0);
+    const float4 a1 = corner_grad<p>(k1, x1);
     const bool two = ok0 && ok1 && a0k != a1k;
     const uint32_t first = ok0 ? a0k : a1k, last = ok1 ? a1k : a0k;
     const uint32_t prev_last = __shfl_up_sync(kFull, last, 1);
@@ -972,6 +981,8 @@ __global__ void __launch_bounds__(256, 3) k_backward(GridView g, const double* _
         const float ds1 = ok1 ? p.d1 * density_ds(v1.s, sg1, ib) * (Tn1 * vv1 - S1) : 0.f;
         touch_pair(g, v0, v1, ok0, ok1, lane);
         if (!kRec) {  // records give the parity order directly
+            if (!ok0) zero_sample_bwd(v0);
+            if (!ok1) zero_sample_bwd(v1);
             to_parity_order(v0);
             to_parity_order(v1);
         }
