@@ -543,8 +543,10 @@ __device__ __forceinline__ bool eval_from_record(const GridView& g, const double
 }
 
 // Laplace density and its derivative.
+// One exponential for both branches: -|s| ib is exactly -s ib for s > 0 and s ib otherwise.
 __device__ __forceinline__ float density(float s, float ib) {
-    return s > 0.f ? ib * (0.5f * expf(-s * ib)) : ib * (1.f - 0.5f * expf(s * ib));
+    const float e = expf(-fabsf(s) * ib);
+    return s > 0.f ? ib * (0.5f * e) : ib * (1.f - 0.5f * e);
 }
 __device__ __forceinline__ float density_ds(float s, float sigma, float ib) {
     return s > 0.f ? -sigma * ib : -(ib - sigma) * ib;
