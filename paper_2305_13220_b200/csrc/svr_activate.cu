@@ -50,6 +50,18 @@ __device__ __forceinline__ void warp_insert(bool have, unsigned long long key,
     if (lane == __ffs(peers) - 1) append_key(key, keyset_insert(ks.slots, ks.mask, key), ks, count);
 }
 
+// Pixels along an image row map to runs of equal block keys: one insert per run (a lane whose
+// left neighbour holds the same key skips it) -- cheaper than a full match, and a key that
+// reappears later in the warp is simply inserted again (the set keeps it once).
+__device__ __forceinline__ void warp_insert_runs(bool have, unsigned long long key,
+                                                 const svr_internal::KeySet& ks,
+                                                 unsigned long long* count) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long k = have ? key : ~0ull;
+    const unsigned long long prev = __shfl_up_sync(kFull, k, 1);
+    if (have && (lane == 0 || prev != k)) append_key(key, keyset_insert(ks.slots, ks.mask, key), ks, count);
+}
+
 // block_of_point (grid.hpp:136-141): floor(x / L) of the correctly rounded quotient.  Fast
 // path: q = x * (1/L) (both rounded) is within |x/L| 2^-51.9 <= 2^-31.9 of x/L for the
 // representable block range |x/L| < 2^20, and RN(x/L) within 2^-33 of it; so when q's
@@ -176,7 +188,7 @@ __global__ void __launch_bounds__(256) k_depth_to_keys(const float* __restrict__
                 }
             }
             used += have ? 1u : 0u;
-            warp_insert(have, key, ks, count);
+            warp_insert_runs(have, key, ks, count);
         }
         }
     }
