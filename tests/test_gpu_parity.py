@@ -266,3 +266,44 @@ def test_march_empty_space_jumps_bit_exact(jump, lookup):
     assert np.array_equal(m["t"][mask], mo["t"][mask])
     assert np.array_equal(m["delta"][mask], mo["delta"][mask])
     assert (m["counts"] > 0).sum() > n // 3
+
+
+@pytest.mark.parametrize("far", [None, 5000], ids=["bricks", "superblocks-only"])
+def test_march_hash_mode_jump_structures_exact(far):
+    """Hash mode's three march paths give the same samples bit for bit: block-distance bricks
+    near the blocks (superblock grid <= 2^26), the superblock distance field alone (a far block
+    makes the superblock grid 625^3 > 2^26: no bricks), and the plain per-block hash probe walk
+    (march_jump = 0, the reference's march_intervals restated; bit-exact with the oracle in
+    test_march_bit_exact)."""
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    h = 0.01
+    L = 8 * h
+    rng = np.random.default_rng(5)
+    centres = rng.integers(0, 64, size=(30, 3))
+    cl = np.concatenate([c + rng.integers(-2, 3, size=(25, 3)) for c in centres])
+    if far is not None:
+        cl = np.concatenate([cl, [[far, far, far]]])
+    coords = np.unique(cl, axis=0).astype(np.int32)
+    A = len(coords)
+    g = SparseDenseGrid(h, 8, 1)
+    g.allocate_blocks(coords)
+    g.set_payload(0, A, weight=np.ones((A, 512), np.float32))
+    g.set_lookup(1)
+    assert g.info().lookup_mode == 1
+    n = 20_000
+    o = rng.uniform(-0.5, 64 * L + 0.5, size=(n, 3))
+    tgt = (coords[rng.integers(0, A, size=n)] + rng.uniform(0, 1, size=(n, 3))) * L
+    d = tgt - o
+    d[: n // 10, 1:] = 0.0  # axis-parallel
+    d[: n // 10, 0] = np.where(d[: n // 10, 0] >= 0, 1.0, -1.0)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    g.set_tuning("march_jump", 1)
+    mj = g.march(o, d, h / 2, 64)
+    g.set_tuning("march_jump", 0)
+    mp = g.march(o, d, h / 2, 64)
+    assert np.array_equal(mj["counts"], mp["counts"])
+    mask = np.arange(64)[None, :] < mj["counts"][:, None]
+    assert np.array_equal(mj["t"][mask].view(np.uint64), mp["t"][mask].view(np.uint64))
+    assert np.array_equal(mj["delta"][mask].view(np.uint64), mp["delta"][mask].view(np.uint64))
+    assert (mj["counts"] > 0).sum() > n // 2
