@@ -502,19 +502,25 @@ struct svr_grid {
                 use_sb = 1;
                 n_bricks = 0;
                 if (sc <= (1ull << 26)) {  // block-distance bricks of the superblocks near blocks
+                    // (at most 27 per occupied superblock, so <= 27 n of them)
+                    const uint64_t max_b = std::min<uint64_t>(sc, 27ull * n());
                     sb_info.ensure(sc * 4);
-                    brick_sb.ensure(sc * 4);
+                    brick_sb.ensure(max_b * 4);
                     brick_cnt.ensure(4);
                     const uint32_t nb = svr_internal::launch_brick_assign(
                         sb_dim, sbdist.as<uint8_t>(), sb_info.as<uint32_t>(), brick_sb.as<uint32_t>(),
                         brick_cnt.as<uint32_t>(), stream);
-                    bricks.ensure(static_cast<size_t>(nb) * 512);
-                    bricks_tmp.ensure(static_cast<size_t>(nb) * 512);
-                    svr_internal::launch_brick_fill(coords4, static_cast<uint32_t>(n()), sb_lo, sb_dim,
-                                                    sb_info.as<uint32_t>(), brick_sb.as<uint32_t>(), nb,
-                                                    bricks.as<uint8_t>(), bricks_tmp.as<uint8_t>(), stream);
-                    SVR_LAUNCHED();
-                    n_bricks = nb;
+                    // 1 KB per brick (two buffers): built only while that stays small next to the
+                    // blocks' own 26 KB (a grid of isolated blocks keeps the superblock field alone)
+                    if (nb <= 2 * n() + 65536) {
+                        bricks.ensure(static_cast<size_t>(nb) * 512);
+                        bricks_tmp.ensure(static_cast<size_t>(nb) * 512);
+                        svr_internal::launch_brick_fill(coords4, static_cast<uint32_t>(n()), sb_lo, sb_dim,
+                                                        sb_info.as<uint32_t>(), brick_sb.as<uint32_t>(), nb,
+                                                        bricks.as<uint8_t>(), bricks_tmp.as<uint8_t>(), stream);
+                        SVR_LAUNCHED();
+                        n_bricks = nb;
+                    }
                 }
             }
         }

@@ -307,3 +307,34 @@ def test_march_hash_mode_jump_structures_exact(far):
     assert np.array_equal(mj["t"][mask].view(np.uint64), mp["t"][mask].view(np.uint64))
     assert np.array_equal(mj["delta"][mask].view(np.uint64), mp["delta"][mask].view(np.uint64))
     assert (mj["counts"] > 0).sum() > n // 2
+
+
+def test_march_hash_mode_isolated_blocks_exact():
+    """3375 isolated blocks, one per 3-superblock cell: the bricks (27 per occupied superblock)
+    would outweigh the blocks, so hash mode keeps the superblock field alone -- the march must
+    still equal the plain hash-probe walk bit for bit."""
+    from paper_2305_13220_b200 import SparseDenseGrid
+
+    h = 0.01
+    L = 8 * h
+    rng = np.random.default_rng(9)
+    ax = np.arange(15) * 24
+    coords = np.stack(np.meshgrid(ax, ax, ax, indexing="ij"), -1).reshape(-1, 3).astype(np.int32)
+    A = len(coords)
+    g = SparseDenseGrid(h, 8, 1)
+    g.allocate_blocks(coords)
+    g.set_payload(0, A, weight=np.ones((A, 512), np.float32))
+    g.set_lookup(1)
+    n = 20_000
+    o = rng.uniform(-0.5, 15 * 24 * L, size=(n, 3))
+    tgt = (coords[rng.integers(0, A, size=n)] + rng.uniform(0, 1, size=(n, 3))) * L
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    g.set_tuning("march_jump", 1)
+    mj = g.march(o, d, h / 2, 64)
+    g.set_tuning("march_jump", 0)
+    mp = g.march(o, d, h / 2, 64)
+    assert np.array_equal(mj["counts"], mp["counts"])
+    mask = np.arange(64)[None, :] < mj["counts"][:, None]
+    assert np.array_equal(mj["t"][mask].view(np.uint64), mp["t"][mask].view(np.uint64))
+    assert (mj["counts"] > 0).sum() > n // 2
