@@ -39,9 +39,12 @@ def cfg1():
             "dD": np.ascontiguousarray(u[:, 3]), "dN": np.ascontiguousarray(u[:, 4:])}
 
 
-def test_cfg1_forward_backward(cfg1):
+@pytest.mark.parametrize("lookup", [2, 1], ids=["dense", "hash"])
+def test_cfg1_forward_backward(cfg1, lookup):
     g, og = cfg1["g"], cfg1["og"]
     step, beta = H / 2, 2 * H
+    g.set_lookup(lookup)
+    assert g.info().lookup_mode == lookup
     out = g.render_forward(cfg1["o"], cfg1["d"], step, 64, beta)
     OracleGrid.set_threads(8)
     try:
@@ -59,16 +62,20 @@ def test_cfg1_forward_backward(cfg1):
     assert_close(ggs, gs, what="grad_sdf")
     assert_close(ggr, gr, what="grad_rgb")
     assert np.array_equal(g.active_mask(), act)
+    g.set_lookup(0)
 
 
-def test_cfg2_full_image_forward(cfg1):
+@pytest.mark.parametrize("lookup", [2, 1], ids=["dense", "hash"])
+def test_cfg2_full_image_forward(cfg1, lookup):
     g, og = cfg1["g"], cfg1["og"]
     o, d = cfg1["scene"].image_rays(0)
     assert len(o) == 640 * 480
     step, beta = H / 2, 2 * H
+    g.set_lookup(lookup)
     g.set_tuning("records", 0)  # inference
     out = g.render_forward(o, d, step, 64, beta)
     g.set_tuning("records", 1)
+    g.set_lookup(0)
     OracleGrid.set_threads(16)
     try:
         ref = og.render_forward(o, d, step, 64, beta)
