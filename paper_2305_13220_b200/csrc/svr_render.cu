@@ -220,7 +220,12 @@ __device__ __forceinline__ uint32_t march_dev(const GridView& g, const V& o, con
                 }
             }
         }
-        if (dist >= 3) {
+        // jump only when every walking lane of the warp can: a partial set of jumpers would run
+        // the jump's exact crossing counts while the others idle (measured: all 0.536 ms, >= 3/4
+        // 0.545, >= 1/2 0.56, any 0.588); stepping instead is always exact
+        const unsigned walkers = __activemask();
+        const unsigned jumpers = __ballot_sync(walkers, dist >= 3);
+        if (dist >= 3 && jumpers == walkers) {
             open = false;
             const double ts = t + (dist - 2) * L * inv_md;
             if (ts >= t1) break;  // the ray leaves the AABB inside empty space
